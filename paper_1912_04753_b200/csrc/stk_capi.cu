@@ -1,0 +1,1120 @@
+// stk_capi.cu — host runtime behind the C ABI in include/stk.h.
+//
+// One context = one device + one stream.  The runtime validates inputs with
+// the reference's rules and messages, derives the exact bin thresholds and
+// the cell grid, sizes pattern batches to a memory budget, and drives the
+// kernels of stk_kernels.cu:
+//
+//   per batch of R patterns:  generate (K4) -> grid (K1) -> pairs (K2) -> finalize/envelopes (K5)
+//
+// All device work of one call is enqueued on the context stream; the host
+// synchronises once at the end (plus one tiny read-back for validation).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/stk.h"
+#include "stk_kernels.h"
+#include "stk_types.h"
+
+using namespace stk;
+
+namespace {
+
+struct InvalidArg : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct Unsupported : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaFail : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct StateErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw CudaFail(std::string(#expr) + ": " + cudaGetErrorString(e_));                 \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;  // elements
+  void ensure(size_t n) {
+    if (n <= cap) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    cap = std::max<size_t>(n, 1);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// Largest q with RN(sqrt(q)) <= s: d <= s  <=>  q <= Q(s), exactly, because
+// the correctly rounded sqrt is monotone (lets the kernels bin on q).
+double sqrt_threshold(double s) {
+  double q = s * s;
+  while (q > 0 && std::sqrt(q) > s) q = std::nextafter(q, 0.0);
+  for (;;) {
+    const double qn = std::nextafter(q, std::numeric_limits<double>::infinity());
+    if (std::sqrt(qn) <= s) q = qn; else break;
+  }
+  return q;
+}
+
+// geom::segments_properly_intersect (geometry.cpp:70-79)
+bool segments_properly_intersect(const double* a, const double* b, const double* c,
+                                 const double* d) {
+  auto orient = [](const double* p, const double* q, const double* r) {
+    const double v = (q[0] - p[0]) * (r[1] - p[1]) - (q[1] - p[1]) * (r[0] - p[0]);
+    return (v > 0.0) - (v < 0.0);
+  };
+  const int o1 = orient(a, b, c), o2 = orient(a, b, d);
+  const int o3 = orient(c, d, a), o4 = orient(c, d, b);
+  return o1 != o2 && o3 != o4 && o1 != 0 && o2 != 0 && o3 != 0 && o4 != 0;
+}
+
+}  // namespace
+
+struct stk_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int num_sms = 148;
+  uint64_t mem_budget = 16ull << 30;
+
+  // region (geom::StudyRegion)
+  bool have_region = false;
+  std::vector<double> ring;  // open, interleaved
+  uint32_t nv = 0;
+  int64_t p0 = 0, p1 = 0;
+  double area = 0;
+  int64_t duration = 0;
+  double xmin = 0, xmax = 0, ymin = 0, ymax = 0, maxabs = 0;
+  bool fast_rect = false;  // axis-aligned rectangle: every bbox draw is inside
+  DevBuf<double2> d_ring;
+
+  // grid (est::DistanceGrid)
+  bool have_grid = false;
+  std::vector<double> s_values;
+  std::vector<int64_t> t_values;
+  std::vector<double> Q;
+  std::vector<uint16_t> stab, ttab;
+  float s_inv_bw = 0, t_inv_bw = 0;
+  DevBuf<double> d_Q, d_s;
+  DevBuf<int64_t> d_T;
+  DevBuf<uint16_t> d_stab, d_ttab;
+
+  // batch buffers (grow-only)
+  DevBuf<double> x, y, xs, ys;
+  DevBuf<int64_t> t, ts;
+  DevBuf<uint32_t> idx, key, rank, cell_count, cell_start, item_start, task_start, task_counter;
+  DevBuf<uint2> items;
+  DevBuf<unsigned long long> hist, stats, bad;
+  DevBuf<double> K, L, env, obs;
+  DevBuf<int> flags, ovf;
+  DevBuf<double> scratch;
+  DevBuf<double> sx, sy;  // host-upload staging of the observed pattern
+  DevBuf<int64_t> st;
+
+  uint64_t launches = 0;  // kernels launched by the current call
+  std::vector<unsigned long long> obs_raw;
+
+  std::vector<cudaEvent_t> evpool;
+  size_t evnext = 0;
+  cudaEvent_t ev() {
+    if (evnext == evpool.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      evpool.push_back(e);
+    }
+    return evpool[evnext++];
+  }
+};
+
+namespace {
+
+RegionView region_view(stk_ctx* c) {
+  RegionView r;
+  r.ring = c->d_ring.p;
+  r.nv = c->nv;
+  r.p0 = c->p0;
+  r.p1 = c->p1;
+  r.xmin = c->xmin;
+  r.xmax = c->xmax;
+  r.ymin = c->ymin;
+  r.ymax = c->ymax;
+  r.maxabs = c->maxabs;
+  return r;
+}
+
+BinView bin_view(stk_ctx* c) {
+  BinView b;
+  b.Q = c->d_Q.p;
+  b.T = c->d_T.p;
+  b.s_tab = c->d_stab.p;
+  b.t_tab = c->d_ttab.p;
+  b.cs = (uint32_t)c->s_values.size();
+  b.ct = (uint32_t)c->t_values.size();
+  b.Qmax = c->Q.back();
+  b.Tmax = c->t_values.back();
+  b.s_inv_bw = c->s_inv_bw;
+  b.t_inv_bw = c->t_inv_bw;
+  return b;
+}
+
+// Uniform grid with cells >= (s_max, t_max): every in-threshold neighbour of a
+// point lies in the 3x3x3 block of cells around it.
+GridGeom make_grid_geom(stk_ctx* c, uint64_t n) {
+  GridGeom g;
+  const double smax = c->s_values.back();
+  const int64_t tmax = c->t_values.back();
+  double w = smax * (1.0 + 1e-6);
+  int64_t tw = std::max<int64_t>(tmax, 1);
+  const double ex = c->xmax - c->xmin, ey = c->ymax - c->ymin;
+  const uint64_t cap = std::max<uint64_t>(4096, std::min<uint64_t>(2 * n, 1ull << 26));
+  auto ncell = [](double extent, double width) {
+    const double k = std::floor(extent / width) + 1.0;
+    return (int64_t)std::min(k, 1e9);
+  };
+  int64_t nx, ny, nt;
+  for (;;) {
+    nx = ncell(ex, w);
+    ny = ncell(ey, w);
+    nt = (c->p1 - c->p0) / tw + 1;
+    if ((double)nx * (double)ny * (double)nt <= (double)cap) break;
+    if (nx * ny >= nt) w *= 1.5; else tw = tw + tw / 2 + 1;
+  }
+  g.x0 = c->xmin;
+  g.y0 = c->ymin;
+  g.inv_w = 1.0 / w;
+  g.t0 = c->p0;
+  g.tw = tw;
+  g.inv_tw = 1.0 / (double)tw;
+  g.nx = (int32_t)nx;
+  g.ny = (int32_t)ny;
+  g.nt = (int32_t)nt;
+  g.cells = (uint32_t)(nx * ny * nt);
+  return g;
+}
+
+struct Plan {
+  uint64_t n;
+  GridGeom G;
+  uint32_t bins;
+  uint32_t max_items;
+  int R;  // patterns per batch
+};
+
+Plan make_plan(stk_ctx* c, uint64_t n, uint64_t patterns) {
+  Plan P;
+  P.n = n;
+  P.G = make_grid_geom(c, n);
+  P.bins = (uint32_t)(c->s_values.size() * c->t_values.size());
+  P.max_items = (uint32_t)((n + kItemCenters - 1) / kItemCenters + P.G.cells);
+  const uint64_t per = n * (8 * 3 + 8 * 3 + 4 * 3) + (uint64_t)(P.G.cells + 1) * 4 * 3 +
+                       (uint64_t)P.max_items * 8 + (uint64_t)P.bins * 8 * 6 + 64;
+  uint64_t R = std::max<uint64_t>(1, c->mem_budget / per);
+  R = std::min<uint64_t>(R, std::max<uint64_t>(patterns, 1));
+  R = std::min<uint64_t>(R, 4096);
+  P.R = (int)R;
+  return P;
+}
+
+Batch alloc_batch(stk_ctx* c, const Plan& P) {
+  const uint64_t R = P.R, n = P.n;
+  c->x.ensure(R * n);
+  c->y.ensure(R * n);
+  c->t.ensure(R * n);
+  c->xs.ensure(R * n);
+  c->ys.ensure(R * n);
+  c->ts.ensure(R * n);
+  c->idx.ensure(R * n);
+  c->key.ensure(R * n);
+  c->rank.ensure(R * n);
+  c->cell_count.ensure(R * P.G.cells);
+  c->cell_start.ensure(R * (P.G.cells + 1));
+  c->item_start.ensure(R * (P.G.cells + 1));
+  c->items.ensure(R * P.max_items);
+  c->task_start.ensure(R + 1);
+  c->task_counter.ensure(1);
+  c->hist.ensure(R * P.bins * 4);
+  c->stats.ensure(4);
+  c->K.ensure(R * P.bins);
+  c->L.ensure(R * P.bins);
+  c->flags.ensure(R);
+  Batch B;
+  B.R = (int)R;
+  B.n = n;
+  B.x = c->x.p;
+  B.y = c->y.p;
+  B.t = c->t.p;
+  B.xs = c->xs.p;
+  B.ys = c->ys.p;
+  B.ts = c->ts.p;
+  B.idx = c->idx.p;
+  B.key = c->key.p;
+  B.rank = c->rank.p;
+  B.cell_count = c->cell_count.p;
+  B.cell_start = c->cell_start.p;
+  B.item_start = c->item_start.p;
+  B.items = c->items.p;
+  B.max_items = P.max_items;
+  B.task_start = c->task_start.p;
+  B.task_counter = c->task_counter.p;
+  B.h_cnt = c->hist.p;
+  B.h_half = c->hist.p + R * P.bins;
+  B.h_lo = c->hist.p + 2 * R * P.bins;
+  B.h_hi = c->hist.p + 3 * R * P.bins;
+  B.K = c->K.p;
+  B.L = c->L.p;
+  B.stats = c->stats.p;
+  B.flags = c->flags.p;
+  return B;
+}
+
+struct Timers {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gen, grid, pair, fin;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+};
+
+void require_ready(stk_ctx* c) {
+  if (!c->have_region) throw StateErr("study region not set (stk_set_region)");
+  if (!c->have_grid) throw StateErr("distance grid not set (stk_set_grid)");
+}
+
+// Check region.contains(p) for the n points at (dx,dy,dt) on the device.
+void validate_points(stk_ctx* c, const double* dx, const double* dy, const int64_t* dt,
+                     uint64_t n) {
+  c->bad.ensure(1);
+  const unsigned long long init = ~0ULL;
+  CK(cudaMemcpyAsync(c->bad.p, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+  const int blocks = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)c->num_sms * 16);
+  validate_kernel<<<std::max(blocks, 1), 256, 0, c->stream>>>(dx, dy, dt, n, region_view(c),
+                                                               c->bad.p);
+  CK(cudaGetLastError());
+  ++c->launches;
+  unsigned long long bad = 0;
+  CK(cudaMemcpyAsync(&bad, c->bad.p, sizeof(bad), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (bad != ~0ULL) throw InvalidArg("point outside study region or period");
+}
+
+enum class Source { Observed, Csr, Bootstrap, Permutation };
+
+// Fill patterns [p_first, p_first+count) of the batch.  Observed: copy from
+// device pointers (count must be 1).  Otherwise realisation seeds seed0 + j.
+void generate(stk_ctx* c, const Batch& B, Source src, int p_first, int count, uint64_t seed0,
+              const double* ox, const double* oy, const int64_t* ot) {
+  if (count <= 0) return;
+  const uint64_t n = B.n;
+  if (src == Source::Observed) {
+    CK(cudaMemcpyAsync(B.x + (uint64_t)p_first * n, ox, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(B.y + (uint64_t)p_first * n, oy, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(B.t + (uint64_t)p_first * n, ot, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return;
+  }
+  CK(cudaMemsetAsync(B.flags + p_first, 0, sizeof(int) * count, c->stream));
+  if (src == Source::Csr) {
+    const uint64_t ntl = (uint64_t)(c->p1 - c->p0) + 1;  // uniform_int(p0, p1)
+    const uint64_t limit = ~0ULL - (~0ULL % ntl);
+    if (c->fast_rect) {
+      csr_fast_kernel<<<count, 320, 0, c->stream>>>(B, p_first, seed0, region_view(c), ntl, limit);
+      CK(cudaGetLastError());
+  ++c->launches;
+    }
+    csr_seq_kernel<<<(count + 31) / 32, 32, 0, c->stream>>>(B, p_first, count, seed0,
+                                                            region_view(c), ntl, limit,
+                                                            c->fast_rect ? 0 : 1);
+    CK(cudaGetLastError());
+  ++c->launches;
+  } else if (src == Source::Bootstrap) {
+    const uint64_t limit = ~0ULL - (~0ULL % n);
+    bootstrap_kernel<<<count, 320, 0, c->stream>>>(B, p_first, seed0, ox, oy, ot, limit);
+    CK(cudaGetLastError());
+  ++c->launches;
+    resample_seq_kernel<<<(count + 31) / 32, 32, 0, c->stream>>>(B, p_first, count, seed0, ox,
+                                                                 oy, ot, 1);
+    CK(cudaGetLastError());
+  ++c->launches;
+  } else {
+    resample_seq_kernel<<<(count + 31) / 32, 32, 0, c->stream>>>(B, p_first, count, seed0, ox,
+                                                                 oy, ot, 2);
+    CK(cudaGetLastError());
+  ++c->launches;
+  }
+}
+
+// Grid build + pair kernel + finalize for patterns [0, R) of the batch.
+void run_batch(stk_ctx* c, const Plan& P, const Batch& B, Timers& tm, uint32_t shard,
+               uint32_t nshards, int shard_scope, bool restrict_centers, uint64_t c0,
+               uint64_t c1, bool finalize) {
+  const GridGeom& G = P.G;
+  const int R = B.R;
+  cudaEvent_t e0 = c->ev(), e1 = c->ev(), e2 = c->ev();
+  CK(cudaEventRecord(e0, c->stream));
+  CK(cudaMemsetAsync(B.cell_count, 0, sizeof(uint32_t) * (uint64_t)R * G.cells, c->stream));
+  CK(cudaMemsetAsync(B.h_cnt, 0, sizeof(unsigned long long) * (uint64_t)R * P.bins * 4, c->stream));
+  dim3 gp((unsigned)((B.n + 255) / 256), (unsigned)R);
+  key_kernel<<<gp, 256, 0, c->stream>>>(B, G, 0);
+  CK(cudaGetLastError());
+  ++c->launches;
+  scan_kernel<<<R, 1024, 0, c->stream>>>(B, G, 0);
+  CK(cudaGetLastError());
+  ++c->launches;
+  scatter_kernel<<<gp, 256, 0, c->stream>>>(B, G, 0);
+  CK(cudaGetLastError());
+  ++c->launches;
+  dim3 gc((G.cells + 255) / 256, (unsigned)R);
+  items_kernel<<<gc, 256, 0, c->stream>>>(B, G, 0);
+  CK(cudaGetLastError());
+  ++c->launches;
+  tasks_kernel<<<1, 1, 0, c->stream>>>(B, G);
+  CK(cudaGetLastError());
+  ++c->launches;
+  CK(cudaEventRecord(e1, c->stream));
+
+  PairArgs A;
+  A.B = B;
+  A.G = G;
+  A.bins = bin_view(c);
+  A.reg = region_view(c);
+  A.shard = shard;
+  A.nshards = std::max<uint32_t>(nshards, 1);
+  A.shard_scope = A.nshards > 1 ? shard_scope : 0;
+  A.restrict_centers = restrict_centers ? 1 : 0;
+  A.c0 = c0;
+  A.c1 = c1;
+  const size_t smem = pair_kernel_smem(P.bins, A.bins.cs, A.bins.ct);
+  CK(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_kernel, kPairWarps * 32, smem));
+  if (per_sm < 1) throw Unsupported("distance grid too large for the pair kernel's shared histogram");
+  pair_kernel<<<c->num_sms * per_sm, kPairWarps * 32, smem, c->stream>>>(A);
+  CK(cudaGetLastError());
+  ++c->launches;
+  CK(cudaEventRecord(e2, c->stream));
+  tm.grid.push_back({e0, e1});
+  tm.pair.push_back({e1, e2});
+  if (finalize) {
+    cudaEvent_t e3 = c->ev();
+    finalize_kernel<<<R, 256, 0, c->stream>>>(B, A.bins.cs, A.bins.ct, c->d_s.p, c->d_T.p,
+                                              c->area, c->duration, 0);
+    CK(cudaGetLastError());
+  ++c->launches;
+    CK(cudaEventRecord(e3, c->stream));
+    tm.fin.push_back({e2, e3});
+  }
+}
+
+double elapsed(const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+  double s = 0;
+  for (auto& pr : v) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) s += ms;
+  }
+  return s;
+}
+
+void fill_telemetry(stk_ctx* c, Timers& tm, stk_telemetry* tel, uint64_t patterns) {
+  unsigned long long st[4] = {0, 0, 0, 0};
+  CK(cudaMemcpyAsync(st, c->stats.p, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (st[3]) throw Unsupported("more than 64 circle/boundary crossings in one edge weight");
+  if (!tel) return;
+  tel->in_threshold_pairs += st[0];
+  tel->candidate_pairs += st[1];
+  tel->exact_path_pairs += st[2];
+  tel->patterns += patterns;
+  tel->kernel_launches += c->launches;
+  tel->gen_ms += elapsed(tm.gen);
+  tel->grid_ms += elapsed(tm.grid);
+  tel->pair_ms += elapsed(tm.pair);
+  tel->finalize_ms += elapsed(tm.fin);
+  if (tm.t0 && tm.t1) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, tm.t0, tm.t1);
+    tel->total_ms += ms;
+  }
+}
+
+Source source_of(int method) {
+  switch (method) {
+    case STK_METHOD_CSR: return Source::Csr;
+    case STK_METHOD_BOOTSTRAP: return Source::Bootstrap;
+    case STK_METHOD_PERMUTATION: return Source::Permutation;
+  }
+  throw InvalidArg("unknown simulation method");
+}
+
+// The pipeline shared by estimate / simulate / run_job: an optional observed
+// pattern (device pointers) followed by realisations [r_begin, r_end).
+struct JobOut {
+  double* k_obs = nullptr;   // host
+  double* l_obs = nullptr;   // host
+  double* l_all = nullptr;   // host (r_end - r_begin) * bins
+  double* upper = nullptr;   // host
+  double* lower = nullptr;   // host
+  double* diff = nullptr;    // host
+  uint64_t* obs_counts = nullptr;  // host: exact pre-cumulative results of the observed
+  uint64_t* obs_hi = nullptr;      //       pattern (or of its shard)
+  uint64_t* obs_lo = nullptr;
+};
+
+void run_pipeline(stk_ctx* c, const double* dx, const double* dy, const int64_t* dt, uint64_t n,
+                  bool with_observed, int method, uint64_t base_seed, uint32_t r_begin,
+                  uint32_t r_end, const JobOut& out, stk_telemetry* tel,
+                  uint32_t obs_shard = 0, uint32_t obs_nshards = 1) {
+  require_ready(c);
+  c->evnext = 0;
+  Timers tm;
+  tm.t0 = c->ev();
+  tm.t1 = c->ev();
+  CK(cudaEventRecord(tm.t0, c->stream));
+  const uint64_t sims = r_end > r_begin ? r_end - r_begin : 0;
+  const uint64_t patterns = (with_observed ? 1 : 0) + sims;
+  Plan P = make_plan(c, n, patterns);
+  const Source src = source_of(method);
+  CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * 4, c->stream));
+  c->env.ensure(2 * (uint64_t)P.bins);
+  c->obs.ensure(2 * (uint64_t)P.bins);
+  bool env_init = true;
+  uint64_t done = 0;
+  uint32_t next_r = r_begin;
+  while (done < patterns) {
+    const uint64_t R = std::min<uint64_t>((uint64_t)P.R, patterns - done);
+    Plan PB = P;
+    PB.R = (int)R;
+    Batch B = alloc_batch(c, PB);
+    int p = 0;
+    cudaEvent_t g0 = c->ev(), g1 = c->ev();
+    CK(cudaEventRecord(g0, c->stream));
+    const bool obs_here = with_observed && done == 0;
+    if (obs_here) {
+      generate(c, B, Source::Observed, 0, 1, 0, dx, dy, dt);
+      p = 1;
+    }
+    const int nsim = (int)(R - (obs_here ? 1 : 0));
+    generate(c, B, src, p, nsim, base_seed + next_r, dx, dy, dt);
+    CK(cudaEventRecord(g1, c->stream));
+    tm.gen.push_back({g0, g1});
+    run_batch(c, PB, B, tm, obs_shard, obs_here ? obs_nshards : 1, 1, false, 0, 0, true);
+    cudaEvent_t f0 = c->ev(), f1 = c->ev();
+    CK(cudaEventRecord(f0, c->stream));
+    if (obs_here && out.obs_counts) {
+      // raw exact sums of pattern 0 (h_cnt, h_half, h_lo, h_hi rows of pattern 0)
+      c->scratch.ensure(4 * (uint64_t)P.bins);
+      for (int f = 0; f < 4; ++f)
+        CK(cudaMemcpyAsync(c->scratch.p + (uint64_t)f * P.bins, B.h_cnt + (uint64_t)f * R * P.bins,
+                           8 * (uint64_t)P.bins, cudaMemcpyDeviceToDevice, c->stream));
+      c->obs_raw.resize(4 * (size_t)P.bins);
+      CK(cudaMemcpyAsync(c->obs_raw.data(), c->scratch.p, 32 * (uint64_t)P.bins,
+                         cudaMemcpyDeviceToHost, c->stream));
+    }
+    if (obs_here) {
+      CK(cudaMemcpyAsync(c->obs.p, B.K, sizeof(double) * P.bins, cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaMemcpyAsync(c->obs.p + P.bins, B.L, sizeof(double) * P.bins, cudaMemcpyDeviceToDevice,
+                         c->stream));
+    }
+    if (nsim > 0) {
+      envelope_kernel<<<(P.bins + 255) / 256, 256, 0, c->stream>>>(
+          B, P.bins, p, nsim, env_init ? 1 : 0, c->env.p, c->env.p + P.bins);
+      CK(cudaGetLastError());
+  ++c->launches;
+      env_init = false;
+      if (out.l_all)
+        CK(cudaMemcpyAsync(out.l_all + (uint64_t)(next_r - r_begin) * P.bins,
+                           B.L + (uint64_t)p * P.bins, sizeof(double) * P.bins * nsim,
+                           cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaEventRecord(f1, c->stream));
+    tm.fin.push_back({f0, f1});
+    next_r += (uint32_t)nsim;
+    done += R;
+  }
+  const uint32_t bins = P.bins;
+  if (with_observed && sims > 0 && out.diff) {
+    c->scratch.ensure(bins);
+    diff_kernel<<<(bins + 255) / 256, 256, 0, c->stream>>>(c->obs.p + bins, c->env.p, bins,
+                                                           c->scratch.p);
+    CK(cudaGetLastError());
+  ++c->launches;
+    CK(cudaMemcpyAsync(out.diff, c->scratch.p, sizeof(double) * bins, cudaMemcpyDeviceToHost,
+                       c->stream));
+  }
+  if (with_observed && out.k_obs)
+    CK(cudaMemcpyAsync(out.k_obs, c->obs.p, sizeof(double) * bins, cudaMemcpyDeviceToHost, c->stream));
+  if (with_observed && out.l_obs)
+    CK(cudaMemcpyAsync(out.l_obs, c->obs.p + bins, sizeof(double) * bins, cudaMemcpyDeviceToHost,
+                       c->stream));
+  if (sims > 0 && out.upper)
+    CK(cudaMemcpyAsync(out.upper, c->env.p, sizeof(double) * bins, cudaMemcpyDeviceToHost, c->stream));
+  if (sims > 0 && out.lower)
+    CK(cudaMemcpyAsync(out.lower, c->env.p + bins, sizeof(double) * bins, cudaMemcpyDeviceToHost,
+                       c->stream));
+  CK(cudaEventRecord(tm.t1, c->stream));
+  fill_telemetry(c, tm, tel, patterns);
+  if (with_observed && out.obs_counts) {
+    const uint32_t b = P.bins;
+    for (uint32_t i = 0; i < b; ++i) {
+      const unsigned long long cnt = c->obs_raw[i], half = c->obs_raw[b + i],
+                               lo = c->obs_raw[2 * b + i], hi = c->obs_raw[3 * b + i];
+      out.obs_counts[i] = cnt;
+      const unsigned __int128 v = ((unsigned __int128)hi << 64 | lo) +
+                                  ((unsigned __int128)(cnt + half) << 52);
+      if (out.obs_hi) out.obs_hi[i] = (uint64_t)(v >> 64);
+      if (out.obs_lo) out.obs_lo[i] = (uint64_t)v;
+    }
+  }
+}
+
+template <class F>
+int guarded(stk_ctx* c, F&& f) {
+  if (!c) return STK_ESTATE;
+  try {
+    CK(cudaSetDevice(c->device));
+    c->launches = 0;
+    f();
+    c->err.clear();
+    return STK_OK;
+  } catch (const InvalidArg& e) {
+    c->err = e.what();
+    return STK_EINVAL;
+  } catch (const Unsupported& e) {
+    c->err = e.what();
+    return STK_EUNSUPPORTED;
+  } catch (const StateErr& e) {
+    c->err = e.what();
+    return STK_ESTATE;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return STK_ECUDA;
+  }
+}
+
+// Upload the host observed pattern into the context's staging buffers.
+void upload_points(stk_ctx* c, const double* x, const double* y, const int64_t* t, uint64_t n) {
+  c->sx.ensure(n);
+  c->sy.ensure(n);
+  c->st.ensure(n);
+  CK(cudaMemcpyAsync(c->sx.p, x, n * 8, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->sy.p, y, n * 8, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->st.p, t, n * 8, cudaMemcpyHostToDevice, c->stream));
+}
+
+void check_n(uint64_t n) {
+  if (n < 2) throw InvalidArg("K estimation needs n >= 2");
+  if (n > 0xFFFFFFF0ull) throw Unsupported("more than 2^32 points per pattern");
+}
+
+}  // namespace
+
+// =====================================================================
+extern "C" {
+
+const char* stk_version(void) { return "stk 0.1 (sm_100a)"; }
+
+int stk_create(stk_ctx** out, int device) {
+  if (!out) return STK_EINVAL;
+  *out = nullptr;
+  stk_ctx* c = new stk_ctx();
+  c->device = device;
+  try {
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    c->stats.ensure(4);
+  } catch (const std::exception& e) {
+    delete c;
+    return STK_ECUDA;
+  }
+  *out = c;
+  return STK_OK;
+}
+
+void stk_destroy(stk_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto e : c->evpool) cudaEventDestroy(e);
+  c->d_ring.release(); c->d_Q.release(); c->d_s.release(); c->d_T.release();
+  c->d_stab.release(); c->d_ttab.release();
+  c->x.release(); c->y.release(); c->t.release(); c->xs.release(); c->ys.release();
+  c->ts.release(); c->idx.release(); c->key.release(); c->rank.release();
+  c->cell_count.release(); c->cell_start.release(); c->item_start.release();
+  c->task_start.release(); c->task_counter.release(); c->items.release();
+  c->hist.release(); c->stats.release(); c->bad.release(); c->K.release(); c->L.release();
+  c->env.release(); c->obs.release(); c->flags.release(); c->ovf.release();
+  c->scratch.release(); c->sx.release(); c->sy.release(); c->st.release();
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* stk_last_error(const stk_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+void* stk_stream(stk_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int stk_set_memory_budget(stk_ctx* c, uint64_t bytes) {
+  return guarded(c, [&] {
+    if (bytes < (1ull << 20)) throw InvalidArg("memory budget must be >= 1 MiB");
+    c->mem_budget = bytes;
+  });
+}
+
+namespace {
+
+struct RegionInfo {
+  std::vector<double> ring;
+  uint32_t nv;
+  double area;
+  int64_t duration;
+};
+
+// geom::StudyRegion constructor checks (geometry.cpp:113-136), in order.
+RegionInfo check_region(const double* ring_xy, uint32_t nv, int64_t period_start,
+                        int64_t period_end) {
+  if (!ring_xy && nv) throw InvalidArg("null ring");
+  std::vector<double> r(ring_xy, ring_xy + 2 * (size_t)nv);
+  if (r.size() >= 4 && r[0] == r[r.size() - 2] && r[1] == r[r.size() - 1]) r.resize(r.size() - 2);
+  const uint32_t m = (uint32_t)(r.size() / 2);
+  if (m < 3) throw InvalidArg("polygon needs >= 3 vertices");
+  for (double v : r)
+    if (!std::isfinite(v)) throw InvalidArg("polygon vertex not finite");
+  for (uint32_t i = 0; i < m; ++i)
+    for (uint32_t j = i + 1; j < m; ++j) {
+      if (j == i + 1 || (i == 0 && j == m - 1)) continue;
+      if (segments_properly_intersect(&r[2 * i], &r[2 * ((i + 1) % m)], &r[2 * j],
+                                      &r[2 * ((j + 1) % m)]))
+        throw InvalidArg("polygon is self-intersecting");
+    }
+  double acc = 0.0;  // polygon_area (geometry.cpp:99-108)
+  for (uint32_t i = 0, j = m - 1; i < m; j = i++)
+    acc += r[2 * j] * r[2 * i + 1] - r[2 * i] * r[2 * j + 1];
+  const double area = std::abs(acc) / 2.0;
+  if (!(area > 0.0)) throw InvalidArg("degenerate polygon (zero area)");
+  const int64_t duration = period_end - period_start;
+  if (duration <= 0) throw InvalidArg("study period duration must be > 0");
+  return RegionInfo{std::move(r), m, area, duration};
+}
+
+// DistanceGrid::validate (estimator.cpp:14-22).
+void check_grid(const double* s_values, uint32_t cs, const int64_t* t_values, uint32_t ct) {
+  if (cs == 0 || ct == 0) throw InvalidArg("distance grid must be non-empty");
+  if (!(s_values[0] > 0.0) || t_values[0] <= 0)
+    throw InvalidArg("distance grid must exclude s=0 and t=0");
+  for (uint32_t i = 1; i < cs; ++i)
+    if (!(s_values[i - 1] < s_values[i])) throw InvalidArg("distance grid must be strictly increasing");
+  for (uint32_t i = 1; i < ct; ++i)
+    if (!(t_values[i - 1] < t_values[i])) throw InvalidArg("distance grid must be strictly increasing");
+}
+
+int write_msg(const std::exception& e, char* msg, size_t msglen, int code) {
+  if (msg && msglen) {
+    std::strncpy(msg, e.what(), msglen - 1);
+    msg[msglen - 1] = 0;
+  }
+  return code;
+}
+
+}  // namespace
+
+int stk_check_region(const double* ring_xy, uint32_t nv, int64_t period_start,
+                     int64_t period_end, double* area, int64_t* duration, char* msg,
+                     size_t msglen) {
+  try {
+    const RegionInfo ri = check_region(ring_xy, nv, period_start, period_end);
+    if (area) *area = ri.area;
+    if (duration) *duration = ri.duration;
+    return STK_OK;
+  } catch (const InvalidArg& e) {
+    return write_msg(e, msg, msglen, STK_EINVAL);
+  } catch (const std::exception& e) {
+    return write_msg(e, msg, msglen, STK_ECUDA);
+  }
+}
+
+int stk_check_grid(const double* s_values, uint32_t cs, const int64_t* t_values, uint32_t ct,
+                   char* msg, size_t msglen) {
+  try {
+    check_grid(s_values, cs, t_values, ct);
+    return STK_OK;
+  } catch (const InvalidArg& e) {
+    return write_msg(e, msg, msglen, STK_EINVAL);
+  }
+}
+
+int stk_set_region(stk_ctx* c, const double* ring_xy, uint32_t nv, int64_t period_start,
+                   int64_t period_end) {
+  return guarded(c, [&] {
+    c->have_region = false;
+    const RegionInfo ri = check_region(ring_xy, nv, period_start, period_end);
+    const std::vector<double>& r = ri.ring;
+    const uint32_t m = ri.nv;
+    c->ring = r;
+    c->nv = m;
+    c->p0 = period_start;
+    c->p1 = period_end;
+    c->area = ri.area;
+    c->duration = ri.duration;
+    c->xmin = c->xmax = r[0];
+    c->ymin = c->ymax = r[1];
+    c->maxabs = 0;
+    for (uint32_t i = 0; i < m; ++i) {
+      c->xmin = std::min(c->xmin, r[2 * i]);
+      c->xmax = std::max(c->xmax, r[2 * i]);
+      c->ymin = std::min(c->ymin, r[2 * i + 1]);
+      c->ymax = std::max(c->ymax, r[2 * i + 1]);
+      c->maxabs = std::max(c->maxabs, std::max(std::abs(r[2 * i]), std::abs(r[2 * i + 1])));
+    }
+    bool rect = (m == 4);
+    for (uint32_t i = 0; rect && i < m; ++i) {
+      const uint32_t j = (i + 1) % m;
+      rect = (r[2 * i] == r[2 * j]) || (r[2 * i + 1] == r[2 * j + 1]);
+    }
+    c->fast_rect = rect && ri.area == (c->xmax - c->xmin) * (c->ymax - c->ymin);
+    c->d_ring.ensure(m);
+    CK(cudaMemcpyAsync(c->d_ring.p, r.data(), sizeof(double) * r.size(), cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->have_region = true;
+  });
+}
+
+int stk_set_grid(stk_ctx* c, const double* s_values, uint32_t cs, const int64_t* t_values,
+                 uint32_t ct) {
+  return guarded(c, [&] {
+    c->have_grid = false;
+    check_grid(s_values, cs, t_values, ct);
+    if ((uint64_t)cs * ct > (1u << 20)) throw Unsupported("more than 2^20 grid cells");
+    c->s_values.assign(s_values, s_values + cs);
+    c->t_values.assign(t_values, t_values + ct);
+    c->Q.resize(cs);
+    for (uint32_t k = 0; k < cs; ++k) c->Q[k] = sqrt_threshold(s_values[k]);
+    // bucket tables: bucket b holds distances >= b*bw (guaranteed by a 1e-5
+    // margin on the device-side bucket index), so the first bin at or above
+    // b*bw is a lower bound of the true bin.
+    const double smax = s_values[cs - 1];
+    const double sbw = smax / kBucketTable;
+    c->s_inv_bw = (float)((1.0 / sbw) * (1.0 - 1e-5));
+    c->stab.assign(kBucketTable, 0);
+    for (int b = 0, k = 0; b < kBucketTable; ++b) {
+      while (k < (int)cs - 1 && s_values[k] < b * sbw) ++k;
+      c->stab[b] = (uint16_t)std::min<int>(k, 65535);
+    }
+    const double tmax = (double)t_values[ct - 1];
+    const double tbw = tmax / kBucketTable;
+    c->t_inv_bw = (float)((1.0 / tbw) * (1.0 - 1e-5));
+    c->ttab.assign(kBucketTable, 0);
+    for (int b = 0, k = 0; b < kBucketTable; ++b) {
+      while (k < (int)ct - 1 && (double)t_values[k] < b * tbw) ++k;
+      c->ttab[b] = (uint16_t)std::min<int>(k, 65535);
+    }
+    if (cs > 65535 || ct > 65535) throw Unsupported("more than 65535 bins per axis");
+    c->d_Q.ensure(cs);
+    c->d_s.ensure(cs);
+    c->d_T.ensure(ct);
+    c->d_stab.ensure(kBucketTable);
+    c->d_ttab.ensure(kBucketTable);
+    CK(cudaMemcpyAsync(c->d_Q.p, c->Q.data(), 8 * cs, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_s.p, s_values, 8 * cs, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_T.p, t_values, 8 * ct, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_stab.p, c->stab.data(), 2 * kBucketTable, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_ttab.p, c->ttab.data(), 2 * kBucketTable, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->have_grid = true;
+  });
+}
+
+int stk_set_options(stk_ctx* c, int use_index, int use_cache, double coord_tolerance,
+                    double dist_tolerance) {
+  return guarded(c, [&] {
+    (void)use_index;
+    if (use_cache && (coord_tolerance != 0.0 || dist_tolerance != 0.0))
+      throw Unsupported("nonzero weight-cache tolerances are order-dependent in the reference "
+                        "and are not supported on the device path");
+  });
+}
+
+int stk_estimate_surface(stk_ctx* c, const double* x, const double* y, const int64_t* t,
+                         uint64_t n, double* k_out, stk_telemetry* tel) {
+  return guarded(c, [&] {
+    require_ready(c);
+    check_n(n);
+    upload_points(c, x, y, t, n);
+    validate_points(c, c->sx.p, c->sy.p, c->st.p, n);
+    JobOut o;
+    o.k_obs = k_out;
+    run_pipeline(c, c->sx.p, c->sy.p, c->st.p, n, true, STK_METHOD_CSR, 0, 0, 0, o, tel);
+  });
+}
+
+int stk_pair_histogram(stk_ctx* c, const double* x, const double* y, const int64_t* t,
+                       uint64_t n, uint32_t shard, uint32_t nshards, uint64_t* counts,
+                       uint64_t* sum_hi, uint64_t* sum_lo, double* hist, stk_telemetry* tel) {
+  return guarded(c, [&] {
+    require_ready(c);
+    check_n(n);
+    if (nshards == 0 || shard >= nshards) throw InvalidArg("shard index out of range");
+    upload_points(c, x, y, t, n);
+    validate_points(c, c->sx.p, c->sy.p, c->st.p, n);
+    c->evnext = 0;
+    Timers tm;
+    tm.t0 = c->ev();
+    tm.t1 = c->ev();
+    CK(cudaEventRecord(tm.t0, c->stream));
+    Plan P = make_plan(c, n, 1);
+    P.R = 1;
+    Batch B = alloc_batch(c, P);
+    CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * 4, c->stream));
+    generate(c, B, Source::Observed, 0, 1, 0, c->sx.p, c->sy.p, c->st.p);
+    run_batch(c, P, B, tm, shard, nshards, 2, false, 0, 0, false);
+    const uint32_t bins = P.bins;
+    std::vector<unsigned long long> h(4 * (size_t)bins);
+    CK(cudaMemcpyAsync(h.data(), B.h_cnt, sizeof(unsigned long long) * 4 * bins,
+                       cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaEventRecord(tm.t1, c->stream));
+    fill_telemetry(c, tm, tel, 1);
+    for (uint32_t b = 0; b < bins; ++b) {
+      const unsigned long long cnt = h[b], half = h[bins + b], lo = h[2 * bins + b],
+                               hi = h[3 * bins + b];
+      if (counts) counts[b] = cnt;
+      const unsigned __int128 v = ((unsigned __int128)hi << 64 | lo) +
+                                  ((unsigned __int128)(cnt + half) << 52);
+      if (sum_hi) sum_hi[b] = (uint64_t)(v >> 64);
+      if (sum_lo) sum_lo[b] = (uint64_t)v;
+      if (hist) hist[b] = std::ldexp((double)v, -52);  // correctly rounded u128 -> f64
+    }
+  });
+}
+
+int stk_finalize(stk_ctx* c, uint64_t n, const uint64_t* sum_hi, const uint64_t* sum_lo,
+                 double* k_out, double* l_out) {
+  return guarded(c, [&] {
+    require_ready(c);
+    if (n == 0) throw InvalidArg("intensity needs n >= 1");
+    const uint32_t cs = (uint32_t)c->s_values.size(), ct = (uint32_t)c->t_values.size();
+    std::vector<double> K((size_t)cs * ct);
+    for (uint32_t si = 0; si < cs; ++si)
+      for (uint32_t ti = 0; ti < ct; ++ti) {
+        const uint32_t b = si * ct + ti;
+        const unsigned __int128 v = ((unsigned __int128)sum_hi[b] << 64) | sum_lo[b];
+        double acc = std::ldexp((double)v, -52);
+        if (si > 0) acc += K[b - ct];
+        if (ti > 0) acc += K[b - 1];
+        if (si > 0 && ti > 0) acc -= K[b - ct - 1];
+        K[b] = acc;
+      }
+    const double scale = c->area * (double)c->duration / ((double)n * (double)n);
+    const double two_pi = 2.0 * 3.14159265358979323846;
+    for (uint32_t b = 0; b < cs * ct; ++b) {
+      K[b] *= scale;
+      if (k_out) k_out[b] = K[b];
+      if (l_out)
+        l_out[b] = std::sqrt(K[b] / (two_pi * (double)c->t_values[b % ct])) - c->s_values[b / ct];
+    }
+  });
+}
+
+int stk_simulate(stk_ctx* c, const double* x, const double* y, const int64_t* t, uint64_t n,
+                 int method, uint64_t base_seed, uint32_t r_begin, uint32_t r_end,
+                 double* l_all, double* upper_l, double* lower_l, stk_telemetry* tel) {
+  return guarded(c, [&] {
+    require_ready(c);
+    check_n(n);
+    const Source src = source_of(method);
+    const double *dx = nullptr, *dy = nullptr;
+    const int64_t* dt = nullptr;
+    if (src != Source::Csr) {
+      if (!x || !y || !t) throw InvalidArg("bootstrap/permutation need the observed points");
+      upload_points(c, x, y, t, n);
+      validate_points(c, c->sx.p, c->sy.p, c->st.p, n);
+      dx = c->sx.p;
+      dy = c->sy.p;
+      dt = c->st.p;
+    }
+    if (r_end < r_begin) throw InvalidArg("r_end < r_begin");
+    JobOut o;
+    o.l_all = l_all;
+    o.upper = upper_l;
+    o.lower = lower_l;
+    run_pipeline(c, dx, dy, dt, n, false, method, base_seed, r_begin, r_end, o, tel);
+  });
+}
+
+static int run_job_impl(stk_ctx* c, const double* dx, const double* dy, const int64_t* dt,
+                        uint64_t n, uint32_t sims, uint64_t seed, int method, double* k_out,
+                        double* l_out, double* upper_l, double* lower_l, double* diff_upper,
+                        stk_telemetry* tel) {
+  validate_points(c, dx, dy, dt, n);
+  JobOut o;
+  o.k_obs = k_out;
+  o.l_obs = l_out;
+  o.upper = upper_l;
+  o.lower = lower_l;
+  o.diff = diff_upper;
+  run_pipeline(c, dx, dy, dt, n, true, method, seed, 0, sims, o, tel);
+  return 0;
+}
+
+int stk_run_job(stk_ctx* c, const double* x, const double* y, const int64_t* t, uint64_t n,
+                uint32_t sims, uint64_t seed, int method, double* k_out, double* l_out,
+                double* upper_l, double* lower_l, double* diff_upper, stk_telemetry* tel) {
+  return guarded(c, [&] {
+    require_ready(c);
+    check_n(n);
+    (void)source_of(method);
+    upload_points(c, x, y, t, n);
+    run_job_impl(c, c->sx.p, c->sy.p, c->st.p, n, sims, seed, method, k_out, l_out, upper_l, lower_l,
+                 diff_upper, tel);
+  });
+}
+
+int stk_run_job_device(stk_ctx* c, const double* d_x, const double* d_y, const int64_t* d_t,
+                       uint64_t n, uint32_t sims, uint64_t seed, int method, double* k_out,
+                       double* l_out, double* upper_l, double* lower_l, double* diff_upper,
+                       stk_telemetry* tel) {
+  return guarded(c, [&] {
+    require_ready(c);
+    check_n(n);
+    (void)source_of(method);
+    run_job_impl(c, d_x, d_y, d_t, n, sims, seed, method, k_out, l_out, upper_l, lower_l,
+                 diff_upper, tel);
+  });
+}
+
+static void run_shard_impl(stk_ctx* c, const double* dx, const double* dy, const int64_t* dt,
+                           uint64_t n, uint32_t obs_shard, uint32_t obs_nshards, uint32_t r_begin,
+                           uint32_t r_end, uint64_t seed, int method, uint64_t* obs_counts,
+                           uint64_t* obs_sum_hi, uint64_t* obs_sum_lo, double* upper_l,
+                           double* lower_l, stk_telemetry* tel) {
+  if (obs_nshards == 0 || obs_shard >= obs_nshards) throw InvalidArg("shard index out of range");
+  if (r_end < r_begin) throw InvalidArg("r_end < r_begin");
+  if (!obs_counts) throw InvalidArg("obs_counts is required");
+  validate_points(c, dx, dy, dt, n);
+  JobOut o;
+  o.upper = upper_l;
+  o.lower = lower_l;
+  o.obs_counts = obs_counts;
+  o.obs_hi = obs_sum_hi;
+  o.obs_lo = obs_sum_lo;
+  run_pipeline(c, dx, dy, dt, n, true, method, seed, r_begin, r_end, o, tel, obs_shard,
+               obs_nshards);
+}
+
+int stk_run_job_shard(stk_ctx* c, const double* x, const double* y, const int64_t* t, uint64_t n,
+                      uint32_t obs_shard, uint32_t obs_nshards, uint32_t r_begin, uint32_t r_end,
+                      uint64_t seed, int method, uint64_t* obs_counts, uint64_t* obs_sum_hi,
+                      uint64_t* obs_sum_lo, double* upper_l, double* lower_l, stk_telemetry* tel) {
+  return guarded(c, [&] {
+    require_ready(c);
+    check_n(n);
+    (void)source_of(method);
+    upload_points(c, x, y, t, n);
+    run_shard_impl(c, c->sx.p, c->sy.p, c->st.p, n, obs_shard, obs_nshards, r_begin, r_end, seed,
+                   method, obs_counts, obs_sum_hi, obs_sum_lo, upper_l, lower_l, tel);
+  });
+}
+
+int stk_run_job_shard_device(stk_ctx* c, const double* d_x, const double* d_y,
+                             const int64_t* d_t, uint64_t n, uint32_t obs_shard,
+                             uint32_t obs_nshards, uint32_t r_begin, uint32_t r_end,
+                             uint64_t seed, int method, uint64_t* obs_counts,
+                             uint64_t* obs_sum_hi, uint64_t* obs_sum_lo, double* upper_l,
+                             double* lower_l, stk_telemetry* tel) {
+  return guarded(c, [&] {
+    require_ready(c);
+    check_n(n);
+    (void)source_of(method);
+    run_shard_impl(c, d_x, d_y, d_t, n, obs_shard, obs_nshards, r_begin, r_end, seed, method,
+                   obs_counts, obs_sum_hi, obs_sum_lo, upper_l, lower_l, tel);
+  });
+}
+
+int stk_generate_cstr(stk_ctx* c, uint64_t n, uint64_t seed, double* x, double* y, int64_t* t) {
+  return guarded(c, [&] {
+    if (!c->have_region) throw StateErr("study region not set (stk_set_region)");
+    if (n == 0) return;
+    Plan P;
+    P.n = n;
+    P.R = 1;
+    P.bins = 1;
+    P.G.cells = 1;
+    P.max_items = 1;
+    Batch B = alloc_batch(c, P);
+    generate(c, B, Source::Csr, 0, 1, seed, nullptr, nullptr, nullptr);
+    CK(cudaMemcpyAsync(x, B.x, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(y, B.y, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(t, B.t, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int stk_spatial_weights(stk_ctx* c, const double* cx, const double* cy, const double* d,
+                        uint64_t count, double* w_out) {
+  return guarded(c, [&] {
+    if (!c->have_region) throw StateErr("study region not set (stk_set_region)");
+    if (count == 0) return;
+    DevBuf<double> b;
+    b.ensure(4 * count);
+    c->ovf.ensure(1);
+    c->bad.ensure(1);
+    const unsigned long long init = ~0ULL;
+    CK(cudaMemcpyAsync(c->bad.p, &init, 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->ovf.p, 0, sizeof(int), c->stream));
+    CK(cudaMemcpyAsync(b.p, cx, 8 * count, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(b.p + count, cy, 8 * count, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(b.p + 2 * count, d, 8 * count, cudaMemcpyHostToDevice, c->stream));
+    weights_kernel<<<(unsigned)((count + 127) / 128), 128, 0, c->stream>>>(
+        b.p, b.p + count, b.p + 2 * count, count, region_view(c), b.p + 3 * count, c->ovf.p,
+        c->bad.p);
+    CK(cudaGetLastError());
+  ++c->launches;
+    CK(cudaMemcpyAsync(w_out, b.p + 3 * count, 8 * count, cudaMemcpyDeviceToHost, c->stream));
+    unsigned long long bad = 0;
+    int ovf = 0;
+    CK(cudaMemcpyAsync(&bad, c->bad.p, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&ovf, c->ovf.p, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    b.release();
+    if (bad != ~0ULL) throw InvalidArg("weight center outside study region");
+    if (ovf) throw Unsupported("more than 64 circle/boundary crossings in one edge weight");
+  });
+}
+
+int stk_measure_fp64_peak(stk_ctx* c, double* instr_per_s) {
+  return guarded(c, [&] {
+    DevBuf<double> o;
+    o.ensure(1);
+    c->evnext = 0;
+    const int blocks = c->num_sms * 8, threads = 256, iters = 2048;
+    cudaEvent_t a = c->ev(), b = c->ev();
+    dfma_peak_kernel<<<blocks, threads, 0, c->stream>>>(o.p, 64, 1.0000001, 1e-9);  // warm-up
+    CK(cudaEventRecord(a, c->stream));
+    dfma_peak_kernel<<<blocks, threads, 0, c->stream>>>(o.p, iters, 1.0000001, 1e-9);
+    CK(cudaEventRecord(b, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    o.release();
+    *instr_per_s = (double)blocks * threads * (double)iters * 16.0 * 8.0 / (ms * 1e-3);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,215 @@
+// stk_device.cuh — device-side geometry, edge weights, MT19937-64 and exact
+// fixed-point helpers for the space-time K pair path (sm_100a).
+//
+// Every FP64 expression here is compiled with -fmad=false, so no mul+add is
+// contracted into an FMA: results follow the reference's Release build
+// (no -march, no FMA) operation by operation.
+#pragma once
+#include <cstdint>
+
+#include "stk_types.h"
+
+namespace stk {
+
+constexpr double kTwoPi = 2.0 * 3.14159265358979323846;  // == 2.0 * std::numbers::pi
+constexpr double kAngleEps = 1e-9;
+constexpr int kMaxAngles = 64;  // circle/boundary crossings handled per weight
+
+// --------------------------------------------------------------- geometry
+// Restates geom::on_segment (proj/core/src/geometry.cpp:57-66).
+__device__ __forceinline__ bool on_segment(double px, double py, double ax, double ay,
+                                           double bx, double by) {
+  const double cross = (bx - ax) * (py - ay) - (by - ay) * (px - ax);
+  double scale = fmax(fabs(ax), fabs(ay));
+  scale = fmax(scale, fmax(fabs(bx), fabs(by)));
+  scale = fmax(scale, fmax(fabs(px), fabs(py)));
+  scale = fmax(scale, 1.0);
+  if (fabs(cross) > 1e-12 * scale * scale) return false;
+  return px >= fmin(ax, bx) - 1e-12 * scale && px <= fmax(ax, bx) + 1e-12 * scale &&
+         py >= fmin(ay, by) - 1e-12 * scale && py <= fmax(ay, by) + 1e-12 * scale;
+}
+
+// Restates geom::point_in_polygon (geometry.cpp:81-97): boundary-inclusive
+// even-odd ray cast over the open ring.
+__device__ __forceinline__ bool point_in_polygon(double px, double py, const double2* ring,
+                                                 uint32_t nv) {
+  if (nv < 3) return false;
+  for (uint32_t i = 0; i < nv; ++i) {
+    const double2 a = ring[i];
+    const double2 b = ring[(i + 1 == nv) ? 0 : i + 1];
+    if (on_segment(px, py, a.x, a.y, b.x, b.y)) return true;
+  }
+  bool inside = false;
+  for (uint32_t i = 0, j = nv - 1; i < nv; j = i++) {
+    const double2 a = ring[i];
+    const double2 b = ring[j];
+    if ((a.y > py) != (b.y > py)) {
+      const double x_cross = a.x + (py - a.y) / (b.y - a.y) * (b.x - a.x);
+      if (px < x_cross) inside = !inside;
+    }
+  }
+  return inside;
+}
+
+// --------------------------------------------------------- edge weights
+// Restates edge::segment_circle_angles (proj/core/src/edge_correction.cpp:18-38).
+__device__ __forceinline__ int segment_circle_angles(double2 a, double2 b, double cx,
+                                                     double cy, double r, double* out,
+                                                     int n) {
+  const double dx = b.x - a.x, dy = b.y - a.y;
+  const double fx = a.x - cx, fy = a.y - cy;
+  const double qa = dx * dx + dy * dy;
+  if (qa == 0.0) return n;
+  const double qb = 2.0 * (fx * dx + fy * dy);
+  const double qc = fx * fx + fy * fy - r * r;
+  const double disc = qb * qb - 4.0 * qa * qc;
+  const double scale = qb * qb + fabs(4.0 * qa * qc);
+  if (disc <= 1e-9 * scale) return n;
+  const double sq = sqrt(disc);
+  const double t0 = (-qb - sq) / (2.0 * qa);
+  const double t1 = (-qb + sq) / (2.0 * qa);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double t = k == 0 ? t0 : t1;
+    if (t < 0.0 || t > 1.0) continue;
+    const double px = a.x + t * dx, py = a.y + t * dy;
+    double ang = atan2(py - cy, px - cx);
+    if (ang < 0.0) ang += kTwoPi;
+    if (n < kMaxAngles) out[n] = ang;
+    ++n;
+  }
+  return n;
+}
+
+// Restates edge::spatial_isotropic_weight (edge_correction.cpp:42-79) for a
+// center already known to lie inside the region (the estimator validates
+// every point up front, estimator.cpp:123-127, so the reference's throw is
+// unreachable on this path).  *overflow is set if more than kMaxAngles
+// crossings occur (reported as STK_EUNSUPPORTED by the host).
+__device__ __noinline__ double spatial_weight(double cx, double cy, double d, const double2* ring,
+                                              uint32_t nv, int* overflow) {
+  if (d <= 0.0) return 1.0;
+  double ang[kMaxAngles];
+  int n = 0;
+  for (uint32_t i = 0, j = nv - 1; i < nv; j = i++)
+    n = segment_circle_angles(ring[j], ring[i], cx, cy, d, ang, n);
+  if (n > kMaxAngles) {
+    *overflow = 1;
+    n = kMaxAngles;
+  }
+  if (n == 0) return 1.0;
+  for (int a = 1; a < n; ++a) {  // std::sort (ascending; same sequence)
+    const double v = ang[a];
+    int b = a - 1;
+    while (b >= 0 && ang[b] > v) {
+      ang[b + 1] = ang[b];
+      --b;
+    }
+    ang[b + 1] = v;
+  }
+  int u = 0;
+  for (int a = 0; a < n; ++a)
+    if (u == 0 || ang[a] - ang[u - 1] > kAngleEps) ang[u++] = ang[a];
+  if (u > 1 && (ang[0] + kTwoPi) - ang[u - 1] <= kAngleEps) --u;
+  if (u < 2) return 1.0;
+  double inside_span = 0.0;
+  for (int a = 0; a < u; ++a) {
+    const double a0 = ang[a];
+    const double a1 = (a + 1 < u) ? ang[a + 1] : ang[0] + kTwoPi;
+    const double mid = 0.5 * (a0 + a1);
+    double sn, cs;
+    sincos(mid, &sn, &cs);
+    const double px = cx + d * cs, py = cy + d * sn;
+    if (point_in_polygon(px, py, ring, nv)) inside_span += a1 - a0;
+  }
+  return inside_span / kTwoPi;
+}
+
+// Squared radius below which spatial_weight() provably returns exactly 1.0
+// for this center (the circle stays strictly inside every edge's reach by a
+// relative margin far above the rounding error of the reference's quadratic;
+// DESIGN.md §4.2).  Returns -1 when no such radius exists.
+__device__ __forceinline__ double safe_q(double cx, double cy, const double2* ring, uint32_t nv,
+                                         double ring_maxabs) {
+  double r2 = 1.0e308;
+  for (uint32_t i = 0, j = nv - 1; i < nv; j = i++) {
+    const double2 a = ring[j], b = ring[i];
+    const double ex = b.x - a.x, ey = b.y - a.y;
+    const double len2 = ex * ex + ey * ey;
+    double t = 0.0;
+    if (len2 > 0.0) {
+      t = ((cx - a.x) * ex + (cy - a.y) * ey) / len2;
+      t = fmin(fmax(t, 0.0), 1.0);
+    }
+    const double px = a.x + t * ex - cx, py = a.y + t * ey - cy;
+    r2 = fmin(r2, px * px + py * py);
+  }
+  const double rs = sqrt(r2);
+  const double scale = fmax(ring_maxabs, fmax(fabs(cx), fabs(cy)));
+  const double r_ok = rs - 1e-6 * (rs + scale);
+  return r_ok > 0.0 ? r_ok * r_ok * (1.0 - 1e-9) : -1.0;
+}
+
+// -------------------------------------------------- exact accumulation
+// Term 1/w (>= 1) minus 1, as 128-bit fixed point with 52 fractional bits.
+// 1/w >= 1 has ulp >= 2^-52, so the conversion is exact.
+__device__ __forceinline__ void fixed52_minus_one(double term, uint64_t* lo, uint64_t* hi) {
+  const uint64_t bits = __double_as_longlong(term);
+  const int e = int((bits >> 52) & 0x7FF) - 1023;            // term = 1.m * 2^e, e >= 0
+  const uint64_t mant = (bits & 0xFFFFFFFFFFFFFULL) | (1ULL << 52);  // value * 2^52 = mant << e
+  uint64_t l, h;
+  if (e < 0 || e >= 75) {  // cannot happen for w in (0,1]; saturate visibly
+    l = ~0ULL;
+    h = ~0ULL >> 1;
+  } else if (e == 0) {
+    l = mant;
+    h = 0;
+  } else if (e < 64) {
+    l = mant << e;
+    h = mant >> (64 - e);
+  } else {
+    l = 0;
+    h = mant << (e - 64);
+  }
+  // subtract 1.0 == 2^52
+  const uint64_t one = 1ULL << 52;
+  h -= (l < one) ? 1ULL : 0ULL;
+  l -= one;
+  *lo = l;
+  *hi = h;
+}
+
+// Correctly rounded double of the 128-bit unsigned value (hi:lo) * 2^-52.
+__device__ __forceinline__ double fixed128_to_double(uint64_t hi, uint64_t lo) {
+  if (hi == 0) return ldexp((double)lo, -52);  // u64 -> f64 conversion rounds to nearest
+  const int lz = __clzll((long long)hi);
+  const int sh = 64 - lz;  // bits of hi above position 64
+  uint64_t top = lz == 0 ? hi : ((hi << lz) | (lo >> sh));
+  const uint64_t rest = lo << lz;  // low bits that do not fit in top
+  if (rest != 0) top |= 1ULL;      // sticky bit (below the 53-bit rounding point)
+  return ldexp((double)top, sh - 52);
+}
+
+// ------------------------------------------------------ MT19937-64
+// std::mt19937_64 tempering ([rand.eng.mers]); rng::Engine wraps it
+// (proj/core/include/stripley/rng.hpp:10-40).
+__device__ __forceinline__ uint64_t mt_temper(uint64_t z) {
+  z ^= (z >> 29) & 0x5555555555555555ULL;
+  z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+  z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+  z ^= z >> 43;
+  return z;
+}
+__device__ __forceinline__ uint64_t mt_mag(uint64_t y) {
+  return (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+}
+constexpr uint64_t kMtUpper = 0xFFFFFFFF80000000ULL;
+constexpr uint64_t kMtLower = 0x7FFFFFFFULL;
+
+// rng::Engine::real01 (rng.hpp:28) and uniform (rng.hpp:31)
+__device__ __forceinline__ double mt_uniform(uint64_t v, double lo, double hi) {
+  const double r01 = (double)(v >> 11) * 0x1.0p-53;
+  return lo + (hi - lo) * r01;
+}
+
+}  // namespace stk

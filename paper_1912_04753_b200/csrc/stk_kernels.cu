@@ -1,0 +1,787 @@
+// stk_kernels.cu — sm_100a kernels of the space-time K pair path.
+//
+//   K4  csr_fast_kernel / csr_seq_kernel / bootstrap_kernel / permutation_kernel
+//       device MT19937-64 point generators, bit-identical to
+//       sim::generate_cstr / generate_bootstrap / generate_permutation
+//       (proj/core/src/simulation.cpp:10-53, proj/core/include/stripley/rng.hpp:10-40)
+//   K1  key_kernel -> scan_kernel -> scatter_kernel -> items_kernel -> tasks_kernel
+//       counting-sort uniform space-time grid (replaces STRTree::build/range_query,
+//       proj/core/src/st_index.cpp:54-130)
+//   K2  pair_kernel: all in-threshold ordered pairs, exact bins, edge weights,
+//       exact integer / 128-bit fixed-point accumulation (estimate_surface's
+//       add_pair loop, proj/core/src/estimator.cpp:136-178)
+//   K5  finalize_kernel / envelope_kernel / diff_kernel (estimator.cpp:94-114,
+//       51-57,71-82,188-202; simulation.cpp:86-102)
+//
+// Compiled with -fmad=false: no FP64 mul+add contraction anywhere.
+#include <cstdint>
+
+#include "stk_device.cuh"
+#include "stk_kernels.h"
+#include "stk_types.h"
+
+namespace stk {
+
+#define FULL_MASK 0xffffffffu
+
+// ============================================================ validation
+// region.contains(p) for every point (estimator.cpp:123-127): first failing
+// index into *bad (atomicMin), UINT64_MAX when all inside.
+__global__ void validate_kernel(const double* x, const double* y, const int64_t* t, uint64_t n,
+                                RegionView reg, unsigned long long* bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const bool ok = point_in_polygon(x[i], y[i], reg.ring, reg.nv) && t[i] >= reg.p0 &&
+                    t[i] <= reg.p1;
+    if (!ok) atomicMin(bad, (unsigned long long)i);
+  }
+}
+
+// ============================================================ K4 generators
+__device__ __forceinline__ void mt_seed_smem(uint64_t* st, uint64_t seed) {
+  if (threadIdx.x == 0) {
+    uint64_t v = seed;
+    st[0] = v;
+    for (int k = 1; k < 312; ++k) {
+      v = 6364136223846793005ULL * (v ^ (v >> 62)) + (uint64_t)k;
+      st[k] = v;
+    }
+  }
+  __syncthreads();
+}
+
+// One MT19937-64 twist of the 312-word state in shared memory by 312 threads,
+// in the three dependency phases of the recurrence
+// x[k+312] = x[k+156] ^ mag((x[k] & U) | (x[k+1] & L)).
+__device__ __forceinline__ void mt_twist_smem(uint64_t* st) {
+  const int i = threadIdx.x;
+  uint64_t y = 0;
+  if (i < 311) y = (st[i] & kMtUpper) | (st[i + 1] & kMtLower);
+  __syncthreads();
+  if (i < 156) st[i] = st[i + 156] ^ mt_mag(y);
+  __syncthreads();
+  if (i >= 156 && i < 311) st[i] = st[i - 156] ^ mt_mag(y);
+  __syncthreads();
+  if (i == 311) {
+    const uint64_t yy = (st[311] & kMtUpper) | (st[0] & kMtLower);
+    st[311] = st[155] ^ mt_mag(yy);
+  }
+  __syncthreads();
+}
+
+// CSR fast path: point k consumes outputs 3k, 3k+1, 3k+2 (uniform x, uniform y,
+// uniform_int t) unless the bbox draw falls outside the polygon or below()
+// rejects; any such event flags the pattern for the exact sequential kernel.
+// 312 = 3 * 104, so each twist block yields exactly 104 points.
+__global__ void __launch_bounds__(320) csr_fast_kernel(Batch B, int p_first, uint64_t seed0,
+                                                        RegionView reg, uint64_t ntl,
+                                                        uint64_t limit) {
+  __shared__ uint64_t st[312];
+  __shared__ uint64_t out[312];
+  __shared__ int s_flag;
+  const int p = p_first + blockIdx.x;
+  const uint64_t seed = seed0 + (uint64_t)blockIdx.x;
+  if (threadIdx.x == 0) s_flag = 0;
+  mt_seed_smem(st, seed);
+  const uint64_t n = B.n;
+  double* X = B.x + (uint64_t)p * n;
+  double* Y = B.y + (uint64_t)p * n;
+  int64_t* T = B.t + (uint64_t)p * n;
+  for (uint64_t base = 0; base < n; base += 104) {
+    mt_twist_smem(st);
+    if (threadIdx.x < 312) out[threadIdx.x] = mt_temper(st[threadIdx.x]);
+    __syncthreads();
+    const uint64_t k = base + threadIdx.x;
+    if (threadIdx.x < 104 && k < n) {
+      const uint64_t vx = out[3 * threadIdx.x], vy = out[3 * threadIdx.x + 1],
+                     vt = out[3 * threadIdx.x + 2];
+      const double cx = mt_uniform(vx, reg.xmin, reg.xmax);
+      const double cy = mt_uniform(vy, reg.ymin, reg.ymax);
+      if (!point_in_polygon(cx, cy, reg.ring, reg.nv) || vt >= limit) s_flag = 1;
+      X[k] = cx;
+      Y[k] = cy;
+      T[k] = reg.p0 + (int64_t)(vt % ntl);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && s_flag) B.flags[p] = 1;
+}
+
+// Sequential exact generator (one thread per pattern): general polygons, or a
+// pattern the fast path flagged.  Follows generate_cstr line by line.
+__global__ void csr_seq_kernel(Batch B, int p_first, int count, uint64_t seed0, RegionView reg,
+                               uint64_t ntl, uint64_t limit, int force) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= count) return;
+  const int p = p_first + j;
+  if (!force && !B.flags[p]) return;
+  uint64_t st[312];
+  uint64_t v = seed0 + (uint64_t)j;
+  st[0] = v;
+  for (int k = 1; k < 312; ++k) {
+    v = 6364136223846793005ULL * (v ^ (v >> 62)) + (uint64_t)k;
+    st[k] = v;
+  }
+  int pos = 312;
+  auto next = [&]() -> uint64_t {
+    if (pos >= 312) {
+      for (int k = 0; k < 312; ++k) {
+        const uint64_t y = (st[k] & kMtUpper) | (st[(k + 1) % 312] & kMtLower);
+        st[k] = st[(k + 156) % 312] ^ mt_mag(y);
+      }
+      pos = 0;
+    }
+    return mt_temper(st[pos++]);
+  };
+  const uint64_t n = B.n;
+  double* X = B.x + (uint64_t)p * n;
+  double* Y = B.y + (uint64_t)p * n;
+  int64_t* T = B.t + (uint64_t)p * n;
+  uint64_t k = 0;
+  while (k < n) {
+    const double cx = mt_uniform(next(), reg.xmin, reg.xmax);
+    const double cy = mt_uniform(next(), reg.ymin, reg.ymax);
+    if (!point_in_polygon(cx, cy, reg.ring, reg.nv)) continue;
+    uint64_t vt;
+    do {
+      vt = next();
+    } while (vt >= limit);
+    X[k] = cx;
+    Y[k] = cy;
+    T[k] = reg.p0 + (int64_t)(vt % ntl);
+    ++k;
+  }
+  B.flags[p] = 0;
+}
+
+// generate_bootstrap (simulation.cpp:26-35): out[i] = obs[below(n)].  Output i
+// consumes MT output i unless below() rejects (probability n/2^64), which
+// flags the pattern for bootstrap_seq_kernel.
+__global__ void __launch_bounds__(320) bootstrap_kernel(Batch B, int p_first, uint64_t seed0,
+                                                         const double* ox, const double* oy,
+                                                         const int64_t* ot, uint64_t limit) {
+  __shared__ uint64_t st[312];
+  __shared__ int s_flag;
+  const int p = p_first + blockIdx.x;
+  if (threadIdx.x == 0) s_flag = 0;
+  mt_seed_smem(st, seed0 + (uint64_t)blockIdx.x);
+  const uint64_t n = B.n;
+  for (uint64_t base = 0; base < n; base += 312) {
+    mt_twist_smem(st);
+    const uint64_t i = base + threadIdx.x;
+    if (threadIdx.x < 312 && i < n) {
+      const uint64_t v = mt_temper(st[threadIdx.x]);
+      if (v >= limit) s_flag = 1;
+      const uint64_t jx = v % n;
+      B.x[(uint64_t)p * n + i] = ox[jx];
+      B.y[(uint64_t)p * n + i] = oy[jx];
+      B.t[(uint64_t)p * n + i] = ot[jx];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && s_flag) B.flags[p] = 1;
+}
+
+// Sequential generators (one thread per pattern): exact bootstrap fallback
+// (mode 1) and generate_permutation's Fisher-Yates over the time column
+// (mode 2; simulation.cpp:37-53), which is inherently sequential.
+__global__ void resample_seq_kernel(Batch B, int p_first, int count, uint64_t seed0,
+                                    const double* ox, const double* oy, const int64_t* ot,
+                                    int mode) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= count) return;
+  const int p = p_first + j;
+  if (mode == 1 && !B.flags[p]) return;
+  uint64_t st[312];
+  uint64_t v = seed0 + (uint64_t)j;
+  st[0] = v;
+  for (int k = 1; k < 312; ++k) {
+    v = 6364136223846793005ULL * (v ^ (v >> 62)) + (uint64_t)k;
+    st[k] = v;
+  }
+  int pos = 312;
+  auto next = [&]() -> uint64_t {
+    if (pos >= 312) {
+      for (int k = 0; k < 312; ++k) {
+        const uint64_t y = (st[k] & kMtUpper) | (st[(k + 1) % 312] & kMtLower);
+        st[k] = st[(k + 156) % 312] ^ mt_mag(y);
+      }
+      pos = 0;
+    }
+    return mt_temper(st[pos++]);
+  };
+  auto below = [&](uint64_t m) -> uint64_t {  // rng.hpp:17-25
+    if (m == 0) return 0;
+    const uint64_t lim = ~0ULL - (~0ULL % m);
+    uint64_t w;
+    do {
+      w = next();
+    } while (w >= lim);
+    return w % m;
+  };
+  const uint64_t n = B.n;
+  double* X = B.x + (uint64_t)p * n;
+  double* Y = B.y + (uint64_t)p * n;
+  int64_t* T = B.t + (uint64_t)p * n;
+  if (mode == 1) {
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint64_t jx = below(n);
+      X[i] = ox[jx];
+      Y[i] = oy[jx];
+      T[i] = ot[jx];
+    }
+    B.flags[p] = 0;
+  } else {
+    for (uint64_t i = 0; i < n; ++i) {
+      X[i] = ox[i];
+      Y[i] = oy[i];
+      T[i] = ot[i];
+    }
+    for (uint64_t i = n - 1; i > 0; --i) {
+      const uint64_t jx = below(i + 1);
+      const int64_t tmp = T[i];
+      T[i] = T[jx];
+      T[jx] = tmp;
+    }
+  }
+}
+
+// ============================================================ K1 grid build
+__device__ __forceinline__ uint32_t cell_key(double x, double y, int64_t t, const GridGeom& G) {
+  int kx = (int)floor((x - G.x0) * G.inv_w);
+  int ky = (int)floor((y - G.y0) * G.inv_w);
+  kx = min(max(kx, 0), G.nx - 1);
+  ky = min(max(ky, 0), G.ny - 1);
+  const int64_t dt = t - G.t0;
+  int64_t kt = (int64_t)((double)dt * G.inv_tw);
+  if (kt * G.tw > dt) --kt;                   // exact integer floor(dt / tw)
+  else if ((kt + 1) * G.tw <= dt) ++kt;
+  if (kt < 0) kt = 0;
+  if (kt > G.nt - 1) kt = G.nt - 1;
+  return (uint32_t)(((int64_t)kt * G.ny + ky) * G.nx + kx);
+}
+
+__global__ void key_kernel(Batch B, GridGeom G, int p_first) {
+  const int p = p_first + blockIdx.y;
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= B.n) return;
+  const uint64_t o = (uint64_t)p * B.n + i;
+  const uint32_t k = cell_key(B.x[o], B.y[o], B.t[o], G);
+  B.key[o] = k;
+  B.rank[o] = atomicAdd(&B.cell_count[(uint64_t)p * G.cells + k], 1u);
+}
+
+// Block-wide exclusive scan of two u32 streams (cell counts and chunk counts)
+// per pattern; one CTA of 1024 threads per pattern.
+__global__ void __launch_bounds__(1024) scan_kernel(Batch B, GridGeom G, int p_first) {
+  const int p = p_first + blockIdx.x;
+  const uint32_t cells = G.cells;
+  const uint32_t* cnt = B.cell_count + (uint64_t)p * cells;
+  uint32_t* start = B.cell_start + (uint64_t)p * (cells + 1);
+  uint32_t* istart = B.item_start + (uint64_t)p * (cells + 1);
+  __shared__ uint32_t ws_a[32], ws_b[32];
+  __shared__ uint32_t carry_a, carry_b;
+  if (threadIdx.x == 0) carry_a = carry_b = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint32_t base = 0; base < cells; base += 1024) {
+    const uint32_t c = base + threadIdx.x;
+    const uint32_t a = c < cells ? cnt[c] : 0u;
+    const uint32_t b = (a + kItemCenters - 1) / kItemCenters;
+    uint32_t ia = a, ib = b;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t ta = __shfl_up_sync(FULL_MASK, ia, o);
+      const uint32_t tb = __shfl_up_sync(FULL_MASK, ib, o);
+      if (lane >= o) {
+        ia += ta;
+        ib += tb;
+      }
+    }
+    if (lane == 31) {
+      ws_a[wid] = ia;
+      ws_b[wid] = ib;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t va = ws_a[lane], vb = ws_b[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t ta = __shfl_up_sync(FULL_MASK, va, o);
+        const uint32_t tb = __shfl_up_sync(FULL_MASK, vb, o);
+        if (lane >= o) {
+          va += ta;
+          vb += tb;
+        }
+      }
+      ws_a[lane] = va;
+      ws_b[lane] = vb;
+    }
+    __syncthreads();
+    const uint32_t off_a = carry_a + (wid ? ws_a[wid - 1] : 0u);
+    const uint32_t off_b = carry_b + (wid ? ws_b[wid - 1] : 0u);
+    if (c < cells) {
+      start[c] = off_a + ia - a;
+      istart[c] = off_b + ib - b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      carry_a += ws_a[31];
+      carry_b += ws_b[31];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    start[cells] = carry_a;
+    istart[cells] = carry_b;
+  }
+}
+
+__global__ void scatter_kernel(Batch B, GridGeom G, int p_first) {
+  const int p = p_first + blockIdx.y;
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= B.n) return;
+  const uint64_t o = (uint64_t)p * B.n + i;
+  const uint32_t pos = B.cell_start[(uint64_t)p * (G.cells + 1) + B.key[o]] + B.rank[o];
+  const uint64_t d = (uint64_t)p * B.n + pos;
+  B.xs[d] = B.x[o];
+  B.ys[d] = B.y[o];
+  B.ts[d] = B.t[o];
+  B.idx[d] = (uint32_t)i;
+}
+
+__global__ void items_kernel(Batch B, GridGeom G, int p_first) {
+  const int p = p_first + blockIdx.y;
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= G.cells) return;
+  const uint64_t cb = (uint64_t)p * (G.cells + 1);
+  const uint32_t s0 = B.cell_start[cb + c], s1 = B.cell_start[cb + c + 1];
+  uint32_t it = B.item_start[cb + c];
+  uint2* items = B.items + (uint64_t)p * B.max_items;
+  for (uint32_t s = s0; s < s1; s += kItemCenters) items[it++] = make_uint2(c, s);
+}
+
+// task_start over the batch (tiny; one thread).
+__global__ void tasks_kernel(Batch B, GridGeom G) {
+  uint32_t acc = 0;
+  for (int p = 0; p < B.R; ++p) {
+    B.task_start[p] = acc;
+    const uint32_t items = B.item_start[(uint64_t)p * (G.cells + 1) + G.cells];
+    acc += (items + kTaskItems - 1) / kTaskItems;
+  }
+  B.task_start[B.R] = acc;
+  *B.task_counter = 0;
+}
+
+// ============================================================ K2 pair kernel
+struct PairSmem {
+  unsigned long long* lo;  // [bins] arc-path fixed-point sums (low 64)
+  uint32_t* cnt;           // [bins]
+  uint32_t* half;          // [bins]
+  uint32_t* hi;            // [bins]
+  double* Q;               // [cs]
+  int64_t* T;              // [ct]
+  uint16_t* stab;          // [kBucketTable]
+  uint16_t* ttab;          // [kBucketTable]
+  double2* tile;           // [warps][32]
+  int64_t* tt;             // [warps][32]
+  double* aq;              // [warps][kArcQueue]
+  uint32_t* abin;          // [warps][kArcQueue]
+  uint8_t* aown;           // [warps][kArcQueue]
+};
+
+__host__ __device__ inline size_t pair_smem_bytes(uint32_t bins, uint32_t cs, uint32_t ct) {
+  size_t b = 0;
+  b += sizeof(unsigned long long) * bins;
+  b += sizeof(double) * cs;
+  b += sizeof(int64_t) * ct;
+  b += sizeof(double2) * kPairWarps * 32;
+  b += sizeof(int64_t) * kPairWarps * 32;
+  b += sizeof(double) * kPairWarps * kArcQueue;
+  b += sizeof(uint32_t) * bins * 3;
+  b += sizeof(uint32_t) * kPairWarps * kArcQueue;
+  b += sizeof(uint8_t) * kPairWarps * kArcQueue;
+  b = (b + 15) & ~size_t(15);
+  b += sizeof(uint16_t) * kBucketTable * 2;
+  return b;
+}
+
+size_t pair_kernel_smem(uint32_t bins, uint32_t cs, uint32_t ct) {
+  return pair_smem_bytes(bins, cs, ct);
+}
+
+__device__ __forceinline__ PairSmem carve(unsigned char* raw, uint32_t bins, uint32_t cs,
+                                          uint32_t ct) {
+  PairSmem S;
+  unsigned char* p = raw;
+  S.lo = (unsigned long long*)p; p += sizeof(unsigned long long) * bins;
+  S.Q = (double*)p; p += sizeof(double) * cs;
+  S.T = (int64_t*)p; p += sizeof(int64_t) * ct;
+  S.tile = (double2*)p; p += sizeof(double2) * kPairWarps * 32;
+  S.tt = (int64_t*)p; p += sizeof(int64_t) * kPairWarps * 32;
+  S.aq = (double*)p; p += sizeof(double) * kPairWarps * kArcQueue;
+  S.cnt = (uint32_t*)p; p += sizeof(uint32_t) * bins;
+  S.half = (uint32_t*)p; p += sizeof(uint32_t) * bins;
+  S.hi = (uint32_t*)p; p += sizeof(uint32_t) * bins;
+  S.abin = (uint32_t*)p; p += sizeof(uint32_t) * kPairWarps * kArcQueue;
+  S.aown = (uint8_t*)p; p += sizeof(uint8_t) * kPairWarps * kArcQueue;
+  p = raw + (((size_t)(p - raw) + 15) & ~size_t(15));
+  S.stab = (uint16_t*)p; p += sizeof(uint16_t) * kBucketTable;
+  S.ttab = (uint16_t*)p;
+  return S;
+}
+
+// Exact weight of `count` queued arc-path pairs (one per lane), accumulated
+// into the CTA histogram as 128-bit fixed point of (1/(omega*v) - 1).
+__device__ __forceinline__ void drain_arcs(int count, int lane, const double* aq,
+                                           const uint32_t* abin, const uint8_t* aown, double cx,
+                                           double cy, const PairSmem& S, const RegionView& reg,
+                                           int* overflow) {
+  double q = 0.0;
+  uint32_t bw = 0;
+  int own = 0;
+  if (lane < count) {
+    q = aq[lane];
+    bw = abin[lane];
+    own = aown[lane];
+  }
+  const double ocx = __shfl_sync(FULL_MASK, cx, own);
+  const double ocy = __shfl_sync(FULL_MASK, cy, own);
+  if (lane < count) {
+    const double d = sqrt(q);
+    const double ws = spatial_weight(ocx, ocy, d, reg.ring, reg.nv, overflow);
+    const double w = ws * ((bw >> 31) ? 0.5 : 1.0);  // edge::pair_weight (edge_correction.cpp:88-103)
+    const double term = 1.0 / w;                      // PairHistogram::add(.., 1.0 / w)
+    uint64_t lo, hi;
+    fixed52_minus_one(term, &lo, &hi);
+    const uint32_t bin = bw & 0x7fffffffu;
+    if (lo | hi) {
+      const unsigned long long old = atomicAdd(&S.lo[bin], (unsigned long long)lo);
+      if (old + lo < old) ++hi;
+      if (hi) atomicAdd(&S.hi[bin], (uint32_t)hi);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kPairWarps * 32) pair_kernel(PairArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t s_task, s_next;
+  const Batch& B = A.B;
+  const GridGeom& G = A.G;
+  const BinView& BV = A.bins;
+  const uint32_t cs = BV.cs, ct = BV.ct, bins = cs * ct;
+  const PairSmem S = carve(smem_raw, bins, cs, ct);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+
+  for (uint32_t b = tid; b < cs; b += blockDim.x) S.Q[b] = BV.Q[b];
+  for (uint32_t b = tid; b < ct; b += blockDim.x) S.T[b] = BV.T[b];
+  for (uint32_t b = tid; b < kBucketTable; b += blockDim.x) {
+    S.stab[b] = BV.s_tab[b];
+    S.ttab[b] = BV.t_tab[b];
+  }
+  const double Qmax = BV.Qmax;
+  const int64_t Tmax = BV.Tmax;
+  const float s_inv_bw = BV.s_inv_bw, t_inv_bw = BV.t_inv_bw;
+  const uint32_t total_tasks = B.task_start[B.R];
+  const unsigned lanemask_lt = (1u << lane) - 1u;
+  double2* tile = S.tile + w * 32;
+  int64_t* tt = S.tt + w * 32;
+  double* aq = S.aq + w * kArcQueue;
+  uint32_t* abin = S.abin + w * kArcQueue;
+  uint8_t* aown = S.aown + w * kArcQueue;
+  int overflow = 0;
+  unsigned long long tot_in = 0, tot_cand = 0, tot_exact = 0;
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) {
+      s_task = atomicAdd(B.task_counter, 1u);
+      s_next = 0;
+    }
+    for (uint32_t b = tid; b < bins; b += blockDim.x) {
+      S.lo[b] = 0ULL;
+      S.cnt[b] = 0u;
+      S.half[b] = 0u;
+      S.hi[b] = 0u;
+    }
+    __syncthreads();
+    const uint32_t task = s_task;
+    if (task >= total_tasks) break;
+    // pattern of this task
+    int lo_p = 0, hi_p = B.R - 1;
+    while (lo_p < hi_p) {
+      const int mid = (lo_p + hi_p + 1) >> 1;
+      if (B.task_start[mid] <= task) lo_p = mid; else hi_p = mid - 1;
+    }
+    const int p = lo_p;
+    if (A.shard_scope == 2 || (A.shard_scope == 1 && p == 0)) {
+      if ((task - B.task_start[p]) % A.nshards != A.shard) continue;  // CTA-uniform
+    }
+    const uint64_t pb = (uint64_t)p * B.n;
+    const uint32_t* cstart = B.cell_start + (uint64_t)p * (G.cells + 1);
+    const uint32_t items_p = B.item_start[(uint64_t)p * (G.cells + 1) + G.cells];
+    const uint32_t i0 = (task - B.task_start[p]) * kTaskItems;
+    const uint32_t i1 = min(i0 + kTaskItems, items_p);
+    const uint2* items = B.items + (uint64_t)p * B.max_items;
+    const double* xs = B.xs + pb;
+    const double* ys = B.ys + pb;
+    const int64_t* ts = B.ts + pb;
+    const bool restrict_c = A.restrict_centers && p == 0;
+
+    for (;;) {
+      uint32_t it = 0;
+      if (lane == 0) it = atomicAdd(&s_next, 1u);
+      it = __shfl_sync(FULL_MASK, it, 0);
+      if (i0 + it >= i1) break;
+      const uint2 item = items[i0 + it];
+      const uint32_t cell = item.x, start = item.y;
+      const uint32_t cend = cstart[cell + 1];
+      const uint32_t nc = min((uint32_t)kItemCenters, cend - start);
+      const uint32_t mypos = start + lane;
+      bool valid = lane < (int)nc;
+      double cx = 0.0, cy = 0.0, sq = -1.0;
+      int64_t ctm = 0, vthr = 0;
+      if (valid) {
+        cx = xs[mypos];
+        cy = ys[mypos];
+        ctm = ts[mypos];
+        if (restrict_c) {
+          const uint32_t oi = B.idx[pb + mypos];
+          valid = oi >= A.c0 && oi < A.c1;
+        }
+        sq = safe_q(cx, cy, A.reg.ring, A.reg.nv, A.reg.maxabs);
+        vthr = min(ctm - A.reg.p0, A.reg.p1 - ctm);  // edge_correction.cpp:81-86
+      }
+      const unsigned nvalid = __popc(__ballot_sync(FULL_MASK, valid));
+      const int kx = (int)(cell % (uint32_t)G.nx);
+      const uint32_t rest = cell / (uint32_t)G.nx;
+      const int ky = (int)(rest % (uint32_t)G.ny);
+      const int kt = (int)(rest / (uint32_t)G.ny);
+      const int xa = max(kx - 1, 0), xb = min(kx + 1, G.nx - 1);
+      int qn = 0;
+      uint32_t n_in = 0, n_exact = 0;
+      unsigned long long n_cand = 0;
+      for (int dt = -1; dt <= 1; ++dt) {
+        const int tk = kt + dt;
+        if (tk < 0 || tk >= G.nt) continue;
+        for (int dy = -1; dy <= 1; ++dy) {
+          const int yk = ky + dy;
+          if (yk < 0 || yk >= G.ny) continue;
+          const uint32_t row = ((uint32_t)tk * G.ny + yk) * G.nx;
+          const uint32_t rb = cstart[row + xa], re = cstart[row + xb + 1];
+          for (uint32_t j0 = rb; j0 < re; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            if (j < re) {
+              tile[lane] = make_double2(xs[j], ys[j]);
+              tt[lane] = ts[j];
+            }
+            __syncwarp();
+            const int m = (int)min(32u, re - j0);
+            n_cand += (unsigned long long)m;
+            for (int k = 0; k < m; ++k) {
+              const double2 nb = tile[k];
+              const int64_t nt = tt[k];
+              const double dx = cx - nb.x, dy2 = cy - nb.y;
+              const double q = dx * dx + dy2 * dy2;  // spatial_distance^2, no FMA
+              int64_t du = ctm - nt;
+              du = du < 0 ? -du : du;                // temporal_distance
+              const bool in = valid && q <= Qmax && du <= Tmax && (j0 + k) != mypos;
+              bool arc = false;
+              uint32_t ab = 0;
+              if (in) {
+                // bin_pair: first s_k >= d <=> first Q_k >= q; first t_l >= u
+                int bq = (int)(sqrtf((float)q) * s_inv_bw);
+                bq = min(bq, kBucketTable - 1);
+                uint32_t sb = S.stab[bq];
+                while (q > S.Q[sb]) ++sb;
+                int bt = (int)((float)du * t_inv_bw);
+                bt = min(bt, kBucketTable - 1);
+                uint32_t tb = S.ttab[bt];
+                while (du > S.T[tb]) ++tb;
+                const uint32_t bin = sb * ct + tb;
+                atomicAdd(&S.cnt[bin], 1u);
+                const bool half = du > vthr;
+                arc = q >= sq;
+                if (arc) ab = bin | (half ? 0x80000000u : 0u);
+                else if (half) atomicAdd(&S.half[bin], 1u);
+                ++n_in;
+              }
+              const unsigned am = __ballot_sync(FULL_MASK, arc);
+              if (am) {
+                if (arc) {
+                  const int pos = qn + __popc(am & lanemask_lt);
+                  aq[pos] = q;
+                  abin[pos] = ab;
+                  aown[pos] = (uint8_t)lane;
+                  ++n_exact;
+                }
+                qn += __popc(am);
+                if (qn >= 32) {
+                  __syncwarp();
+                  drain_arcs(32, lane, aq, abin, aown, cx, cy, S, A.reg, &overflow);
+                  __syncwarp();
+                  if (lane < qn - 32) {
+                    aq[lane] = aq[32 + lane];
+                    abin[lane] = abin[32 + lane];
+                    aown[lane] = aown[32 + lane];
+                  }
+                  __syncwarp();
+                  qn -= 32;
+                }
+              }
+            }
+            __syncwarp();
+          }
+        }
+      }
+      if (qn > 0) {
+        __syncwarp();
+        drain_arcs(qn, lane, aq, abin, aown, cx, cy, S, A.reg, &overflow);
+        __syncwarp();
+      }
+      tot_in += n_in;
+      tot_exact += n_exact;
+      if (lane == 0) tot_cand += n_cand * nvalid;
+    }
+    __syncthreads();
+    // flush the CTA histogram of pattern p (exact integer adds)
+    const uint64_t hb = (uint64_t)p * bins;
+    for (uint32_t b = tid; b < bins; b += blockDim.x) {
+      const uint32_t c = S.cnt[b];
+      if (c) atomicAdd(&B.h_cnt[hb + b], (unsigned long long)c);
+      const uint32_t h = S.half[b];
+      if (h) atomicAdd(&B.h_half[hb + b], (unsigned long long)h);
+      const unsigned long long lo = S.lo[b];
+      unsigned long long hi = S.hi[b];
+      if (lo) {
+        const unsigned long long old = atomicAdd(&B.h_lo[hb + b], lo);
+        if (old + lo < old) ++hi;
+      }
+      if (hi) atomicAdd(&B.h_hi[hb + b], hi);
+    }
+  }
+  // block-level stats
+  for (int o = 16; o > 0; o >>= 1) {
+    tot_in += __shfl_down_sync(FULL_MASK, tot_in, o);
+    tot_exact += __shfl_down_sync(FULL_MASK, tot_exact, o);
+  }
+  if (lane == 0) {
+    atomicAdd(&B.stats[0], tot_in);
+    atomicAdd(&B.stats[1], tot_cand);
+    atomicAdd(&B.stats[2], tot_exact);
+  }
+  if (overflow) atomicOr(&B.stats[3], 1ULL);
+}
+
+// ============================================================ K5 finalize
+// est::finalize_surface (estimator.cpp:94-114) + est::to_l (:51-57,71-82) per
+// pattern, in the reference's operation order.  One CTA per pattern: the exact
+// 128-bit sums are rounded once in parallel, the 2-D prefix runs as one
+// sequential chain (its order is part of the reference's rounding), then
+// scale and L in parallel.
+__global__ void __launch_bounds__(256) finalize_kernel(Batch B, uint32_t cs, uint32_t ct,
+                                                        const double* s_values,
+                                                        const int64_t* t_values, double area,
+                                                        int64_t duration, int p_first) {
+  const int p = p_first + blockIdx.x;
+  const uint32_t bins = cs * ct;
+  const uint64_t hb = (uint64_t)p * bins;
+  double* K = B.K + hb;
+  double* L = B.L + hb;
+  for (uint32_t b = threadIdx.x; b < bins; b += blockDim.x) {
+    const unsigned long long c = B.h_cnt[hb + b] + B.h_half[hb + b];
+    const unsigned long long lo0 = B.h_lo[hb + b];
+    const unsigned long long lo = lo0 + (c << 52);
+    const unsigned long long hi = B.h_hi[hb + b] + (c >> 12) + (lo < lo0 ? 1ULL : 0ULL);
+    K[b] = fixed128_to_double(hi, lo);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t si = 0; si < cs; ++si) {
+      double left = 0.0;
+      for (uint32_t ti = 0; ti < ct; ++ti) {
+        const uint32_t b = si * ct + ti;
+        double acc = K[b];
+        if (si > 0) acc += K[b - ct];
+        if (ti > 0) acc += left;
+        if (si > 0 && ti > 0) acc -= K[b - ct - 1];
+        K[b] = acc;
+        left = acc;
+      }
+    }
+  }
+  __syncthreads();
+  const double scale = area * (double)duration / ((double)B.n * (double)B.n);
+  for (uint32_t b = threadIdx.x; b < bins; b += blockDim.x) {
+    const double k = K[b] * scale;
+    K[b] = k;
+    const uint32_t si = b / ct, ti = b % ct;
+    L[b] = sqrt(k / (kTwoPi * (double)t_values[ti])) - s_values[si];
+  }
+}
+
+// sim::envelopes (simulation.cpp:86-102): running pointwise max/min over the
+// L surfaces of patterns [p_first, p_first + count), folded into upper/lower
+// (initialised from the first pattern when init != 0).
+__global__ void envelope_kernel(Batch B, uint32_t bins, int p_first, int count, int init,
+                                double* upper, double* lower) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= bins || count <= 0) return;
+  int r0 = 0;
+  double up, lo;
+  if (init) {
+    up = lo = B.L[(uint64_t)p_first * bins + b];
+    r0 = 1;
+  } else {
+    up = upper[b];
+    lo = lower[b];
+  }
+  for (int r = r0; r < count; ++r) {
+    const double v = B.L[(uint64_t)(p_first + r) * bins + b];
+    up = (up < v) ? v : up;  // std::max
+    lo = (v < lo) ? v : lo;  // std::min
+  }
+  upper[b] = up;
+  lower[b] = lo;
+}
+
+// est::diff_surface (estimator.cpp:188-202)
+__global__ void diff_kernel(const double* est_l, const double* upper, uint32_t bins,
+                            double* diff) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= bins) return;
+  const double e = est_l[b], u = upper[b];
+  diff[b] = e > u ? e - u : 0.0;
+}
+
+// ============================================================ utilities
+__global__ void weights_kernel(const double* cx, const double* cy, const double* d,
+                               uint64_t count, RegionView reg, double* w, int* overflow,
+                               unsigned long long* bad) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  if (d[i] > 0.0 && !point_in_polygon(cx[i], cy[i], reg.ring, reg.nv)) {
+    atomicMin(bad, (unsigned long long)i);
+    w[i] = 0.0;
+    return;
+  }
+  w[i] = spatial_weight(cx[i], cy[i], d[i], reg.ring, reg.nv, overflow);
+}
+
+// FP64 issue peak: 8 independent DFMA chains per thread.
+__global__ void __launch_bounds__(256) dfma_peak_kernel(double* out, int iters, double a,
+                                                         double b) {
+  double v0 = threadIdx.x, v1 = v0 + 1, v2 = v0 + 2, v3 = v0 + 3, v4 = v0 + 4, v5 = v0 + 5,
+         v6 = v0 + 6, v7 = v0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      v0 = fma(v0, a, b); v1 = fma(v1, a, b); v2 = fma(v2, a, b); v3 = fma(v3, a, b);
+      v4 = fma(v4, a, b); v5 = fma(v5, a, b); v6 = fma(v6, a, b); v7 = fma(v7, a, b);
+    }
+  }
+  const double s = v0 + v1 + v2 + v3 + v4 + v5 + v6 + v7;
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+}  // namespace stk

@@ -1,0 +1,52 @@
+// stk_kernels.h — kernel entry points and launch arguments (internal).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "stk_types.h"
+
+namespace stk {
+
+struct PairArgs {
+  Batch B;
+  GridGeom G;
+  BinView bins;
+  RegionView reg;
+  uint32_t shard, nshards;  // a pattern's local task t is processed iff t % nshards == shard
+  int shard_scope;          // 0: no sharding, 1: pattern 0 of the batch only, 2: all patterns
+  int restrict_centers;     // pattern 0 only: centers with input index in [c0, c1)
+  uint64_t c0, c1;
+};
+
+__global__ void validate_kernel(const double* x, const double* y, const int64_t* t, uint64_t n,
+                                RegionView reg, unsigned long long* bad);
+__global__ void csr_fast_kernel(Batch B, int p_first, uint64_t seed0, RegionView reg,
+                                uint64_t ntl, uint64_t limit);
+__global__ void csr_seq_kernel(Batch B, int p_first, int count, uint64_t seed0, RegionView reg,
+                               uint64_t ntl, uint64_t limit, int force);
+__global__ void bootstrap_kernel(Batch B, int p_first, uint64_t seed0, const double* ox,
+                                 const double* oy, const int64_t* ot, uint64_t limit);
+__global__ void resample_seq_kernel(Batch B, int p_first, int count, uint64_t seed0,
+                                    const double* ox, const double* oy, const int64_t* ot,
+                                    int mode);
+__global__ void key_kernel(Batch B, GridGeom G, int p_first);
+__global__ void scan_kernel(Batch B, GridGeom G, int p_first);
+__global__ void scatter_kernel(Batch B, GridGeom G, int p_first);
+__global__ void items_kernel(Batch B, GridGeom G, int p_first);
+__global__ void tasks_kernel(Batch B, GridGeom G);
+__global__ void pair_kernel(PairArgs A);
+__global__ void finalize_kernel(Batch B, uint32_t cs, uint32_t ct, const double* s_values,
+                                const int64_t* t_values, double area, int64_t duration,
+                                int p_first);
+__global__ void envelope_kernel(Batch B, uint32_t bins, int p_first, int count, int init,
+                                double* upper, double* lower);
+__global__ void diff_kernel(const double* est_l, const double* upper, uint32_t bins,
+                            double* diff);
+__global__ void weights_kernel(const double* cx, const double* cy, const double* d,
+                               uint64_t count, RegionView reg, double* w, int* overflow,
+                               unsigned long long* bad);
+__global__ void dfma_peak_kernel(double* out, int iters, double a, double b);
+
+size_t pair_kernel_smem(uint32_t bins, uint32_t cs, uint32_t ct);
+
+}  // namespace stk

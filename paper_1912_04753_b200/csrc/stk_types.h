@@ -1,0 +1,80 @@
+// stk_types.h — plain structs shared by the host runtime and the kernels.
+#pragma once
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace stk {
+
+constexpr int kItemCenters = 32;    // centers per warp work item (one per lane)
+constexpr int kTaskItems = 32;      // warp items per CTA task (one smem histogram flush)
+constexpr int kPairWarps = 8;       // warps per pair-kernel CTA
+constexpr int kBucketTable = 1024;  // bucket table size for bin guesses
+constexpr int kArcQueue = 64;       // per-warp arc queue capacity
+
+// Study region on the device (geom::StudyRegion, geometry.hpp:95-120).
+struct RegionView {
+  const double2* ring;  // open ring, nv vertices
+  uint32_t nv;
+  int64_t p0, p1;       // study period (inclusive)
+  double xmin, xmax, ymin, ymax;
+  double maxabs;        // max |coordinate| over the ring
+};
+
+// Distance grid in the forms the kernels consume.
+struct BinView {
+  const double* Q;         // Q[k] = largest q with RN(sqrt(q)) <= s_values[k]
+  const int64_t* T;        // t_values
+  const uint16_t* s_tab;   // bucket (on d) -> lower bound of the s bin
+  const uint16_t* t_tab;   // bucket (on u) -> lower bound of the t bin
+  uint32_t cs, ct;
+  double Qmax;
+  int64_t Tmax;
+  float s_inv_bw, t_inv_bw;  // buckets per unit distance / per time unit (with margin)
+};
+
+// Uniform space-time cell grid (replaces the STR R-tree, st_index.cpp:54-130).
+struct GridGeom {
+  double x0, y0;   // origin of cell (0,0)
+  double inv_w;    // 1 / spatial cell width (width >= s_max)
+  int64_t t0;      // period start
+  int64_t tw;      // temporal cell width (>= t_max)
+  double inv_tw;
+  int32_t nx, ny, nt;
+  uint32_t cells;  // nx*ny*nt
+};
+
+// One batch of R point patterns of n points each, laid out [R][n].
+struct Batch {
+  int R;
+  uint64_t n;
+  // unsorted input points
+  double* x;
+  double* y;
+  int64_t* t;
+  // grid-sorted structure-of-arrays
+  double* xs;
+  double* ys;
+  int64_t* ts;
+  uint32_t* idx;  // input index of each sorted point
+  uint32_t* key;  // cell key per unsorted point
+  uint32_t* rank; // rank within the cell per unsorted point
+  uint32_t* cell_count;  // [R][cells]
+  uint32_t* cell_start;  // [R][cells+1]
+  uint32_t* item_start;  // [R][cells+1] exclusive scan of ceil(count/32)
+  uint2* items;          // [R][max_items]: (cell, first sorted position)
+  uint32_t max_items;
+  uint32_t* task_start;  // [R+1] exclusive scan of ceil(items_r / kTaskItems)
+  uint32_t* task_counter;
+  // exact histograms [R][bins]
+  unsigned long long* h_cnt;   // in-threshold pairs
+  unsigned long long* h_half;  // interior pairs with v = 1/2 (contribute 2)
+  unsigned long long* h_lo;    // arc-path sum of (1/w - 1), 128-bit fixed 52
+  unsigned long long* h_hi;
+  double* K;  // [R][bins]
+  double* L;  // [R][bins]
+  unsigned long long* stats;   // [0] in_threshold [1] candidates [2] exact_path [3] overflow
+  int* flags;                  // [R] generator fallback flags
+};
+
+}  // namespace stk

@@ -1,0 +1,107 @@
+"""Device contexts: one ``stk_ctx`` (one CUDA device, one stream) per device.
+
+A context caches the region and grid it was last configured with, so repeated
+calls on the same study setup upload nothing but points.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+import numpy as np
+
+from .. import _lib
+
+
+class Device:
+    def __init__(self, device: int = 0):
+        lib = _lib.load()
+        h = C.c_void_p()
+        rc = lib.stk_create(C.byref(h), int(device))
+        if rc != 0 or not h.value:
+            raise RuntimeError(
+                f"stk_create(device={device}) failed: no usable CUDA device "
+                "(the B200 path has no CPU fallback)")
+        self.lib = lib
+        self.h = h
+        self.index = int(device)
+        self._region_key = None
+        self._grid_key = None
+
+    # -- errors -----------------------------------------------------------
+    def check(self, rc: int):
+        if rc == _lib.STK_OK:
+            return
+        msg = self.lib.stk_last_error(self.h).decode()
+        if rc == _lib.STK_EINVAL:
+            raise ValueError(msg)
+        if rc == _lib.STK_EUNSUPPORTED:
+            raise NotImplementedError(msg)
+        raise _lib.StkError(f"stk error {rc}: {msg}")
+
+    # -- configuration ----------------------------------------------------
+    def configure(self, region, grid=None, options=None):
+        rk = region.key()
+        if rk != self._region_key:
+            ring = np.ascontiguousarray(region.boundary().reshape(-1))
+            self.check(self.lib.stk_set_region(self.h, _lib.ptr(ring), len(ring) // 2,
+                                               region.period_start(), region.period_end()))
+            self._region_key = rk
+        if grid is not None:
+            gk = grid.key()
+            if gk != self._grid_key:
+                s = _lib.f64(grid.s_values)
+                t = _lib.i64(grid.t_values)
+                self.check(self.lib.stk_set_grid(self.h, _lib.ptr(s), len(s),
+                                                 _lib.ptr(t, C.c_int64), len(t)))
+                self._grid_key = gk
+        if options is not None:
+            self.check(self.lib.stk_set_options(self.h, int(options.use_index),
+                                                int(options.use_cache),
+                                                float(options.coord_tolerance),
+                                                float(options.dist_tolerance)))
+
+    def stream_handle(self) -> int:
+        return int(self.lib.stk_stream(self.h) or 0)
+
+    def set_memory_budget(self, nbytes: int):
+        self.check(self.lib.stk_set_memory_budget(self.h, int(nbytes)))
+
+    def fp64_peak(self) -> float:
+        v = C.c_double()
+        self.check(self.lib.stk_measure_fp64_peak(self.h, C.byref(v)))
+        return v.value
+
+    def close(self):
+        if self.h is not None and self.h.value:
+            self.lib.stk_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_devices: dict[int, Device] = {}
+_lock = threading.Lock()
+
+
+def get(device: int | None = None) -> Device:
+    """The shared context of ``device`` (default: current torch device or 0)."""
+    if device is None:
+        device = 0
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                device = torch.cuda.current_device()
+        except Exception:
+            pass
+    with _lock:
+        d = _devices.get(device)
+        if d is None:
+            d = Device(device)
+            _devices[device] = d
+        return d

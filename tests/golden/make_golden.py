@@ -1,0 +1,115 @@
+"""Regenerate the golden fixtures in tests/golden/ from the reference itself.
+
+Run HERE (the container that has /root/reference):  python tests/golden/make_golden.py
+The fixtures are what the GPU-box tests compare against (the reference tree
+does not exist there).  Every array is produced by the reference compiled from
+its own sources (oracle/_ref) or read from its bundled golden output
+(proj/data/sample_result.json); nothing is hand-written.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402
+from oracle import ref  # noqa: E402
+from paper_1912_04753_b200 import configs  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+DATA = "/root/reference/proj/data"
+
+
+def sample():
+    d = json.load(open(os.path.join(DATA, "sample_result.json")))
+    rows = [l.strip().split(",") for l in open(os.path.join(DATA, "sample_points.csv")).read().strip().split("\n")[1:]]
+    x = np.array([float(r[1]) for r in rows])
+    y = np.array([float(r[2]) for r in rows])
+    t = np.array([int(r[3]) for r in rows], dtype=np.int64)
+    ring = np.array([[0, 0], [10000, 0], [10000, 10000], [0, 10000]], float)  # sample_boundary.wkt
+    s, tv = ref.regular_grid(100, 2000, 5, 100)
+    r = ref.run_job(x, y, t, ring, 0, 365, s, tv, sims=19, seed=42, partitions=1, workers=1,
+                    use_index=True, use_cache=True)
+    golden = dict(k=np.array(d["k_hat"]), l=np.array(d["l_hat"]),
+                  upper=np.array(d["envelope"]["upper_l"]), lower=np.array(d["envelope"]["lower_l"]),
+                  diff=np.array(d["diff_upper"]))
+    for k, v in golden.items():  # the reference reproduces its own golden file bit-exactly
+        assert np.array_equal(r[k], v), k
+    assert r["in_threshold"] == d["telemetry"]["comparisons"]["in_threshold_pairs"]
+    counts = ref.pair_counts(x, y, t, s, tv)
+    np.savez_compressed(os.path.join(OUT, "sample_result.npz"), x=x, y=y, t=t, ring=ring,
+                        p0=0, p1=365, s=s, tv=tv, sims=19, seed=42,
+                        in_threshold_total=r["in_threshold"], counts_observed=counts, **golden)
+
+
+def polygons(count=24):
+    """Criterion-1 style datasets (tests/acceptance/acceptance_main.cpp:45-78)."""
+    sets = {}
+    s, tv = ref.regular_grid(120.0, 360.0, 12, 36)
+    for rep in range(count):
+        if rep % 2 == 0:
+            ring = ref.random_convex_ring(1000 + rep, 900.0, 700.0, 10)
+        else:
+            ring = ref.random_star_ring(1000 + rep, 800.0, 14)
+        n = int(10 + (rep * 37) % 290)
+        if rep % 3 == 0:
+            x, y, t = ref.clustered_points(2000 + rep, ring, 0, 60, n, 4, 90.0, 5.0)
+        else:
+            x, y, t = ref.uniform_points(2000 + rep, ring, 0, 60, n)
+        k_idx, pairs, _ = ref.estimate_surface(x, y, t, ring, 0, 60, s, tv, use_index=True)
+        k_bf = ref.brute_force_k(x, y, t, ring, 0, 60, s, tv)
+        counts = ref.pair_counts(x, y, t, s, tv)
+        for key, v in dict(ring=ring, x=x, y=y, t=t, k=k_idx, k_bf=k_bf, counts=counts,
+                           pairs=pairs).items():
+            sets[f"{rep}_{key}"] = v
+    np.savez_compressed(os.path.join(OUT, "polygons.npz"), s=s, tv=tv, count=count, **sets)
+
+
+def weights():
+    """(center, d) -> omega from edge::spatial_isotropic_weight on squares and stars."""
+    rng = np.random.default_rng(5)
+    out = {}
+    rings = [np.array([[0, 0], [10000, 0], [10000, 10000], [0, 10000]], float),
+             ref.random_star_ring(77, 1000.0, 12), ref.random_convex_ring(78, 900, 700, 10),
+             ref.random_star_ring(79, 800.0, 64)]
+    for k, ring in enumerate(rings):
+        xmin, ymin = ring.min(0)
+        xmax, ymax = ring.max(0)
+        cx, cy, dd, ww = [], [], [], []
+        while len(cx) < 400:
+            px, py = rng.uniform(xmin, xmax), rng.uniform(ymin, ymax)
+            if not ref.point_in_polygon(px, py, ring):
+                continue
+            d = rng.uniform(0.0, 0.9 * max(xmax - xmin, ymax - ymin))
+            cx.append(px); cy.append(py); dd.append(d)
+            ww.append(ref.spatial_weight(px, py, d, ring))
+        out[f"{k}_ring"] = ring
+        out[f"{k}_cx"] = np.array(cx); out[f"{k}_cy"] = np.array(cy)
+        out[f"{k}_d"] = np.array(dd); out[f"{k}_w"] = np.array(ww)
+    np.savez_compressed(os.path.join(OUT, "weights.npz"), count=len(rings), **out)
+
+
+def c1():
+    """C1 (configs[0]) through the reference: K, per-bin counts, in_threshold."""
+    cfg = configs.CONFIGS["C1"]
+    s, tv = configs.grid_values(cfg)
+    ring = cfg.ring()
+    x, y, t = ref.generate_cstr(cfg.n, ring, 0, cfg.period_s, cfg.seed)
+    k, pairs, _ = ref.estimate_surface(x, y, t, ring, 0, cfg.period_s, s, tv, use_index=True)
+    counts = ref.pair_counts(x, y, t, s, tv)
+    np.savez_compressed(os.path.join(OUT, "c1.npz"), k=k, counts=counts, pairs=pairs, s=s, tv=tv,
+                        x_head=x[:16], t_head=t[:16])
+
+
+def mt():
+    seeds = [1, 42, 5489, 2**63 + 12345]
+    np.savez_compressed(os.path.join(OUT, "mt19937_64.npz"), seeds=np.array(seeds, np.uint64),
+                        **{f"s{i}": ref.mt_outputs(sd, 1000) for i, sd in enumerate(seeds)})
+
+
+if __name__ == "__main__":
+    oracle.build(with_ref=True)
+    sample(); polygons(); weights(); c1(); mt()
+    print("golden fixtures written to", OUT)

@@ -1,0 +1,184 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle and the golden
+fixtures produced by the reference itself.
+
+Bars: bit-exact for counts, generated points and bins; <= 1e-9 relative for
+weighted K/L (north_star), and in practice ~1e-15.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden, rel_err, surfaces_close
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9  # north_star: weighted K/L within 1e-9 relative (FP64 accumulation)
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_1912_04753_b200.stripley import device, est, geom, rt, sim
+
+    device.get(0)  # fail loudly if the CUDA path is unavailable
+    return dict(est=est, geom=geom, rt=rt, sim=sim, dev=device.get(0))
+
+
+@pytest.fixture(scope="module")
+def port():
+    from oracle import port
+
+    return port
+
+
+def test_device_mt_csr_matches_reference_stream(api, port):
+    sim, geom = api["sim"], api["geom"]
+    ring = np.array([[0.0, 0.0], [1000.0, 0.0], [1000.0, 1000.0], [0.0, 1000.0]])
+    region = geom.StudyRegion(ring, 0, 31_536_000)
+    for seed, n in [(1, 10_000), (42, 1), (7, 103), (7, 105), (2**63 + 5, 2_000)]:
+        pts = sim.generate_cstr(n, region, seed)
+        x, y, t = port.generate_cstr(n, ring, 0, 31_536_000, seed)
+        assert np.array_equal(pts.x, x) and np.array_equal(pts.y, y) and np.array_equal(pts.t, t)
+    g = golden("c1.npz")
+    pts = sim.generate_cstr(10_000, region, 1)
+    assert np.array_equal(pts.x[:16], g["x_head"]) and np.array_equal(pts.t[:16], g["t_head"])
+
+
+def test_device_csr_general_polygon_sequential_path(api, port):
+    sim, geom = api["sim"], api["geom"]
+    g = golden("polygons.npz")
+    ring = g["1_ring"]
+    region = geom.StudyRegion(ring, 0, 60)
+    pts = sim.generate_cstr(777, region, 99)
+    x, y, t = port.generate_cstr(777, ring, 0, 60, 99)
+    assert np.array_equal(pts.x, x) and np.array_equal(pts.y, y) and np.array_equal(pts.t, t)
+
+
+def test_spatial_weights_vs_reference(api):
+    import ctypes as C
+
+    from paper_1912_04753_b200 import _lib
+
+    g = golden("weights.npz")
+    dev = api["dev"]
+    geom = api["geom"]
+    for k in range(int(g["count"])):
+        ring = g[f"{k}_ring"]
+        dev.configure(geom.StudyRegion(ring, 0, 1))
+        cx, cy, d, w_ref = g[f"{k}_cx"], g[f"{k}_cy"], g[f"{k}_d"], g[f"{k}_w"]
+        w = np.zeros_like(w_ref)
+        dev.check(dev.lib.stk_spatial_weights(dev.h, _lib.ptr(cx), _lib.ptr(cy), _lib.ptr(d),
+                                              len(cx), _lib.ptr(w)))
+        assert rel_err(w, w_ref) <= 1e-12, k
+
+
+def test_edge_correction_known_answers(api):
+    """proj/tests/test_edge_correction.cpp:10-29 through the device."""
+    from paper_1912_04753_b200 import _lib
+
+    dev, geom = api["dev"], api["geom"]
+    dev.configure(geom.StudyRegion([[0, 0], [10000, 0], [10000, 10000], [0, 10000]], 0, 100))
+    cx = np.array([5000, 5000, 1500, 5000, 0, 0, 10000.0])
+    cy = np.array([5000, 5000, 1500, 0, 5000, 0, 10000.0])
+    d = np.array([1000, 0.0, 1499, 100, 250, 100, 400])
+    want = np.array([1.0, 1.0, 1.0, 0.5, 0.5, 0.25, 0.25])
+    w = np.zeros(7)
+    dev.check(dev.lib.stk_spatial_weights(dev.h, _lib.ptr(cx), _lib.ptr(cy), _lib.ptr(d), 7,
+                                          _lib.ptr(w)))
+    assert w[0] == 1.0 and w[1] == 1.0
+    assert np.allclose(w, want, rtol=1e-12)
+    with pytest.raises(ValueError, match="weight center outside study region"):
+        x = np.array([20000.0]); y = np.array([5.0]); dd = np.array([10.0]); o = np.zeros(1)
+        dev.check(dev.lib.stk_spatial_weights(dev.h, _lib.ptr(x), _lib.ptr(y), _lib.ptr(dd), 1,
+                                              _lib.ptr(o)))
+
+
+def test_golden_sample_run_job(api):
+    """proj/data/sample_result.json (1,000 pts, 20x20, 19 CSR sims, seed 42)."""
+    est, geom, rt = api["est"], api["geom"], api["rt"]
+    g = golden("sample_result.npz")
+    region = geom.StudyRegion(g["ring"], int(g["p0"]), int(g["p1"]))
+    grid = est.DistanceGrid(g["s"], g["tv"])
+    spec = rt.JobSpec(grid=grid, sims=int(g["sims"]), seed=int(g["seed"]))
+    res = rt.run_job((g["x"], g["y"], g["t"]), region, spec)
+    for key, surf in [("k", res.k_hat), ("l", res.l_hat), ("upper", res.upper_l),
+                      ("lower", res.lower_l), ("diff", res.diff_upper)]:
+        assert surfaces_close(surf.values, g[key], TOL), key
+    assert res.telemetry.in_threshold_pairs == int(g["in_threshold_total"])
+    h = est.pair_histogram((g["x"], g["y"], g["t"]), region, grid)
+    assert np.array_equal(h["counts"], g["counts_observed"])
+
+
+def test_polygons_vs_reference(api, port):
+    """Criterion-1 style random convex/star polygons (acceptance_main.cpp:45-78)."""
+    est, geom = api["est"], api["geom"]
+    g = golden("polygons.npz")
+    grid = est.DistanceGrid(g["s"], g["tv"])
+    for rep in range(int(g["count"])):
+        ring = g[f"{rep}_ring"]
+        region = geom.StudyRegion(ring, 0, 60)
+        pts = (g[f"{rep}_x"], g[f"{rep}_y"], g[f"{rep}_t"])
+        tel = est.EstimatorTelemetry()
+        k = est.estimate_surface(pts, region, grid, telemetry=tel)
+        assert surfaces_close(k.values, g[f"{rep}_k"], TOL), rep
+        assert surfaces_close(k.values, g[f"{rep}_k_bf"], TOL), rep
+        assert tel.in_threshold_pairs == int(g[f"{rep}_pairs"]), rep
+        h = est.pair_histogram(pts, region, grid)
+        assert np.array_equal(h["counts"], g[f"{rep}_counts"]), rep
+        o = port.pair_histogram(*pts, ring, 0, 60, g["s"], g["tv"])
+        assert np.array_equal(h["sum_hi"], o["sum_hi"]) or rel_err(h["hist"], o["hist"]) <= 1e-13
+
+
+def test_c1_full_size(api, port):
+    """configs[0]: N=10,000 CSR, 10x10 grid — counts bit-exact, K <= 1e-9."""
+    from paper_1912_04753_b200 import configs
+
+    est, geom, sim = api["est"], api["geom"], api["sim"]
+    cfg = configs.CONFIGS["C1"]
+    s, tv = configs.grid_values(cfg)
+    region = geom.StudyRegion(cfg.ring(), 0, cfg.period_s)
+    grid = est.DistanceGrid(s, tv)
+    pts = sim.generate_cstr(cfg.n, region, cfg.seed)
+    g = golden("c1.npz")
+    h = est.pair_histogram(pts, region, grid)
+    assert np.array_equal(h["counts"], g["counts"])
+    assert h["in_threshold"] == int(g["pairs"])
+    k = est.estimate_surface(pts, region, grid)
+    assert surfaces_close(k.values, g["k"], TOL)
+    o = port.pair_histogram(pts.x, pts.y, pts.t, cfg.ring(), 0, cfg.period_s, s, tv)
+    assert rel_err(h["hist"], o["hist"]) <= 1e-13
+
+
+def test_shards_sum_exactly(api):
+    est, geom, rt = api["est"], api["geom"], api["rt"]
+    g = golden("sample_result.npz")
+    region = geom.StudyRegion(g["ring"], 0, 365)
+    grid = est.DistanceGrid(g["s"], g["tv"])
+    pts = (g["x"], g["y"], g["t"])
+    full = est.pair_histogram(pts, region, grid)
+    for W in (2, 3, 8):
+        parts = [est.pair_histogram(pts, region, grid, s, W) for s in range(W)]
+        c = sum(p["counts"].astype(object) for p in parts)
+        v = sum(p["sum_hi"].astype(object) * (1 << 64) + p["sum_lo"].astype(object) for p in parts)
+        assert np.array_equal(c.astype(np.uint64), full["counts"])
+        fv = full["sum_hi"].astype(object) * (1 << 64) + full["sum_lo"].astype(object)
+        assert (v == fv).all()
+
+
+def test_errors_mirror_reference(api):
+    est, geom = api["est"], api["geom"]
+    region = geom.StudyRegion([[0, 0], [100, 0], [100, 100], [0, 100]], 0, 100)
+    grid = est.DistanceGrid([10.0], [10])
+    with pytest.raises(ValueError, match="K estimation needs n >= 2"):
+        est.estimate_surface(([1.0], [1.0], [1]), region, grid)
+    with pytest.raises(ValueError, match="point outside study region or period"):
+        est.estimate_surface(([1.0, 500.0], [1.0, 1.0], [1, 1]), region, grid)
+    with pytest.raises(ValueError, match="point outside study region or period"):
+        est.estimate_surface(([1.0, 2.0], [1.0, 2.0], [1, 999]), region, grid)
+
+
+def test_two_point_hand_value(api):
+    """proj/tests/test_estimator.cpp:62-76: K = 5e9."""
+    est, geom = api["est"], api["geom"]
+    region = geom.StudyRegion([[0, 0], [10000, 0], [10000, 10000], [0, 10000]], 0, 100)
+    k = est.estimate_surface(([4000.0, 5000.0], [5000.0, 5000.0], [50, 55]), region,
+                             est.DistanceGrid([2000.0], [10]))
+    assert k.values[0, 0] == pytest.approx(5.0e9, rel=1e-15)
