@@ -127,6 +127,7 @@ struct stk_ctx {
   DevBuf<int64_t> t, ts;
   DevBuf<uint32_t> idx, key, rank, cell_count, cell_start, item_start, task_start, task_counter;
   DevBuf<uint2> items;
+  DevBuf<uint32_t> sel_start, center_pos;
   DevBuf<unsigned long long> hist, stats, bad;
   DevBuf<double> K, L, env, obs;
   DevBuf<int> flags, ovf;
@@ -254,7 +255,7 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   c->item_start.ensure(R * (P.G.cells + 1));
   c->items.ensure(R * P.max_items);
   c->task_start.ensure(R + 1);
-  c->task_counter.ensure(1);
+  c->task_counter.ensure(2);
   c->hist.ensure(R * P.bins * 4);
   c->stats.ensure(4);
   c->K.ensure(R * P.bins);
@@ -287,6 +288,13 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   B.L = c->L.p;
   B.stats = c->stats.p;
   B.flags = c->flags.p;
+  B.n_sel = 0;
+  B.shard = 0;
+  B.nshards = 1;
+  B.c0 = 0;
+  B.c1 = ~0ULL;
+  B.sel_start = nullptr;
+  B.center_pos = nullptr;
   return B;
 }
 
@@ -363,9 +371,11 @@ void generate(stk_ctx* c, const Batch& B, Source src, int p_first, int count, ui
 }
 
 // Grid build + pair kernel + finalize for patterns [0, R) of the batch.
-void run_batch(stk_ctx* c, const Plan& P, const Batch& B, Timers& tm, uint32_t shard,
-               uint32_t nshards, int shard_scope, bool restrict_centers, uint64_t c0,
-               uint64_t c1, bool finalize) {
+// Grid build + pair kernel (+ finalize) for the batch.  Center selection
+// (shard of nshards by input index, and input-index range [c0, c1)) applies to
+// patterns [0, n_sel).
+void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint32_t shard,
+               uint32_t nshards, uint64_t c0, uint64_t c1, bool finalize) {
   const GridGeom& G = P.G;
   const int R = B.R;
   cudaEvent_t e0 = c->ev(), e1 = c->ev(), e2 = c->ev();
@@ -376,17 +386,45 @@ void run_batch(stk_ctx* c, const Plan& P, const Batch& B, Timers& tm, uint32_t s
   key_kernel<<<gp, 256, 0, c->stream>>>(B, G, 0);
   CK(cudaGetLastError());
   ++c->launches;
-  scan_kernel<<<R, 1024, 0, c->stream>>>(B, G, 0);
+  scan_kernel<<<R, 1024, 0, c->stream>>>(B.cell_count, B.cell_start, B.item_start, G.cells);
   CK(cudaGetLastError());
   ++c->launches;
   scatter_kernel<<<gp, 256, 0, c->stream>>>(B, G, 0);
   CK(cudaGetLastError());
   ++c->launches;
+  B.n_sel = std::min(n_sel, R);
+  B.shard = shard;
+  B.nshards = std::max<uint32_t>(nshards, 1);
+  B.c0 = c0;
+  B.c1 = c1;
+  if (B.n_sel > 0) {
+    c->sel_start.ensure((uint64_t)B.n_sel * (G.cells + 1));
+    c->center_pos.ensure((uint64_t)B.n_sel * B.n);
+    B.sel_start = c->sel_start.p;
+    B.center_pos = c->center_pos.p;
+    CK(cudaMemsetAsync(B.cell_count, 0, sizeof(uint32_t) * (uint64_t)B.n_sel * G.cells, c->stream));
+    dim3 gs((unsigned)((B.n + 255) / 256), (unsigned)B.n_sel);
+    select_count_kernel<<<gs, 256, 0, c->stream>>>(B, G);
+    CK(cudaGetLastError());
+    ++c->launches;
+    scan_kernel<<<B.n_sel, 1024, 0, c->stream>>>(B.cell_count, B.sel_start, B.item_start, G.cells);
+    CK(cudaGetLastError());
+    ++c->launches;
+    select_scatter_kernel<<<gs, 256, 0, c->stream>>>(B, G);
+    CK(cudaGetLastError());
+    ++c->launches;
+  }
   dim3 gc((G.cells + 255) / 256, (unsigned)R);
   items_kernel<<<gc, 256, 0, c->stream>>>(B, G, 0);
   CK(cudaGetLastError());
   ++c->launches;
-  tasks_kernel<<<1, 1, 0, c->stream>>>(B, G);
+  const size_t smem = pair_kernel_smem(P.bins, (uint32_t)c->s_values.size(),
+                                       (uint32_t)c->t_values.size());
+  CK(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_kernel, kPairWarps * 32, smem));
+  if (per_sm < 1) throw Unsupported("distance grid too large for the pair kernel's shared histogram");
+  tasks_kernel<<<1, 1, 0, c->stream>>>(B, G, (uint32_t)(c->num_sms * per_sm));
   CK(cudaGetLastError());
   ++c->launches;
   CK(cudaEventRecord(e1, c->stream));
@@ -396,17 +434,6 @@ void run_batch(stk_ctx* c, const Plan& P, const Batch& B, Timers& tm, uint32_t s
   A.G = G;
   A.bins = bin_view(c);
   A.reg = region_view(c);
-  A.shard = shard;
-  A.nshards = std::max<uint32_t>(nshards, 1);
-  A.shard_scope = A.nshards > 1 ? shard_scope : 0;
-  A.restrict_centers = restrict_centers ? 1 : 0;
-  A.c0 = c0;
-  A.c1 = c1;
-  const size_t smem = pair_kernel_smem(P.bins, A.bins.cs, A.bins.ct);
-  CK(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_kernel, kPairWarps * 32, smem));
-  if (per_sm < 1) throw Unsupported("distance grid too large for the pair kernel's shared histogram");
   pair_kernel<<<c->num_sms * per_sm, kPairWarps * 32, smem, c->stream>>>(A);
   CK(cudaGetLastError());
   ++c->launches;
@@ -515,7 +542,8 @@ void run_pipeline(stk_ctx* c, const double* dx, const double* dy, const int64_t*
     generate(c, B, src, p, nsim, base_seed + next_r, dx, dy, dt);
     CK(cudaEventRecord(g1, c->stream));
     tm.gen.push_back({g0, g1});
-    run_batch(c, PB, B, tm, obs_shard, obs_here ? obs_nshards : 1, 1, false, 0, 0, true);
+    run_batch(c, PB, B, tm, (obs_here && obs_nshards > 1) ? 1 : 0, obs_shard, obs_nshards, 0,
+              ~0ULL, true);
     cudaEvent_t f0 = c->ev(), f1 = c->ev();
     CK(cudaEventRecord(f0, c->stream));
     if (obs_here && out.obs_counts) {
@@ -662,6 +690,7 @@ void stk_destroy(stk_ctx* c) {
   c->task_start.release(); c->task_counter.release(); c->items.release();
   c->hist.release(); c->stats.release(); c->bad.release(); c->K.release(); c->L.release();
   c->env.release(); c->obs.release(); c->flags.release(); c->ovf.release();
+  c->sel_start.release(); c->center_pos.release();
   c->scratch.release(); c->sx.release(); c->sy.release(); c->st.release();
   cudaStreamDestroy(c->stream);
   delete c;
@@ -884,7 +913,7 @@ int stk_pair_histogram(stk_ctx* c, const double* x, const double* y, const int64
     Batch B = alloc_batch(c, P);
     CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * 4, c->stream));
     generate(c, B, Source::Observed, 0, 1, 0, c->sx.p, c->sy.p, c->st.p);
-    run_batch(c, P, B, tm, shard, nshards, 2, false, 0, 0, false);
+    run_batch(c, P, B, tm, nshards > 1 ? 1 : 0, shard, nshards, 0, ~0ULL, false);
     const uint32_t bins = P.bins;
     std::vector<unsigned long long> h(4 * (size_t)bins);
     CK(cudaMemcpyAsync(h.data(), B.h_cnt, sizeof(unsigned long long) * 4 * bins,

@@ -30,13 +30,24 @@ __device__ __forceinline__ bool on_segment(double px, double py, double ax, doub
 }
 
 // Restates geom::point_in_polygon (geometry.cpp:81-97): boundary-inclusive
-// even-odd ray cast over the open ring.
+// even-odd ray cast over the open ring.  on_segment is entered only when the
+// cross product passes the bound with the largest possible scale
+// (smax = max(1, |ring|, |p|) >= scale): |cross| > 1e-12*smax*smax implies
+// |cross| > 1e-12*scale*scale (RN is monotone), i.e. on_segment == false, so
+// the skipped calls are exactly the ones that return false.
 __device__ __forceinline__ bool point_in_polygon(double px, double py, const double2* ring,
-                                                 uint32_t nv) {
+                                                 uint32_t nv, double ring_maxabs = -1.0) {
   if (nv < 3) return false;
+  const double smax =
+      ring_maxabs < 0.0 ? -1.0 : fmax(fmax(ring_maxabs, 1.0), fmax(fabs(px), fabs(py)));
+  const double bound = 1e-12 * smax * smax;
   for (uint32_t i = 0; i < nv; ++i) {
     const double2 a = ring[i];
     const double2 b = ring[(i + 1 == nv) ? 0 : i + 1];
+    if (smax > 0.0) {
+      const double cross = (b.x - a.x) * (py - a.y) - (b.y - a.y) * (px - a.x);
+      if (fabs(cross) > bound) continue;
+    }
     if (on_segment(px, py, a.x, a.y, b.x, b.y)) return true;
   }
   bool inside = false;
@@ -87,7 +98,7 @@ __device__ __forceinline__ int segment_circle_angles(double2 a, double2 b, doubl
 // unreachable on this path).  *overflow is set if more than kMaxAngles
 // crossings occur (reported as STK_EUNSUPPORTED by the host).
 __device__ __noinline__ double spatial_weight(double cx, double cy, double d, const double2* ring,
-                                              uint32_t nv, int* overflow) {
+                                              uint32_t nv, double ring_maxabs, int* overflow) {
   if (d <= 0.0) return 1.0;
   double ang[kMaxAngles];
   int n = 0;
@@ -120,7 +131,7 @@ __device__ __noinline__ double spatial_weight(double cx, double cy, double d, co
     double sn, cs;
     sincos(mid, &sn, &cs);
     const double px = cx + d * cs, py = cy + d * sn;
-    if (point_in_polygon(px, py, ring, nv)) inside_span += a1 - a0;
+    if (point_in_polygon(px, py, ring, nv, ring_maxabs)) inside_span += a1 - a0;
   }
   return inside_span / kTwoPi;
 }

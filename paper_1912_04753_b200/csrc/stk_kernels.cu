@@ -271,14 +271,14 @@ __global__ void key_kernel(Batch B, GridGeom G, int p_first) {
   B.rank[o] = atomicAdd(&B.cell_count[(uint64_t)p * G.cells + k], 1u);
 }
 
-// Block-wide exclusive scan of two u32 streams (cell counts and chunk counts)
-// per pattern; one CTA of 1024 threads per pattern.
-__global__ void __launch_bounds__(1024) scan_kernel(Batch B, GridGeom G, int p_first) {
-  const int p = p_first + blockIdx.x;
-  const uint32_t cells = G.cells;
-  const uint32_t* cnt = B.cell_count + (uint64_t)p * cells;
-  uint32_t* start = B.cell_start + (uint64_t)p * (cells + 1);
-  uint32_t* istart = B.item_start + (uint64_t)p * (cells + 1);
+// Block-wide exclusive scan of two u32 streams (per-cell counts and their
+// 32-center chunk counts); one CTA of 1024 threads per pattern (blockIdx.x).
+__global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* counts, uint32_t* start_all,
+                                                     uint32_t* istart_all, uint32_t cells) {
+  const int p = blockIdx.x;
+  const uint32_t* cnt = counts + (uint64_t)p * cells;
+  uint32_t* start = start_all + (uint64_t)p * (cells + 1);
+  uint32_t* istart = istart_all + (uint64_t)p * (cells + 1);
   __shared__ uint32_t ws_a[32], ws_b[32];
   __shared__ uint32_t carry_a, carry_b;
   if (threadIdx.x == 0) carry_a = carry_b = 0;
@@ -350,27 +350,67 @@ __global__ void scatter_kernel(Batch B, GridGeom G, int p_first) {
   B.idx[d] = (uint32_t)i;
 }
 
+// Center selection (patterns [0, n_sel)): count selected centers per cell.
+// Runs after scatter, so rank[] (per sorted position now) is free to reuse.
+__device__ __forceinline__ bool selected(const Batch& B, uint32_t i) {
+  return i >= B.c0 && i < B.c1 && (i % B.nshards) == B.shard;
+}
+
+__global__ void select_count_kernel(Batch B, GridGeom G) {
+  const int p = blockIdx.y;
+  const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (j >= B.n) return;
+  const uint64_t pb = (uint64_t)p * B.n;
+  const uint32_t i = B.idx[pb + j];
+  uint32_t r = 0xFFFFFFFFu;
+  if (selected(B, i)) r = atomicAdd(&B.cell_count[(uint64_t)p * G.cells + B.key[pb + i]], 1u);
+  B.rank[pb + j] = r;
+}
+
+__global__ void select_scatter_kernel(Batch B, GridGeom G) {
+  const int p = blockIdx.y;
+  const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (j >= B.n) return;
+  const uint64_t pb = (uint64_t)p * B.n;
+  const uint32_t r = B.rank[pb + j];
+  if (r == 0xFFFFFFFFu) return;
+  const uint32_t cell = B.key[pb + B.idx[pb + j]];
+  B.center_pos[pb + B.sel_start[(uint64_t)p * (G.cells + 1) + cell] + r] = (uint32_t)j;
+}
+
+// Work items: (cell, first entry of the cell's center list) per 32 centers.
+// The center list is the cell's sorted range, or its selected centers.
 __global__ void items_kernel(Batch B, GridGeom G, int p_first) {
   const int p = p_first + blockIdx.y;
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= G.cells) return;
   const uint64_t cb = (uint64_t)p * (G.cells + 1);
-  const uint32_t s0 = B.cell_start[cb + c], s1 = B.cell_start[cb + c + 1];
+  const uint32_t* lst = p < B.n_sel ? B.sel_start : B.cell_start;
+  const uint32_t s0 = lst[cb + c], s1 = lst[cb + c + 1];
   uint32_t it = B.item_start[cb + c];
   uint2* items = B.items + (uint64_t)p * B.max_items;
   for (uint32_t s = s0; s < s1; s += kItemCenters) items[it++] = make_uint2(c, s);
 }
 
-// task_start over the batch (tiny; one thread).
-__global__ void tasks_kernel(Batch B, GridGeom G) {
+// task_start over the batch (tiny; one thread).  Task size adapts so the
+// batch holds ~8 tasks per resident CTA: enough to balance the tail, few
+// enough that the per-task histogram flush and barrier stay cheap.
+__global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas) {
+  uint64_t total = 0;
+  for (int p = 0; p < B.R; ++p) total += B.item_start[(uint64_t)p * (G.cells + 1) + G.cells];
+  uint64_t ti = total / (8ull * resident_ctas);
+  ti = ti < (uint64_t)kTaskMinItems ? (uint64_t)kTaskMinItems : ti;
+  ti = ti > (uint64_t)kTaskMaxItems ? (uint64_t)kTaskMaxItems : ti;
+  const uint32_t task_items = (uint32_t)ti;
   uint32_t acc = 0;
   for (int p = 0; p < B.R; ++p) {
     B.task_start[p] = acc;
     const uint32_t items = B.item_start[(uint64_t)p * (G.cells + 1) + G.cells];
-    acc += (items + kTaskItems - 1) / kTaskItems;
+    acc += (items + task_items - 1) / task_items;
   }
   B.task_start[B.R] = acc;
-  *B.task_counter = 0;
+  B.task_counter[0] = 0;
+  B.task_counter[1] = task_items;
 }
 
 // ============================================================ K2 pair kernel
@@ -390,44 +430,54 @@ struct PairSmem {
   uint8_t* aown;           // [warps][kArcQueue]
 };
 
-__host__ __device__ inline size_t pair_smem_bytes(uint32_t bins, uint32_t cs, uint32_t ct) {
+// Shared-memory layout of the pair kernel; 16-byte aligned sections first.
+__host__ __device__ inline size_t pair_smem_layout(uint32_t bins, uint32_t cs, uint32_t ct,
+                                                   size_t* off) {
   size_t b = 0;
-  b += sizeof(unsigned long long) * bins;
-  b += sizeof(double) * cs;
-  b += sizeof(int64_t) * ct;
-  b += sizeof(double2) * kPairWarps * 32;
-  b += sizeof(int64_t) * kPairWarps * 32;
-  b += sizeof(double) * kPairWarps * kArcQueue;
-  b += sizeof(uint32_t) * bins * 3;
-  b += sizeof(uint32_t) * kPairWarps * kArcQueue;
-  b += sizeof(uint8_t) * kPairWarps * kArcQueue;
-  b = (b + 15) & ~size_t(15);
-  b += sizeof(uint16_t) * kBucketTable * 2;
-  return b;
+  auto take = [&](int k, size_t bytes) {
+    b = (b + 15) & ~size_t(15);
+    off[k] = b;
+    b += bytes;
+  };
+  take(0, sizeof(double2) * kPairWarps * 32);              // tile
+  take(1, sizeof(int64_t) * kPairWarps * 32);              // tt
+  take(2, sizeof(double) * kPairWarps * kArcQueue);        // aq
+  take(3, sizeof(unsigned long long) * bins);              // lo
+  take(4, sizeof(double) * cs);                            // Q
+  take(5, sizeof(int64_t) * ct);                           // T
+  take(6, sizeof(uint32_t) * bins);                        // cnt
+  take(7, sizeof(uint32_t) * bins);                        // half
+  take(8, sizeof(uint32_t) * bins);                        // hi
+  take(9, sizeof(uint32_t) * kPairWarps * kArcQueue);      // abin
+  take(10, sizeof(uint8_t) * kPairWarps * kArcQueue);      // aown
+  take(11, sizeof(uint16_t) * kBucketTable);               // stab
+  take(12, sizeof(uint16_t) * kBucketTable);               // ttab
+  return (b + 15) & ~size_t(15);
 }
 
 size_t pair_kernel_smem(uint32_t bins, uint32_t cs, uint32_t ct) {
-  return pair_smem_bytes(bins, cs, ct);
+  size_t off[13];
+  return pair_smem_layout(bins, cs, ct, off);
 }
 
 __device__ __forceinline__ PairSmem carve(unsigned char* raw, uint32_t bins, uint32_t cs,
                                           uint32_t ct) {
+  size_t off[13];
+  pair_smem_layout(bins, cs, ct, off);
   PairSmem S;
-  unsigned char* p = raw;
-  S.lo = (unsigned long long*)p; p += sizeof(unsigned long long) * bins;
-  S.Q = (double*)p; p += sizeof(double) * cs;
-  S.T = (int64_t*)p; p += sizeof(int64_t) * ct;
-  S.tile = (double2*)p; p += sizeof(double2) * kPairWarps * 32;
-  S.tt = (int64_t*)p; p += sizeof(int64_t) * kPairWarps * 32;
-  S.aq = (double*)p; p += sizeof(double) * kPairWarps * kArcQueue;
-  S.cnt = (uint32_t*)p; p += sizeof(uint32_t) * bins;
-  S.half = (uint32_t*)p; p += sizeof(uint32_t) * bins;
-  S.hi = (uint32_t*)p; p += sizeof(uint32_t) * bins;
-  S.abin = (uint32_t*)p; p += sizeof(uint32_t) * kPairWarps * kArcQueue;
-  S.aown = (uint8_t*)p; p += sizeof(uint8_t) * kPairWarps * kArcQueue;
-  p = raw + (((size_t)(p - raw) + 15) & ~size_t(15));
-  S.stab = (uint16_t*)p; p += sizeof(uint16_t) * kBucketTable;
-  S.ttab = (uint16_t*)p;
+  S.tile = (double2*)(raw + off[0]);
+  S.tt = (int64_t*)(raw + off[1]);
+  S.aq = (double*)(raw + off[2]);
+  S.lo = (unsigned long long*)(raw + off[3]);
+  S.Q = (double*)(raw + off[4]);
+  S.T = (int64_t*)(raw + off[5]);
+  S.cnt = (uint32_t*)(raw + off[6]);
+  S.half = (uint32_t*)(raw + off[7]);
+  S.hi = (uint32_t*)(raw + off[8]);
+  S.abin = (uint32_t*)(raw + off[9]);
+  S.aown = (uint8_t*)(raw + off[10]);
+  S.stab = (uint16_t*)(raw + off[11]);
+  S.ttab = (uint16_t*)(raw + off[12]);
   return S;
 }
 
@@ -449,7 +499,7 @@ __device__ __forceinline__ void drain_arcs(int count, int lane, const double* aq
   const double ocy = __shfl_sync(FULL_MASK, cy, own);
   if (lane < count) {
     const double d = sqrt(q);
-    const double ws = spatial_weight(ocx, ocy, d, reg.ring, reg.nv, overflow);
+    const double ws = spatial_weight(ocx, ocy, d, reg.ring, reg.nv, reg.maxabs, overflow);
     const double w = ws * ((bw >> 31) ? 0.5 : 1.0);  // edge::pair_weight (edge_correction.cpp:88-103)
     const double term = 1.0 / w;                      // PairHistogram::add(.., 1.0 / w)
     uint64_t lo, hi;
@@ -463,7 +513,7 @@ __device__ __forceinline__ void drain_arcs(int count, int lane, const double* aq
   }
 }
 
-__global__ void __launch_bounds__(kPairWarps * 32) pair_kernel(PairArgs A) {
+__global__ void __launch_bounds__(kPairWarps * 32, 4) pair_kernel(PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_task, s_next;
   const Batch& B = A.B;
@@ -483,6 +533,7 @@ __global__ void __launch_bounds__(kPairWarps * 32) pair_kernel(PairArgs A) {
   const int64_t Tmax = BV.Tmax;
   const float s_inv_bw = BV.s_inv_bw, t_inv_bw = BV.t_inv_bw;
   const uint32_t total_tasks = B.task_start[B.R];
+  const uint32_t task_items = B.task_counter[1];
   const unsigned lanemask_lt = (1u << lane) - 1u;
   double2* tile = S.tile + w * 32;
   int64_t* tt = S.tt + w * 32;
@@ -514,19 +565,18 @@ __global__ void __launch_bounds__(kPairWarps * 32) pair_kernel(PairArgs A) {
       if (B.task_start[mid] <= task) lo_p = mid; else hi_p = mid - 1;
     }
     const int p = lo_p;
-    if (A.shard_scope == 2 || (A.shard_scope == 1 && p == 0)) {
-      if ((task - B.task_start[p]) % A.nshards != A.shard) continue;  // CTA-uniform
-    }
     const uint64_t pb = (uint64_t)p * B.n;
     const uint32_t* cstart = B.cell_start + (uint64_t)p * (G.cells + 1);
     const uint32_t items_p = B.item_start[(uint64_t)p * (G.cells + 1) + G.cells];
-    const uint32_t i0 = (task - B.task_start[p]) * kTaskItems;
-    const uint32_t i1 = min(i0 + kTaskItems, items_p);
+    const uint32_t i0 = (task - B.task_start[p]) * task_items;
+    const uint32_t i1 = min(i0 + task_items, items_p);
     const uint2* items = B.items + (uint64_t)p * B.max_items;
     const double* xs = B.xs + pb;
     const double* ys = B.ys + pb;
     const int64_t* ts = B.ts + pb;
-    const bool restrict_c = A.restrict_centers && p == 0;
+    const bool sel_p = p < B.n_sel;
+    const uint32_t* clist = sel_p ? B.sel_start + (uint64_t)p * (G.cells + 1) : cstart;
+    const uint32_t* cpos = B.center_pos + pb;
 
     for (;;) {
       uint32_t it = 0;
@@ -535,20 +585,17 @@ __global__ void __launch_bounds__(kPairWarps * 32) pair_kernel(PairArgs A) {
       if (i0 + it >= i1) break;
       const uint2 item = items[i0 + it];
       const uint32_t cell = item.x, start = item.y;
-      const uint32_t cend = cstart[cell + 1];
+      const uint32_t cend = clist[cell + 1];
       const uint32_t nc = min((uint32_t)kItemCenters, cend - start);
-      const uint32_t mypos = start + lane;
-      bool valid = lane < (int)nc;
+      const bool valid = lane < (int)nc;
+      uint32_t mypos = 0xFFFFFFFFu;
       double cx = 0.0, cy = 0.0, sq = -1.0;
       int64_t ctm = 0, vthr = 0;
       if (valid) {
+        mypos = sel_p ? cpos[start + lane] : start + lane;
         cx = xs[mypos];
         cy = ys[mypos];
         ctm = ts[mypos];
-        if (restrict_c) {
-          const uint32_t oi = B.idx[pb + mypos];
-          valid = oi >= A.c0 && oi < A.c1;
-        }
         sq = safe_q(cx, cy, A.reg.ring, A.reg.nv, A.reg.maxabs);
         vthr = min(ctm - A.reg.p0, A.reg.p1 - ctm);  // edge_correction.cpp:81-86
       }
@@ -765,7 +812,7 @@ __global__ void weights_kernel(const double* cx, const double* cy, const double*
     w[i] = 0.0;
     return;
   }
-  w[i] = spatial_weight(cx[i], cy[i], d[i], reg.ring, reg.nv, overflow);
+  w[i] = spatial_weight(cx[i], cy[i], d[i], reg.ring, reg.nv, reg.maxabs, overflow);
 }
 
 // FP64 issue peak: 8 independent DFMA chains per thread.

@@ -12,10 +12,6 @@ struct PairArgs {
   GridGeom G;
   BinView bins;
   RegionView reg;
-  uint32_t shard, nshards;  // a pattern's local task t is processed iff t % nshards == shard
-  int shard_scope;          // 0: no sharding, 1: pattern 0 of the batch only, 2: all patterns
-  int restrict_centers;     // pattern 0 only: centers with input index in [c0, c1)
-  uint64_t c0, c1;
 };
 
 __global__ void validate_kernel(const double* x, const double* y, const int64_t* t, uint64_t n,
@@ -30,10 +26,13 @@ __global__ void resample_seq_kernel(Batch B, int p_first, int count, uint64_t se
                                     const double* ox, const double* oy, const int64_t* ot,
                                     int mode);
 __global__ void key_kernel(Batch B, GridGeom G, int p_first);
-__global__ void scan_kernel(Batch B, GridGeom G, int p_first);
+__global__ void scan_kernel(const uint32_t* counts, uint32_t* start, uint32_t* istart,
+                            uint32_t cells);
+__global__ void select_count_kernel(Batch B, GridGeom G);
+__global__ void select_scatter_kernel(Batch B, GridGeom G);
 __global__ void scatter_kernel(Batch B, GridGeom G, int p_first);
 __global__ void items_kernel(Batch B, GridGeom G, int p_first);
-__global__ void tasks_kernel(Batch B, GridGeom G);
+__global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas);
 __global__ void pair_kernel(PairArgs A);
 __global__ void finalize_kernel(Batch B, uint32_t cs, uint32_t ct, const double* s_values,
                                 const int64_t* t_values, double area, int64_t duration,

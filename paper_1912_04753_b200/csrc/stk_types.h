@@ -7,7 +7,8 @@
 namespace stk {
 
 constexpr int kItemCenters = 32;    // centers per warp work item (one per lane)
-constexpr int kTaskItems = 32;      // warp items per CTA task (one smem histogram flush)
+constexpr int kTaskMinItems = 4;    // warp items per CTA task: adaptive in [min, max] so the
+constexpr int kTaskMaxItems = 256;  // batch has ~8 tasks per resident CTA
 constexpr int kPairWarps = 8;       // warps per pair-kernel CTA
 constexpr int kBucketTable = 1024;  // bucket table size for bin guesses
 constexpr int kArcQueue = 64;       // per-warp arc queue capacity
@@ -64,8 +65,17 @@ struct Batch {
   uint32_t* item_start;  // [R][cells+1] exclusive scan of ceil(count/32)
   uint2* items;          // [R][max_items]: (cell, first sorted position)
   uint32_t max_items;
-  uint32_t* task_start;  // [R+1] exclusive scan of ceil(items_r / kTaskItems)
-  uint32_t* task_counter;
+  // center selection (patterns [0, n_sel) only): a sorted point is a center
+  // iff its input index i satisfies c0 <= i < c1 and i % nshards == shard.
+  // The selected SET is independent of the (arbitrary) order within a cell,
+  // so shards of one pattern computed by separate calls partition its pairs.
+  int n_sel;
+  uint32_t shard, nshards;
+  uint64_t c0, c1;
+  uint32_t* sel_start;   // [n_sel][cells+1] exclusive scan of selected per cell
+  uint32_t* center_pos;  // [n_sel][n] sorted positions of selected centers, by cell
+  uint32_t* task_start;  // [R+1] exclusive scan of ceil(items_r / task_items)
+  uint32_t* task_counter;  // [0] dynamic task counter, [1] task_items
   // exact histograms [R][bins]
   unsigned long long* h_cnt;   // in-threshold pairs
   unsigned long long* h_half;  // interior pairs with v = 1/2 (contribute 2)
