@@ -85,10 +85,8 @@ def poi(cfg: Config, clusters=2000, frac_clustered=0.7):
     n_cl = int(round(frac_clustered * n))
     sizes = rng.lognormal(5.0, 1.0, clusters)
     sizes = np.floor(sizes / sizes.sum() * n_cl).astype(np.int64)
-    short = n_cl - sizes.sum()
-    sizes[rng.choice(clusters, size=short, replace=True)] += 1
-    sizes = np.bincount(np.concatenate([np.repeat(np.arange(clusters), sizes)]),
-                        minlength=clusters)
+    short = int(n_cl - sizes.sum())
+    np.add.at(sizes, rng.choice(clusters, size=short, replace=True), 1)
     cxs = rng.uniform(0, e, clusters)
     cys = rng.uniform(0, e, clusters)
     cts = rng.uniform(0, P, clusters)
