@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libstk.so")
+LIB_PATH = os.environ.get("STK_LIB_PATH") or os.path.join(HERE, "libstk.so")
 
 STK_OK, STK_EINVAL, STK_EUNSUPPORTED, STK_ECUDA, STK_ESTATE = 0, 1, 2, 3, 4
 METHOD_CSR, METHOD_BOOTSTRAP, METHOD_PERMUTATION = 0, 1, 2

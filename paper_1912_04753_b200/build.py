@@ -41,15 +41,17 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build_library(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build_library(force: bool = False, verbose: bool = False, extra=(), out=None) -> str:
+    lib = out or LIB
+    if not force and not extra and out is None and not _stale():
         return LIB
     nvcc = _nvcc()
     objs = []
     procs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [nvcc, *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = obj.replace(".o", ".%d.o" % os.getpid()) if out else obj
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
             print(" ".join(cmd), file=sys.stderr)
@@ -58,16 +60,16 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     for p in procs:
         if p.wait() != 0:
             raise RuntimeError("nvcc failed building libstk.so")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     subprocess.run(link, check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         try:
             os.remove(o)
         except OSError:
             pass
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

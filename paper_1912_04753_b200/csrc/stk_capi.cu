@@ -124,10 +124,12 @@ struct stk_ctx {
 
   // batch buffers (grow-only)
   DevBuf<double> x, y, xs, ys;
-  DevBuf<int64_t> t, ts;
+  DevBuf<int64_t> t, ts, pvt;
+  DevBuf<double> psq;
   DevBuf<uint32_t> idx, key, rank, cell_count, cell_start, item_start, task_start, task_counter;
   DevBuf<uint2> items;
   DevBuf<uint32_t> sel_start, center_pos;
+  DevBuf<uint4> arcq;
   DevBuf<unsigned long long> hist, stats, bad;
   DevBuf<double> K, L, env, obs;
   DevBuf<int> flags, ovf;
@@ -163,6 +165,7 @@ RegionView region_view(stk_ctx* c) {
   r.ymin = c->ymin;
   r.ymax = c->ymax;
   r.maxabs = c->maxabs;
+  r.rect = c->fast_rect ? 1 : 0;
   return r;
 }
 
@@ -230,7 +233,7 @@ Plan make_plan(stk_ctx* c, uint64_t n, uint64_t patterns) {
   P.G = make_grid_geom(c, n);
   P.bins = (uint32_t)(c->s_values.size() * c->t_values.size());
   P.max_items = (uint32_t)((n + kItemCenters - 1) / kItemCenters + P.G.cells);
-  const uint64_t per = n * (8 * 3 + 8 * 3 + 4 * 3) + (uint64_t)(P.G.cells + 1) * 4 * 3 +
+  const uint64_t per = n * (8 * 3 + 8 * 5 + 4 * 4) + (uint64_t)(P.G.cells + 1) * 4 * 3 +
                        (uint64_t)P.max_items * 8 + (uint64_t)P.bins * 8 * 6 + 64;
   uint64_t R = std::max<uint64_t>(1, c->mem_budget / per);
   R = std::min<uint64_t>(R, std::max<uint64_t>(patterns, 1));
@@ -248,6 +251,8 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   c->ys.ensure(R * n);
   c->ts.ensure(R * n);
   c->idx.ensure(R * n);
+  c->psq.ensure(R * n);
+  c->pvt.ensure(R * n);
   c->key.ensure(R * n);
   c->rank.ensure(R * n);
   c->cell_count.ensure(R * P.G.cells);
@@ -271,6 +276,8 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   B.ys = c->ys.p;
   B.ts = c->ts.p;
   B.idx = c->idx.p;
+  B.psq = c->psq.p;
+  B.pvt = c->pvt.p;
   B.key = c->key.p;
   B.rank = c->rank.p;
   B.cell_count = c->cell_count.p;
@@ -389,7 +396,7 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   scan_kernel<<<R, 1024, 0, c->stream>>>(B.cell_count, B.cell_start, B.item_start, G.cells);
   CK(cudaGetLastError());
   ++c->launches;
-  scatter_kernel<<<gp, 256, 0, c->stream>>>(B, G, 0);
+  scatter_kernel<<<gp, 256, 0, c->stream>>>(B, G, region_view(c), 0);
   CK(cudaGetLastError());
   ++c->launches;
   B.n_sel = std::min(n_sel, R);
@@ -434,7 +441,10 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   A.G = G;
   A.bins = bin_view(c);
   A.reg = region_view(c);
-  pair_kernel<<<c->num_sms * per_sm, kPairWarps * 32, smem, c->stream>>>(A);
+  const uint64_t ctas = (uint64_t)c->num_sms * per_sm;
+  c->arcq.ensure(ctas * kPairWarps * kArcRing);
+  A.B.arcq = c->arcq.p;
+  pair_kernel<<<(unsigned)ctas, kPairWarps * 32, smem, c->stream>>>(A);
   CK(cudaGetLastError());
   ++c->launches;
   CK(cudaEventRecord(e2, c->stream));
@@ -685,12 +695,12 @@ void stk_destroy(stk_ctx* c) {
   c->d_ring.release(); c->d_Q.release(); c->d_s.release(); c->d_T.release();
   c->d_stab.release(); c->d_ttab.release();
   c->x.release(); c->y.release(); c->t.release(); c->xs.release(); c->ys.release();
-  c->ts.release(); c->idx.release(); c->key.release(); c->rank.release();
+  c->ts.release(); c->idx.release(); c->psq.release(); c->pvt.release(); c->key.release(); c->rank.release();
   c->cell_count.release(); c->cell_start.release(); c->item_start.release();
   c->task_start.release(); c->task_counter.release(); c->items.release();
   c->hist.release(); c->stats.release(); c->bad.release(); c->K.release(); c->L.release();
   c->env.release(); c->obs.release(); c->flags.release(); c->ovf.release();
-  c->sel_start.release(); c->center_pos.release();
+  c->sel_start.release(); c->center_pos.release(); c->arcq.release();
   c->scratch.release(); c->sx.release(); c->sy.release(); c->st.release();
   cudaStreamDestroy(c->stream);
   delete c;

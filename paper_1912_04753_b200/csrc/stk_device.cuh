@@ -136,6 +136,148 @@ __device__ __noinline__ double spatial_weight(double cx, double cy, double d, co
   return inside_span / kTwoPi;
 }
 
+// spatial_isotropic_weight for rings of at most 32 vertices, organised for
+// SIMT: (1) a uniform pass over the segments marks those whose quadratic has
+// an accepted discriminant; (2) each lane walks only its accepted segments
+// (recomputing the same quadratic) and records the crossing vectors; (3) one
+// loop of atan2 over the crossings; then sort / de-duplicate / arc midpoints
+// exactly as spatial_weight().  Lanes crossing different edges no longer
+// serialise their atan2 and divisions.  Crossing data live in a caller
+// scratch (shared memory, element k at buf[k * stride], 2*cap elements).
+// Same arithmetic and order as the reference; returns -1 when more than `cap`
+// crossings occur (caller falls back to spatial_weight()).
+// point_in_polygon for an axis-aligned rectangle ring [x0,x1] x [y0,y1]
+// (RegionView::rect), exactly equal to the general routine on that ring:
+// * ray cast: horizontal edges never satisfy (a.y > py) != (b.y > py); a
+//   vertical edge at X gives x_cross = X + q*(b.x-a.x) = X + q*0 = X exactly
+//   and toggles iff y0 <= py < y1; two toggles cancel, so the parity is
+//   (y0 <= py < y1) && (x0 <= px < x1);
+// * boundary: on_segment is evaluated (exactly as the reference) only for the
+//   edges whose cross product passes the tolerance with the largest scale;
+//   all other edges return false there (see point_in_polygon).
+__device__ __forceinline__ bool point_in_rect(double px, double py, const RegionView& R) {
+  if (py >= R.ymin && py < R.ymax && px >= R.xmin && px < R.xmax) {
+    // strictly-inside parity is true; on_segment could only add true
+    return true;
+  }
+  const double smax = fmax(fmax(R.maxabs, 1.0), fmax(fabs(px), fabs(py)));
+  const double bound = 1e-12 * smax * smax;
+  for (uint32_t i = 0; i < 4; ++i) {
+    const double2 a = R.ring[i];
+    const double2 b = R.ring[(i + 1) & 3];
+    const double cross = (b.x - a.x) * (py - a.y) - (b.y - a.y) * (px - a.x);
+    if (fabs(cross) > bound) continue;
+    if (on_segment(px, py, a.x, a.y, b.x, b.y)) return true;
+  }
+  return false;
+}
+
+#ifndef STK_WEIGHT_INLINE
+#define STK_WEIGHT_INLINE __forceinline__
+#endif
+// spatial_isotropic_weight for rings of at most 32 vertices, organised for
+// SIMT: (1) a uniform pass over the segments marks those whose quadratic has
+// an accepted discriminant; (2) each lane walks only its accepted segments
+// (recomputing the same quadratic) and records the crossing vectors; (3) one
+// loop of atan2 over the crossings; then sort / de-duplicate / arc midpoints
+// exactly as spatial_weight().  Lanes crossing different edges no longer
+// serialise their atan2 and divisions.  Crossing data live in a caller
+// scratch (shared memory, element k at buf[k * stride], 2*cap elements).
+// For rectangles, pass (1) skips edges whose line lies farther than
+// r*(1 + 1e-6) from the center: their true discriminant is negative by a
+// margin far above the rounding error (<~1e-15 * scale), so the reference
+// rejects them too; and PIP uses point_in_rect.
+// Same arithmetic and order as the reference; returns -1 when more than `cap`
+// crossings occur (caller falls back to spatial_weight()).
+__device__ STK_WEIGHT_INLINE double spatial_weight_buf(double cx, double cy, double d,
+                                                       const RegionView& R, double* buf,
+                                                       int stride, int cap) {
+  if (d <= 0.0) return 1.0;
+  const uint32_t nv = R.nv;
+  const double2* ring = R.ring;
+  const double r2 = d * d;
+  const double reach = d * (1.0 + 1e-6);
+  uint32_t acc = 0;
+  for (uint32_t i = 0; i < nv; ++i) {  // segment (ring[i-1], ring[i])
+    const double2 A = ring[i == 0 ? nv - 1 : i - 1], Bv = ring[i];
+    if (R.rect) {
+      const double h = A.x == Bv.x ? fabs(A.x - cx) : fabs(A.y - cy);
+      if (h > reach) continue;
+    }
+    const double dx = Bv.x - A.x, dy = Bv.y - A.y;
+    const double fx = A.x - cx, fy = A.y - cy;
+    const double qa = dx * dx + dy * dy;
+    const double qb = 2.0 * (fx * dx + fy * dy);
+    const double qc = fx * fx + fy * fy - r2;
+    const double disc = qb * qb - 4.0 * qa * qc;
+    const double scale = qb * qb + fabs(4.0 * qa * qc);
+    if (qa != 0.0 && disc > 1e-9 * scale) acc |= 1u << i;
+  }
+  if (acc == 0) return 1.0;
+  int n = 0;
+  while (acc) {
+    const uint32_t i = __ffs(acc) - 1;
+    acc &= acc - 1;
+    const double2 A = ring[i == 0 ? nv - 1 : i - 1], Bv = ring[i];
+    const double dx = Bv.x - A.x, dy = Bv.y - A.y;
+    const double fx = A.x - cx, fy = A.y - cy;
+    const double qa = dx * dx + dy * dy;
+    const double qb = 2.0 * (fx * dx + fy * dy);
+    const double qc = fx * fx + fy * fy - r2;
+    const double disc = qb * qb - 4.0 * qa * qc;
+    const double sq = sqrt(disc);
+    const double t0 = (-qb - sq) / (2.0 * qa);
+    const double t1 = (-qb + sq) / (2.0 * qa);
+    if (t0 >= 0.0 && t0 <= 1.0) {
+      if (n >= cap) return -1.0;
+      buf[(2 * n) * stride] = (A.y + t0 * dy) - cy;
+      buf[(2 * n + 1) * stride] = (A.x + t0 * dx) - cx;
+      ++n;
+    }
+    if (t1 >= 0.0 && t1 <= 1.0) {
+      if (n >= cap) return -1.0;
+      buf[(2 * n) * stride] = (A.y + t1 * dy) - cy;
+      buf[(2 * n + 1) * stride] = (A.x + t1 * dx) - cx;
+      ++n;
+    }
+  }
+  if (n == 0) return 1.0;
+  for (int k = 0; k < n; ++k) {  // angle k overwrites slot k (vector k sits at 2k, 2k+1)
+    double ang = atan2(buf[(2 * k) * stride], buf[(2 * k + 1) * stride]);
+    if (ang < 0.0) ang += kTwoPi;
+    buf[k * stride] = ang;
+  }
+  for (int a = 1; a < n; ++a) {  // std::sort (ascending; same sequence)
+    const double v = buf[a * stride];
+    int b = a - 1;
+    while (b >= 0 && buf[b * stride] > v) {
+      buf[(b + 1) * stride] = buf[b * stride];
+      --b;
+    }
+    buf[(b + 1) * stride] = v;
+  }
+  int u = 0;
+  for (int a = 0; a < n; ++a) {
+    const double v = buf[a * stride];
+    if (u == 0 || v - buf[(u - 1) * stride] > kAngleEps) buf[(u++) * stride] = v;
+  }
+  const double first = buf[0];
+  if (u > 1 && (first + kTwoPi) - buf[(u - 1) * stride] <= kAngleEps) --u;
+  if (u < 2) return 1.0;
+  double inside_span = 0.0;
+  for (int a = 0; a < u; ++a) {
+    const double a0 = buf[a * stride];
+    const double a1 = (a + 1 < u) ? buf[(a + 1) * stride] : first + kTwoPi;
+    const double mid = 0.5 * (a0 + a1);
+    double sn, cs;
+    sincos(mid, &sn, &cs);
+    const double px = cx + d * cs, py = cy + d * sn;
+    const bool in = R.rect ? point_in_rect(px, py, R) : point_in_polygon(px, py, ring, nv, R.maxabs);
+    if (in) inside_span += a1 - a0;
+  }
+  return inside_span / kTwoPi;
+}
+
 // Squared radius below which spatial_weight() provably returns exactly 1.0
 // for this center (the circle stays strictly inside every edge's reach by a
 // relative margin far above the rounding error of the reference's quadratic;

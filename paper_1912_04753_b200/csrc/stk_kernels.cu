@@ -337,17 +337,24 @@ __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* counts, uint
   }
 }
 
-__global__ void scatter_kernel(Batch B, GridGeom G, int p_first) {
+__global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first) {
   const int p = p_first + blockIdx.y;
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= B.n) return;
   const uint64_t o = (uint64_t)p * B.n + i;
   const uint32_t pos = B.cell_start[(uint64_t)p * (G.cells + 1) + B.key[o]] + B.rank[o];
   const uint64_t d = (uint64_t)p * B.n + pos;
-  B.xs[d] = B.x[o];
-  B.ys[d] = B.y[o];
-  B.ts[d] = B.t[o];
+  const double x = B.x[o], y = B.y[o];
+  const int64_t t = B.t[o];
+  B.xs[d] = x;
+  B.ys[d] = y;
+  B.ts[d] = t;
   B.idx[d] = (uint32_t)i;
+  // per-point memo replacing the reference's weight cache (weight_cache.hpp:39-129):
+  // radius^2 under which omega == 1 exactly, and the temporal-weight threshold
+  // v == 1 <=> u <= min(t - P0, P1 - t) (edge_correction.cpp:81-86)
+  B.psq[d] = safe_q(x, y, R.ring, R.nv, R.maxabs);
+  B.pvt[d] = min(t - R.p0, R.p1 - t);
 }
 
 // Center selection (patterns [0, n_sel)): count selected centers per cell.
@@ -414,106 +421,121 @@ __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas) {
 }
 
 // ============================================================ K2 pair kernel
+// Each unordered in-threshold pair {i, j} is found once: from the center in
+// the lower cell of the forward half-stencil (13 of the 26 neighbour cells),
+// or, inside one cell, from the lower sorted position (lower input index
+// when centers are selected, so shards partition the pairs whatever the
+// order inside a cell).  d, u and the bin are shared by both ordered pairs
+// (d_ij == d_ji bitwise: the squares of x-y and y-x are equal); each ordered
+// pair keeps its own center's weights (safe radius and temporal threshold
+// memoised per point at scatter time).
 struct PairSmem {
-  unsigned long long* lo;  // [bins] arc-path fixed-point sums (low 64)
-  uint32_t* cnt;           // [bins]
-  uint32_t* half;          // [bins]
-  uint32_t* hi;            // [bins]
-  double* Q;               // [cs]
-  int64_t* T;              // [ct]
-  uint16_t* stab;          // [kBucketTable]
-  uint16_t* ttab;          // [kBucketTable]
-  double2* tile;           // [warps][32]
-  int64_t* tt;             // [warps][32]
-  double* aq;              // [warps][kArcQueue]
-  uint32_t* abin;          // [warps][kArcQueue]
-  uint8_t* aown;           // [warps][kArcQueue]
+  double2* tile;            // [warps][32] neighbour x, y
+  int64_t* tt;              // [warps][32] neighbour t
+  double* tsq;              // [warps][32] neighbour safe q
+  int64_t* tvt;             // [warps][32] neighbour temporal threshold
+  uint32_t* tix;            // [warps][32] neighbour input index
+  double* angs;             // [warps][kAngleSlots][32] per-lane crossing-angle scratch
+  unsigned long long* lo;   // [bins] arc-path fixed-point sums (low 64)
+  double* Q;                // [cs]
+  int64_t* T;               // [ct]
+  uint32_t* cnt;            // [bins]
+  uint32_t* half;           // [bins]
+  uint32_t* hi;             // [bins]
+  uint16_t* stab;           // [kBucketTable]
+  uint16_t* ttab;           // [kBucketTable]
 };
 
-// Shared-memory layout of the pair kernel; 16-byte aligned sections first.
 __host__ __device__ inline size_t pair_smem_layout(uint32_t bins, uint32_t cs, uint32_t ct,
                                                    size_t* off) {
   size_t b = 0;
-  auto take = [&](int k, size_t bytes) {
+  int k = 0;
+  auto take = [&](size_t bytes) {
     b = (b + 15) & ~size_t(15);
-    off[k] = b;
+    off[k++] = b;
     b += bytes;
   };
-  take(0, sizeof(double2) * kPairWarps * 32);              // tile
-  take(1, sizeof(int64_t) * kPairWarps * 32);              // tt
-  take(2, sizeof(double) * kPairWarps * kArcQueue);        // aq
-  take(3, sizeof(unsigned long long) * bins);              // lo
-  take(4, sizeof(double) * cs);                            // Q
-  take(5, sizeof(int64_t) * ct);                           // T
-  take(6, sizeof(uint32_t) * bins);                        // cnt
-  take(7, sizeof(uint32_t) * bins);                        // half
-  take(8, sizeof(uint32_t) * bins);                        // hi
-  take(9, sizeof(uint32_t) * kPairWarps * kArcQueue);      // abin
-  take(10, sizeof(uint8_t) * kPairWarps * kArcQueue);      // aown
-  take(11, sizeof(uint16_t) * kBucketTable);               // stab
-  take(12, sizeof(uint16_t) * kBucketTable);               // ttab
+  take(sizeof(double2) * kPairWarps * 32);
+  take(sizeof(int64_t) * kPairWarps * 32);
+  take(sizeof(double) * kPairWarps * 32);
+  take(sizeof(int64_t) * kPairWarps * 32);
+  take(sizeof(uint32_t) * kPairWarps * 32);
+  take(sizeof(double) * kPairWarps * kAngleSlots * 32);
+  take(sizeof(unsigned long long) * bins);
+  take(sizeof(double) * cs);
+  take(sizeof(int64_t) * ct);
+  take(sizeof(uint32_t) * bins);
+  take(sizeof(uint32_t) * bins);
+  take(sizeof(uint32_t) * bins);
+  take(sizeof(uint16_t) * kBucketTable);
+  take(sizeof(uint16_t) * kBucketTable);
   return (b + 15) & ~size_t(15);
 }
 
 size_t pair_kernel_smem(uint32_t bins, uint32_t cs, uint32_t ct) {
-  size_t off[13];
+  size_t off[14];
   return pair_smem_layout(bins, cs, ct, off);
 }
 
 __device__ __forceinline__ PairSmem carve(unsigned char* raw, uint32_t bins, uint32_t cs,
                                           uint32_t ct) {
-  size_t off[13];
-  pair_smem_layout(bins, cs, ct, off);
+  size_t o[14];
+  pair_smem_layout(bins, cs, ct, o);
   PairSmem S;
-  S.tile = (double2*)(raw + off[0]);
-  S.tt = (int64_t*)(raw + off[1]);
-  S.aq = (double*)(raw + off[2]);
-  S.lo = (unsigned long long*)(raw + off[3]);
-  S.Q = (double*)(raw + off[4]);
-  S.T = (int64_t*)(raw + off[5]);
-  S.cnt = (uint32_t*)(raw + off[6]);
-  S.half = (uint32_t*)(raw + off[7]);
-  S.hi = (uint32_t*)(raw + off[8]);
-  S.abin = (uint32_t*)(raw + off[9]);
-  S.aown = (uint8_t*)(raw + off[10]);
-  S.stab = (uint16_t*)(raw + off[11]);
-  S.ttab = (uint16_t*)(raw + off[12]);
+  S.tile = (double2*)(raw + o[0]);
+  S.tt = (int64_t*)(raw + o[1]);
+  S.tsq = (double*)(raw + o[2]);
+  S.tvt = (int64_t*)(raw + o[3]);
+  S.tix = (uint32_t*)(raw + o[4]);
+  S.angs = (double*)(raw + o[5]);
+  S.lo = (unsigned long long*)(raw + o[6]);
+  S.Q = (double*)(raw + o[7]);
+  S.T = (int64_t*)(raw + o[8]);
+  S.cnt = (uint32_t*)(raw + o[9]);
+  S.half = (uint32_t*)(raw + o[10]);
+  S.hi = (uint32_t*)(raw + o[11]);
+  S.stab = (uint16_t*)(raw + o[12]);
+  S.ttab = (uint16_t*)(raw + o[13]);
   return S;
 }
 
-// Exact weight of `count` queued arc-path pairs (one per lane), accumulated
-// into the CTA histogram as 128-bit fixed point of (1/(omega*v) - 1).
-__device__ __forceinline__ void drain_arcs(int count, int lane, const double* aq,
-                                           const uint32_t* abin, const uint8_t* aown, double cx,
-                                           double cy, const PairSmem& S, const RegionView& reg,
-                                           int* overflow) {
-  double q = 0.0;
-  uint32_t bw = 0;
-  int own = 0;
-  if (lane < count) {
-    q = aq[lane];
-    bw = abin[lane];
-    own = aown[lane];
-  }
-  const double ocx = __shfl_sync(FULL_MASK, cx, own);
-  const double ocy = __shfl_sync(FULL_MASK, cy, own);
-  if (lane < count) {
-    const double d = sqrt(q);
-    const double ws = spatial_weight(ocx, ocy, d, reg.ring, reg.nv, reg.maxabs, overflow);
-    const double w = ws * ((bw >> 31) ? 0.5 : 1.0);  // edge::pair_weight (edge_correction.cpp:88-103)
-    const double term = 1.0 / w;                      // PairHistogram::add(.., 1.0 / w)
-    uint64_t lo, hi;
-    fixed52_minus_one(term, &lo, &hi);
-    const uint32_t bin = bw & 0x7fffffffu;
-    if (lo | hi) {
-      const unsigned long long old = atomicAdd(&S.lo[bin], (unsigned long long)lo);
-      if (old + lo < old) ++hi;
-      if (hi) atomicAdd(&S.hi[bin], (uint32_t)hi);
-    }
+// Exact weight of `count` queued arc-path ordered pairs (one per lane),
+// accumulated into the CTA histogram as 128-bit fixed point of (1/(omega*v) - 1).
+// Entries live in the warp's ring (global, L1/L2-resident): {center sorted
+// position, bin | (v == 1/2) << 31, q = d^2 as two words}.
+__device__ __forceinline__ void drain_arcs(int count, int lane, const uint4* ring_q,
+                                           uint32_t head, double* angs, const double* xs,
+                                           const double* ys, const PairSmem& S,
+                                           const RegionView& reg, int* overflow) {
+#ifdef STK_NO_ARC
+  return;
+#endif
+  if (lane >= count) return;
+  const uint4 e = ring_q[(head + lane) & (kArcRing - 1)];
+  const uint32_t cp = e.x;
+  const double cx = xs[cp], cy = ys[cp];
+  const double q = __hiloint2double((int)e.w, (int)e.z);
+  const uint32_t bw = e.y;
+  const double d = sqrt(q);
+  double ws = -1.0;
+  if (reg.nv <= 32) ws = spatial_weight_buf(cx, cy, d, reg, angs + lane, 32, kAngleSlots / 2);
+  if (ws < 0.0) ws = spatial_weight(cx, cy, d, reg.ring, reg.nv, reg.maxabs, overflow);
+  const double w = ws * ((bw >> 31) ? 0.5 : 1.0);  // edge::pair_weight (edge_correction.cpp:88-103)
+  const double term = 1.0 / w;                      // PairHistogram::add(.., 1.0 / w)
+  uint64_t lo, hi;
+  fixed52_minus_one(term, &lo, &hi);
+  const uint32_t bin = bw & 0x7fffffffu;
+  if (lo | hi) {
+    const unsigned long long old = atomicAdd(&S.lo[bin], (unsigned long long)lo);
+    if (old + lo < old) ++hi;
+    if (hi) atomicAdd(&S.hi[bin], (uint32_t)hi);
   }
 }
 
-__global__ void __launch_bounds__(kPairWarps * 32, 4) pair_kernel(PairArgs A) {
+#ifndef STK_PAIR_MINB
+#define STK_PAIR_MINB 3
+#endif
+__global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_task, s_next;
   const Batch& B = A.B;
@@ -537,9 +559,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, 4) pair_kernel(PairArgs A) {
   const unsigned lanemask_lt = (1u << lane) - 1u;
   double2* tile = S.tile + w * 32;
   int64_t* tt = S.tt + w * 32;
-  double* aq = S.aq + w * kArcQueue;
-  uint32_t* abin = S.abin + w * kArcQueue;
-  uint8_t* aown = S.aown + w * kArcQueue;
+  double* tsq = S.tsq + w * 32;
+  int64_t* tvt = S.tvt + w * 32;
+  uint32_t* tix = S.tix + w * 32;
+  uint4* arcq = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * kArcRing;
+  double* angs = S.angs + w * kAngleSlots * 32;
   int overflow = 0;
   unsigned long long tot_in = 0, tot_cand = 0, tot_exact = 0;
 
@@ -558,8 +582,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, 4) pair_kernel(PairArgs A) {
     __syncthreads();
     const uint32_t task = s_task;
     if (task >= total_tasks) break;
-    // pattern of this task
-    int lo_p = 0, hi_p = B.R - 1;
+    int lo_p = 0, hi_p = B.R - 1;  // pattern of this task
     while (lo_p < hi_p) {
       const int mid = (lo_p + hi_p + 1) >> 1;
       if (B.task_start[mid] <= task) lo_p = mid; else hi_p = mid - 1;
@@ -574,6 +597,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, 4) pair_kernel(PairArgs A) {
     const double* xs = B.xs + pb;
     const double* ys = B.ys + pb;
     const int64_t* ts = B.ts + pb;
+    const double* psq = B.psq + pb;
+    const int64_t* pvt = B.pvt + pb;
+    const uint32_t* pix = B.idx + pb;
     const bool sel_p = p < B.n_sel;
     const uint32_t* clist = sel_p ? B.sel_start + (uint64_t)p * (G.cells + 1) : cstart;
     const uint32_t* cpos = B.center_pos + pb;
@@ -585,56 +611,70 @@ __global__ void __launch_bounds__(kPairWarps * 32, 4) pair_kernel(PairArgs A) {
       if (i0 + it >= i1) break;
       const uint2 item = items[i0 + it];
       const uint32_t cell = item.x, start = item.y;
-      const uint32_t cend = clist[cell + 1];
-      const uint32_t nc = min((uint32_t)kItemCenters, cend - start);
+      const uint32_t nc = min((uint32_t)kItemCenters, clist[cell + 1] - start);
       const bool valid = lane < (int)nc;
-      uint32_t mypos = 0xFFFFFFFFu;
-      double cx = 0.0, cy = 0.0, sq = -1.0;
-      int64_t ctm = 0, vthr = 0;
+      uint32_t mypos = 0, myidx = 0;
+      double cx = 0.0, cy = 0.0, sq_i = 0.0;
+      int64_t ctm = 0, vt_i = 0;
       if (valid) {
         mypos = sel_p ? cpos[start + lane] : start + lane;
         cx = xs[mypos];
         cy = ys[mypos];
         ctm = ts[mypos];
-        sq = safe_q(cx, cy, A.reg.ring, A.reg.nv, A.reg.maxabs);
-        vthr = min(ctm - A.reg.p0, A.reg.p1 - ctm);  // edge_correction.cpp:81-86
+        sq_i = psq[mypos];
+        vt_i = pvt[mypos];
+        myidx = pix[mypos];
       }
       const unsigned nvalid = __popc(__ballot_sync(FULL_MASK, valid));
       const int kx = (int)(cell % (uint32_t)G.nx);
       const uint32_t rest = cell / (uint32_t)G.nx;
       const int ky = (int)(rest % (uint32_t)G.ny);
       const int kt = (int)(rest / (uint32_t)G.ny);
-      const int xa = max(kx - 1, 0), xb = min(kx + 1, G.nx - 1);
-      int qn = 0;
+      const uint32_t own_end = cstart[cell + 1];
+      uint32_t qh = 0, qt = 0;  // ring head / tail (monotone)
       uint32_t n_in = 0, n_exact = 0;
       unsigned long long n_cand = 0;
-      for (int dt = -1; dt <= 1; ++dt) {
-        const int tk = kt + dt;
-        if (tk < 0 || tk >= G.nt) continue;
-        for (int dy = -1; dy <= 1; ++dy) {
-          const int yk = ky + dy;
-          if (yk < 0 || yk >= G.ny) continue;
+      // forward half-stencil as 5 contiguous ranges of the sorted array
+      for (int r = 0; r < 5; ++r) {
+        uint32_t rb, re;
+        if (r == 0) {  // own cell (+ the cell at kx+1, contiguous)
+          rb = sel_p ? cstart[cell] : start + 1;
+          re = cstart[cell + (kx + 1 < G.nx ? 2 : 1)];
+        } else {
+          const int yk = r == 1 ? ky + 1 : ky + (r - 3);
+          const int tk = r == 1 ? kt : kt + 1;
+          if (yk < 0 || yk >= G.ny || tk >= G.nt) continue;
           const uint32_t row = ((uint32_t)tk * G.ny + yk) * G.nx;
-          const uint32_t rb = cstart[row + xa], re = cstart[row + xb + 1];
-          for (uint32_t j0 = rb; j0 < re; j0 += 32) {
-            const uint32_t j = j0 + lane;
-            if (j < re) {
-              tile[lane] = make_double2(xs[j], ys[j]);
-              tt[lane] = ts[j];
-            }
-            __syncwarp();
-            const int m = (int)min(32u, re - j0);
-            n_cand += (unsigned long long)m;
-            for (int k = 0; k < m; ++k) {
+          rb = cstart[row + max(kx - 1, 0)];
+          re = cstart[row + min(kx + 1, G.nx - 1) + 1];
+        }
+        for (uint32_t j0 = rb; j0 < re; j0 += 32) {
+          const uint32_t j = j0 + lane;
+          if (j < re) {
+            tile[lane] = make_double2(xs[j], ys[j]);
+            tt[lane] = ts[j];
+            tsq[lane] = psq[j];
+            tvt[lane] = pvt[j];
+            tix[lane] = pix[j];
+          }
+          __syncwarp();
+          const int m = (int)min(32u, re - j0);
+          n_cand += (unsigned long long)m;
+          for (int kc = 0; kc < m; kc += kArcChunk) {
+            const int kend = min(kc + kArcChunk, m);
+            for (int k = kc; k < kend; ++k) {
               const double2 nb = tile[k];
               const int64_t nt = tt[k];
-              const double dx = cx - nb.x, dy2 = cy - nb.y;
-              const double q = dx * dx + dy2 * dy2;  // spatial_distance^2, no FMA
+              const double dx = cx - nb.x, dy = cy - nb.y;
+              const double q = dx * dx + dy * dy;  // spatial_distance^2, no FMA
               int64_t du = ctm - nt;
-              du = du < 0 ? -du : du;                // temporal_distance
-              const bool in = valid && q <= Qmax && du <= Tmax && (j0 + k) != mypos;
-              bool arc = false;
-              uint32_t ab = 0;
+              du = du < 0 ? -du : du;              // temporal_distance
+              const uint32_t jp = j0 + k;
+              const bool owner = jp >= own_end || (sel_p ? tix[k] > myidx : jp > mypos);
+              const bool in = valid && owner && q <= Qmax && du <= Tmax;
+              bool arc_i = false, arc_j = false;
+              uint32_t bin = 0;
+              bool half_i = false, half_j = false;
               if (in) {
                 // bin_pair: first s_k >= d <=> first Q_k >= q; first t_l >= u
                 int bq = (int)(sqrtf((float)q) * s_inv_bw);
@@ -645,47 +685,47 @@ __global__ void __launch_bounds__(kPairWarps * 32, 4) pair_kernel(PairArgs A) {
                 bt = min(bt, kBucketTable - 1);
                 uint32_t tb = S.ttab[bt];
                 while (du > S.T[tb]) ++tb;
-                const uint32_t bin = sb * ct + tb;
-                atomicAdd(&S.cnt[bin], 1u);
-                const bool half = du > vthr;
-                arc = q >= sq;
-                if (arc) ab = bin | (half ? 0x80000000u : 0u);
-                else if (half) atomicAdd(&S.half[bin], 1u);
-                ++n_in;
+                bin = sb * ct + tb;
+                atomicAdd(&S.cnt[bin], 2u);
+                half_i = du > vt_i;
+                half_j = du > tvt[k];
+                arc_i = q >= sq_i;
+                arc_j = q >= tsq[k];
+                const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
+                if (h) atomicAdd(&S.half[bin], h);
+                n_in += 2;
               }
-              const unsigned am = __ballot_sync(FULL_MASK, arc);
-              if (am) {
-                if (arc) {
-                  const int pos = qn + __popc(am & lanemask_lt);
-                  aq[pos] = q;
-                  abin[pos] = ab;
-                  aown[pos] = (uint8_t)lane;
-                  ++n_exact;
-                }
-                qn += __popc(am);
-                if (qn >= 32) {
-                  __syncwarp();
-                  drain_arcs(32, lane, aq, abin, aown, cx, cy, S, A.reg, &overflow);
-                  __syncwarp();
-                  if (lane < qn - 32) {
-                    aq[lane] = aq[32 + lane];
-                    abin[lane] = abin[32 + lane];
-                    aown[lane] = aown[32 + lane];
-                  }
-                  __syncwarp();
-                  qn -= 32;
-                }
+              const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
+              const unsigned mj = __ballot_sync(FULL_MASK, arc_j);
+              if (mi | mj) {
+                const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
+                if (arc_i)
+                  arcq[(qt + __popc(mi & lanemask_lt)) & (kArcRing - 1)] =
+                      make_uint4(mypos, bin | (half_i ? 0x80000000u : 0u), qlo, qhi);
+                qt += __popc(mi);
+                if (arc_j)
+                  arcq[(qt + __popc(mj & lanemask_lt)) & (kArcRing - 1)] =
+                      make_uint4(jp, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
+                qt += __popc(mj);
+                n_exact += (uint32_t)arc_i + (uint32_t)arc_j;
               }
             }
-            __syncwarp();
+            // drain outside the candidate loop: pending < 32 + kArcChunk * 64 <= ring size
+            while (qt - qh >= 32) {
+              __syncwarp();
+              drain_arcs(32, lane, arcq, qh, angs, xs, ys, S, A.reg, &overflow);
+              qh += 32;
+            }
           }
+          __syncwarp();
         }
       }
-      if (qn > 0) {
+      if (qt != qh) {
         __syncwarp();
-        drain_arcs(qn, lane, aq, abin, aown, cx, cy, S, A.reg, &overflow);
-        __syncwarp();
+        drain_arcs((int)(qt - qh), lane, arcq, qh, angs, xs, ys, S, A.reg, &overflow);
+        qh = qt;
       }
+      __syncwarp();
       tot_in += n_in;
       tot_exact += n_exact;
       if (lane == 0) tot_cand += n_cand * nvalid;
@@ -707,7 +747,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, 4) pair_kernel(PairArgs A) {
       if (hi) atomicAdd(&B.h_hi[hb + b], hi);
     }
   }
-  // block-level stats
   for (int o = 16; o > 0; o >>= 1) {
     tot_in += __shfl_down_sync(FULL_MASK, tot_in, o);
     tot_exact += __shfl_down_sync(FULL_MASK, tot_exact, o);
@@ -805,6 +844,7 @@ __global__ void diff_kernel(const double* est_l, const double* upper, uint32_t b
 __global__ void weights_kernel(const double* cx, const double* cy, const double* d,
                                uint64_t count, RegionView reg, double* w, int* overflow,
                                unsigned long long* bad) {
+  __shared__ double angs[kAngleSlots * 128];
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= count) return;
   if (d[i] > 0.0 && !point_in_polygon(cx[i], cy[i], reg.ring, reg.nv)) {
@@ -812,7 +852,11 @@ __global__ void weights_kernel(const double* cx, const double* cy, const double*
     w[i] = 0.0;
     return;
   }
-  w[i] = spatial_weight(cx[i], cy[i], d[i], reg.ring, reg.nv, reg.maxabs, overflow);
+  double ws = -1.0;
+  if (reg.nv <= 32)
+    ws = spatial_weight_buf(cx[i], cy[i], d[i], reg, angs + threadIdx.x, 128, kAngleSlots / 2);
+  if (ws < 0.0) ws = spatial_weight(cx[i], cy[i], d[i], reg.ring, reg.nv, reg.maxabs, overflow);
+  w[i] = ws;
 }
 
 // FP64 issue peak: 8 independent DFMA chains per thread.

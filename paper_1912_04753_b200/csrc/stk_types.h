@@ -11,7 +11,13 @@ constexpr int kTaskMinItems = 4;    // warp items per CTA task: adaptive in [min
 constexpr int kTaskMaxItems = 256;  // batch has ~8 tasks per resident CTA
 constexpr int kPairWarps = 8;       // warps per pair-kernel CTA
 constexpr int kBucketTable = 1024;  // bucket table size for bin guesses
-constexpr int kArcQueue = 64;       // per-warp arc queue capacity
+constexpr int kAngleSlots = 16;    // per-lane crossing scratch: 2 doubles x 8 crossings
+constexpr int kRingSmem = 32;      // ring vertices staged in shared memory (bitmask path)
+#ifndef STK_ARC_CHUNK
+#define STK_ARC_CHUNK 12
+#endif
+constexpr int kArcChunk = STK_ARC_CHUNK;        // candidate steps between arc drains
+constexpr int kArcRing = 1024;      // per-warp arc ring entries (> 31 + kArcChunk * 64)
 
 // Study region on the device (geom::StudyRegion, geometry.hpp:95-120).
 struct RegionView {
@@ -20,6 +26,7 @@ struct RegionView {
   int64_t p0, p1;       // study period (inclusive)
   double xmin, xmax, ymin, ymax;
   double maxabs;        // max |coordinate| over the ring
+  int rect;             // 4-vertex axis-aligned rectangle (exact fast paths apply)
 };
 
 // Distance grid in the forms the kernels consume.
@@ -58,6 +65,8 @@ struct Batch {
   double* ys;
   int64_t* ts;
   uint32_t* idx;  // input index of each sorted point
+  double* psq;    // per sorted point: squared radius below which omega == 1 exactly
+  int64_t* pvt;   // per sorted point: v == 1 iff u <= pvt
   uint32_t* key;  // cell key per unsorted point
   uint32_t* rank; // rank within the cell per unsorted point
   uint32_t* cell_count;  // [R][cells]
@@ -85,6 +94,7 @@ struct Batch {
   double* L;  // [R][bins]
   unsigned long long* stats;   // [0] in_threshold [1] candidates [2] exact_path [3] overflow
   int* flags;                  // [R] generator fallback flags
+  uint4* arcq;                 // [grid CTAs][warps][kArcRing] arc-path rings
 };
 
 }  // namespace stk

@@ -1,0 +1,47 @@
+"""Instruction / stall-sample share per code region of the pair kernel.
+Usage: python profiles/ncu_regions.py report.ncu-rep"""
+import csv
+import io
+import subprocess
+import sys
+
+out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source",
+                      "cuda,sass"], capture_output=True, text=True).stdout
+path = None
+agg = {}
+src = open("paper_1912_04753_b200/csrc/stk_kernels.cu").read().splitlines()
+def region(path, ln):
+    if path == "stk_device.cuh":
+        return "arc weight (stk_device.cuh)"
+    if path != "stk_kernels.cu":
+        return "intrinsics " + path
+    # find the enclosing function by scanning upward for a marker
+    for k in range(ln - 1, -1, -1):
+        line = src[k]
+        if "drain_arcs(" in line and "void" in line:
+            return "arc drain"
+        if "for (int k = 0; k < m; ++k)" in line:
+            return "candidate/bin loop"
+        if "flush the CTA histogram" in line:
+            return "flush"
+        if "__global__" in line:
+            return "kernel setup/items"
+    return "other"
+for rec in csv.reader(io.StringIO(out)):
+    if not rec:
+        continue
+    if rec[0] == "File Path":
+        path = rec[1].split("/")[-1]
+        continue
+    if rec[0] in ("Function Name", "Line No") or len(rec) < 8 or rec[2] != "-":
+        continue
+    try:
+        samp = float(rec[4] or 0); inst = float(rec[7] or 0); ln = int(rec[0])
+    except ValueError:
+        continue
+    key = region(path, ln)
+    a = agg.setdefault(key, [0, 0]); a[0] += samp; a[1] += inst
+ts = sum(v[0] for v in agg.values()) or 1
+ti = sum(v[1] for v in agg.values()) or 1
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    print(f"{k:36s} samples {100*v[0]/ts:5.1f}%  instr {100*v[1]/ti:5.1f}%  ({v[1]:.3e} warp-instr)")
