@@ -163,6 +163,12 @@ int stk_run_job_shard_device(stk_ctx* ctx, const double* d_x, const double* d_y,
 int stk_generate_cstr(stk_ctx* ctx, uint64_t n, uint64_t seed, double* x, double* y,
                       int64_t* t);
 
+/* sim::generate (core/src/simulation.cpp:55-65) on the device: CSR
+ * (generate_cstr, needs only n), bootstrap or permutation of the observed
+ * points (ox, oy, ot; n of them).  Outputs n points (host buffers). */
+int stk_generate(stk_ctx* ctx, int method, uint64_t n, const double* ox, const double* oy,
+                 const int64_t* ot, uint64_t seed, double* x, double* y, int64_t* t);
+
 /* edge::spatial_isotropic_weight for a batch of (center, d) queries
  * (core/src/edge_correction.cpp:42-79); centers must lie inside the region
  * (STK_EINVAL "weight center outside study region" otherwise). */

@@ -43,7 +43,7 @@ EXPORTED = [
     "stk_set_options", "stk_estimate_surface", "stk_pair_histogram", "stk_finalize",
     "stk_simulate", "stk_run_job", "stk_run_job_device", "stk_generate_cstr",
     "stk_spatial_weights", "stk_measure_fp64_peak", "stk_run_job_shard",
-    "stk_run_job_shard_device",
+    "stk_run_job_shard_device", "stk_generate",
 ]
 
 _dp = C.POINTER(C.c_double)
@@ -74,6 +74,7 @@ _SIGS = {
     "stk_run_job_shard": (C.c_int, [_vp, _dp, _dp, _ip, _u64, _u32, _u32, _u32, _u32, _u64, C.c_int, _up, _up, _up, _dp, _dp, _tp]),
     "stk_run_job_shard_device": (C.c_int, [_vp, _vp, _vp, _vp, _u64, _u32, _u32, _u32, _u32, _u64, C.c_int, _up, _up, _up, _dp, _dp, _tp]),
     "stk_generate_cstr": (C.c_int, [_vp, _u64, _u64, _dp, _dp, _ip]),
+    "stk_generate": (C.c_int, [_vp, C.c_int, _u64, _dp, _dp, _ip, _u64, _dp, _dp, _ip]),
     "stk_spatial_weights": (C.c_int, [_vp, _dp, _dp, _dp, _u64, _dp]),
     "stk_measure_fp64_peak": (C.c_int, [_vp, _dp]),
 }

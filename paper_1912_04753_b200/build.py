@@ -11,6 +11,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libstk.so")
 
 SOURCES = ["stk_kernels.cu", "stk_capi.cu"]
+CXX_SOURCES = ["stripley_api.cpp"]
 HEADERS = ["stk_device.cuh", "stk_kernels.h", "stk_types.h"]
 
 # -fmad=false: no FP64 mul+add contraction (the reference's Release build has
@@ -35,7 +36,8 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS + CXX_SOURCES]
+    deps.append(os.path.join(ROOT, "include", "stripley_gpu.hpp"))
     deps.append(os.path.join(ROOT, "include", "stk.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
@@ -57,9 +59,15 @@ def build_library(force: bool = False, verbose: bool = False, extra=(), out=None
             print(" ".join(cmd), file=sys.stderr)
         procs.append(subprocess.Popen(cmd))
         objs.append(obj)
+    for src in CXX_SOURCES:
+        obj = os.path.join(CSRC, src.replace(".cpp", ".o"))
+        obj = obj.replace(".o", ".%d.o" % os.getpid()) if out else obj
+        procs.append(subprocess.Popen(["g++", "-std=c++20", "-O2", "-fPIC", "-c",
+                                       os.path.join(CSRC, src), "-o", obj]))
+        objs.append(obj)
     for p in procs:
         if p.wait() != 0:
-            raise RuntimeError("nvcc failed building libstk.so")
+            raise RuntimeError("compiler failed building libstk.so")
     tmp = lib + ".tmp"
     link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     subprocess.run(link, check=True)
@@ -70,6 +78,20 @@ def build_library(force: bool = False, verbose: bool = False, extra=(), out=None
         except OSError:
             pass
     return lib
+
+
+TEST_BIN = os.path.join(ROOT, "tests", "cpp", "test_api")
+
+
+def build_cpp_tests(force: bool = False) -> str:
+    """The C++ API test program (tests/cpp/test_api.cpp), linked to libstk.so."""
+    src = os.path.join(ROOT, "tests", "cpp", "test_api.cpp")
+    if not force and os.path.exists(TEST_BIN) and os.path.getmtime(TEST_BIN) > max(
+            os.path.getmtime(src), os.path.getmtime(LIB)):
+        return TEST_BIN
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), src, "-o",
+                    TEST_BIN, "-L", HERE, "-lstk", "-Wl,-rpath," + HERE], check=True)
+    return TEST_BIN
 
 
 if __name__ == "__main__":

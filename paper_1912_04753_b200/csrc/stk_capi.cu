@@ -1105,6 +1105,33 @@ int stk_generate_cstr(stk_ctx* c, uint64_t n, uint64_t seed, double* x, double* 
   });
 }
 
+int stk_generate(stk_ctx* c, int method, uint64_t n, const double* ox, const double* oy,
+                 const int64_t* ot, uint64_t seed, double* x, double* y, int64_t* t) {
+  return guarded(c, [&] {
+    if (!c->have_region) throw StateErr("study region not set (stk_set_region)");
+    const Source src = source_of(method);
+    if (n == 0) {
+      if (src != Source::Csr) throw InvalidArg(method == STK_METHOD_BOOTSTRAP
+                                                   ? "bootstrap needs n >= 1"
+                                                   : "permutation needs n >= 1");
+      return;
+    }
+    if (src != Source::Csr) upload_points(c, ox, oy, ot, n);
+    Plan P;
+    P.n = n;
+    P.R = 1;
+    P.bins = 1;
+    P.G.cells = 1;
+    P.max_items = 1;
+    Batch B = alloc_batch(c, P);
+    generate(c, B, src, 0, 1, seed, c->sx.p, c->sy.p, c->st.p);
+    CK(cudaMemcpyAsync(x, B.x, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(y, B.y, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(t, B.t, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
 int stk_spatial_weights(stk_ctx* c, const double* cx, const double* cy, const double* d,
                         uint64_t count, double* w_out) {
   return guarded(c, [&] {

@@ -1,0 +1,287 @@
+"""GPU parity, second set: the C++ reference-facing API, null models, edge
+cases of the reference's tests, multi-rank combination, larger configs.
+
+Bars as in test_gpu_parity.py: bit-exact counts / points / bins; weighted
+K/L within TOL = 1e-9 relative (north_star), typically ~1e-15.
+"""
+import json
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden, rel_err, surfaces_close
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_1912_04753_b200.stripley import device, est, geom, rt, sim
+
+    device.get(0)
+    return dict(est=est, geom=geom, rt=rt, sim=sim, dev=device.get(0))
+
+
+@pytest.fixture(scope="module")
+def port():
+    from oracle import port
+
+    return port
+
+
+def square(side, p0=0, p1=100):
+    return np.array([[0, 0], [side, 0], [side, side], [0, side]], float), p0, p1
+
+
+# ------------------------------------------------------------ C++ API
+def _write(path, *arrays):
+    with open(path, "wb") as f:
+        for a in arrays:
+            f.write(np.asarray(a).tobytes())
+
+
+def test_cpp_api_selftest():
+    from paper_1912_04753_b200.build import build_cpp_tests
+
+    exe = build_cpp_tests()
+    r = subprocess.run([exe, "selftest"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "failures=0" in r.stdout
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_cpp_run_job_golden_sample(world):
+    """rt::run_job through the C++ API on proj/data/sample_result.json's input;
+    world > 1 emulates ranks sequentially through the exact reduction hooks."""
+    from paper_1912_04753_b200.build import build_cpp_tests
+
+    exe = build_cpp_tests()
+    g = golden("sample_result.npz")
+    with tempfile.TemporaryDirectory() as d:
+        pts, ring, grid = (os.path.join(d, f) for f in ("p.bin", "r.bin", "g.bin"))
+        n = len(g["x"])
+        _write(pts, np.uint64(n), g["x"], g["y"], g["t"].astype(np.int64))
+        _write(ring, np.uint64(g["ring"].size), g["ring"].reshape(-1))
+        _write(grid, np.uint64(len(g["s"])), g["s"], np.uint64(len(g["tv"])), g["tv"].astype(np.int64))
+        r = subprocess.run([exe, "runjob", pts, ring, "0", "365", grid, str(int(g["sims"])),
+                            str(int(g["seed"])), str(world)], capture_output=True, text=True,
+                           timeout=300)
+    assert r.returncode == 0, r.stderr
+    out = json.loads(r.stdout)
+    shape = g["k"].shape
+    for key in ("k", "l", "upper", "lower", "diff"):
+        assert surfaces_close(np.array(out[key]).reshape(shape), g[key], TOL), key
+
+
+# ------------------------------------------------------------ null models
+def test_device_bootstrap_and_permutation_bit_exact(api, port):
+    import ctypes as C
+
+    from paper_1912_04753_b200 import _lib
+
+    dev, geom = api["dev"], api["geom"]
+    g = golden("sample_result.npz")
+    x, y, t = g["x"], g["y"], g["t"].astype(np.int64)
+    dev.configure(geom.StudyRegion(g["ring"], 0, 365))
+    n = len(x)
+    for method, ref_fn in ((1, port.generate_bootstrap), (2, port.generate_permutation)):
+        for seed in (1, 42, 2**40 + 7):
+            ox, oy, ot = np.zeros(n), np.zeros(n), np.zeros(n, np.int64)
+            dev.check(dev.lib.stk_generate(dev.h, method, n, _lib.ptr(x), _lib.ptr(y),
+                                           _lib.ptr(t, C.c_int64), seed, _lib.ptr(ox), _lib.ptr(oy),
+                                           _lib.ptr(ot, C.c_int64)))
+            rx, ry, rt_ = ref_fn(x, y, t, seed)
+            assert np.array_equal(ox, rx) and np.array_equal(oy, ry) and np.array_equal(ot, rt_)
+
+
+@pytest.mark.parametrize("method", [1, 2])
+def test_run_simulations_null_models_vs_port(api, port, method):
+    est, geom, sim = api["est"], api["geom"], api["sim"]
+    g = golden("sample_result.npz")
+    x, y, t, ring = g["x"], g["y"], g["t"], g["ring"]
+    region = geom.StudyRegion(ring, 0, 365)
+    grid = est.DistanceGrid(g["s"], g["tv"])
+    surfs = sim.run_simulations((x, y, t), region, grid, sim.Method(method), 4, 9)
+    gen = port.generate_bootstrap if method == 1 else port.generate_permutation
+    for r in range(4):
+        sx, sy, st = gen(x, y, t, 9 + r)
+        want = port.estimate(sx, sy, st, ring, 0, 365, g["s"], g["tv"])["l"]
+        assert surfaces_close(surfs[r].values, want, TOL), r
+
+
+# ------------------------------------------------------------ edge cases
+def _compare(api, port, x, y, t, ring, p0, p1, s, tv, tol=TOL):
+    est, geom = api["est"], api["geom"]
+    region = geom.StudyRegion(ring, p0, p1)
+    grid = est.DistanceGrid(s, tv)
+    h = est.pair_histogram((x, y, t), region, grid)
+    o = port.pair_histogram(x, y, t, ring, p0, p1, np.asarray(s, float), np.asarray(tv, np.int64))
+    assert np.array_equal(h["counts"], o["counts"])
+    assert rel_err(h["hist"], o["hist"]) <= 1e-13
+    k = est.estimate_surface((x, y, t), region, grid)
+    ko = port.finalize(o["hist"], len(x), port.area(ring), p1 - p0)
+    assert surfaces_close(k.values, ko, tol)
+    return h
+
+
+def test_coincident_points_pair_with_weight_one(api, port):
+    """Self-exclusion is by index; coincident distinct points pair at d = 0
+    with omega = 1 (edge_correction.cpp:47)."""
+    ring, p0, p1 = square(100.0)
+    x = np.array([0.0, 0.0, 50.0, 50.0, 50.0, 100.0])
+    y = np.array([0.0, 0.0, 50.0, 50.0, 50.0, 100.0])
+    t = np.array([0, 0, 10, 10, 12, 100])
+    h = _compare(api, port, x, y, t, ring, p0, p1, [1.0, 10.0, 200.0], [1, 5, 100])
+    assert h["counts"][0, 0] == 4  # (0,0)x2 at u=0 and the two (50,50) points at u=0
+    assert h["counts"][0, 1] == 4  # (50,50) pairs at u=2
+
+
+def test_points_on_boundary_corners_and_period_ends(api, port):
+    ring, p0, p1 = square(1000.0, 0, 1000)
+    rng = np.random.default_rng(1)
+    n = 400
+    x = rng.uniform(0, 1000, n)
+    y = rng.uniform(0, 1000, n)
+    t = rng.integers(0, 1000, n, endpoint=True)
+    x[:40] = 0.0          # left edge
+    y[40:80] = 1000.0     # top edge
+    x[80:90] = 1000.0; y[80:90] = 0.0  # corner
+    t[90:120] = 0         # period start
+    t[120:150] = 1000     # period end
+    _compare(api, port, x, y, t, ring, p0, p1, [50.0, 125.0, 250.0, 400.0], [10, 100, 300])
+
+
+def test_thresholds_inclusive_exact_distances(api, port):
+    """d == s_k and u == t_l land in bin k / l (lower_bound, inclusive)."""
+    ring, p0, p1 = square(1000.0, 0, 100)
+    x = np.array([100.0, 130.0, 100.0, 100.0, 500.0])
+    y = np.array([100.0, 140.0, 150.0, 100.0, 500.0])  # distances 50 (3-4-5), 50, 0
+    t = np.array([10, 20, 30, 10, 50])
+    h = _compare(api, port, x, y, t, ring, p0, p1, [25.0, 50.0], [10, 20])
+    assert h["counts"].sum() > 0
+
+
+def test_single_cell_all_pairs(api, port):
+    """C3-like: s_max and t_max exceed the box, so every pair is in threshold."""
+    ring, p0, p1 = square(1000.0, 0, 8_640_000)
+    from oracle import port as orc
+
+    x, y, t = orc.generate_cstr(3000, ring, p0, p1, 3)
+    s = [93.75 * (k + 1) for k in range(16)]
+    tv = [540_000 * (k + 1) for k in range(16)]
+    h = _compare(api, port, x, y, t, ring, p0, p1, s, tv)
+    assert int(h["counts"].sum()) == 3000 * 2999
+
+
+def test_one_bin_grid_and_tiny_n(api, port):
+    ring, p0, p1 = square(10.0, 0, 10)
+    _compare(api, port, np.array([1.0, 2.0]), np.array([1.0, 2.0]), np.array([0, 10]), ring, p0,
+             p1, [20.0], [20])
+
+
+def test_star_polygons_bitmask_and_fallback_paths(api, port):
+    """14- and 64-vertex rings: the >32-vertex ring takes the general path,
+    and circles with > 8 crossings take the fallback."""
+    g = golden("weights.npz")
+    for k in (1, 3):  # 12-vertex star, 64-vertex star
+        ring = g[f"{k}_ring"]
+        cx, cy = g[f"{k}_cx"][:300], g[f"{k}_cy"][:300]
+        rng = np.random.default_rng(k)
+        t = rng.integers(0, 100, len(cx))
+        span = float(np.ptp(ring[:, 0]))
+        s = [span * f for f in (0.1, 0.3, 0.6, 1.0)]
+        _compare(api, port, cx, cy, t, ring, 0, 100, s, [10, 50, 100])
+
+
+def test_deterministic_across_runs(api):
+    est, geom, sim = api["est"], api["geom"], api["sim"]
+    ring, p0, p1 = square(5000.0, 0, 1_000_000)
+    region = geom.StudyRegion(ring, p0, p1)
+    grid = est.DistanceGrid([100.0 * (k + 1) for k in range(10)], [50_000 * (k + 1) for k in range(8)])
+    pts = sim.generate_cstr(20_000, region, 5)
+    a = est.pair_histogram(pts, region, grid)
+    b = est.pair_histogram(pts, region, grid)
+    assert np.array_equal(a["sum_hi"], b["sum_hi"]) and np.array_equal(a["sum_lo"], b["sum_lo"])
+    k1 = est.estimate_surface(pts, region, grid).values
+    k2 = est.estimate_surface(pts, region, grid).values
+    assert np.array_equal(k1, k2)
+
+
+# ------------------------------------------------------------ multi-rank
+def test_run_job_ranks_combine_bit_identically(api):
+    """rt.run_job's multi-process path (stk_run_job_shard per rank + exact
+    SUM / MAX / MIN) emulated sequentially: identical K at any world size."""
+    import ctypes as C
+
+    from paper_1912_04753_b200 import _lib
+
+    est, geom, rt = api["est"], api["geom"], api["rt"]
+    dev = api["dev"]
+    g = golden("sample_result.npz")
+    region = geom.StudyRegion(g["ring"], 0, 365)
+    grid = est.DistanceGrid(g["s"], g["tv"])
+    x, y, t = (np.ascontiguousarray(a) for a in (g["x"], g["y"], g["t"].astype(np.int64)))
+    dev.configure(region, grid)
+    shape = g["k"].shape
+    single = rt.run_job((x, y, t), region, rt.JobSpec(grid=grid, sims=19, seed=42))
+    for world in (2, 4):
+        cnt = np.zeros(shape, object); tot = np.zeros(shape, object)
+        up = np.full(shape, -np.inf); lo = np.full(shape, np.inf)
+        for rank in range(world):
+            r0, r1 = rt.shard_range(19, rank, world)
+            c_ = np.zeros(shape, np.uint64); hi = np.zeros(shape, np.uint64)
+            lw = np.zeros(shape, np.uint64)
+            u_ = np.full(shape, -np.inf); l_ = np.full(shape, np.inf)
+            tel = _lib.StkTelemetry()
+            dev.check(dev.lib.stk_run_job_shard(
+                dev.h, _lib.ptr(x), _lib.ptr(y), _lib.ptr(t, C.c_int64), len(x), rank, world,
+                r0, r1, 42, 0, _lib.ptr(c_, C.c_uint64), _lib.ptr(hi, C.c_uint64),
+                _lib.ptr(lw, C.c_uint64), _lib.ptr(u_), _lib.ptr(l_), C.byref(tel)))
+            cnt += c_.astype(object)
+            tot += hi.astype(object) * (1 << 64) + lw.astype(object)
+            up = np.maximum(up, u_); lo = np.minimum(lo, l_)
+        hi = np.array([[int(v) >> 64 for v in row] for row in tot], np.uint64)
+        lw = np.array([[int(v) & ((1 << 64) - 1) for v in row] for row in tot], np.uint64)
+        k, l = est.finalize_exact(hi, lw, len(x), region, grid)
+        assert np.array_equal(k.values, single.k_hat.values)
+        assert np.array_equal(l.values, single.l_hat.values)
+        assert np.array_equal(up, single.upper_l.values)
+        assert np.array_equal(lo, single.lower_l.values)
+        assert np.array_equal(cnt.astype(np.uint64),
+                              est.pair_histogram((x, y, t), region, grid)["counts"])
+
+
+# ------------------------------------------------------------ larger configs
+def test_c2_observed_thomas_full_size(api, port):
+    """configs[1]'s observed pattern (N ~ 100k Thomas clusters): counts bit-exact."""
+    from paper_1912_04753_b200 import configs
+
+    cfg = configs.CONFIGS["C2"]
+    s, tv = configs.grid_values(cfg)
+    x, y, t = configs.thomas(cfg)
+    _compare(api, port, x, y, t, cfg.ring(), 0, cfg.period_s, s, tv)
+
+
+@pytest.mark.slow
+def test_c3_full_size_properties(api):
+    """configs[2] at full N = 200,000 (4e10 pairs): every ordered pair in
+    threshold; K monotone; the top cell of K equals A*D/n^2 * sum of 1/w,
+    with total count N(N-1)."""
+    from paper_1912_04753_b200 import configs
+
+    est, geom, sim = api["est"], api["geom"], api["sim"]
+    cfg = configs.CONFIGS["C3"]
+    s, tv = configs.grid_values(cfg)
+    region = geom.StudyRegion(cfg.ring(), 0, cfg.period_s)
+    grid = est.DistanceGrid(s, tv)
+    pts = sim.generate_cstr(cfg.n, region, cfg.seed)
+    h = est.pair_histogram(pts, region, grid)
+    assert int(h["counts"].sum()) == cfg.n * (cfg.n - 1)
+    k = est.estimate_surface(pts, region, grid).values
+    assert np.all(np.diff(k, axis=0) >= 0) and np.all(np.diff(k, axis=1) >= 0)
+    scale = region.area() * region.duration() / float(cfg.n) ** 2
+    assert k[-1, -1] == pytest.approx(scale * h["hist"].sum(), rel=1e-12)
