@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <stdexcept>
@@ -99,6 +100,7 @@ struct stk_ctx {
   std::string err;
   int num_sms = 148;
   uint64_t mem_budget = 16ull << 30;
+  int stencil_radius = 2;  // preferred cell refinement (STK_STENCIL_RADIUS env overrides)
 
   // region (geom::StudyRegion)
   bool have_region = false;
@@ -184,38 +186,50 @@ BinView bin_view(stk_ctx* c) {
   return b;
 }
 
-// Uniform grid with cells >= (s_max, t_max): every in-threshold neighbour of a
-// point lies in the 3x3x3 block of cells around it.
+// Uniform grid with cells >= (s_max / R, t_max / R): every in-threshold
+// neighbour of a point lies within R cells in each dimension.  R = 2 (finer
+// cells: the half-stencil holds ~0.56x the candidates of R = 1) when the
+// pattern is dense enough to fill the cells, else R = 1.
 GridGeom make_grid_geom(stk_ctx* c, uint64_t n) {
   GridGeom g;
   const double smax = c->s_values.back();
   const int64_t tmax = c->t_values.back();
-  double w = smax * (1.0 + 1e-6);
-  int64_t tw = std::max<int64_t>(tmax, 1);
   const double ex = c->xmax - c->xmin, ey = c->ymax - c->ymin;
   const uint64_t cap = std::max<uint64_t>(4096, std::min<uint64_t>(2 * n, 1ull << 26));
   auto ncell = [](double extent, double width) {
     const double k = std::floor(extent / width) + 1.0;
     return (int64_t)std::min(k, 1e9);
   };
-  int64_t nx, ny, nt;
-  for (;;) {
-    nx = ncell(ex, w);
-    ny = ncell(ey, w);
-    nt = (c->p1 - c->p0) / tw + 1;
-    if ((double)nx * (double)ny * (double)nt <= (double)cap) break;
-    if (nx * ny >= nt) w *= 1.5; else tw = tw + tw / 2 + 1;
+  for (int R = c->stencil_radius; R >= 1; --R) {
+    // w * R = s_max * (1 + 1e-6): a true |dx| <= s_max (the computed d <= s_max
+    // implies it up to 1e-16) spans at most R cells even after FP rounding of
+    // the cell index; integer time cells of width ceil(t_max / R) are exact.
+    double w = smax * (1.0 + 1e-6) / R;
+    int64_t tw = std::max<int64_t>((tmax + R - 1) / R, 1);
+    int64_t nx, ny, nt;
+    for (;;) {
+      nx = ncell(ex, w);
+      ny = ncell(ey, w);
+      nt = (c->p1 - c->p0) / tw + 1;
+      if ((double)nx * (double)ny * (double)nt <= (double)cap) break;
+      if (nx * ny >= nt) w *= 1.5; else tw = tw + tw / 2 + 1;
+    }
+    const double per_cell = (double)n / ((double)nx * ny * nt);
+    if (R > 1 && per_cell < 8.0) continue;  // too sparse for finer cells
+    g.x0 = c->xmin;
+    g.y0 = c->ymin;
+    g.inv_w = 1.0 / w;
+    g.t0 = c->p0;
+    g.tw = tw;
+    g.inv_tw = 1.0 / (double)tw;
+    g.nx = (int32_t)nx;
+    g.ny = (int32_t)ny;
+    g.nt = (int32_t)nt;
+    g.cells = (uint32_t)(nx * ny * nt);
+    g.rs = R;
+    g.rt = R;
+    break;
   }
-  g.x0 = c->xmin;
-  g.y0 = c->ymin;
-  g.inv_w = 1.0 / w;
-  g.t0 = c->p0;
-  g.tw = tw;
-  g.inv_tw = 1.0 / (double)tw;
-  g.nx = (int32_t)nx;
-  g.ny = (int32_t)ny;
-  g.nt = (int32_t)nt;
-  g.cells = (uint32_t)(nx * ny * nt);
   return g;
 }
 
@@ -474,6 +488,7 @@ void fill_telemetry(stk_ctx* c, Timers& tm, stk_telemetry* tel, uint64_t pattern
   unsigned long long st[4] = {0, 0, 0, 0};
   CK(cudaMemcpyAsync(st, c->stats.p, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  if (st[3] & 2) throw CudaFail("internal error: arc ring overflow in the pair kernel");
   if (st[3]) throw Unsupported("more than 64 circle/boundary crossings in one edge weight");
   if (!tel) return;
   tel->in_threshold_pairs += st[0];
@@ -678,6 +693,7 @@ int stk_create(stk_ctx** out, int device) {
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    if (const char* r = std::getenv("STK_STENCIL_RADIUS")) c->stencil_radius = std::max(1, std::min(2, std::atoi(r)));
     c->stats.ensure(4);
   } catch (const std::exception& e) {
     delete c;

@@ -434,7 +434,8 @@ struct PairSmem {
   int64_t* tt;              // [warps][32] neighbour t
   double* tsq;              // [warps][32] neighbour safe q
   int64_t* tvt;             // [warps][32] neighbour temporal threshold
-  uint32_t* tix;            // [warps][32] neighbour input index
+  uint32_t* tix;            // [warps][32] input index
+  uint32_t* tpos;           // [warps][32] sorted position
   double* angs;             // [warps][kAngleSlots][32] per-lane crossing-angle scratch
   unsigned long long* lo;   // [bins] arc-path fixed-point sums (low 64)
   double* Q;                // [cs]
@@ -460,6 +461,7 @@ __host__ __device__ inline size_t pair_smem_layout(uint32_t bins, uint32_t cs, u
   take(sizeof(double) * kPairWarps * 32);
   take(sizeof(int64_t) * kPairWarps * 32);
   take(sizeof(uint32_t) * kPairWarps * 32);
+  take(sizeof(uint32_t) * kPairWarps * 32);
   take(sizeof(double) * kPairWarps * kAngleSlots * 32);
   take(sizeof(unsigned long long) * bins);
   take(sizeof(double) * cs);
@@ -473,13 +475,13 @@ __host__ __device__ inline size_t pair_smem_layout(uint32_t bins, uint32_t cs, u
 }
 
 size_t pair_kernel_smem(uint32_t bins, uint32_t cs, uint32_t ct) {
-  size_t off[14];
+  size_t off[15];
   return pair_smem_layout(bins, cs, ct, off);
 }
 
 __device__ __forceinline__ PairSmem carve(unsigned char* raw, uint32_t bins, uint32_t cs,
                                           uint32_t ct) {
-  size_t o[14];
+  size_t o[15];
   pair_smem_layout(bins, cs, ct, o);
   PairSmem S;
   S.tile = (double2*)(raw + o[0]);
@@ -487,15 +489,16 @@ __device__ __forceinline__ PairSmem carve(unsigned char* raw, uint32_t bins, uin
   S.tsq = (double*)(raw + o[2]);
   S.tvt = (int64_t*)(raw + o[3]);
   S.tix = (uint32_t*)(raw + o[4]);
-  S.angs = (double*)(raw + o[5]);
-  S.lo = (unsigned long long*)(raw + o[6]);
-  S.Q = (double*)(raw + o[7]);
-  S.T = (int64_t*)(raw + o[8]);
-  S.cnt = (uint32_t*)(raw + o[9]);
-  S.half = (uint32_t*)(raw + o[10]);
-  S.hi = (uint32_t*)(raw + o[11]);
-  S.stab = (uint16_t*)(raw + o[12]);
-  S.ttab = (uint16_t*)(raw + o[13]);
+  S.tpos = (uint32_t*)(raw + o[5]);
+  S.angs = (double*)(raw + o[6]);
+  S.lo = (unsigned long long*)(raw + o[7]);
+  S.Q = (double*)(raw + o[8]);
+  S.T = (int64_t*)(raw + o[9]);
+  S.cnt = (uint32_t*)(raw + o[10]);
+  S.half = (uint32_t*)(raw + o[11]);
+  S.hi = (uint32_t*)(raw + o[12]);
+  S.stab = (uint16_t*)(raw + o[13]);
+  S.ttab = (uint16_t*)(raw + o[14]);
   return S;
 }
 
@@ -503,7 +506,10 @@ __device__ __forceinline__ PairSmem carve(unsigned char* raw, uint32_t bins, uin
 // accumulated into the CTA histogram as 128-bit fixed point of (1/(omega*v) - 1).
 // Entries live in the warp's ring (global, L1/L2-resident): {center sorted
 // position, bin | (v == 1/2) << 31, q = d^2 as two words}.
-__device__ __forceinline__ void drain_arcs(int count, int lane, const uint4* ring_q,
+#ifndef STK_DRAIN_INLINE
+#define STK_DRAIN_INLINE __forceinline__
+#endif
+__device__ STK_DRAIN_INLINE void drain_arcs(int count, int lane, const uint4* ring_q,
                                            uint32_t head, double* angs, const double* xs,
                                            const double* ys, const PairSmem& S,
                                            const RegionView& reg, int* overflow) {
@@ -562,6 +568,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   double* tsq = S.tsq + w * 32;
   int64_t* tvt = S.tvt + w * 32;
   uint32_t* tix = S.tix + w * 32;
+  uint32_t* tpos = S.tpos + w * 32;
   uint4* arcq = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * kArcRing;
   double* angs = S.angs + w * kAngleSlots * 32;
   int overflow = 0;
@@ -612,123 +619,160 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       const uint2 item = items[i0 + it];
       const uint32_t cell = item.x, start = item.y;
       const uint32_t nc = min((uint32_t)kItemCenters, clist[cell + 1] - start);
-      const bool valid = lane < (int)nc;
-      uint32_t mypos = 0, myidx = 0;
-      double cx = 0.0, cy = 0.0, sq_i = 0.0;
-      int64_t ctm = 0, vt_i = 0;
-      if (valid) {
-        mypos = sel_p ? cpos[start + lane] : start + lane;
-        cx = xs[mypos];
-        cy = ys[mypos];
-        ctm = ts[mypos];
-        sq_i = psq[mypos];
-        vt_i = pvt[mypos];
-        myidx = pix[mypos];
+      // stage the item's centers (<= 32) in shared memory: the inner loop
+      // broadcasts one center to the 32 neighbour lanes
+      __syncwarp();
+      if (lane < (int)nc) {
+        const uint32_t pos = sel_p ? cpos[start + lane] : start + lane;
+        tile[lane] = make_double2(xs[pos], ys[pos]);
+        tt[lane] = ts[pos];
+        tsq[lane] = psq[pos];
+        tvt[lane] = pvt[pos];
+        tix[lane] = pix[pos];
+        tpos[lane] = pos;
       }
-      const unsigned nvalid = __popc(__ballot_sync(FULL_MASK, valid));
+      __syncwarp();
+      const uint32_t first_pos = sel_p ? 0u : start;  // lowest center position (non-selected)
       const int kx = (int)(cell % (uint32_t)G.nx);
       const uint32_t rest = cell / (uint32_t)G.nx;
       const int ky = (int)(rest % (uint32_t)G.ny);
       const int kt = (int)(rest / (uint32_t)G.ny);
       const uint32_t own_end = cstart[cell + 1];
-      uint32_t qh = 0, qt = 0;  // ring head / tail (monotone)
-      uint32_t n_in = 0, n_exact = 0;
-      unsigned long long n_cand = 0;
-      // forward half-stencil as 5 contiguous ranges of the sorted array
-      for (int r = 0; r < 5; ++r) {
-        uint32_t rb, re;
-        if (r == 0) {  // own cell (+ the cell at kx+1, contiguous)
-          rb = sel_p ? cstart[cell] : start + 1;
-          re = cstart[cell + (kx + 1 < G.nx ? 2 : 1)];
+      const int RS = G.rs, RT = G.rt;
+      // forward half-stencil rows (lane r holds row r): layer dt = 0 rows
+      // dy = 0..RS, layers dt = 1..RT rows dy = -RS..RS; row dy = 0 of layer 0
+      // starts at the own cell (ordered rule) and runs to dx = +RS.  Each row
+      // is one contiguous range [rb, re) of the sorted array.
+      const int nrows = (RS + 1) + RT * (2 * RS + 1);
+      uint32_t my_rb = 0, my_re = 0;
+      if (lane < nrows) {
+        int dt, dy;
+        if (lane <= RS) {
+          dt = 0;
+          dy = lane;
         } else {
-          const int yk = r == 1 ? ky + 1 : ky + (r - 3);
-          const int tk = r == 1 ? kt : kt + 1;
-          if (yk < 0 || yk >= G.ny || tk >= G.nt) continue;
-          const uint32_t row = ((uint32_t)tk * G.ny + yk) * G.nx;
-          rb = cstart[row + max(kx - 1, 0)];
-          re = cstart[row + min(kx + 1, G.nx - 1) + 1];
+          dt = 1 + (lane - RS - 1) / (2 * RS + 1);
+          dy = (lane - RS - 1) % (2 * RS + 1) - RS;
         }
-        for (uint32_t j0 = rb; j0 < re; j0 += 32) {
-          const uint32_t j = j0 + lane;
-          if (j < re) {
-            tile[lane] = make_double2(xs[j], ys[j]);
-            tt[lane] = ts[j];
-            tsq[lane] = psq[j];
-            tvt[lane] = pvt[j];
-            tix[lane] = pix[j];
-          }
-          __syncwarp();
-          const int m = (int)min(32u, re - j0);
-          n_cand += (unsigned long long)m;
-          for (int kc = 0; kc < m; kc += kArcChunk) {
-            const int kend = min(kc + kArcChunk, m);
-            for (int k = kc; k < kend; ++k) {
-              const double2 nb = tile[k];
-              const int64_t nt = tt[k];
-              const double dx = cx - nb.x, dy = cy - nb.y;
-              const double q = dx * dx + dy * dy;  // spatial_distance^2, no FMA
-              int64_t du = ctm - nt;
-              du = du < 0 ? -du : du;              // temporal_distance
-              const uint32_t jp = j0 + k;
-              const bool owner = jp >= own_end || (sel_p ? tix[k] > myidx : jp > mypos);
-              const bool in = valid && owner && q <= Qmax && du <= Tmax;
-              bool arc_i = false, arc_j = false;
-              uint32_t bin = 0;
-              bool half_i = false, half_j = false;
-              if (in) {
-                // bin_pair: first s_k >= d <=> first Q_k >= q; first t_l >= u
-                int bq = (int)(sqrtf((float)q) * s_inv_bw);
-                bq = min(bq, kBucketTable - 1);
-                uint32_t sb = S.stab[bq];
-                while (q > S.Q[sb]) ++sb;
-                int bt = (int)((float)du * t_inv_bw);
-                bt = min(bt, kBucketTable - 1);
-                uint32_t tb = S.ttab[bt];
-                while (du > S.T[tb]) ++tb;
-                bin = sb * ct + tb;
-                atomicAdd(&S.cnt[bin], 2u);
-                half_i = du > vt_i;
-                half_j = du > tvt[k];
-                arc_i = q >= sq_i;
-                arc_j = q >= tsq[k];
-                const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
-                if (h) atomicAdd(&S.half[bin], h);
-                n_in += 2;
-              }
-              const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
-              const unsigned mj = __ballot_sync(FULL_MASK, arc_j);
-              if (mi | mj) {
-                const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
-                if (arc_i)
-                  arcq[(qt + __popc(mi & lanemask_lt)) & (kArcRing - 1)] =
-                      make_uint4(mypos, bin | (half_i ? 0x80000000u : 0u), qlo, qhi);
-                qt += __popc(mi);
-                if (arc_j)
-                  arcq[(qt + __popc(mj & lanemask_lt)) & (kArcRing - 1)] =
-                      make_uint4(jp, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
-                qt += __popc(mj);
-                n_exact += (uint32_t)arc_i + (uint32_t)arc_j;
-              }
-            }
-            // drain outside the candidate loop: pending < 32 + kArcChunk * 64 <= ring size
-            while (qt - qh >= 32) {
-              __syncwarp();
-              drain_arcs(32, lane, arcq, qh, angs, xs, ys, S, A.reg, &overflow);
-              qh += 32;
-            }
-          }
-          __syncwarp();
+        const int tk = kt + dt, yk = ky + dy;
+        if (tk < G.nt && yk >= 0 && yk < G.ny) {
+          const uint32_t row = ((uint32_t)tk * G.ny + yk) * G.nx;
+          my_rb = (dt == 0 && dy == 0) ? (sel_p ? cstart[cell] : first_pos + 1)
+                                        : cstart[row + max(kx - RS, 0)];
+          my_re = cstart[row + min(kx + RS, G.nx - 1) + 1];
+          if (my_rb > my_re) my_rb = my_re;
         }
       }
-      if (qt != qh) {
-        __syncwarp();
-        drain_arcs((int)(qt - qh), lane, arcq, qh, angs, xs, ys, S, A.reg, &overflow);
-        qh = qt;
+      const unsigned nonempty = __ballot_sync(FULL_MASK, my_rb < my_re);
+      uint32_t qh = 0, qt = 0;  // arc ring head / tail (monotone)
+      uint32_t n_in = 0, n_exact = 0;
+      unsigned long long n_cand = 0;
+      // flat walk over (row, tile, center chunk); one inline copy of the drain
+      unsigned rows_left = nonempty;
+      int r = rows_left ? __ffs(rows_left) - 1 : 32;
+      uint32_t j0 = __shfl_sync(FULL_MASK, my_rb, r & 31);
+      uint32_t re = __shfl_sync(FULL_MASK, my_re, r & 31);
+      int kc = 0;
+      double nx_ = 0.0, ny_ = 0.0, nsq = 0.0;
+      int64_t nt = 0, nvt = 0;
+      uint32_t nix = 0, jp = 0;
+      bool has = false, same_cell = false;
+      for (;;) {
+        const bool done = rows_left == 0;
+        // the single drain site, ahead of new candidates so the ring never
+        // holds more than 31 + kArcChunk * 64 entries: full batches while
+        // any are pending, and the remainder at the end
+        const uint32_t pending = qt - qh;
+        if (pending > (uint32_t)kArcRing) overflow |= 2;  // must never happen: reported as an error
+        if (pending >= 32 || (done && pending > 0)) {
+          const int cnt_ = (int)min(pending, 32u);
+          __syncwarp();
+          drain_arcs(cnt_, lane, arcq, qh, angs, xs, ys, S, A.reg, &overflow);
+          qh += (uint32_t)cnt_;
+          continue;
+        }
+        if (done) break;
+        {
+          if (kc == 0) {  // new tile: this lane's neighbour into registers
+            jp = j0 + lane;
+            has = jp < re;
+            if (has) {
+              nx_ = xs[jp];
+              ny_ = ys[jp];
+              nt = ts[jp];
+              nsq = psq[jp];
+              nvt = pvt[jp];
+              nix = pix[jp];
+            }
+            same_cell = r == 0 && jp < own_end;
+            n_cand += (unsigned long long)min(32u, re - j0) * nc;
+          }
+          const int kend = min(kc + kArcChunk, (int)nc);
+          for (int k = kc; k < kend; ++k) {
+            const double2 cxy = tile[k];  // center k (broadcast)
+            const int64_t ctm = tt[k];
+            const double dx = cxy.x - nx_, dy2 = cxy.y - ny_;
+            const double q = dx * dx + dy2 * dy2;  // spatial_distance^2, no FMA
+            int64_t du = ctm - nt;
+            du = du < 0 ? -du : du;                // temporal_distance
+            const bool owner = !same_cell || (sel_p ? nix > tix[k] : jp > tpos[k]);
+            const bool in = has && owner && q <= Qmax && du <= Tmax;
+            bool arc_i = false, arc_j = false;
+            uint32_t bin = 0;
+            bool half_i = false, half_j = false;
+            if (in) {
+              // bin_pair: first s_k >= d <=> first Q_k >= q; first t_l >= u
+              int bq = (int)(sqrtf((float)q) * s_inv_bw);
+              bq = min(bq, kBucketTable - 1);
+              uint32_t sb = S.stab[bq];
+              while (q > S.Q[sb]) ++sb;
+              int bt = (int)((float)du * t_inv_bw);
+              bt = min(bt, kBucketTable - 1);
+              uint32_t tb = S.ttab[bt];
+              while (du > S.T[tb]) ++tb;
+              bin = sb * ct + tb;
+              atomicAdd(&S.cnt[bin], 2u);
+              half_i = du > tvt[k];
+              half_j = du > nvt;
+              arc_i = q >= tsq[k];
+              arc_j = q >= nsq;
+              const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
+              if (h) atomicAdd(&S.half[bin], h);
+              n_in += 2;
+            }
+            const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
+            const unsigned mj = __ballot_sync(FULL_MASK, arc_j);
+            if (mi | mj) {
+              const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
+              if (arc_i)
+                arcq[(qt + __popc(mi & lanemask_lt)) & (kArcRing - 1)] =
+                    make_uint4(tpos[k], bin | (half_i ? 0x80000000u : 0u), qlo, qhi);
+              qt += __popc(mi);
+              if (arc_j)
+                arcq[(qt + __popc(mj & lanemask_lt)) & (kArcRing - 1)] =
+                    make_uint4(jp, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
+              qt += __popc(mj);
+              n_exact += (uint32_t)arc_i + (uint32_t)arc_j;
+            }
+          }
+          // advance: next chunk, next tile, next non-empty row
+          kc = kend;
+          if (kc >= (int)nc) {
+            kc = 0;
+            j0 += 32;
+            if (j0 >= re) {
+              rows_left &= rows_left - 1;
+              r = rows_left ? __ffs(rows_left) - 1 : 32;
+              j0 = __shfl_sync(FULL_MASK, my_rb, r & 31);
+              re = __shfl_sync(FULL_MASK, my_re, r & 31);
+            }
+          }
+        }
       }
       __syncwarp();
       tot_in += n_in;
       tot_exact += n_exact;
-      if (lane == 0) tot_cand += n_cand * nvalid;
+      if (lane == 0) tot_cand += n_cand;
     }
     __syncthreads();
     // flush the CTA histogram of pattern p (exact integer adds)
@@ -756,7 +800,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     atomicAdd(&B.stats[1], tot_cand);
     atomicAdd(&B.stats[2], tot_exact);
   }
-  if (overflow) atomicOr(&B.stats[3], 1ULL);
+  if (overflow) atomicOr(&B.stats[3], (unsigned long long)overflow);
 }
 
 // ============================================================ K5 finalize

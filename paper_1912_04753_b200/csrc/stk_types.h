@@ -50,6 +50,7 @@ struct GridGeom {
   double inv_tw;
   int32_t nx, ny, nt;
   uint32_t cells;  // nx*ny*nt
+  int32_t rs, rt;  // stencil radius in cells (space, time): cell >= s_max/rs, >= t_max/rt
 };
 
 // One batch of R point patterns of n points each, laid out [R][n].

@@ -20,7 +20,7 @@ def region(path, ln):
         line = src[k]
         if "drain_arcs(" in line and "void" in line:
             return "arc drain"
-        if "for (int k = kc; k < kend; ++k)" in line or "for (int k = 0; k < m; ++k)" in line:
+        if "for (int k = kc; k < kend; ++k)" in line or "for (int k = 0; k < m; ++k)" in line or "for (uint32_t j0 = rb; j0 < re; j0 += 32)" in line:
             return "candidate/bin loop"
         if "flush the CTA histogram" in line:
             return "flush"

@@ -177,6 +177,19 @@ def test_single_cell_all_pairs(api, port):
     assert int(h["counts"].sum()) == 3000 * 2999
 
 
+def test_dense_arc_pairs_with_duplicates(api, port):
+    """Every pair near a corner, many exact duplicates (bootstrap-like): the
+    densest arc-path load per warp (stresses the per-warp arc ring)."""
+    ring, p0, p1 = square(1000.0, 0, 100)
+    rng = np.random.default_rng(7)
+    base_x = rng.uniform(0, 60, 200)
+    base_y = rng.uniform(0, 60, 200)
+    base_t = rng.integers(0, 100, 200, endpoint=True)
+    pick = rng.integers(0, 200, 2500)
+    x, y, t = base_x[pick], base_y[pick], base_t[pick]
+    _compare(api, port, x, y, t, ring, p0, p1, [10.0, 40.0, 90.0], [20, 60, 100])
+
+
 def test_one_bin_grid_and_tiny_n(api, port):
     ring, p0, p1 = square(10.0, 0, 10)
     _compare(api, port, np.array([1.0, 2.0]), np.array([1.0, 2.0]), np.array([0, 10]), ring, p0,
