@@ -125,9 +125,10 @@ struct stk_ctx {
   DevBuf<uint16_t> d_stab, d_ttab;
 
   // batch buffers (grow-only)
-  DevBuf<double> x, y, xs, ys;
-  DevBuf<int64_t> t, ts, pvt;
-  DevBuf<double> psq;
+  DevBuf<double> x, y;
+  DevBuf<int64_t> t;
+  DevBuf<double2> pxy;
+  DevBuf<unsigned char> pmeta;
   DevBuf<uint32_t> idx, key, rank, cell_count, cell_start, item_start, task_start, task_counter;
   DevBuf<uint2> items;
   DevBuf<uint32_t> sel_start, center_pos;
@@ -168,6 +169,12 @@ RegionView region_view(stk_ctx* c) {
   r.ymax = c->ymax;
   r.maxabs = c->maxabs;
   r.rect = c->fast_rect ? 1 : 0;
+  // Largest coordinate magnitude a probe can have: the ring's plus the largest
+  // distance (a probe is at distance d <= s_max from a center in the region).
+  const double smax = c->s_values.empty() ? 0.0 : c->s_values.back();
+  const double S = std::max(1.0, c->maxabs + smax);
+  const double min_edge = std::max(std::min(c->xmax - c->xmin, c->ymax - c->ymin), 1e-300);
+  r.box_m = 4e-12 * S * std::max(1.0, S / min_edge);
   return r;
 }
 
@@ -247,7 +254,7 @@ Plan make_plan(stk_ctx* c, uint64_t n, uint64_t patterns) {
   P.G = make_grid_geom(c, n);
   P.bins = (uint32_t)(c->s_values.size() * c->t_values.size());
   P.max_items = (uint32_t)((n + kItemCenters - 1) / kItemCenters + P.G.cells);
-  const uint64_t per = n * (8 * 3 + 8 * 5 + 4 * 4) + (uint64_t)(P.G.cells + 1) * 4 * 3 +
+  const uint64_t per = n * (8 * 3 + 16 + 24 + 4 * 4) + (uint64_t)(P.G.cells + 1) * 4 * 3 +
                        (uint64_t)P.max_items * 8 + (uint64_t)P.bins * 8 * 6 + 64;
   uint64_t R = std::max<uint64_t>(1, c->mem_budget / per);
   R = std::min<uint64_t>(R, std::max<uint64_t>(patterns, 1));
@@ -261,12 +268,10 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   c->x.ensure(R * n);
   c->y.ensure(R * n);
   c->t.ensure(R * n);
-  c->xs.ensure(R * n);
-  c->ys.ensure(R * n);
-  c->ts.ensure(R * n);
+  const int wide = (c->p1 - c->p0) >= 0x7fffffffLL ? 1 : 0;
+  c->pxy.ensure(R * n);
+  c->pmeta.ensure(R * n * (wide ? sizeof(PtMeta<int64_t>) : sizeof(PtMeta<int32_t>)));
   c->idx.ensure(R * n);
-  c->psq.ensure(R * n);
-  c->pvt.ensure(R * n);
   c->key.ensure(R * n);
   c->rank.ensure(R * n);
   c->cell_count.ensure(R * P.G.cells);
@@ -286,12 +291,10 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   B.x = c->x.p;
   B.y = c->y.p;
   B.t = c->t.p;
-  B.xs = c->xs.p;
-  B.ys = c->ys.p;
-  B.ts = c->ts.p;
+  B.pxy = c->pxy.p;
+  B.pmeta = c->pmeta.p;
+  B.wide = wide;
   B.idx = c->idx.p;
-  B.psq = c->psq.p;
-  B.pvt = c->pvt.p;
   B.key = c->key.p;
   B.rank = c->rank.p;
   B.cell_count = c->cell_count.p;
@@ -439,11 +442,9 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   items_kernel<<<gc, 256, 0, c->stream>>>(B, G, 0);
   CK(cudaGetLastError());
   ++c->launches;
-  const size_t smem = pair_kernel_smem(P.bins, (uint32_t)c->s_values.size(),
-                                       (uint32_t)c->t_values.size());
-  CK(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t smem = pair_kernel_smem(P.bins, B.wide);
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_kernel, kPairWarps * 32, smem));
+  CK(pair_kernel_prepare(B.wide, smem, &per_sm));
   if (per_sm < 1) throw Unsupported("distance grid too large for the pair kernel's shared histogram");
   tasks_kernel<<<1, 1, 0, c->stream>>>(B, G, (uint32_t)(c->num_sms * per_sm));
   CK(cudaGetLastError());
@@ -458,7 +459,7 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   const uint64_t ctas = (uint64_t)c->num_sms * per_sm;
   c->arcq.ensure(ctas * kPairWarps * kArcRing);
   A.B.arcq = c->arcq.p;
-  pair_kernel<<<(unsigned)ctas, kPairWarps * 32, smem, c->stream>>>(A);
+  pair_kernel_launch(B.wide, (unsigned)ctas, smem, c->stream, A);
   CK(cudaGetLastError());
   ++c->launches;
   CK(cudaEventRecord(e2, c->stream));
@@ -710,8 +711,8 @@ void stk_destroy(stk_ctx* c) {
   for (auto e : c->evpool) cudaEventDestroy(e);
   c->d_ring.release(); c->d_Q.release(); c->d_s.release(); c->d_T.release();
   c->d_stab.release(); c->d_ttab.release();
-  c->x.release(); c->y.release(); c->t.release(); c->xs.release(); c->ys.release();
-  c->ts.release(); c->idx.release(); c->psq.release(); c->pvt.release(); c->key.release(); c->rank.release();
+  c->x.release(); c->y.release(); c->t.release();
+  c->pxy.release(); c->pmeta.release(); c->idx.release(); c->key.release(); c->rank.release();
   c->cell_count.release(); c->cell_start.release(); c->item_start.release();
   c->task_start.release(); c->task_counter.release(); c->items.release();
   c->hist.release(); c->stats.release(); c->bad.release(); c->K.release(); c->L.release();
@@ -858,6 +859,8 @@ int stk_set_grid(stk_ctx* c, const double* s_values, uint32_t cs, const int64_t*
     c->have_grid = false;
     check_grid(s_values, cs, t_values, ct);
     if ((uint64_t)cs * ct > (1u << 20)) throw Unsupported("more than 2^20 grid cells");
+    if (cs > (uint32_t)kMaxAxis || ct > (uint32_t)kMaxAxis)
+      throw Unsupported("more than 512 distance thresholds per axis");
     c->s_values.assign(s_values, s_values + cs);
     c->t_values.assign(t_values, t_values + ct);
     c->Q.resize(cs);

@@ -160,6 +160,12 @@ __device__ __forceinline__ bool point_in_rect(double px, double py, const Region
     // strictly-inside parity is true; on_segment could only add true
     return true;
   }
+  // outside the box expanded by box_m no edge's on_segment can hold: its
+  // cross product exceeds 1e-12*scale^2 or the point leaves the segment's
+  // bounding box by more than 1e-12*scale (box_m bounds both, host-side)
+  if (px < R.xmin - R.box_m || px > R.xmax + R.box_m || py < R.ymin - R.box_m ||
+      py > R.ymax + R.box_m)
+    return false;
   const double smax = fmax(fmax(R.maxabs, 1.0), fmax(fabs(px), fabs(py)));
   const double bound = 1e-12 * smax * smax;
   for (uint32_t i = 0; i < 4; ++i) {
@@ -170,6 +176,28 @@ __device__ __forceinline__ bool point_in_rect(double px, double py, const Region
     if (on_segment(px, py, a.x, a.y, b.x, b.y)) return true;
   }
   return false;
+}
+
+// Certified point_in_rect of the probe c + d*(cos mid, sin mid) from an FP32
+// approximation: |__sincosf error| <= 2^-21.4 on [-pi, pi] plus the float
+// rounding of the reduced angle (<= 2^-24 * pi) bounds the approximate probe's
+// distance to the exact one by d * 2e-6 (+ rounding).  When the approximate
+// probe is farther than that from the decision boundaries (strict interior,
+// expanded exterior) the exact probe is on the same side; otherwise return -1
+// and the caller evaluates the exact probe.
+__device__ __forceinline__ int rect_probe_certified(double cx, double cy, double d, double mid,
+                                                    const RegionView& R) {
+  double m = mid;
+  if (m > 3.14159265358979323846) m -= kTwoPi;
+  if (m > 3.14159265358979323846) m -= kTwoPi;
+  float sf, cf;
+  __sincosf((float)m, &sf, &cf);
+  const double px = cx + d * (double)cf, py = cy + d * (double)sf;
+  const double e = d * 2e-6 + 1e-12 * (R.maxabs + d + 1.0);
+  if (px >= R.xmin + e && px < R.xmax - e && py >= R.ymin + e && py < R.ymax - e) return 1;
+  const double o = e + R.box_m;
+  if (px < R.xmin - o || px > R.xmax + o || py < R.ymin - o || py > R.ymax + o) return 0;
+  return -1;
 }
 
 #ifndef STK_WEIGHT_INLINE
@@ -269,11 +297,14 @@ __device__ STK_WEIGHT_INLINE double spatial_weight_buf(double cx, double cy, dou
     const double a0 = buf[a * stride];
     const double a1 = (a + 1 < u) ? buf[(a + 1) * stride] : first + kTwoPi;
     const double mid = 0.5 * (a0 + a1);
-    double sn, cs;
-    sincos(mid, &sn, &cs);
-    const double px = cx + d * cs, py = cy + d * sn;
-    const bool in = R.rect ? point_in_rect(px, py, R) : point_in_polygon(px, py, ring, nv, R.maxabs);
-    if (in) inside_span += a1 - a0;
+    int dec = R.rect ? rect_probe_certified(cx, cy, d, mid, R) : -1;
+    if (dec < 0) {
+      double sn, cs;
+      sincos(mid, &sn, &cs);
+      const double px = cx + d * cs, py = cy + d * sn;
+      dec = (R.rect ? point_in_rect(px, py, R) : point_in_polygon(px, py, ring, nv, R.maxabs)) ? 1 : 0;
+    }
+    if (dec) inside_span += a1 - a0;
   }
   return inside_span / kTwoPi;
 }

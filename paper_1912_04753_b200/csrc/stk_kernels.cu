@@ -337,6 +337,12 @@ __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* counts, uint
   }
 }
 
+// Largest float <= v (a conservative safe radius^2 stays conservative).
+__device__ __forceinline__ float float_floor(double v) {
+  float f = __double2float_rd(v);
+  return f;
+}
+
 __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first) {
   const int p = p_first + blockIdx.y;
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -346,15 +352,17 @@ __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first) {
   const uint64_t d = (uint64_t)p * B.n + pos;
   const double x = B.x[o], y = B.y[o];
   const int64_t t = B.t[o];
-  B.xs[d] = x;
-  B.ys[d] = y;
-  B.ts[d] = t;
+  B.pxy[d] = make_double2(x, y);
   B.idx[d] = (uint32_t)i;
-  // per-point memo replacing the reference's weight cache (weight_cache.hpp:39-129):
-  // radius^2 under which omega == 1 exactly, and the temporal-weight threshold
-  // v == 1 <=> u <= min(t - P0, P1 - t) (edge_correction.cpp:81-86)
-  B.psq[d] = safe_q(x, y, R.ring, R.nv, R.maxabs);
-  B.pvt[d] = min(t - R.p0, R.p1 - t);
+  const float sq = float_floor(safe_q(x, y, R.ring, R.nv, R.maxabs));
+  const int64_t vt = min(t - R.p0, R.p1 - t);
+  if (B.wide) {
+    PtMeta<int64_t> m{t - R.p0, vt, sq, (uint32_t)i};
+    reinterpret_cast<PtMeta<int64_t>*>(B.pmeta)[d] = m;
+  } else {
+    PtMeta<int32_t> m{(int32_t)(t - R.p0), (int32_t)vt, sq, (uint32_t)i};
+    reinterpret_cast<PtMeta<int32_t>*>(B.pmeta)[d] = m;
+  }
 }
 
 // Center selection (patterns [0, n_sel)): count selected centers per cell.
@@ -422,33 +430,31 @@ __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas) {
 
 // ============================================================ K2 pair kernel
 // Each unordered in-threshold pair {i, j} is found once: from the center in
-// the lower cell of the forward half-stencil (13 of the 26 neighbour cells),
-// or, inside one cell, from the lower sorted position (lower input index
-// when centers are selected, so shards partition the pairs whatever the
-// order inside a cell).  d, u and the bin are shared by both ordered pairs
-// (d_ij == d_ji bitwise: the squares of x-y and y-x are equal); each ordered
-// pair keeps its own center's weights (safe radius and temporal threshold
-// memoised per point at scatter time).
+// the lower cell of the forward half-stencil, or, inside one cell, from the
+// lower sorted position (lower input index when centers are selected, so
+// shards partition the pairs whatever the order inside a cell).  d, u and the
+// bin are shared by both ordered pairs (d_ij == d_ji bitwise: the squares of
+// x-y and y-x are equal); each ordered pair keeps its own center's weights.
+// Mapping: a warp item is <= 32 centers of one cell, staged in smem; lanes
+// hold 32 stencil neighbours in registers and loop over the centers.
+template <typename TT>
 struct PairSmem {
-  double2* tile;            // [warps][32] neighbour x, y
-  int64_t* tt;              // [warps][32] neighbour t
-  double* tsq;              // [warps][32] neighbour safe q
-  int64_t* tvt;             // [warps][32] neighbour temporal threshold
-  uint32_t* tix;            // [warps][32] input index
-  uint32_t* tpos;           // [warps][32] sorted position
-  double* angs;             // [warps][kAngleSlots][32] per-lane crossing-angle scratch
+  double2* cxy;             // [warps][32] item centers
+  PtMeta<TT>* cmeta;        // [warps][32]
+  uint32_t* cpos;           // [warps][32] sorted positions
+  double* angs;             // [warps][kAngleSlots][32] per-lane crossing scratch
+  double* Q;                // [kMaxAxis] squared-distance thresholds
+  TT* T;                    // [kMaxAxis] time thresholds (clamped to TT)
+  uint16_t* stab;           // [kBucketTable]
+  uint16_t* ttab;           // [kBucketTable]
   unsigned long long* lo;   // [bins] arc-path fixed-point sums (low 64)
-  double* Q;                // [cs]
-  int64_t* T;               // [ct]
   uint32_t* cnt;            // [bins]
   uint32_t* half;           // [bins]
   uint32_t* hi;             // [bins]
-  uint16_t* stab;           // [kBucketTable]
-  uint16_t* ttab;           // [kBucketTable]
 };
 
-__host__ __device__ inline size_t pair_smem_layout(uint32_t bins, uint32_t cs, uint32_t ct,
-                                                   size_t* off) {
+template <typename TT>
+__host__ __device__ inline size_t pair_smem_layout(uint32_t bins, size_t* off) {
   size_t b = 0;
   int k = 0;
   auto take = [&](size_t bytes) {
@@ -457,48 +463,42 @@ __host__ __device__ inline size_t pair_smem_layout(uint32_t bins, uint32_t cs, u
     b += bytes;
   };
   take(sizeof(double2) * kPairWarps * 32);
-  take(sizeof(int64_t) * kPairWarps * 32);
-  take(sizeof(double) * kPairWarps * 32);
-  take(sizeof(int64_t) * kPairWarps * 32);
-  take(sizeof(uint32_t) * kPairWarps * 32);
+  take(sizeof(PtMeta<TT>) * kPairWarps * 32);
   take(sizeof(uint32_t) * kPairWarps * 32);
   take(sizeof(double) * kPairWarps * kAngleSlots * 32);
+  take(sizeof(double) * kMaxAxis);
+  take(sizeof(TT) * kMaxAxis);
+  take(sizeof(uint16_t) * kBucketTable);
+  take(sizeof(uint16_t) * kBucketTable);
   take(sizeof(unsigned long long) * bins);
-  take(sizeof(double) * cs);
-  take(sizeof(int64_t) * ct);
   take(sizeof(uint32_t) * bins);
   take(sizeof(uint32_t) * bins);
   take(sizeof(uint32_t) * bins);
-  take(sizeof(uint16_t) * kBucketTable);
-  take(sizeof(uint16_t) * kBucketTable);
   return (b + 15) & ~size_t(15);
 }
 
-size_t pair_kernel_smem(uint32_t bins, uint32_t cs, uint32_t ct) {
-  size_t off[15];
-  return pair_smem_layout(bins, cs, ct, off);
+size_t pair_kernel_smem(uint32_t bins, int wide) {
+  size_t off[12];
+  return wide ? pair_smem_layout<int64_t>(bins, off) : pair_smem_layout<int32_t>(bins, off);
 }
 
-__device__ __forceinline__ PairSmem carve(unsigned char* raw, uint32_t bins, uint32_t cs,
-                                          uint32_t ct) {
-  size_t o[15];
-  pair_smem_layout(bins, cs, ct, o);
-  PairSmem S;
-  S.tile = (double2*)(raw + o[0]);
-  S.tt = (int64_t*)(raw + o[1]);
-  S.tsq = (double*)(raw + o[2]);
-  S.tvt = (int64_t*)(raw + o[3]);
-  S.tix = (uint32_t*)(raw + o[4]);
-  S.tpos = (uint32_t*)(raw + o[5]);
-  S.angs = (double*)(raw + o[6]);
-  S.lo = (unsigned long long*)(raw + o[7]);
-  S.Q = (double*)(raw + o[8]);
-  S.T = (int64_t*)(raw + o[9]);
-  S.cnt = (uint32_t*)(raw + o[10]);
-  S.half = (uint32_t*)(raw + o[11]);
-  S.hi = (uint32_t*)(raw + o[12]);
-  S.stab = (uint16_t*)(raw + o[13]);
-  S.ttab = (uint16_t*)(raw + o[14]);
+template <typename TT>
+__device__ __forceinline__ PairSmem<TT> carve(unsigned char* raw, uint32_t bins) {
+  size_t o[12];
+  pair_smem_layout<TT>(bins, o);
+  PairSmem<TT> S;
+  S.cxy = (double2*)(raw + o[0]);
+  S.cmeta = (PtMeta<TT>*)(raw + o[1]);
+  S.cpos = (uint32_t*)(raw + o[2]);
+  S.angs = (double*)(raw + o[3]);
+  S.Q = (double*)(raw + o[4]);
+  S.T = (TT*)(raw + o[5]);
+  S.stab = (uint16_t*)(raw + o[6]);
+  S.ttab = (uint16_t*)(raw + o[7]);
+  S.lo = (unsigned long long*)(raw + o[8]);
+  S.cnt = (uint32_t*)(raw + o[9]);
+  S.half = (uint32_t*)(raw + o[10]);
+  S.hi = (uint32_t*)(raw + o[11]);
   return S;
 }
 
@@ -506,41 +506,35 @@ __device__ __forceinline__ PairSmem carve(unsigned char* raw, uint32_t bins, uin
 // accumulated into the CTA histogram as 128-bit fixed point of (1/(omega*v) - 1).
 // Entries live in the warp's ring (global, L1/L2-resident): {center sorted
 // position, bin | (v == 1/2) << 31, q = d^2 as two words}.
-#ifndef STK_DRAIN_INLINE
-#define STK_DRAIN_INLINE __forceinline__
-#endif
-__device__ STK_DRAIN_INLINE void drain_arcs(int count, int lane, const uint4* ring_q,
-                                           uint32_t head, double* angs, const double* xs,
-                                           const double* ys, const PairSmem& S,
+__device__ __forceinline__ void drain_arcs(int count, int lane, const uint4* ring_q,
+                                           uint32_t head, double* angs, const double2* pxy,
+                                           unsigned long long* s_lo, uint32_t* s_hi,
                                            const RegionView& reg, int* overflow) {
-#ifdef STK_NO_ARC
-  return;
-#endif
   if (lane >= count) return;
   const uint4 e = ring_q[(head + lane) & (kArcRing - 1)];
-  const uint32_t cp = e.x;
-  const double cx = xs[cp], cy = ys[cp];
+  const double2 c = pxy[e.x];
   const double q = __hiloint2double((int)e.w, (int)e.z);
   const uint32_t bw = e.y;
   const double d = sqrt(q);
   double ws = -1.0;
-  if (reg.nv <= 32) ws = spatial_weight_buf(cx, cy, d, reg, angs + lane, 32, kAngleSlots / 2);
-  if (ws < 0.0) ws = spatial_weight(cx, cy, d, reg.ring, reg.nv, reg.maxabs, overflow);
+  if (reg.nv <= 32) ws = spatial_weight_buf(c.x, c.y, d, reg, angs + lane, 32, kAngleSlots / 2);
+  if (ws < 0.0) ws = spatial_weight(c.x, c.y, d, reg.ring, reg.nv, reg.maxabs, overflow);
   const double w = ws * ((bw >> 31) ? 0.5 : 1.0);  // edge::pair_weight (edge_correction.cpp:88-103)
   const double term = 1.0 / w;                      // PairHistogram::add(.., 1.0 / w)
   uint64_t lo, hi;
   fixed52_minus_one(term, &lo, &hi);
   const uint32_t bin = bw & 0x7fffffffu;
   if (lo | hi) {
-    const unsigned long long old = atomicAdd(&S.lo[bin], (unsigned long long)lo);
+    const unsigned long long old = atomicAdd(&s_lo[bin], (unsigned long long)lo);
     if (old + lo < old) ++hi;
-    if (hi) atomicAdd(&S.hi[bin], (uint32_t)hi);
+    if (hi) atomicAdd(&s_hi[bin], (uint32_t)hi);
   }
 }
 
 #ifndef STK_PAIR_MINB
 #define STK_PAIR_MINB 3
 #endif
+template <typename TT>
 __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_task, s_next;
@@ -548,27 +542,27 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   const GridGeom& G = A.G;
   const BinView& BV = A.bins;
   const uint32_t cs = BV.cs, ct = BV.ct, bins = cs * ct;
-  const PairSmem S = carve(smem_raw, bins, cs, ct);
+  const PairSmem<TT> S = carve<TT>(smem_raw, bins);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 
   for (uint32_t b = tid; b < cs; b += blockDim.x) S.Q[b] = BV.Q[b];
-  for (uint32_t b = tid; b < ct; b += blockDim.x) S.T[b] = BV.T[b];
+  // times relative to the period start never exceed the duration, so
+  // clamping larger thresholds to TT's range preserves every comparison
+  const int64_t tclamp = sizeof(TT) == 4 ? 0x7fffffffLL : 0x7fffffffffffffffLL;
+  for (uint32_t b = tid; b < ct; b += blockDim.x) S.T[b] = (TT)min(BV.T[b], tclamp);
   for (uint32_t b = tid; b < kBucketTable; b += blockDim.x) {
     S.stab[b] = BV.s_tab[b];
     S.ttab[b] = BV.t_tab[b];
   }
   const double Qmax = BV.Qmax;
-  const int64_t Tmax = BV.Tmax;
+  const TT Tmax = (TT)min(BV.Tmax, tclamp);
   const float s_inv_bw = BV.s_inv_bw, t_inv_bw = BV.t_inv_bw;
   const uint32_t total_tasks = B.task_start[B.R];
   const uint32_t task_items = B.task_counter[1];
   const unsigned lanemask_lt = (1u << lane) - 1u;
-  double2* tile = S.tile + w * 32;
-  int64_t* tt = S.tt + w * 32;
-  double* tsq = S.tsq + w * 32;
-  int64_t* tvt = S.tvt + w * 32;
-  uint32_t* tix = S.tix + w * 32;
-  uint32_t* tpos = S.tpos + w * 32;
+  double2* cxy_w = S.cxy + w * 32;
+  PtMeta<TT>* cm_w = S.cmeta + w * 32;
+  uint32_t* cpos_w = S.cpos + w * 32;
   uint4* arcq = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * kArcRing;
   double* angs = S.angs + w * kAngleSlots * 32;
   int overflow = 0;
@@ -601,15 +595,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     const uint32_t i0 = (task - B.task_start[p]) * task_items;
     const uint32_t i1 = min(i0 + task_items, items_p);
     const uint2* items = B.items + (uint64_t)p * B.max_items;
-    const double* xs = B.xs + pb;
-    const double* ys = B.ys + pb;
-    const int64_t* ts = B.ts + pb;
-    const double* psq = B.psq + pb;
-    const int64_t* pvt = B.pvt + pb;
-    const uint32_t* pix = B.idx + pb;
+    const double2* pxy = B.pxy + pb;
+    const PtMeta<TT>* pmeta = reinterpret_cast<const PtMeta<TT>*>(B.pmeta) + pb;
     const bool sel_p = p < B.n_sel;
     const uint32_t* clist = sel_p ? B.sel_start + (uint64_t)p * (G.cells + 1) : cstart;
-    const uint32_t* cpos = B.center_pos + pb;
+    const uint32_t* cposl = B.center_pos + pb;
 
     for (;;) {
       uint32_t it = 0;
@@ -623,13 +613,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       // broadcasts one center to the 32 neighbour lanes
       __syncwarp();
       if (lane < (int)nc) {
-        const uint32_t pos = sel_p ? cpos[start + lane] : start + lane;
-        tile[lane] = make_double2(xs[pos], ys[pos]);
-        tt[lane] = ts[pos];
-        tsq[lane] = psq[pos];
-        tvt[lane] = pvt[pos];
-        tix[lane] = pix[pos];
-        tpos[lane] = pos;
+        const uint32_t pos = sel_p ? cposl[start + lane] : start + lane;
+        cxy_w[lane] = pxy[pos];
+        cm_w[lane] = pmeta[pos];
+        cpos_w[lane] = pos;
       }
       __syncwarp();
       const uint32_t first_pos = sel_p ? 0u : start;  // lowest center position (non-selected)
@@ -673,9 +660,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       uint32_t j0 = __shfl_sync(FULL_MASK, my_rb, r & 31);
       uint32_t re = __shfl_sync(FULL_MASK, my_re, r & 31);
       int kc = 0;
-      double nx_ = 0.0, ny_ = 0.0, nsq = 0.0;
-      int64_t nt = 0, nvt = 0;
-      uint32_t nix = 0, jp = 0;
+      double2 nxy = make_double2(0.0, 0.0);
+      PtMeta<TT> nm{0, 0, 0.0f, 0u};
+      uint32_t jp = 0;
       bool has = false, same_cell = false;
       for (;;) {
         const bool done = rows_left == 0;
@@ -687,85 +674,79 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         if (pending >= 32 || (done && pending > 0)) {
           const int cnt_ = (int)min(pending, 32u);
           __syncwarp();
-          drain_arcs(cnt_, lane, arcq, qh, angs, xs, ys, S, A.reg, &overflow);
+          drain_arcs(cnt_, lane, arcq, qh, angs, pxy, S.lo, S.hi, A.reg, &overflow);
           qh += (uint32_t)cnt_;
           continue;
         }
         if (done) break;
-        {
-          if (kc == 0) {  // new tile: this lane's neighbour into registers
-            jp = j0 + lane;
-            has = jp < re;
-            if (has) {
-              nx_ = xs[jp];
-              ny_ = ys[jp];
-              nt = ts[jp];
-              nsq = psq[jp];
-              nvt = pvt[jp];
-              nix = pix[jp];
-            }
-            same_cell = r == 0 && jp < own_end;
-            n_cand += (unsigned long long)min(32u, re - j0) * nc;
+        if (kc == 0) {  // new tile: this lane's neighbour into registers
+          jp = j0 + lane;
+          has = jp < re;
+          if (has) {
+            nxy = pxy[jp];
+            nm = pmeta[jp];
           }
-          const int kend = min(kc + kArcChunk, (int)nc);
-          for (int k = kc; k < kend; ++k) {
-            const double2 cxy = tile[k];  // center k (broadcast)
-            const int64_t ctm = tt[k];
-            const double dx = cxy.x - nx_, dy2 = cxy.y - ny_;
-            const double q = dx * dx + dy2 * dy2;  // spatial_distance^2, no FMA
-            int64_t du = ctm - nt;
-            du = du < 0 ? -du : du;                // temporal_distance
-            const bool owner = !same_cell || (sel_p ? nix > tix[k] : jp > tpos[k]);
-            const bool in = has && owner && q <= Qmax && du <= Tmax;
-            bool arc_i = false, arc_j = false;
-            uint32_t bin = 0;
-            bool half_i = false, half_j = false;
-            if (in) {
-              // bin_pair: first s_k >= d <=> first Q_k >= q; first t_l >= u
-              int bq = (int)(sqrtf((float)q) * s_inv_bw);
-              bq = min(bq, kBucketTable - 1);
-              uint32_t sb = S.stab[bq];
-              while (q > S.Q[sb]) ++sb;
-              int bt = (int)((float)du * t_inv_bw);
-              bt = min(bt, kBucketTable - 1);
-              uint32_t tb = S.ttab[bt];
-              while (du > S.T[tb]) ++tb;
-              bin = sb * ct + tb;
-              atomicAdd(&S.cnt[bin], 2u);
-              half_i = du > tvt[k];
-              half_j = du > nvt;
-              arc_i = q >= tsq[k];
-              arc_j = q >= nsq;
-              const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
-              if (h) atomicAdd(&S.half[bin], h);
-              n_in += 2;
-            }
-            const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
-            const unsigned mj = __ballot_sync(FULL_MASK, arc_j);
-            if (mi | mj) {
-              const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
-              if (arc_i)
-                arcq[(qt + __popc(mi & lanemask_lt)) & (kArcRing - 1)] =
-                    make_uint4(tpos[k], bin | (half_i ? 0x80000000u : 0u), qlo, qhi);
-              qt += __popc(mi);
-              if (arc_j)
-                arcq[(qt + __popc(mj & lanemask_lt)) & (kArcRing - 1)] =
-                    make_uint4(jp, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
-              qt += __popc(mj);
-              n_exact += (uint32_t)arc_i + (uint32_t)arc_j;
-            }
+          same_cell = r == 0 && jp < own_end;
+          n_cand += (unsigned long long)min(32u, re - j0) * nc;
+        }
+        const int kend = min(kc + kArcChunk, (int)nc);
+        for (int k = kc; k < kend; ++k) {
+          const double2 c = cxy_w[k];  // center k (broadcast)
+          const PtMeta<TT> cmk = cm_w[k];
+          const double dx = c.x - nxy.x, dy = c.y - nxy.y;
+          const double q = dx * dx + dy * dy;  // spatial_distance^2, no FMA
+          TT du = cmk.t - nm.t;
+          du = du < 0 ? -du : du;              // temporal_distance
+          const bool owner = !same_cell || (sel_p ? nm.idx > cmk.idx : jp > cpos_w[k]);
+          const bool in = has && owner && q <= Qmax && du <= Tmax;
+          bool arc_i = false, arc_j = false;
+          uint32_t bin = 0;
+          bool half_i = false, half_j = false;
+          if (in) {
+            // bin_pair: first s_k >= d <=> first Q_k >= q; first t_l >= u
+            int bq = (int)(sqrtf((float)q) * s_inv_bw);
+            bq = min(bq, kBucketTable - 1);
+            uint32_t sb = S.stab[bq];
+            while (q > S.Q[sb]) ++sb;
+            int bt = (int)((float)du * t_inv_bw);
+            bt = min(bt, kBucketTable - 1);
+            uint32_t tb = S.ttab[bt];
+            while (du > S.T[tb]) ++tb;
+            bin = sb * ct + tb;
+            atomicAdd(&S.cnt[bin], 2u);
+            half_i = du > cmk.vt;
+            half_j = du > nm.vt;
+            arc_i = q >= (double)cmk.sq;
+            arc_j = q >= (double)nm.sq;
+            const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
+            if (h) atomicAdd(&S.half[bin], h);
+            n_in += 2;
           }
-          // advance: next chunk, next tile, next non-empty row
-          kc = kend;
-          if (kc >= (int)nc) {
-            kc = 0;
-            j0 += 32;
-            if (j0 >= re) {
-              rows_left &= rows_left - 1;
-              r = rows_left ? __ffs(rows_left) - 1 : 32;
-              j0 = __shfl_sync(FULL_MASK, my_rb, r & 31);
-              re = __shfl_sync(FULL_MASK, my_re, r & 31);
-            }
+          const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
+          const unsigned mj = __ballot_sync(FULL_MASK, arc_j);
+          if (mi | mj) {
+            const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
+            if (arc_i)
+              arcq[(qt + __popc(mi & lanemask_lt)) & (kArcRing - 1)] =
+                  make_uint4(cpos_w[k], bin | (half_i ? 0x80000000u : 0u), qlo, qhi);
+            qt += __popc(mi);
+            if (arc_j)
+              arcq[(qt + __popc(mj & lanemask_lt)) & (kArcRing - 1)] =
+                  make_uint4(jp, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
+            qt += __popc(mj);
+            n_exact += (uint32_t)arc_i + (uint32_t)arc_j;
+          }
+        }
+        // advance: next chunk, next tile, next non-empty row
+        kc = kend;
+        if (kc >= (int)nc) {
+          kc = 0;
+          j0 += 32;
+          if (j0 >= re) {
+            rows_left &= rows_left - 1;
+            r = rows_left ? __ffs(rows_left) - 1 : 32;
+            j0 = __shfl_sync(FULL_MASK, my_rb, r & 31);
+            re = __shfl_sync(FULL_MASK, my_re, r & 31);
           }
         }
       }
@@ -801,6 +782,22 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     atomicAdd(&B.stats[2], tot_exact);
   }
   if (overflow) atomicOr(&B.stats[3], (unsigned long long)overflow);
+}
+
+// Host-side launch helpers (keep the kernel templates in this translation unit).
+cudaError_t pair_kernel_prepare(int wide, size_t smem, int* per_sm) {
+  const void* fn = wide ? (const void*)pair_kernel<int64_t> : (const void*)pair_kernel<int32_t>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fn, kPairWarps * 32, smem);
+}
+
+void pair_kernel_launch(int wide, unsigned ctas, size_t smem, cudaStream_t stream,
+                        const PairArgs& A) {
+  if (wide)
+    pair_kernel<int64_t><<<ctas, kPairWarps * 32, smem, stream>>>(A);
+  else
+    pair_kernel<int32_t><<<ctas, kPairWarps * 32, smem, stream>>>(A);
 }
 
 // ============================================================ K5 finalize

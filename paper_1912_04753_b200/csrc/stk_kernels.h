@@ -33,7 +33,9 @@ __global__ void select_scatter_kernel(Batch B, GridGeom G);
 __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first);
 __global__ void items_kernel(Batch B, GridGeom G, int p_first);
 __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas);
-__global__ void pair_kernel(PairArgs A);
+cudaError_t pair_kernel_prepare(int wide, size_t smem, int* per_sm);
+void pair_kernel_launch(int wide, unsigned ctas, size_t smem, cudaStream_t stream,
+                        const PairArgs& A);
 __global__ void finalize_kernel(Batch B, uint32_t cs, uint32_t ct, const double* s_values,
                                 const int64_t* t_values, double area, int64_t duration,
                                 int p_first);
@@ -46,6 +48,6 @@ __global__ void weights_kernel(const double* cx, const double* cy, const double*
                                unsigned long long* bad);
 __global__ void dfma_peak_kernel(double* out, int iters, double a, double b);
 
-size_t pair_kernel_smem(uint32_t bins, uint32_t cs, uint32_t ct);
+size_t pair_kernel_smem(uint32_t bins, int wide);
 
 }  // namespace stk

@@ -27,6 +27,7 @@ struct RegionView {
   double xmin, xmax, ymin, ymax;
   double maxabs;        // max |coordinate| over the ring
   int rect;             // 4-vertex axis-aligned rectangle (exact fast paths apply)
+  double box_m;         // rect: on_segment is impossible farther than this outside the box
 };
 
 // Distance grid in the forms the kernels consume.
@@ -53,6 +54,21 @@ struct GridGeom {
   int32_t rs, rt;  // stencil radius in cells (space, time): cell >= s_max/rs, >= t_max/rt
 };
 
+constexpr int kMaxAxis = 512;       // max bins per axis (smem-resident thresholds)
+
+// Per sorted point: time relative to the period start, the temporal-weight
+// threshold (v == 1 iff u <= vt, edge_correction.cpp:81-86), the squared
+// radius below which omega == 1 exactly (rounded DOWN to float: still a
+// conservative bound), and the input index.  Replaces the reference's
+// weight cache (weight_cache.hpp:39-129) with a per-point memo.
+template <typename TT>
+struct PtMeta {
+  TT t;
+  TT vt;
+  float sq;
+  uint32_t idx;
+};
+
 // One batch of R point patterns of n points each, laid out [R][n].
 struct Batch {
   int R;
@@ -61,13 +77,11 @@ struct Batch {
   double* x;
   double* y;
   int64_t* t;
-  // grid-sorted structure-of-arrays
-  double* xs;
-  double* ys;
-  int64_t* ts;
+  // grid-sorted layout: interleaved coordinates + one meta record per point
+  double2* pxy;   // (x, y)
+  void* pmeta;    // PtMeta<int32_t> (16 B) or PtMeta<int64_t> (24 B) when `wide`
+  int wide;       // study period >= 2^31 time units: 64-bit relative times
   uint32_t* idx;  // input index of each sorted point
-  double* psq;    // per sorted point: squared radius below which omega == 1 exactly
-  int64_t* pvt;   // per sorted point: v == 1 iff u <= pvt
   uint32_t* key;  // cell key per unsorted point
   uint32_t* rank; // rank within the cell per unsorted point
   uint32_t* cell_count;  // [R][cells]

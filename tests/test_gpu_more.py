@@ -190,6 +190,20 @@ def test_dense_arc_pairs_with_duplicates(api, port):
     _compare(api, port, x, y, t, ring, p0, p1, [10.0, 40.0, 90.0], [20, 60, 100])
 
 
+def test_wide_period_64bit_times(api, port):
+    """Study periods >= 2^31 time units take the 64-bit-time kernel."""
+    p0, p1 = -(1 << 40), (1 << 40) + 12345
+    ring = np.array([[0, 0], [2000, 0], [2000, 2000], [0, 2000]], float)
+    rng = np.random.default_rng(11)
+    n = 3000
+    x = rng.uniform(0, 2000, n)
+    y = rng.uniform(0, 2000, n)
+    t = rng.integers(p0, p1, n, endpoint=True)
+    t[:1500] = rng.integers(-(1 << 33), 1 << 33, 1500)  # dense middle: many temporal pairs
+    tv = [1 << 30, 1 << 31, 1 << 33, 1 << 35]
+    _compare(api, port, x, y, t, ring, p0, p1, [100.0, 300.0, 600.0], tv)
+
+
 def test_one_bin_grid_and_tiny_n(api, port):
     ring, p0, p1 = square(10.0, 0, 10)
     _compare(api, port, np.array([1.0, 2.0]), np.array([1.0, 2.0]), np.array([0, 10]), ring, p0,
