@@ -120,6 +120,7 @@ struct stk_ctx {
   std::vector<double> Q;
   std::vector<uint16_t> stab, ttab;
   float s_inv_bw = 0, t_inv_bw = 0;
+  bool single_step = false;
   DevBuf<double> d_Q, d_s;
   DevBuf<int64_t> d_T;
   DevBuf<uint16_t> d_stab, d_ttab;
@@ -190,6 +191,7 @@ BinView bin_view(stk_ctx* c) {
   b.Tmax = c->t_values.back();
   b.s_inv_bw = c->s_inv_bw;
   b.t_inv_bw = c->t_inv_bw;
+  b.single_step = c->single_step ? 1 : 0;
   return b;
 }
 
@@ -442,7 +444,13 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   items_kernel<<<gc, 256, 0, c->stream>>>(B, G, 0);
   CK(cudaGetLastError());
   ++c->launches;
-  const size_t smem = pair_kernel_smem(P.bins, B.wide);
+  // Crossing scratch: a circle of radius d <= s_max around a point of a
+  // rectangle reaches at most two edges (<= 4 crossings) when s_max is below
+  // half the shorter side; otherwise allow 8 crossings (more use the
+  // general local-memory path).
+  const double smin_side = std::min(c->xmax - c->xmin, c->ymax - c->ymin);
+  const int slots = (c->fast_rect && c->s_values.back() < 0.5 * smin_side) ? 8 : kAngleSlots;
+  const size_t smem = pair_kernel_smem(P.bins, B.wide, slots);
   int per_sm = 0;
   CK(pair_kernel_prepare(B.wide, smem, &per_sm));
   if (per_sm < 1) throw Unsupported("distance grid too large for the pair kernel's shared histogram");
@@ -452,12 +460,13 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   CK(cudaEventRecord(e1, c->stream));
 
   PairArgs A;
+  A.angle_slots = slots;
   A.B = B;
   A.G = G;
   A.bins = bin_view(c);
   A.reg = region_view(c);
   const uint64_t ctas = (uint64_t)c->num_sms * per_sm;
-  c->arcq.ensure(ctas * kPairWarps * kArcRing);
+  c->arcq.ensure(ctas * kPairWarps * kArcRing * kArcClasses);
   A.B.arcq = c->arcq.p;
   pair_kernel_launch(B.wide, (unsigned)ctas, smem, c->stream, A);
   CK(cudaGetLastError());
@@ -860,7 +869,7 @@ int stk_set_grid(stk_ctx* c, const double* s_values, uint32_t cs, const int64_t*
     check_grid(s_values, cs, t_values, ct);
     if ((uint64_t)cs * ct > (1u << 20)) throw Unsupported("more than 2^20 grid cells");
     if (cs > (uint32_t)kMaxAxis || ct > (uint32_t)kMaxAxis)
-      throw Unsupported("more than 512 distance thresholds per axis");
+      throw Unsupported("more than " + std::to_string(kMaxAxis) + " distance thresholds per axis");
     c->s_values.assign(s_values, s_values + cs);
     c->t_values.assign(t_values, t_values + ct);
     c->Q.resize(cs);
@@ -885,6 +894,19 @@ int stk_set_grid(stk_ctx* c, const double* s_values, uint32_t cs, const int64_t*
       c->ttab[b] = (uint16_t)std::min<int>(k, 65535);
     }
     if (cs > 65535 || ct > 65535) throw Unsupported("more than 65535 bins per axis");
+    // single-step binning is exact when no bucket's distance range (with the
+    // device-side margins) contains two thresholds
+    auto at_most_one = [](const auto& vals, double bw) {
+      for (int b = 0; b < kBucketTable; ++b) {
+        const double lo = b * bw, hi = (b + 1) * bw * (1.0 + 4e-5);
+        int cnt = 0;
+        for (const auto v : vals)
+          if ((double)v >= lo && (double)v <= hi) ++cnt;
+        if (cnt > 1) return false;
+      }
+      return true;
+    };
+    c->single_step = at_most_one(c->s_values, sbw) && at_most_one(c->t_values, tbw);
     c->d_Q.ensure(cs);
     c->d_s.ensure(cs);
     c->d_T.ensure(ct);

@@ -15,6 +15,7 @@
 //
 // Compiled with -fmad=false: no FP64 mul+add contraction anywhere.
 #include <cstdint>
+#include <type_traits>
 
 #include "stk_device.cuh"
 #include "stk_kernels.h"
@@ -454,7 +455,7 @@ struct PairSmem {
 };
 
 template <typename TT>
-__host__ __device__ inline size_t pair_smem_layout(uint32_t bins, size_t* off) {
+__host__ __device__ inline size_t pair_smem_layout(uint32_t bins, int slots, size_t* off) {
   size_t b = 0;
   int k = 0;
   auto take = [&](size_t bytes) {
@@ -465,7 +466,7 @@ __host__ __device__ inline size_t pair_smem_layout(uint32_t bins, size_t* off) {
   take(sizeof(double2) * kPairWarps * 32);
   take(sizeof(PtMeta<TT>) * kPairWarps * 32);
   take(sizeof(uint32_t) * kPairWarps * 32);
-  take(sizeof(double) * kPairWarps * kAngleSlots * 32);
+  take(sizeof(double) * kPairWarps * slots * 32);
   take(sizeof(double) * kMaxAxis);
   take(sizeof(TT) * kMaxAxis);
   take(sizeof(uint16_t) * kBucketTable);
@@ -477,15 +478,16 @@ __host__ __device__ inline size_t pair_smem_layout(uint32_t bins, size_t* off) {
   return (b + 15) & ~size_t(15);
 }
 
-size_t pair_kernel_smem(uint32_t bins, int wide) {
+size_t pair_kernel_smem(uint32_t bins, int wide, int slots) {
   size_t off[12];
-  return wide ? pair_smem_layout<int64_t>(bins, off) : pair_smem_layout<int32_t>(bins, off);
+  return wide ? pair_smem_layout<int64_t>(bins, slots, off)
+              : pair_smem_layout<int32_t>(bins, slots, off);
 }
 
 template <typename TT>
-__device__ __forceinline__ PairSmem<TT> carve(unsigned char* raw, uint32_t bins) {
+__device__ __forceinline__ PairSmem<TT> carve(unsigned char* raw, uint32_t bins, int slots) {
   size_t o[12];
-  pair_smem_layout<TT>(bins, o);
+  pair_smem_layout<TT>(bins, slots, o);
   PairSmem<TT> S;
   S.cxy = (double2*)(raw + o[0]);
   S.cmeta = (PtMeta<TT>*)(raw + o[1]);
@@ -507,9 +509,10 @@ __device__ __forceinline__ PairSmem<TT> carve(unsigned char* raw, uint32_t bins)
 // Entries live in the warp's ring (global, L1/L2-resident): {center sorted
 // position, bin | (v == 1/2) << 31, q = d^2 as two words}.
 __device__ __forceinline__ void drain_arcs(int count, int lane, const uint4* ring_q,
-                                           uint32_t head, double* angs, const double2* pxy,
-                                           unsigned long long* s_lo, uint32_t* s_hi,
-                                           const RegionView& reg, int* overflow) {
+                                           uint32_t head, double* angs, int slots,
+                                           const double2* pxy, unsigned long long* s_lo,
+                                           uint32_t* s_hi, const RegionView& reg,
+                                           int* overflow) {
   if (lane >= count) return;
   const uint4 e = ring_q[(head + lane) & (kArcRing - 1)];
   const double2 c = pxy[e.x];
@@ -517,7 +520,7 @@ __device__ __forceinline__ void drain_arcs(int count, int lane, const uint4* rin
   const uint32_t bw = e.y;
   const double d = sqrt(q);
   double ws = -1.0;
-  if (reg.nv <= 32) ws = spatial_weight_buf(c.x, c.y, d, reg, angs + lane, 32, kAngleSlots / 2);
+  if (reg.nv <= 32) ws = spatial_weight_buf(c.x, c.y, d, reg, angs + lane, 32, slots / 2);
   if (ws < 0.0) ws = spatial_weight(c.x, c.y, d, reg.ring, reg.nv, reg.maxabs, overflow);
   const double w = ws * ((bw >> 31) ? 0.5 : 1.0);  // edge::pair_weight (edge_correction.cpp:88-103)
   const double term = 1.0 / w;                      // PairHistogram::add(.., 1.0 / w)
@@ -532,7 +535,7 @@ __device__ __forceinline__ void drain_arcs(int count, int lane, const uint4* rin
 }
 
 #ifndef STK_PAIR_MINB
-#define STK_PAIR_MINB 3
+#define STK_PAIR_MINB 4
 #endif
 template <typename TT>
 __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(PairArgs A) {
@@ -542,7 +545,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   const GridGeom& G = A.G;
   const BinView& BV = A.bins;
   const uint32_t cs = BV.cs, ct = BV.ct, bins = cs * ct;
-  const PairSmem<TT> S = carve<TT>(smem_raw, bins);
+  const int slots = A.angle_slots;
+  const PairSmem<TT> S = carve<TT>(smem_raw, bins, slots);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 
   for (uint32_t b = tid; b < cs; b += blockDim.x) S.Q[b] = BV.Q[b];
@@ -563,8 +567,15 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   double2* cxy_w = S.cxy + w * 32;
   PtMeta<TT>* cm_w = S.cmeta + w * 32;
   uint32_t* cpos_w = S.cpos + w * 32;
-  uint4* arcq = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * kArcRing;
-  double* angs = S.angs + w * kAngleSlots * 32;
+  uint4* arcq = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * kArcRing * kArcClasses;
+  const bool classes = A.reg.rect != 0;
+  // a circle of radius d around c reaches two rectangle edges (a corner:
+  // up to 8 crossings) only if both edge distances are below d; a hint that
+  // routes entries to the ring whose drains run uniform trip counts
+  const float rxmin = (float)A.reg.xmin, rxmax = (float)A.reg.xmax;
+  const float rymin = (float)A.reg.ymin, rymax = (float)A.reg.ymax;
+  const int single_step = BV.single_step;
+  double* angs = S.angs + w * slots * 32;
   int overflow = 0;
   unsigned long long tot_in = 0, tot_cand = 0, tot_exact = 0;
 
@@ -651,7 +662,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         }
       }
       const unsigned nonempty = __ballot_sync(FULL_MASK, my_rb < my_re);
-      uint32_t qh = 0, qt = 0;  // arc ring head / tail (monotone)
+      uint32_t qh0 = 0, qt0 = 0, qh1 = 0, qt1 = 0;  // arc rings: head / tail (monotone)
       uint32_t n_in = 0, n_exact = 0;
       unsigned long long n_cand = 0;
       // flat walk over (row, tile, center chunk); one inline copy of the drain
@@ -669,13 +680,18 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         // the single drain site, ahead of new candidates so the ring never
         // holds more than 31 + kArcChunk * 64 entries: full batches while
         // any are pending, and the remainder at the end
-        const uint32_t pending = qt - qh;
-        if (pending > (uint32_t)kArcRing) overflow |= 2;  // must never happen: reported as an error
-        if (pending >= 32 || (done && pending > 0)) {
-          const int cnt_ = (int)min(pending, 32u);
+        const uint32_t pend0 = qt0 - qh0, pend1 = qt1 - qh1;
+        if (pend0 > (uint32_t)kArcRing || pend1 > (uint32_t)kArcRing) overflow |= 2;  // never
+        const bool d0 = pend0 >= 32 || (done && pend0 > 0);
+        const bool d1 = !d0 && (pend1 >= 32 || (done && pend1 > 0));
+        if (d0 || d1) {
+          const uint32_t pend = d0 ? pend0 : pend1;
+          const uint32_t head = d0 ? qh0 : qh1;
+          const int cnt_ = (int)min(pend, 32u);
           __syncwarp();
-          drain_arcs(cnt_, lane, arcq, qh, angs, pxy, S.lo, S.hi, A.reg, &overflow);
-          qh += (uint32_t)cnt_;
+          drain_arcs(cnt_, lane, arcq + (d0 ? 0 : kArcRing), head, angs, slots, pxy, S.lo, S.hi,
+                     A.reg, &overflow);
+          if (d0) qh0 += (uint32_t)cnt_; else qh1 += (uint32_t)cnt_;
           continue;
         }
         if (done) break;
@@ -690,53 +706,82 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           n_cand += (unsigned long long)min(32u, re - j0) * nc;
         }
         const int kend = min(kc + kArcChunk, (int)nc);
-        for (int k = kc; k < kend; ++k) {
-          const double2 c = cxy_w[k];  // center k (broadcast)
-          const PtMeta<TT> cmk = cm_w[k];
-          const double dx = c.x - nxy.x, dy = c.y - nxy.y;
-          const double q = dx * dx + dy * dy;  // spatial_distance^2, no FMA
-          TT du = cmk.t - nm.t;
-          du = du < 0 ? -du : du;              // temporal_distance
-          const bool owner = !same_cell || (sel_p ? nm.idx > cmk.idx : jp > cpos_w[k]);
-          const bool in = has && owner && q <= Qmax && du <= Tmax;
-          bool arc_i = false, arc_j = false;
-          uint32_t bin = 0;
-          bool half_i = false, half_j = false;
-          if (in) {
-            // bin_pair: first s_k >= d <=> first Q_k >= q; first t_l >= u
-            int bq = (int)(sqrtf((float)q) * s_inv_bw);
-            bq = min(bq, kBucketTable - 1);
-            uint32_t sb = S.stab[bq];
-            while (q > S.Q[sb]) ++sb;
-            int bt = (int)((float)du * t_inv_bw);
-            bt = min(bt, kBucketTable - 1);
-            uint32_t tb = S.ttab[bt];
-            while (du > S.T[tb]) ++tb;
-            bin = sb * ct + tb;
-            atomicAdd(&S.cnt[bin], 2u);
-            half_i = du > cmk.vt;
-            half_j = du > nm.vt;
-            arc_i = q >= (double)cmk.sq;
-            arc_j = q >= (double)nm.sq;
-            const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
-            if (h) atomicAdd(&S.half[bin], h);
-            n_in += 2;
+        auto chunk = [&](auto own_tag) {
+          constexpr bool OWN = decltype(own_tag)::value;
+          for (int k = kc; k < kend; ++k) {
+            const double2 c = cxy_w[k];  // center k (broadcast)
+            const PtMeta<TT> cmk = cm_w[k];
+            const double dx = c.x - nxy.x, dy = c.y - nxy.y;
+            const double q = dx * dx + dy * dy;  // spatial_distance^2, no FMA
+            TT du = cmk.t - nm.t;
+            du = du < 0 ? -du : du;              // temporal_distance
+            bool owner = true;
+            if (OWN) owner = !same_cell || (sel_p ? nm.idx > cmk.idx : jp > cpos_w[k]);
+            const bool in = has && owner && q <= Qmax && du <= Tmax;
+            bool arc_i = false, arc_j = false;
+            uint32_t bin = 0;
+            bool half_i = false, half_j = false;
+            if (in) {
+              // bin_pair: first s_k >= d <=> first Q_k >= q; first t_l >= u
+              int bq = (int)(sqrtf((float)q) * s_inv_bw);
+              bq = min(bq, kBucketTable - 1);
+              uint32_t sb = S.stab[bq];
+              int bt = (int)((float)du * t_inv_bw);
+              bt = min(bt, kBucketTable - 1);
+              uint32_t tb = S.ttab[bt];
+              if (single_step) {
+                sb += q > S.Q[sb] ? 1u : 0u;
+                tb += du > S.T[tb] ? 1u : 0u;
+              } else {
+                while (q > S.Q[sb]) ++sb;
+                while (du > S.T[tb]) ++tb;
+              }
+              bin = sb * ct + tb;
+              atomicAdd(&S.cnt[bin], 2u);
+              half_i = du > cmk.vt;
+              half_j = du > nm.vt;
+              arc_i = q >= (double)cmk.sq;
+              arc_j = q >= (double)nm.sq;
+              const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
+              if (h) atomicAdd(&S.half[bin], h);
+              n_in += 2;
+            }
+            if (__any_sync(FULL_MASK, arc_i || arc_j)) {
+              // class hint: does the circle reach two rectangle edges?
+              bool ci = false, cj = false;
+              if (classes) {
+                const float qf = (float)q * 1.0001f;
+                const float hxi = fminf((float)c.x - rxmin, rxmax - (float)c.x);
+                const float hyi = fminf((float)c.y - rymin, rymax - (float)c.y);
+                const float hxj = fminf((float)nxy.x - rxmin, rxmax - (float)nxy.x);
+                const float hyj = fminf((float)nxy.y - rymin, rymax - (float)nxy.y);
+                ci = hxi * hxi < qf && hyi * hyi < qf;
+                cj = hxj * hxj < qf && hyj * hyj < qf;
+              }
+              const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
+              const uint4 ei = make_uint4(cpos_w[k], bin | (half_i ? 0x80000000u : 0u), qlo, qhi);
+              const uint4 ej = make_uint4(jp, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
+              const unsigned mi0 = __ballot_sync(FULL_MASK, arc_i && !ci);
+              const unsigned mi1 = __ballot_sync(FULL_MASK, arc_i && ci);
+              const unsigned mj0 = __ballot_sync(FULL_MASK, arc_j && !cj);
+              const unsigned mj1 = __ballot_sync(FULL_MASK, arc_j && cj);
+              if (arc_i) {
+                if (!ci) arcq[(qt0 + __popc(mi0 & lanemask_lt)) & (kArcRing - 1)] = ei;
+                else arcq[kArcRing + ((qt1 + __popc(mi1 & lanemask_lt)) & (kArcRing - 1))] = ei;
+              }
+              qt0 += __popc(mi0);
+              qt1 += __popc(mi1);
+              if (arc_j) {
+                if (!cj) arcq[(qt0 + __popc(mj0 & lanemask_lt)) & (kArcRing - 1)] = ej;
+                else arcq[kArcRing + ((qt1 + __popc(mj1 & lanemask_lt)) & (kArcRing - 1))] = ej;
+              }
+              qt0 += __popc(mj0);
+              qt1 += __popc(mj1);
+              n_exact += (uint32_t)arc_i + (uint32_t)arc_j;
+            }
           }
-          const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
-          const unsigned mj = __ballot_sync(FULL_MASK, arc_j);
-          if (mi | mj) {
-            const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
-            if (arc_i)
-              arcq[(qt + __popc(mi & lanemask_lt)) & (kArcRing - 1)] =
-                  make_uint4(cpos_w[k], bin | (half_i ? 0x80000000u : 0u), qlo, qhi);
-            qt += __popc(mi);
-            if (arc_j)
-              arcq[(qt + __popc(mj & lanemask_lt)) & (kArcRing - 1)] =
-                  make_uint4(jp, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
-            qt += __popc(mj);
-            n_exact += (uint32_t)arc_i + (uint32_t)arc_j;
-          }
-        }
+        };
+        if (r == 0 && j0 < own_end) chunk(std::true_type{}); else chunk(std::false_type{});
         // advance: next chunk, next tile, next non-empty row
         kc = kend;
         if (kc >= (int)nc) {
@@ -786,6 +831,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
 
 // Host-side launch helpers (keep the kernel templates in this translation unit).
 cudaError_t pair_kernel_prepare(int wide, size_t smem, int* per_sm) {
+  // (dynamic shared memory only; the launch bounds fix the register budget)
   const void* fn = wide ? (const void*)pair_kernel<int64_t> : (const void*)pair_kernel<int32_t>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -8,6 +8,7 @@
 namespace stk {
 
 struct PairArgs {
+  int angle_slots;  // per-lane crossing scratch (2 doubles per crossing)
   Batch B;
   GridGeom G;
   BinView bins;
@@ -48,6 +49,6 @@ __global__ void weights_kernel(const double* cx, const double* cy, const double*
                                unsigned long long* bad);
 __global__ void dfma_peak_kernel(double* out, int iters, double a, double b);
 
-size_t pair_kernel_smem(uint32_t bins, int wide);
+size_t pair_kernel_smem(uint32_t bins, int wide, int slots);
 
 }  // namespace stk

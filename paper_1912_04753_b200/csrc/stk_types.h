@@ -17,7 +17,8 @@ constexpr int kRingSmem = 32;      // ring vertices staged in shared memory (bit
 #define STK_ARC_CHUNK 12
 #endif
 constexpr int kArcChunk = STK_ARC_CHUNK;        // candidate steps between arc drains
-constexpr int kArcRing = 1024;      // per-warp arc ring entries (> 31 + kArcChunk * 64)
+constexpr int kArcRing = 1024;      // per-warp arc ring entries per class (> 31 + kArcChunk * 64)
+constexpr int kArcClasses = 2;      // rectangles: single-edge vs corner entries drain separately
 
 // Study region on the device (geom::StudyRegion, geometry.hpp:95-120).
 struct RegionView {
@@ -40,6 +41,7 @@ struct BinView {
   double Qmax;
   int64_t Tmax;
   float s_inv_bw, t_inv_bw;  // buckets per unit distance / per time unit (with margin)
+  int single_step;           // every bucket straddles <= 1 threshold: one compare finds the bin
 };
 
 // Uniform space-time cell grid (replaces the STR R-tree, st_index.cpp:54-130).
@@ -54,7 +56,10 @@ struct GridGeom {
   int32_t rs, rt;  // stencil radius in cells (space, time): cell >= s_max/rs, >= t_max/rt
 };
 
-constexpr int kMaxAxis = 512;       // max bins per axis (smem-resident thresholds)
+#ifndef STK_MAX_AXIS
+#define STK_MAX_AXIS 512
+#endif
+constexpr int kMaxAxis = STK_MAX_AXIS;  // max bins per axis (smem-resident thresholds)
 
 // Per sorted point: time relative to the period start, the temporal-weight
 // threshold (v == 1 iff u <= vt, edge_correction.cpp:81-86), the squared
