@@ -310,14 +310,15 @@ def run_ours(args):
     e2e_ms, e2e_tels = timed(False, args.steps)
 
     pairs_rank = sum(t_.in_threshold_pairs for t_ in tels)
-    arc_rank = sum(t_.exact_path_pairs for t_ in tels)
+    arc_rank = sum(t_.arc_pairs for t_ in tels)  # omega != 1 (SURVEY 8(d) arc pairs)
+    exact_rank = sum(t_.exact_path_pairs for t_ in tels)
     pair_ms_rank = sum(t_.pair_ms for t_ in tels)
     grid_ms_rank = sum(t_.grid_ms for t_ in tels)
     patterns_rank = sum(t_.patterns for t_ in tels)
     launches = sum(t_.kernel_launches for t_ in tels) // max(args.steps, 1)
 
     # max over ranks of time, sum over ranks of work
-    tot = np.array([pairs_rank, arc_rank, patterns_rank], dtype=np.float64)
+    tot = np.array([pairs_rank, arc_rank, patterns_rank, exact_rank], dtype=np.float64)
     tmax = np.array([ms, e2e_ms, pair_ms_rank, grid_ms_rank], dtype=np.float64)
     if world > 1:
         import torch.distributed as dist
@@ -327,7 +328,7 @@ def run_ours(args):
         dist.all_reduce(a, op=dist.ReduceOp.SUM)
         dist.all_reduce(b, op=dist.ReduceOp.MAX)
         tot, tmax = a.cpu().numpy(), b.cpu().numpy()
-    pairs, arcs, patterns = tot
+    pairs, arcs, patterns, exact = tot
     ms, e2e_ms, pair_ms, grid_ms = tmax
 
     if rank != 0:
@@ -362,7 +363,8 @@ def run_ours(args):
         "config": config_dict(cfg, sims, world),
         "realisations_per_s": patterns / (ms * 1e-3),
         "pairs_per_step": pairs / args.steps,
-        "exact_path_fraction": arcs / pairs if pairs else None,
+        "arc_fraction": arcs / pairs if pairs else None,
+        "exact_path_fraction": exact / pairs if pairs else None,
         "e2e": {"value": e2e_value, "unit": "pairs/s",
                 "h2d_bytes_per_step": int(24 * n),
                 "d2h_bytes_per_step": int(8 * bins * (5 if world == 1 else 0) +
@@ -371,7 +373,7 @@ def run_ours(args):
         "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                      "unit": "FP64 Tinstr/s", "frac": achieved / peak if peak else None,
                      "traffic": None,
-                     "note": f"pair kernel: ({W_INT} x interior + {W_ARC} x exact-path pairs) "
+                     "note": f"pair kernel: ({W_INT} x interior + {W_ARC} x arc (omega != 1) pairs) "
                              "FP64 instr / CUDA-event pair-kernel time; peak = live DFMA "
                              "microbenchmark (stk_measure_fp64_peak)",
                      "kernel_ms_per_step": pair_ms / args.steps,

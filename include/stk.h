@@ -50,6 +50,7 @@ typedef struct {
   double finalize_ms;          /* device time: prefix/scale/L/envelopes              */
   double total_ms;             /* device time of the whole call                      */
   uint64_t kernel_launches;    /* libstk kernels launched by the call                */
+  uint64_t arc_pairs;          /* in-threshold ordered pairs with omega != 1          */
 } stk_telemetry;
 
 /* ---- context-free validation (no device needed) ------------------------- */

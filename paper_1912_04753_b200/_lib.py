@@ -30,6 +30,7 @@ class StkTelemetry(C.Structure):
         ("finalize_ms", C.c_double),
         ("total_ms", C.c_double),
         ("kernel_launches", C.c_uint64),
+        ("arc_pairs", C.c_uint64),
     ]
 
     def as_dict(self):

@@ -283,7 +283,7 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   c->task_start.ensure(R + 1);
   c->task_counter.ensure(2);
   c->hist.ensure(R * P.bins * 4);
-  c->stats.ensure(4);
+  c->stats.ensure(8);
   c->K.ensure(R * P.bins);
   c->L.ensure(R * P.bins);
   c->flags.ensure(R);
@@ -495,7 +495,7 @@ double elapsed(const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
 }
 
 void fill_telemetry(stk_ctx* c, Timers& tm, stk_telemetry* tel, uint64_t patterns) {
-  unsigned long long st[4] = {0, 0, 0, 0};
+  unsigned long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   CK(cudaMemcpyAsync(st, c->stats.p, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (st[3] & 2) throw CudaFail("internal error: arc ring overflow in the pair kernel");
@@ -504,6 +504,7 @@ void fill_telemetry(stk_ctx* c, Timers& tm, stk_telemetry* tel, uint64_t pattern
   tel->in_threshold_pairs += st[0];
   tel->candidate_pairs += st[1];
   tel->exact_path_pairs += st[2];
+  tel->arc_pairs += st[4];
   tel->patterns += patterns;
   tel->kernel_launches += c->launches;
   tel->gen_ms += elapsed(tm.gen);
@@ -554,7 +555,7 @@ void run_pipeline(stk_ctx* c, const double* dx, const double* dy, const int64_t*
   const uint64_t patterns = (with_observed ? 1 : 0) + sims;
   Plan P = make_plan(c, n, patterns);
   const Source src = source_of(method);
-  CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * 4, c->stream));
+  CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * 8, c->stream));
   c->env.ensure(2 * (uint64_t)P.bins);
   c->obs.ensure(2 * (uint64_t)P.bins);
   bool env_init = true;
@@ -704,7 +705,7 @@ int stk_create(stk_ctx** out, int device) {
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* r = std::getenv("STK_STENCIL_RADIUS")) c->stencil_radius = std::max(1, std::min(2, std::atoi(r)));
-    c->stats.ensure(4);
+    c->stats.ensure(8);
   } catch (const std::exception& e) {
     delete c;
     return STK_ECUDA;
@@ -962,7 +963,7 @@ int stk_pair_histogram(stk_ctx* c, const double* x, const double* y, const int64
     Plan P = make_plan(c, n, 1);
     P.R = 1;
     Batch B = alloc_batch(c, P);
-    CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * 4, c->stream));
+    CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * 8, c->stream));
     generate(c, B, Source::Observed, 0, 1, 0, c->sx.p, c->sy.p, c->st.p);
     run_batch(c, P, B, tm, nshards > 1 ? 1 : 0, shard, nshards, 0, ~0ULL, false);
     const uint32_t bins = P.bins;

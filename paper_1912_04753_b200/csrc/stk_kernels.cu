@@ -512,7 +512,7 @@ __device__ __forceinline__ void drain_arcs(int count, int lane, const uint4* rin
                                            uint32_t head, double* angs, int slots,
                                            const double2* pxy, unsigned long long* s_lo,
                                            uint32_t* s_hi, const RegionView& reg,
-                                           int* overflow) {
+                                           int* overflow, uint32_t* n_arc) {
   if (lane >= count) return;
   const uint4 e = ring_q[(head + lane) & (kArcRing - 1)];
   const double2 c = pxy[e.x];
@@ -522,6 +522,7 @@ __device__ __forceinline__ void drain_arcs(int count, int lane, const uint4* rin
   double ws = -1.0;
   if (reg.nv <= 32) ws = spatial_weight_buf(c.x, c.y, d, reg, angs + lane, 32, slots / 2);
   if (ws < 0.0) ws = spatial_weight(c.x, c.y, d, reg.ring, reg.nv, reg.maxabs, overflow);
+  if (ws != 1.0) ++*n_arc;                           // omega != 1 (SURVEY's arc-pair definition)
   const double w = ws * ((bw >> 31) ? 0.5 : 1.0);  // edge::pair_weight (edge_correction.cpp:88-103)
   const double term = 1.0 / w;                      // PairHistogram::add(.., 1.0 / w)
   uint64_t lo, hi;
@@ -577,7 +578,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   const int single_step = BV.single_step;
   double* angs = S.angs + w * slots * 32;
   int overflow = 0;
-  unsigned long long tot_in = 0, tot_cand = 0, tot_exact = 0;
+  unsigned long long tot_in = 0, tot_cand = 0, tot_exact = 0, tot_arc = 0;
 
   for (;;) {
     __syncthreads();
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       }
       const unsigned nonempty = __ballot_sync(FULL_MASK, my_rb < my_re);
       uint32_t qh0 = 0, qt0 = 0, qh1 = 0, qt1 = 0;  // arc rings: head / tail (monotone)
-      uint32_t n_in = 0, n_exact = 0;
+      uint32_t n_in = 0, n_exact = 0, n_arc = 0;
       unsigned long long n_cand = 0;
       // flat walk over (row, tile, center chunk); one inline copy of the drain
       unsigned rows_left = nonempty;
@@ -690,7 +691,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           const int cnt_ = (int)min(pend, 32u);
           __syncwarp();
           drain_arcs(cnt_, lane, arcq + (d0 ? 0 : kArcRing), head, angs, slots, pxy, S.lo, S.hi,
-                     A.reg, &overflow);
+                     A.reg, &overflow, &n_arc);
           if (d0) qh0 += (uint32_t)cnt_; else qh1 += (uint32_t)cnt_;
           continue;
         }
@@ -798,6 +799,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       __syncwarp();
       tot_in += n_in;
       tot_exact += n_exact;
+      tot_arc += n_arc;
       if (lane == 0) tot_cand += n_cand;
     }
     __syncthreads();
@@ -820,11 +822,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   for (int o = 16; o > 0; o >>= 1) {
     tot_in += __shfl_down_sync(FULL_MASK, tot_in, o);
     tot_exact += __shfl_down_sync(FULL_MASK, tot_exact, o);
+    tot_arc += __shfl_down_sync(FULL_MASK, tot_arc, o);
   }
   if (lane == 0) {
     atomicAdd(&B.stats[0], tot_in);
     atomicAdd(&B.stats[1], tot_cand);
     atomicAdd(&B.stats[2], tot_exact);
+    atomicAdd(&B.stats[4], tot_arc);
   }
   if (overflow) atomicOr(&B.stats[3], (unsigned long long)overflow);
 }

@@ -112,7 +112,7 @@ struct Batch {
   unsigned long long* h_hi;
   double* K;  // [R][bins]
   double* L;  // [R][bins]
-  unsigned long long* stats;   // [0] in_threshold [1] candidates [2] exact_path [3] overflow
+  unsigned long long* stats;   // [0] in_threshold [1] candidates [2] exact_path [3] overflow [4] arc (omega != 1)
   int* flags;                  // [R] generator fallback flags
   uint4* arcq;                 // [grid CTAs][warps][kArcRing] arc-path rings
 };
