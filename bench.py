@@ -215,12 +215,19 @@ def run_ours(args):
     from paper_1912_04753_b200.stripley import est, geom, rt
 
     rank, world, local = dist_env()
+    # STK_BENCH_DEVICE / STK_DIST_BACKEND let the multi-rank path be exercised
+    # on one GPU with gloo (host-side reductions only, no cross-rank kernels)
+    local = int(os.environ.get("STK_BENCH_DEVICE", local))
+    backend = os.environ.get("STK_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     group = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         group = dist.group.WORLD
     dev = devmod.get(local)
     lib = dev.lib
@@ -323,8 +330,9 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        a = torch.from_numpy(tot).cuda()
-        b = torch.from_numpy(tmax).cuda()
+        dev_ = "cuda" if backend == "nccl" else "cpu"
+        a = torch.from_numpy(tot).to(dev_)
+        b = torch.from_numpy(tmax).to(dev_)
         dist.all_reduce(a, op=dist.ReduceOp.SUM)
         dist.all_reduce(b, op=dist.ReduceOp.MAX)
         tot, tmax = a.cpu().numpy(), b.cpu().numpy()

@@ -704,7 +704,7 @@ int stk_create(stk_ctx** out, int device) {
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
-    if (const char* r = std::getenv("STK_STENCIL_RADIUS")) c->stencil_radius = std::max(1, std::min(2, std::atoi(r)));
+    if (const char* r = std::getenv("STK_STENCIL_RADIUS")) c->stencil_radius = std::max(1, std::min(3, std::atoi(r)));
     c->stats.ensure(8);
   } catch (const std::exception& e) {
     delete c;

@@ -624,12 +624,16 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       // stage the item's centers (<= 32) in shared memory: the inner loop
       // broadcasts one center to the 32 neighbour lanes
       __syncwarp();
+      bool cdeep = true;
       if (lane < (int)nc) {
         const uint32_t pos = sel_p ? cposl[start + lane] : start + lane;
+        const PtMeta<TT> m = pmeta[pos];
         cxy_w[lane] = pxy[pos];
-        cm_w[lane] = pmeta[pos];
+        cm_w[lane] = m;
         cpos_w[lane] = pos;
+        cdeep = (double)m.sq >= Qmax && m.vt >= Tmax;
       }
+      const bool item_deep = __all_sync(FULL_MASK, cdeep);
       __syncwarp();
       const uint32_t first_pos = sel_p ? 0u : start;  // lowest center position (non-selected)
       const int kx = (int)(cell % (uint32_t)G.nx);
@@ -675,7 +679,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       double2 nxy = make_double2(0.0, 0.0);
       PtMeta<TT> nm{0, 0, 0.0f, 0u};
       uint32_t jp = 0;
-      bool has = false, same_cell = false;
+      bool has = false, same_cell = false, tile_deep = false;
       for (;;) {
         const bool done = rows_left == 0;
         // the single drain site, ahead of new candidates so the ring never
@@ -704,11 +708,16 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             nm = pmeta[jp];
           }
           same_cell = r == 0 && jp < own_end;
+          tile_deep = __all_sync(FULL_MASK, !has || ((double)nm.sq >= Qmax && nm.vt >= Tmax));
           n_cand += (unsigned long long)min(32u, re - j0) * nc;
         }
         const int kend = min(kc + kArcChunk, (int)nc);
-        auto chunk = [&](auto own_tag) {
+        auto chunk = [&](auto own_tag, auto deep_tag) {
           constexpr bool OWN = decltype(own_tag)::value;
+          // DEEP: every center of the item and every neighbour of the tile has
+          // safe radius >= s_max and temporal threshold >= t_max, so all their
+          // in-threshold pairs have omega == 1 and v == 1: count only
+          constexpr bool DEEP = decltype(deep_tag)::value;
           for (int k = kc; k < kend; ++k) {
             const double2 c = cxy_w[k];  // center k (broadcast)
             const PtMeta<TT> cmk = cm_w[k];
@@ -739,14 +748,16 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               }
               bin = sb * ct + tb;
               atomicAdd(&S.cnt[bin], 2u);
+              n_in += 2;
+              if (DEEP) continue;
               half_i = du > cmk.vt;
               half_j = du > nm.vt;
               arc_i = q >= (double)cmk.sq;
               arc_j = q >= (double)nm.sq;
               const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
               if (h) atomicAdd(&S.half[bin], h);
-              n_in += 2;
             }
+            if (DEEP) continue;
             if (__any_sync(FULL_MASK, arc_i || arc_j)) {
               // class hint: does the circle reach two rectangle edges?
               bool ci = false, cj = false;
@@ -782,7 +793,14 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             }
           }
         };
-        if (r == 0 && j0 < own_end) chunk(std::true_type{}); else chunk(std::false_type{});
+        const bool own_tile = r == 0 && j0 < own_end;
+        if (tile_deep && item_deep) {
+          if (own_tile) chunk(std::true_type{}, std::true_type{});
+          else chunk(std::false_type{}, std::true_type{});
+        } else {
+          if (own_tile) chunk(std::true_type{}, std::false_type{});
+          else chunk(std::false_type{}, std::false_type{});
+        }
         // advance: next chunk, next tile, next non-empty row
         kc = kend;
         if (kc >= (int)nc) {
