@@ -538,6 +538,13 @@ __device__ __forceinline__ void drain_arcs(int count, int lane, const uint4* rin
 #ifndef STK_PAIR_MINB
 #define STK_PAIR_MINB 4
 #endif
+#ifndef STK_K_UNROLL
+#define STK_K_UNROLL 1
+#endif
+constexpr int kKUnroll = STK_K_UNROLL;
+#ifndef STK_SPECIALIZE
+#define STK_SPECIALIZE 1  // 2: own-tile x deep variants, 1: deep only, 0: one generic loop
+#endif
 template <typename TT>
 __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -718,6 +725,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           // safe radius >= s_max and temporal threshold >= t_max, so all their
           // in-threshold pairs have omega == 1 and v == 1: count only
           constexpr bool DEEP = decltype(deep_tag)::value;
+#pragma unroll kKUnroll
           for (int k = kc; k < kend; ++k) {
             const double2 c = cxy_w[k];  // center k (broadcast)
             const PtMeta<TT> cmk = cm_w[k];
@@ -794,6 +802,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           }
         };
         const bool own_tile = r == 0 && j0 < own_end;
+#if STK_SPECIALIZE == 2
         if (tile_deep && item_deep) {
           if (own_tile) chunk(std::true_type{}, std::true_type{});
           else chunk(std::false_type{}, std::true_type{});
@@ -801,6 +810,14 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           if (own_tile) chunk(std::true_type{}, std::false_type{});
           else chunk(std::false_type{}, std::false_type{});
         }
+#elif STK_SPECIALIZE == 1
+        (void)own_tile;
+        if (tile_deep && item_deep) chunk(std::true_type{}, std::true_type{});
+        else chunk(std::true_type{}, std::false_type{});
+#else
+        (void)own_tile;
+        chunk(std::true_type{}, std::false_type{});
+#endif
         // advance: next chunk, next tile, next non-empty row
         kc = kend;
         if (kc >= (int)nc) {
