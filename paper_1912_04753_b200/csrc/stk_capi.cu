@@ -452,7 +452,7 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   const int slots = (c->fast_rect && c->s_values.back() < 0.5 * smin_side) ? 8 : kAngleSlots;
   const size_t smem = pair_kernel_smem(P.bins, B.wide, slots);
   int per_sm = 0;
-  CK(pair_kernel_prepare(B.wide, smem, &per_sm));
+  CK(pair_kernel_prepare(B.wide, slots, smem, &per_sm));
   if (per_sm < 1) throw Unsupported("distance grid too large for the pair kernel's shared histogram");
   tasks_kernel<<<1, 1, 0, c->stream>>>(B, G, (uint32_t)(c->num_sms * per_sm));
   CK(cudaGetLastError());
@@ -468,7 +468,7 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   const uint64_t ctas = (uint64_t)c->num_sms * per_sm;
   c->arcq.ensure(ctas * kPairWarps * kArcRing * kArcClasses);
   A.B.arcq = c->arcq.p;
-  pair_kernel_launch(B.wide, (unsigned)ctas, smem, c->stream, A);
+  pair_kernel_launch(B.wide, slots, (unsigned)ctas, smem, c->stream, A);
   CK(cudaGetLastError());
   ++c->launches;
   CK(cudaEventRecord(e2, c->stream));

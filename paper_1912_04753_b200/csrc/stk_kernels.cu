@@ -438,70 +438,35 @@ __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas) {
 // x-y and y-x are equal); each ordered pair keeps its own center's weights.
 // Mapping: a warp item is <= 32 centers of one cell, staged in smem; lanes
 // hold 32 stencil neighbours in registers and loop over the centers.
-template <typename TT>
-struct PairSmem {
-  double2* cxy;             // [warps][32] item centers
-  PtMeta<TT>* cmeta;        // [warps][32]
-  uint32_t* cpos;           // [warps][32] sorted positions
-  double* angs;             // [warps][kAngleSlots][32] per-lane crossing scratch
-  double* Q;                // [kMaxAxis] squared-distance thresholds
-  TT* T;                    // [kMaxAxis] time thresholds (clamped to TT)
-  uint16_t* stab;           // [kBucketTable]
-  uint16_t* ttab;           // [kBucketTable]
-  unsigned long long* lo;   // [bins] arc-path fixed-point sums (low 64)
-  uint32_t* cnt;            // [bins]
-  uint32_t* half;           // [bins]
-  uint32_t* hi;             // [bins]
+// Shared memory of the pair kernel.  Every section the inner loops touch has
+// a compile-time offset (sizes depend only on template parameters); only the
+// arc-sum section (touched once per 32 arc pairs) follows the runtime-sized
+// count section.
+struct ArcSum {
+  unsigned long long lo;  // arc-path fixed-point sum, low 64 bits
+  uint32_t hi;            // carries into bit 64
+  uint32_t pad;
 };
 
-template <typename TT>
-__host__ __device__ inline size_t pair_smem_layout(uint32_t bins, int slots, size_t* off) {
-  size_t b = 0;
-  int k = 0;
-  auto take = [&](size_t bytes) {
-    b = (b + 15) & ~size_t(15);
-    off[k++] = b;
-    b += bytes;
-  };
-  take(sizeof(double2) * kPairWarps * 32);
-  take(sizeof(PtMeta<TT>) * kPairWarps * 32);
-  take(sizeof(uint32_t) * kPairWarps * 32);
-  take(sizeof(double) * kPairWarps * slots * 32);
-  take(sizeof(double) * kMaxAxis);
-  take(sizeof(TT) * kMaxAxis);
-  take(sizeof(uint16_t) * kBucketTable);
-  take(sizeof(uint16_t) * kBucketTable);
-  take(sizeof(unsigned long long) * bins);
-  take(sizeof(uint32_t) * bins);
-  take(sizeof(uint32_t) * bins);
-  take(sizeof(uint32_t) * bins);
-  return (b + 15) & ~size_t(15);
-}
+template <typename TT, int SLOTS>
+struct PairLayout {
+  __host__ __device__ static constexpr size_t al(size_t b) { return (b + 15) & ~size_t(15); }
+  static constexpr size_t cxy = 0;
+  static constexpr size_t cmeta = al(cxy + sizeof(double2) * kPairWarps * 32);
+  static constexpr size_t cpos = al(cmeta + sizeof(PtMeta<TT>) * kPairWarps * 32);
+  static constexpr size_t Q = al(cpos + sizeof(uint32_t) * kPairWarps * 32);
+  static constexpr size_t T = al(Q + sizeof(double) * kMaxAxis);
+  static constexpr size_t stab = al(T + sizeof(TT) * kMaxAxis);
+  static constexpr size_t ttab = al(stab + sizeof(uint16_t) * kBucketTable);
+  static constexpr size_t angs = al(ttab + sizeof(uint16_t) * kBucketTable);
+  static constexpr size_t ch = al(angs + sizeof(double) * kPairWarps * SLOTS * 32);
+  static size_t __host__ __device__ lh(uint32_t bins) { return al(ch + sizeof(uint2) * bins); }
+  static size_t __host__ __device__ total(uint32_t bins) { return al(lh(bins) + sizeof(ArcSum) * bins); }
+};
 
 size_t pair_kernel_smem(uint32_t bins, int wide, int slots) {
-  size_t off[12];
-  return wide ? pair_smem_layout<int64_t>(bins, slots, off)
-              : pair_smem_layout<int32_t>(bins, slots, off);
-}
-
-template <typename TT>
-__device__ __forceinline__ PairSmem<TT> carve(unsigned char* raw, uint32_t bins, int slots) {
-  size_t o[12];
-  pair_smem_layout<TT>(bins, slots, o);
-  PairSmem<TT> S;
-  S.cxy = (double2*)(raw + o[0]);
-  S.cmeta = (PtMeta<TT>*)(raw + o[1]);
-  S.cpos = (uint32_t*)(raw + o[2]);
-  S.angs = (double*)(raw + o[3]);
-  S.Q = (double*)(raw + o[4]);
-  S.T = (TT*)(raw + o[5]);
-  S.stab = (uint16_t*)(raw + o[6]);
-  S.ttab = (uint16_t*)(raw + o[7]);
-  S.lo = (unsigned long long*)(raw + o[8]);
-  S.cnt = (uint32_t*)(raw + o[9]);
-  S.half = (uint32_t*)(raw + o[10]);
-  S.hi = (uint32_t*)(raw + o[11]);
-  return S;
+  if (wide) return slots > 8 ? PairLayout<int64_t, 16>::total(bins) : PairLayout<int64_t, 8>::total(bins);
+  return slots > 8 ? PairLayout<int32_t, 16>::total(bins) : PairLayout<int32_t, 8>::total(bins);
 }
 
 // Exact weight of `count` queued arc-path ordered pairs (one per lane),
@@ -510,9 +475,9 @@ __device__ __forceinline__ PairSmem<TT> carve(unsigned char* raw, uint32_t bins,
 // position, bin | (v == 1/2) << 31, q = d^2 as two words}.
 __device__ __forceinline__ void drain_arcs(int count, int lane, const uint4* ring_q,
                                            uint32_t head, double* angs, int slots,
-                                           const double2* pxy, unsigned long long* s_lo,
-                                           uint32_t* s_hi, const RegionView& reg,
-                                           int* overflow, uint32_t* n_arc) {
+                                           const double2* pxy, ArcSum* s_arc,
+                                           const RegionView& reg, int* overflow,
+                                           uint32_t* n_arc) {
   if (lane >= count) return;
   const uint4 e = ring_q[(head + lane) & (kArcRing - 1)];
   const double2 c = pxy[e.x];
@@ -529,9 +494,9 @@ __device__ __forceinline__ void drain_arcs(int count, int lane, const uint4* rin
   fixed52_minus_one(term, &lo, &hi);
   const uint32_t bin = bw & 0x7fffffffu;
   if (lo | hi) {
-    const unsigned long long old = atomicAdd(&s_lo[bin], (unsigned long long)lo);
+    const unsigned long long old = atomicAdd(&s_arc[bin].lo, (unsigned long long)lo);
     if (old + lo < old) ++hi;
-    if (hi) atomicAdd(&s_hi[bin], (uint32_t)hi);
+    if (hi) atomicAdd(&s_arc[bin].hi, (uint32_t)hi);
   }
 }
 
@@ -545,16 +510,38 @@ constexpr int kKUnroll = STK_K_UNROLL;
 #ifndef STK_SPECIALIZE
 #define STK_SPECIALIZE 1  // 2: own-tile x deep variants, 1: deep only, 0: one generic loop
 #endif
-template <typename TT>
+template <typename TT, int SLOTS>
 __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_task, s_next;
+  using Lay = PairLayout<TT, SLOTS>;
   const Batch& B = A.B;
   const GridGeom& G = A.G;
   const BinView& BV = A.bins;
   const uint32_t cs = BV.cs, ct = BV.ct, bins = cs * ct;
-  const int slots = A.angle_slots;
-  const PairSmem<TT> S = carve<TT>(smem_raw, bins, slots);
+  constexpr int slots = SLOTS;
+  struct {
+    double2* cxy;
+    PtMeta<TT>* cmeta;
+    uint32_t* cpos;
+    double* Q;
+    TT* T;
+    uint16_t* stab;
+    uint16_t* ttab;
+    double* angs;
+    uint2* ch;  // (count, half-count) per bin
+    ArcSum* arc;
+  } S;
+  S.cxy = (double2*)(smem_raw + Lay::cxy);
+  S.cmeta = (PtMeta<TT>*)(smem_raw + Lay::cmeta);
+  S.cpos = (uint32_t*)(smem_raw + Lay::cpos);
+  S.Q = (double*)(smem_raw + Lay::Q);
+  S.T = (TT*)(smem_raw + Lay::T);
+  S.stab = (uint16_t*)(smem_raw + Lay::stab);
+  S.ttab = (uint16_t*)(smem_raw + Lay::ttab);
+  S.angs = (double*)(smem_raw + Lay::angs);
+  S.ch = (uint2*)(smem_raw + Lay::ch);
+  S.arc = (ArcSum*)(smem_raw + Lay::lh(bins));
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 
   for (uint32_t b = tid; b < cs; b += blockDim.x) S.Q[b] = BV.Q[b];
@@ -594,10 +581,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       s_next = 0;
     }
     for (uint32_t b = tid; b < bins; b += blockDim.x) {
-      S.lo[b] = 0ULL;
-      S.cnt[b] = 0u;
-      S.half[b] = 0u;
-      S.hi[b] = 0u;
+      S.ch[b] = make_uint2(0u, 0u);
+      S.arc[b].lo = 0ULL;
+      S.arc[b].hi = 0u;
     }
     __syncthreads();
     const uint32_t task = s_task;
@@ -701,7 +687,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           const uint32_t head = d0 ? qh0 : qh1;
           const int cnt_ = (int)min(pend, 32u);
           __syncwarp();
-          drain_arcs(cnt_, lane, arcq + (d0 ? 0 : kArcRing), head, angs, slots, pxy, S.lo, S.hi,
+          drain_arcs(cnt_, lane, arcq + (d0 ? 0 : kArcRing), head, angs, slots, pxy, S.arc,
                      A.reg, &overflow, &n_arc);
           if (d0) qh0 += (uint32_t)cnt_; else qh1 += (uint32_t)cnt_;
           continue;
@@ -755,7 +741,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
                 while (du > S.T[tb]) ++tb;
               }
               bin = sb * ct + tb;
-              atomicAdd(&S.cnt[bin], 2u);
+              atomicAdd(&S.ch[bin].x, 2u);
               n_in += 2;
               if (DEEP) continue;
               half_i = du > cmk.vt;
@@ -763,7 +749,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               arc_i = q >= (double)cmk.sq;
               arc_j = q >= (double)nm.sq;
               const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
-              if (h) atomicAdd(&S.half[bin], h);
+              if (h) atomicAdd(&S.ch[bin].y, h);
             }
             if (DEEP) continue;
             if (__any_sync(FULL_MASK, arc_i || arc_j)) {
@@ -841,12 +827,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     // flush the CTA histogram of pattern p (exact integer adds)
     const uint64_t hb = (uint64_t)p * bins;
     for (uint32_t b = tid; b < bins; b += blockDim.x) {
-      const uint32_t c = S.cnt[b];
-      if (c) atomicAdd(&B.h_cnt[hb + b], (unsigned long long)c);
-      const uint32_t h = S.half[b];
-      if (h) atomicAdd(&B.h_half[hb + b], (unsigned long long)h);
-      const unsigned long long lo = S.lo[b];
-      unsigned long long hi = S.hi[b];
+      const uint2 chb = S.ch[b];
+      if (chb.x) atomicAdd(&B.h_cnt[hb + b], (unsigned long long)chb.x);
+      if (chb.y) atomicAdd(&B.h_half[hb + b], (unsigned long long)chb.y);
+      const unsigned long long lo = S.arc[b].lo;
+      unsigned long long hi = S.arc[b].hi;
       if (lo) {
         const unsigned long long old = atomicAdd(&B.h_lo[hb + b], lo);
         if (old + lo < old) ++hi;
@@ -869,20 +854,27 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
 }
 
 // Host-side launch helpers (keep the kernel templates in this translation unit).
-cudaError_t pair_kernel_prepare(int wide, size_t smem, int* per_sm) {
-  // (dynamic shared memory only; the launch bounds fix the register budget)
-  const void* fn = wide ? (const void*)pair_kernel<int64_t> : (const void*)pair_kernel<int32_t>;
+static const void* pair_fn(int wide, int slots) {
+  if (wide) return slots > 8 ? (const void*)pair_kernel<int64_t, 16> : (const void*)pair_kernel<int64_t, 8>;
+  return slots > 8 ? (const void*)pair_kernel<int32_t, 16> : (const void*)pair_kernel<int32_t, 8>;
+}
+
+cudaError_t pair_kernel_prepare(int wide, int slots, size_t smem, int* per_sm) {
+  const void* fn = pair_fn(wide, slots);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fn, kPairWarps * 32, smem);
 }
 
-void pair_kernel_launch(int wide, unsigned ctas, size_t smem, cudaStream_t stream,
+void pair_kernel_launch(int wide, int slots, unsigned ctas, size_t smem, cudaStream_t stream,
                         const PairArgs& A) {
-  if (wide)
-    pair_kernel<int64_t><<<ctas, kPairWarps * 32, smem, stream>>>(A);
-  else
-    pair_kernel<int32_t><<<ctas, kPairWarps * 32, smem, stream>>>(A);
+  if (wide) {
+    if (slots > 8) pair_kernel<int64_t, 16><<<ctas, kPairWarps * 32, smem, stream>>>(A);
+    else pair_kernel<int64_t, 8><<<ctas, kPairWarps * 32, smem, stream>>>(A);
+  } else {
+    if (slots > 8) pair_kernel<int32_t, 16><<<ctas, kPairWarps * 32, smem, stream>>>(A);
+    else pair_kernel<int32_t, 8><<<ctas, kPairWarps * 32, smem, stream>>>(A);
+  }
 }
 
 // ============================================================ K5 finalize
