@@ -507,6 +507,9 @@ __device__ __forceinline__ void drain_arcs(int count, int lane, const uint4* rin
 #define STK_K_UNROLL 1
 #endif
 constexpr int kKUnroll = STK_K_UNROLL;
+#ifndef STK_PREFETCH
+#define STK_PREFETCH 1
+#endif
 #ifndef STK_SPECIALIZE
 #define STK_SPECIALIZE 1  // 2: own-tile x deep variants, 1: deep only, 0: one generic loop
 #endif
@@ -700,6 +703,12 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             nxy = pxy[jp];
             nm = pmeta[jp];
           }
+#if STK_PREFETCH
+          if (jp + 32 < re) {  // next tile of this row into L1 while this one is processed
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pxy + jp + 32));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pmeta + jp + 32));
+          }
+#endif
           same_cell = r == 0 && jp < own_end;
           tile_deep = __all_sync(FULL_MASK, !has || ((double)nm.sq >= Qmax && nm.vt >= Tmax));
           n_cand += (unsigned long long)min(32u, re - j0) * nc;
