@@ -466,7 +466,7 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   A.bins = bin_view(c);
   A.reg = region_view(c);
   const uint64_t ctas = (uint64_t)c->num_sms * per_sm;
-  c->arcq.ensure(ctas * kPairWarps * kArcRing * kArcClasses);
+  c->arcq.ensure(ctas * kPairWarps * kArcRing);
   A.B.arcq = c->arcq.p;
   pair_kernel_launch(B.wide, slots, (unsigned)ctas, smem, c->stream, A);
   CK(cudaGetLastError());

@@ -565,14 +565,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   double2* cxy_w = S.cxy + w * 32;
   PtMeta<TT>* cm_w = S.cmeta + w * 32;
   uint32_t* cpos_w = S.cpos + w * 32;
-  uint4* arcq = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * kArcRing * kArcClasses;
-  const bool classes = A.reg.rect != 0;
-  // a circle of radius d around c reaches two rectangle edges (a corner:
-  // up to 8 crossings) only if both edge distances are below d; a hint that
-  // routes entries to the ring whose drains run uniform trip counts
-  const float rxmin = (float)A.reg.xmin, rxmax = (float)A.reg.xmax;
-  const float rymin = (float)A.reg.ymin, rymax = (float)A.reg.ymax;
-  const int single_step = BV.single_step;
+  uint4* arcq = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * kArcRing;
+    const int single_step = BV.single_step;
   double* angs = S.angs + w * slots * 32;
   int overflow = 0;
   unsigned long long tot_in = 0, tot_cand = 0, tot_exact = 0, tot_arc = 0;
@@ -663,7 +657,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         }
       }
       const unsigned nonempty = __ballot_sync(FULL_MASK, my_rb < my_re);
-      uint32_t qh0 = 0, qt0 = 0, qh1 = 0, qt1 = 0;  // arc rings: head / tail (monotone)
+      uint32_t qh = 0, qt = 0;  // arc ring head / tail (monotone)
       uint32_t n_in = 0, n_exact = 0, n_arc = 0;
       unsigned long long n_cand = 0;
       // flat walk over (row, tile, center chunk); one inline copy of the drain
@@ -681,18 +675,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         // the single drain site, ahead of new candidates so the ring never
         // holds more than 31 + kArcChunk * 64 entries: full batches while
         // any are pending, and the remainder at the end
-        const uint32_t pend0 = qt0 - qh0, pend1 = qt1 - qh1;
-        if (pend0 > (uint32_t)kArcRing || pend1 > (uint32_t)kArcRing) overflow |= 2;  // never
-        const bool d0 = pend0 >= 32 || (done && pend0 > 0);
-        const bool d1 = !d0 && (pend1 >= 32 || (done && pend1 > 0));
-        if (d0 || d1) {
-          const uint32_t pend = d0 ? pend0 : pend1;
-          const uint32_t head = d0 ? qh0 : qh1;
-          const int cnt_ = (int)min(pend, 32u);
+        const uint32_t pending = qt - qh;
+        if (pending > (uint32_t)kArcRing) overflow |= 2;  // must never happen: reported as an error
+        if (pending >= 32 || (done && pending > 0)) {
+          const int cnt_ = (int)min(pending, 32u);
           __syncwarp();
-          drain_arcs(cnt_, lane, arcq + (d0 ? 0 : kArcRing), head, angs, slots, pxy, S.arc,
-                     A.reg, &overflow, &n_arc);
-          if (d0) qh0 += (uint32_t)cnt_; else qh1 += (uint32_t)cnt_;
+          drain_arcs(cnt_, lane, arcq, qh, angs, slots, pxy, S.arc, A.reg, &overflow, &n_arc);
+          qh += (uint32_t)cnt_;
           continue;
         }
         if (done) break;
@@ -761,37 +750,18 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               if (h) atomicAdd(&S.ch[bin].y, h);
             }
             if (DEEP) continue;
-            if (__any_sync(FULL_MASK, arc_i || arc_j)) {
-              // class hint: does the circle reach two rectangle edges?
-              bool ci = false, cj = false;
-              if (classes) {
-                const float qf = (float)q * 1.0001f;
-                const float hxi = fminf((float)c.x - rxmin, rxmax - (float)c.x);
-                const float hyi = fminf((float)c.y - rymin, rymax - (float)c.y);
-                const float hxj = fminf((float)nxy.x - rxmin, rxmax - (float)nxy.x);
-                const float hyj = fminf((float)nxy.y - rymin, rymax - (float)nxy.y);
-                ci = hxi * hxi < qf && hyi * hyi < qf;
-                cj = hxj * hxj < qf && hyj * hyj < qf;
-              }
+            const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
+            const unsigned mj = __ballot_sync(FULL_MASK, arc_j);
+            if (mi | mj) {
               const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
-              const uint4 ei = make_uint4(cpos_w[k], bin | (half_i ? 0x80000000u : 0u), qlo, qhi);
-              const uint4 ej = make_uint4(jp, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
-              const unsigned mi0 = __ballot_sync(FULL_MASK, arc_i && !ci);
-              const unsigned mi1 = __ballot_sync(FULL_MASK, arc_i && ci);
-              const unsigned mj0 = __ballot_sync(FULL_MASK, arc_j && !cj);
-              const unsigned mj1 = __ballot_sync(FULL_MASK, arc_j && cj);
-              if (arc_i) {
-                if (!ci) arcq[(qt0 + __popc(mi0 & lanemask_lt)) & (kArcRing - 1)] = ei;
-                else arcq[kArcRing + ((qt1 + __popc(mi1 & lanemask_lt)) & (kArcRing - 1))] = ei;
-              }
-              qt0 += __popc(mi0);
-              qt1 += __popc(mi1);
-              if (arc_j) {
-                if (!cj) arcq[(qt0 + __popc(mj0 & lanemask_lt)) & (kArcRing - 1)] = ej;
-                else arcq[kArcRing + ((qt1 + __popc(mj1 & lanemask_lt)) & (kArcRing - 1))] = ej;
-              }
-              qt0 += __popc(mj0);
-              qt1 += __popc(mj1);
+              if (arc_i)
+                arcq[(qt + __popc(mi & lanemask_lt)) & (kArcRing - 1)] =
+                    make_uint4(cpos_w[k], bin | (half_i ? 0x80000000u : 0u), qlo, qhi);
+              qt += __popc(mi);
+              if (arc_j)
+                arcq[(qt + __popc(mj & lanemask_lt)) & (kArcRing - 1)] =
+                    make_uint4(jp, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
+              qt += __popc(mj);
               n_exact += (uint32_t)arc_i + (uint32_t)arc_j;
             }
           }

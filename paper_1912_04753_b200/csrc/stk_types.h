@@ -17,8 +17,7 @@ constexpr int kRingSmem = 32;      // ring vertices staged in shared memory (bit
 #define STK_ARC_CHUNK 12
 #endif
 constexpr int kArcChunk = STK_ARC_CHUNK;        // candidate steps between arc drains
-constexpr int kArcRing = 1024;      // per-warp arc ring entries per class (> 31 + kArcChunk * 64)
-constexpr int kArcClasses = 2;      // rectangles: single-edge vs corner entries drain separately
+constexpr int kArcRing = 1024;      // per-warp arc ring entries (> 31 + kArcChunk * 64)
 
 // Study region on the device (geom::StudyRegion, geometry.hpp:95-120).
 struct RegionView {
