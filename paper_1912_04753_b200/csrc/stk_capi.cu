@@ -176,6 +176,14 @@ RegionView region_view(stk_ctx* c) {
   const double S = std::max(1.0, c->maxabs + smax);
   const double min_edge = std::max(std::min(c->xmax - c->xmin, c->ymax - c->ymin), 1e-300);
   r.box_m = 4e-12 * S * std::max(1.0, S / min_edge);
+  for (int i = 0; i < 4; ++i)
+    r.rv[i] = (r.rect && c->ring.size() == 8) ? make_double2(c->ring[2 * i], c->ring[2 * i + 1])
+                                              : make_double2(0.0, 0.0);
+  // the closed form needs the reach margin d*1e-6 far above
+  // coordinate rounding (d >= 1e-8 S) and the outside probe clear of every
+  // on_segment tolerance (d - h > 4 box_m)
+  r.sw_dmin = 1e-8 * S;
+  r.sw_margin = 4.0 * r.box_m;
   return r;
 }
 
@@ -466,7 +474,7 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   A.bins = bin_view(c);
   A.reg = region_view(c);
   const uint64_t ctas = (uint64_t)c->num_sms * per_sm;
-  c->arcq.ensure(ctas * kPairWarps * kArcRing);
+  c->arcq.ensure(ctas * kPairWarps * (kArcRing + kCplxRing));
   A.B.arcq = c->arcq.p;
   pair_kernel_launch(B.wide, slots, (unsigned)ctas, smem, c->stream, A);
   CK(cudaGetLastError());

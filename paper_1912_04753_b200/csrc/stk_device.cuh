@@ -347,6 +347,59 @@ __device__ STK_WEIGHT_INLINE double spatial_weight_buf(double cx, double cy, dou
   return inside_span / kTwoPi;
 }
 
+// spatial_isotropic_weight in closed form for the dominant rectangle case:
+// the center strictly inside, exactly one edge within reach d*(1+1e-6) and
+// that edge's quadratic accepted (the same expression as the reference, so
+// the accept / reject decision is identical).  The reference then finds two
+// crossings strictly inside the edge (the perpendicular edges are out of
+// reach, so the chord ends lie >= 1e-6 d inside the segment), two distinct
+// angles (separation 2*theta >= 4e-5), an outside arc of 2*theta whose
+// midpoint probe lies beyond the edge by ~(d - h) > 4 box_m (PIP false) and
+// an inside arc whose probe is >= 1e-6 d inside (PIP true):
+//   omega_ref = (2*pi - 2*theta_ref) / (2*pi),  cos(theta) = h / d.
+// theta_ref carries the reference's own rounding (the quadratic's
+// cancellation: <= 2^-53 * scale / (len * sqrt(disc) * d) rad), which the
+// gate qa*disc*d^2 >= 1e-10*scale^2 bounds by ~1e-11; ours, from
+// atan2(sqrt((d-h)(d+h)), h), is within ~1e-11 too.
+// Returns -1 when the gate fails (the caller uses the general routine).
+__device__ __forceinline__ double rect_single_edge_weight(double cx, double cy, double d,
+                                                          const RegionView& R) {
+  if (d <= 0.0) return 1.0;
+  if (!(cx > R.xmin && cx < R.xmax && cy > R.ymin && cy < R.ymax) || d < R.sw_dmin) return -1.0;
+  const double reach = d * (1.0 + 1e-6);
+  int m = 0;
+  double2 A = R.rv[0], Bv = R.rv[0];
+  double h = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double2 a = R.rv[(i + 3) & 3], b = R.rv[i];
+    const double hi = a.x == b.x ? fabs(a.x - cx) : fabs(a.y - cy);
+    if (hi <= reach) {
+      ++m;
+      A = a;
+      Bv = b;
+      h = hi;
+    }
+  }
+  if (m == 0) return 1.0;  // the reference accepts no edge (reach argument)
+  if (m > 1) return -1.0;
+  const double r2 = d * d;
+  const double dx = Bv.x - A.x, dy = Bv.y - A.y;
+  const double fx = A.x - cx, fy = A.y - cy;
+  const double qa = dx * dx + dy * dy;
+  const double qb = 2.0 * (fx * dx + fy * dy);
+  const double qc = fx * fx + fy * fy - r2;
+  const double disc = qb * qb - 4.0 * qa * qc;
+  const double scale = qb * qb + fabs(4.0 * qa * qc);
+  if (!(qa != 0.0 && disc > 1e-9 * scale)) return 1.0;  // no crossing: omega == 1
+  if (qa * disc * r2 < 1e-10 * scale * scale) return -1.0;
+  const double dm = d - h;
+  if (dm <= R.sw_margin + 1e-12 * d) return -1.0;
+  const double w = sqrt(dm * (d + h));
+  const double theta = fast_atan2(w, h);
+  return 1.0 - theta * 0.31830988618379067154;  // 1 - theta / pi
+}
+
 // Squared radius below which spatial_weight() provably returns exactly 1.0
 // for this center (the circle stays strictly inside every edge's reach by a
 // relative margin far above the rounding error of the reference's quadratic;

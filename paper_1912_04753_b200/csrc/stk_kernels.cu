@@ -469,24 +469,10 @@ size_t pair_kernel_smem(uint32_t bins, int wide, int slots) {
   return slots > 8 ? PairLayout<int32_t, 16>::total(bins) : PairLayout<int32_t, 8>::total(bins);
 }
 
-// Exact weight of `count` queued arc-path ordered pairs (one per lane),
-// accumulated into the CTA histogram as 128-bit fixed point of (1/(omega*v) - 1).
-// Entries live in the warp's ring (global, L1/L2-resident): {center sorted
-// position, bin | (v == 1/2) << 31, q = d^2 as two words}.
-__device__ __forceinline__ void drain_arcs(int count, int lane, const uint4* ring_q,
-                                           uint32_t head, double* angs, int slots,
-                                           const double2* pxy, ArcSum* s_arc,
-                                           const RegionView& reg, int* overflow,
-                                           uint32_t* n_arc) {
-  if (lane >= count) return;
-  const uint4 e = ring_q[(head + lane) & (kArcRing - 1)];
-  const double2 c = pxy[e.x];
-  const double q = __hiloint2double((int)e.w, (int)e.z);
-  const uint32_t bw = e.y;
-  const double d = sqrt(q);
-  double ws = -1.0;
-  if (reg.nv <= 32) ws = spatial_weight_buf(c.x, c.y, d, reg, angs + lane, 32, slots / 2);
-  if (ws < 0.0) ws = spatial_weight(c.x, c.y, d, reg.ring, reg.nv, reg.maxabs, overflow);
+// Adds one arc-path ordered pair to the CTA histogram as 128-bit fixed point
+// of (1/(omega*v) - 1); bw = bin | (v == 1/2) << 31.
+__device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, ArcSum* s_arc,
+                                             uint32_t* n_arc) {
   if (ws != 1.0) ++*n_arc;                           // omega != 1 (SURVEY's arc-pair definition)
   const double w = ws * ((bw >> 31) ? 0.5 : 1.0);  // edge::pair_weight (edge_correction.cpp:88-103)
   const double term = 1.0 / w;                      // PairHistogram::add(.., 1.0 / w)
@@ -498,6 +484,51 @@ __device__ __forceinline__ void drain_arcs(int count, int lane, const uint4* rin
     if (old + lo < old) ++hi;
     if (hi) atomicAdd(&s_arc[bin].hi, (uint32_t)hi);
   }
+}
+
+// Ring entries: {center sorted position, bin | (v == 1/2) << 31, q = d^2 as
+// two words}, in the warp's rings (global, L1/L2-resident).
+//
+// Main ring, 32 entries at a time: rectangle entries that pass the closed
+// form's gate are weighted here; the rest (and every entry of a general
+// polygon) move to the warp's deferred ring, so the general routine runs on
+// full warps of entries that need it.
+__device__ __forceinline__ void drain_main(int count, int lane, const uint4* ring, uint32_t head,
+                                           uint4* cring, uint32_t* ctail, unsigned lanemask_lt,
+                                           const double2* pxy, ArcSum* s_arc,
+                                           const RegionView& reg, uint32_t* n_arc) {
+  const bool valid = lane < count;
+  uint4 e = make_uint4(0u, 0u, 0u, 0u);
+  double ws = -1.0;
+  if (valid) {
+    e = ring[(head + lane) & (kArcRing - 1)];
+    if (reg.rect) {
+      const double2 c = pxy[e.x];
+      const double d = sqrt(__hiloint2double((int)e.w, (int)e.z));
+      ws = rect_single_edge_weight(c.x, c.y, d, reg);
+    }
+  }
+  const bool defer = valid && ws < 0.0;
+  const unsigned m = __ballot_sync(FULL_MASK, defer);
+  if (defer) cring[(*ctail + __popc(m & lanemask_lt)) & (kCplxRing - 1)] = e;
+  *ctail += __popc(m);
+  if (valid && !defer) add_arc_term(ws, e.y, s_arc, n_arc);
+}
+
+// Deferred ring: the reference's general spatial_isotropic_weight.
+__device__ __forceinline__ void drain_general(int count, int lane, const uint4* cring,
+                                              uint32_t head, double* angs, int slots,
+                                              const double2* pxy, ArcSum* s_arc,
+                                              const RegionView& reg, int* overflow,
+                                              uint32_t* n_arc) {
+  if (lane >= count) return;
+  const uint4 e = cring[(head + lane) & (kCplxRing - 1)];
+  const double2 c = pxy[e.x];
+  const double d = sqrt(__hiloint2double((int)e.w, (int)e.z));
+  double ws = -1.0;
+  if (reg.nv <= 32) ws = spatial_weight_buf(c.x, c.y, d, reg, angs + lane, 32, slots / 2);
+  if (ws < 0.0) ws = spatial_weight(c.x, c.y, d, reg.ring, reg.nv, reg.maxabs, overflow);
+  add_arc_term(ws, e.y, s_arc, n_arc);
 }
 
 #ifndef STK_PAIR_MINB
@@ -565,7 +596,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   double2* cxy_w = S.cxy + w * 32;
   PtMeta<TT>* cm_w = S.cmeta + w * 32;
   uint32_t* cpos_w = S.cpos + w * 32;
-  uint4* arcq = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * kArcRing;
+  uint4* arcq = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * (kArcRing + kCplxRing);
+  uint4* cring = arcq + kArcRing;
     const int single_step = BV.single_step;
   double* angs = S.angs + w * slots * 32;
   int overflow = 0;
@@ -657,7 +689,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         }
       }
       const unsigned nonempty = __ballot_sync(FULL_MASK, my_rb < my_re);
-      uint32_t qh = 0, qt = 0;  // arc ring head / tail (monotone)
+      uint32_t qh = 0, qt = 0;    // arc ring head / tail (monotone)
+      uint32_t ch_ = 0, ct_ = 0;  // deferred ring head / tail
       uint32_t n_in = 0, n_exact = 0, n_arc = 0;
       unsigned long long n_cand = 0;
       // flat walk over (row, tile, center chunk); one inline copy of the drain
@@ -675,12 +708,20 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         // the single drain site, ahead of new candidates so the ring never
         // holds more than 31 + kArcChunk * 64 entries: full batches while
         // any are pending, and the remainder at the end
-        const uint32_t pending = qt - qh;
+        const uint32_t pending = qt - qh, cpending = ct_ - ch_;
         if (pending > (uint32_t)kArcRing) overflow |= 2;  // must never happen: reported as an error
+        // deferred entries first (<= 31 + 32 pending), then the main ring
+        if (cpending >= 32 || (done && pending == 0 && cpending > 0)) {
+          const int cnt_ = (int)min(cpending, 32u);
+          __syncwarp();
+          drain_general(cnt_, lane, cring, ch_, angs, slots, pxy, S.arc, A.reg, &overflow, &n_arc);
+          ch_ += (uint32_t)cnt_;
+          continue;
+        }
         if (pending >= 32 || (done && pending > 0)) {
           const int cnt_ = (int)min(pending, 32u);
           __syncwarp();
-          drain_arcs(cnt_, lane, arcq, qh, angs, slots, pxy, S.arc, A.reg, &overflow, &n_arc);
+          drain_main(cnt_, lane, arcq, qh, cring, &ct_, lanemask_lt, pxy, S.arc, A.reg, &n_arc);
           qh += (uint32_t)cnt_;
           continue;
         }
@@ -949,8 +990,9 @@ __global__ void weights_kernel(const double* cx, const double* cy, const double*
     w[i] = 0.0;
     return;
   }
-  double ws = -1.0;
-  if (reg.nv <= 32)
+  // the pair kernel's order: closed form (rectangles), then the general routines
+  double ws = reg.rect ? rect_single_edge_weight(cx[i], cy[i], d[i], reg) : -1.0;
+  if (ws < 0.0 && reg.nv <= 32)
     ws = spatial_weight_buf(cx[i], cy[i], d[i], reg, angs + threadIdx.x, 128, kAngleSlots / 2);
   if (ws < 0.0) ws = spatial_weight(cx[i], cy[i], d[i], reg.ring, reg.nv, reg.maxabs, overflow);
   w[i] = ws;

@@ -18,6 +18,7 @@ constexpr int kRingSmem = 32;      // ring vertices staged in shared memory (bit
 #endif
 constexpr int kArcChunk = STK_ARC_CHUNK;        // candidate steps between arc drains
 constexpr int kArcRing = 1024;      // per-warp arc ring entries (> 31 + kArcChunk * 64)
+constexpr int kCplxRing = 128;      // per-warp ring of entries deferred to the general weight (> 63)
 
 // Study region on the device (geom::StudyRegion, geometry.hpp:95-120).
 struct RegionView {
@@ -28,6 +29,9 @@ struct RegionView {
   double maxabs;        // max |coordinate| over the ring
   int rect;             // 4-vertex axis-aligned rectangle (exact fast paths apply)
   double box_m;         // rect: on_segment is impossible farther than this outside the box
+  double2 rv[4];        // rect: the ring's vertices (kernel-parameter copy)
+  double sw_dmin;       // rect single-edge closed form: smallest radius it accepts
+  double sw_margin;     // ... and smallest d - h (outside midpoint clear of the boundary)
 };
 
 // Distance grid in the forms the kernels consume.
@@ -113,7 +117,7 @@ struct Batch {
   double* L;  // [R][bins]
   unsigned long long* stats;   // [0] in_threshold [1] candidates [2] exact_path [3] overflow [4] arc (omega != 1)
   int* flags;                  // [R] generator fallback flags
-  uint4* arcq;                 // [grid CTAs][warps][kArcRing] arc-path rings
+  uint4* arcq;                 // [grid CTAs][warps][kArcRing + kCplxRing] arc-path rings
 };
 
 }  // namespace stk

@@ -91,6 +91,50 @@ def weights():
     np.savez_compressed(os.path.join(OUT, "weights.npz"), count=len(rings), **out)
 
 
+def rect_stress():
+    """Rectangle (center, d) cases around the single-edge closed form's gates:
+    circles just reaching one edge (d/h - 1 from 1e-15 to 1), just missing it,
+    near corners, tiny radii, and regions at large coordinate offsets."""
+    rng = np.random.default_rng(11)
+    out = {}
+    rects = [(0.0, 0.0, 10000.0, 10000.0), (500000.0, 4000000.0, 550000.0, 4030000.0),
+             (-3.5, 2.25, 1.5, 9.0), (0.0, 0.0, 100000.0, 100000.0)]
+    for k, (x0, y0, x1, y1) in enumerate(rects):
+        ring = np.array([[x0, y0], [x1, y0], [x1, y1], [x0, y1]], float)
+        W, H = x1 - x0, y1 - y0
+        cx, cy, dd, ww = [], [], [], []
+        while len(cx) < 1500:
+            edge = rng.integers(4)
+            h = W * 10.0 ** rng.uniform(-7, -0.4)
+            along = rng.uniform(0.0, 1.0)
+            if edge == 0:
+                px, py = x0 + h, y0 + along * H
+            elif edge == 1:
+                px, py = x1 - h, y0 + along * H
+            elif edge == 2:
+                px, py = x0 + along * W, y0 + h
+            else:
+                px, py = x0 + along * W, y1 - h
+            if not (x0 < px < x1 and y0 < py < y1):
+                continue
+            h_true = min(px - x0, x1 - px, py - y0, y1 - py)
+            mode = rng.integers(4)
+            if mode == 0:
+                d = h_true * (1.0 + 10.0 ** rng.uniform(-15, 0))
+            elif mode == 1:
+                d = h_true * (1.0 - 10.0 ** rng.uniform(-15, -1))
+            elif mode == 2:
+                d = h_true * rng.uniform(1.0, 3.0)
+            else:
+                d = h_true + 10.0 ** rng.uniform(-12, 0) * max(abs(x0), abs(x1), 1.0) * 1e-3
+            cx.append(px); cy.append(py); dd.append(d)
+            ww.append(ref.spatial_weight(px, py, d, ring))
+        out[f"{k}_ring"] = ring
+        out[f"{k}_cx"] = np.array(cx); out[f"{k}_cy"] = np.array(cy)
+        out[f"{k}_d"] = np.array(dd); out[f"{k}_w"] = np.array(ww)
+    np.savez_compressed(os.path.join(OUT, "rect_stress.npz"), count=len(rects), **out)
+
+
 def c1():
     """C1 (configs[0]) through the reference: K, per-bin counts, in_threshold."""
     cfg = configs.CONFIGS["C1"]
@@ -111,5 +155,5 @@ def mt():
 
 if __name__ == "__main__":
     oracle.build(with_ref=True)
-    sample(); polygons(); weights(); c1(); mt()
+    sample(); polygons(); weights(); rect_stress(); c1(); mt()
     print("golden fixtures written to", OUT)

@@ -70,6 +70,27 @@ def test_spatial_weights_vs_reference(api):
         assert rel_err(w, w_ref) <= 1e-12, k
 
 
+def test_rect_closed_form_vs_reference(api):
+    """Rectangle weights around the single-edge closed form's gates (near
+    tangency, near misses, tiny radii, large coordinate offsets) against the
+    reference's edge::spatial_isotropic_weight (tests/golden/rect_stress.npz).
+    Tolerance: 1e-10 relative per weight (DESIGN.md §4.5 bounds the closed
+    form's deviation from the reference by ~1e-11)."""
+    from paper_1912_04753_b200 import _lib
+
+    g = golden("rect_stress.npz")
+    dev, geom = api["dev"], api["geom"]
+    for k in range(int(g["count"])):
+        dev.configure(geom.StudyRegion(g[f"{k}_ring"], 0, 1))
+        cx, cy, d, w_ref = g[f"{k}_cx"], g[f"{k}_cy"], g[f"{k}_d"], g[f"{k}_w"]
+        w = np.zeros_like(w_ref)
+        dev.check(dev.lib.stk_spatial_weights(dev.h, _lib.ptr(cx), _lib.ptr(cy), _lib.ptr(d),
+                                              len(cx), _lib.ptr(w)))
+        assert np.array_equal(w == 1.0, w_ref == 1.0), k  # same accept / reject decisions
+        print("rect_stress", k, "max rel err", rel_err(w, w_ref))
+        assert rel_err(w, w_ref) <= 1e-10, (k, rel_err(w, w_ref))
+
+
 def test_edge_correction_known_answers(api):
     """proj/tests/test_edge_correction.cpp:10-29 through the device."""
     from paper_1912_04753_b200 import _lib
