@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--sims", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-sims", type=int, default=1)
+    ap.add_argument("--ring", type=int, default=0,
+                    help="replace the square by a regular polygon of this many vertices "
+                         "(acceptance criterion 6 shape)")
     return ap.parse_args()
 
 
@@ -108,10 +111,12 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def workload(cfg_name, sims_override=None):
+def workload(cfg_name, sims_override=None, ring_vertices=0):
     from paper_1912_04753_b200 import configs
 
     cfg = configs.CONFIGS[cfg_name]
+    if ring_vertices:
+        cfg = cfg.with_ring(ring_vertices)
     s, tv = configs.grid_values(cfg)
     sims = cfg.sims if sims_override is None else sims_override
     return cfg, s, tv, sims
@@ -148,7 +153,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    cfg, s, tv, sims = workload(args.config, args.sims)
+    cfg, s, tv, sims = workload(args.config, args.sims, args.ring)
     import oracle
 
     x, y, t = observed_points_cpu(cfg)
@@ -198,7 +203,9 @@ def observed_points_cpu(cfg):
 
 
 def config_dict(cfg, sims, world):
-    return {"workload": f"{cfg.name}: {cfg.kind} N={cfg.n} in {cfg.extent_m:g} m square x "
+    shape = (f"{cfg.ring_vertices}-vertex polygon inscribed in a {cfg.extent_m:g} m square"
+             if cfg.ring_vertices else f"{cfg.extent_m:g} m square")
+    return {"workload": f"{cfg.name}: {cfg.kind} N={cfg.n} in {shape} x "
                         f"{cfg.period_s} s, grid {cfg.s_max:g} m/{cfg.t_max} s, 1 observed + "
                         f"{sims} CSR realisations (rt::run_job)",
             "n_points": cfg.n, "realisations": 1 + sims, "parallelism": f"realisations+pairs x{world}",
@@ -231,7 +238,7 @@ def run_ours(args):
         group = dist.group.WORLD
     dev = devmod.get(local)
     lib = dev.lib
-    cfg, s, tv, sims = workload(args.config, args.sims)
+    cfg, s, tv, sims = workload(args.config, args.sims, args.ring)
     region = geom.StudyRegion(cfg.ring(), 0, cfg.period_s)
     grid = est.DistanceGrid(s, tv)
     dev.configure(region, grid)

@@ -101,7 +101,7 @@ int stk_estimate_surface(stk_ctx* ctx, const double* x, const double* y, const i
 /* Per-bin (pre-cumulative) histogram of est::PairHistogram
  * (core/include/stripley/estimator.hpp:55-81) plus exact per-bin counts.
  * hist[b] is the exact sum of 1/(omega*v) rounded once; sum_hi/sum_lo (may
- * be NULL) give it as 128-bit fixed point with 52 fractional bits.
+ * be NULL) give it as 128-bit fixed point with 53 fractional bits.
  * Shards: the pair work of the pattern is split into nshards disjoint slices;
  * shard s computes only its slice (counts/sums add exactly across shards —
  * the single-huge-pattern multi-GPU path).  nshards = 1 for the whole. */

@@ -16,8 +16,9 @@
  * no FMA contraction: the distance is sqrt(RN(RN(dx*dx)+RN(dy*dy))) exactly as
  * the reference Release build computes it.
  *
- * Weighted sums are accumulated EXACTLY as 128-bit fixed point with 52
- * fractional bits (every term 1/w >= 1 has ulp >= 2^-52), then rounded once
+ * Weighted sums are accumulated EXACTLY as 128-bit fixed point with 53
+ * fractional bits (every term 1/w >= 1/2 has ulp >= 2^-53; the reference's
+ * omega can exceed 1 by an ulp, so terms just below 1 occur), then rounded once
  * to double.  The reference uses Kahan summation (core/include/stripley/
  * estimator.hpp:61-67), which agrees with the exact sum to ~1 ulp; both are
  * well inside the 1e-9 contract.
@@ -249,21 +250,21 @@ int orc_bin_pair(const double* s_values, uint32_t cs, const int64_t* t_values, u
   return 1;
 }
 
-/* 1/w as exact 128-bit fixed point with 52 fractional bits (w in (0,1] so
- * 1/w >= 1 and its ulp is >= 2^-52). */
-static u128 fixed52(double term) {
+/* 1/w as exact 128-bit fixed point with 53 fractional bits (w = omega*v with
+ * omega <= 1 + ulps, v >= 1/2, so 1/w >= 1/2 and its ulp is >= 2^-53). */
+static u128 fixed53(double term) {
   int e;
   const double m = frexp(term, &e); /* term = m * 2^e, m in [0.5,1) */
   const uint64_t mant = (uint64_t)ldexp(m, 53); /* exact 53-bit integer */
-  const int sh = e - 53 + 52;                   /* term * 2^52 = mant * 2^sh */
+  const int sh = e;                             /* term * 2^53 = mant * 2^e */
   if (sh >= 0) return (sh >= 128) ? ~(u128)0 : ((u128)mant << sh);
-  return (u128)(mant >> (-sh)); /* never taken for term >= 1 */
+  return (u128)(mant >> (-sh)); /* never taken for term >= 1/2 */
 }
 
-/* Correctly rounded double of a 128-bit fixed-point value (52 frac bits). */
+/* Correctly rounded double of a 128-bit fixed-point value (53 frac bits). */
 double orc_fixed_to_double(uint64_t hi, uint64_t lo) {
   const u128 v = ((u128)hi << 64) | lo;
-  return ldexp((double)v, -52); /* gcc's u128 -> double conversion is correctly rounded */
+  return ldexp((double)v, -53); /* gcc's u128 -> double conversion is correctly rounded */
 }
 
 typedef struct {
@@ -284,6 +285,7 @@ typedef struct {
   /* outputs (private) */
   uint64_t* counts;
   u128* fixed;
+  unsigned char* inf; /* bin received 1/0 (omega == 0) */
   uint64_t in_threshold, arc_pairs, half_pairs, bad_center;
 } orc_job;
 
@@ -314,7 +316,10 @@ static void pair_worker_center(orc_job* J, uint64_t pos) {
       const double w = ws * wt;
       const uint32_t b = si * J->ct + ti;
       J->counts[b]++;
-      J->fixed[b] += fixed52(1.0 / w);
+      if (w == 0.0)
+        J->inf[b] = 1; /* the reference adds 1/0 = inf; its Kahan sum ends NaN */
+      else
+        J->fixed[b] += fixed53(1.0 / w);
       J->in_threshold++;
       if (ws != 1.0) J->arc_pairs++;
       if (wt != 1.0) J->half_pairs++;
@@ -340,7 +345,7 @@ static int cmp_by_x(const void* a, const void* b) {
 /*
  * Per-bin (non-cumulative) in-threshold ordered-pair counts and exact
  * weighted sums over centers with input index in [c0, c1) (pass 0, n for all).
- * Output: counts[cs*ct], sum_hi/sum_lo[cs*ct] (128-bit fixed, 52 frac bits),
+ * Output: counts[cs*ct], sum_hi/sum_lo[cs*ct] (128-bit fixed, 53 frac bits),
  * hist[cs*ct] = correctly rounded double of the exact sum.
  * stats[0..3] = in_threshold, arc (omega != 1), half (v = 1/2), bad centers.
  * Restates estimate_surface's add_pair loop (estimator.cpp:136-144,170-177).
@@ -370,6 +375,7 @@ int orc_pair_histogram(const double* x, const double* y, const int64_t* t, uint6
     J->c0 = c0; J->c1 = c1; J->nthreads = nthreads; J->tid = w;
     J->counts = (uint64_t*)calloc(bins, sizeof(uint64_t));
     J->fixed = (u128*)calloc(bins, sizeof(u128));
+    J->inf = (unsigned char*)calloc(bins, 1);
     if (nthreads > 1) pthread_create(&th[w], NULL, pair_worker, J);
   }
   if (nthreads == 1) pair_worker(&jobs[0]);
@@ -380,14 +386,17 @@ int orc_pair_histogram(const double* x, const double* y, const int64_t* t, uint6
   for (uint32_t b = 0; b < bins; ++b) {
     uint64_t c = 0;
     u128 s = 0;
+    int inf = 0;
     for (int w = 0; w < nthreads; ++w) {
       c += jobs[w].counts[b];
       s += jobs[w].fixed[b];
+      inf |= jobs[w].inf[b];
     }
+    if (inf) s += (u128)1 << 120; /* the device library's exported mark (stk.h) */
     counts[b] = c;
     sum_hi[b] = (uint64_t)(s >> 64);
     sum_lo[b] = (uint64_t)s;
-    hist[b] = orc_fixed_to_double(sum_hi[b], sum_lo[b]);
+    hist[b] = inf ? NAN : orc_fixed_to_double(sum_hi[b], sum_lo[b]);
   }
   for (int w = 0; w < nthreads; ++w) {
     stats[0] += jobs[w].in_threshold;
@@ -396,6 +405,7 @@ int orc_pair_histogram(const double* x, const double* y, const int64_t* t, uint6
     stats[3] += jobs[w].bad_center;
     free(jobs[w].counts);
     free(jobs[w].fixed);
+    free(jobs[w].inf);
   }
   free(jobs); free(th); free(order); free(xs);
   return stats[3] ? 1 : 0;

@@ -13,6 +13,7 @@ Regions are axis-aligned rectangles with period [0, extent].
 """
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass
 
 import numpy as np
@@ -33,10 +34,35 @@ class Config:
     sims: int
     seed: int
     kind: str           # csr | thomas | poi | uniform
+    ring_vertices: int = 0  # > 0: a regular polygon inscribed in the square (acceptance c6 shape)
 
     def ring(self):
         e = self.extent_m
+        if self.ring_vertices > 0:
+            return circle_ring(self.ring_vertices, e)
         return np.array([[0.0, 0.0], [e, 0.0], [e, e], [0.0, e]])
+
+    def with_ring(self, vertices: int) -> "Config":
+        return dataclasses.replace(self, ring_vertices=int(vertices))
+
+
+def circle_ring(vertices: int, extent: float):
+    """Regular ``vertices``-gon inscribed in the circle of radius extent/2 around
+    the square's center: the shape of the reference's acceptance criterion 6
+    (proj/tests/acceptance/acceptance_main.cpp:295-303), scaled to the square."""
+    a = 2.0 * np.pi * np.arange(vertices) / vertices
+    h = 0.5 * extent
+    return np.stack([h + h * np.cos(a), h + h * np.sin(a)], axis=1)
+
+
+def inside_ring_strict(cfg: "Config", x, y):
+    """Synthetic-data filter: points well inside the polygon (inside its
+    inscribed circle, radius h*cos(pi/V), less a relative margin)."""
+    if cfg.ring_vertices <= 0:
+        return np.ones(len(x), bool)
+    h = 0.5 * cfg.extent_m
+    r_in = h * np.cos(np.pi / cfg.ring_vertices) * (1.0 - 1e-9)
+    return (x - h) ** 2 + (y - h) ** 2 < r_in * r_in
 
 
 CONFIGS = {
@@ -117,10 +143,10 @@ def poi(cfg: Config, clusters=2000, frac_clustered=0.7):
 def observed(cfg: Config, csr_generator=None):
     """Observed pattern of a config.  ``csr_generator(n, ring, p0, p1, seed)`` is
     the reference-exact CSR generator to use for C1/C3 (device or oracle)."""
-    if cfg.kind == "thomas":
-        return thomas(cfg)
-    if cfg.kind == "poi":
-        return poi(cfg)
+    if cfg.kind in ("thomas", "poi"):
+        x, y, t = thomas(cfg) if cfg.kind == "thomas" else poi(cfg)
+        keep = inside_ring_strict(cfg, x, y)
+        return x[keep], y[keep], t[keep]
     if csr_generator is None:
         raise ValueError("CSR configs need the reference-exact generator")
     return csr_generator(cfg.n, cfg.ring(), 0, cfg.period_s, cfg.seed)

@@ -112,6 +112,16 @@ struct stk_ctx {
   double xmin = 0, xmax = 0, ymin = 0, ymax = 0, maxabs = 0;
   bool fast_rect = false;  // axis-aligned rectangle: every bbox draw is inside
   DevBuf<double2> d_ring;
+  // general-polygon indexes: slabs (region only) and edge
+  // cells (region + grid), built lazily by region_view()
+  bool slab_ok = false, ec_ok = false;
+  uint32_t nslab = 0;
+  double slab_y0 = 0, slab_inv_h = 0, pip_lim = 0, pip_ylo = 0, pip_yhi = 0;
+  DevBuf<uint32_t> d_slab_start, d_slab_edge;
+  int ec_nx = 0, ec_ny = 0;
+  double ec_x0 = 0, ec_y0 = 0, ec_inv_w = 0, ec_dmax = 0, ec_reach = 0;
+  DevBuf<uint32_t> d_ec_start, d_ec_edge;
+  DevBuf<RegionView> d_rv;  // device copy of region_view() for out-of-line device code
 
   // grid (est::DistanceGrid)
   bool have_grid = false;
@@ -158,7 +168,143 @@ struct stk_ctx {
 
 namespace {
 
+// Exported per-bin sums (128-bit fixed point, 53 fractional bits) of a bin
+// that received an infinite term (omega == 0) carry + 2^120: real sums stay
+// far below (< 2^110), so summing partials of up to 255 ranks/shards keeps
+// the mark, and fixed_or_nan() turns it into the reference's NaN.
+constexpr unsigned __int128 kInfSentinel = (unsigned __int128)1 << 120;
+double fixed_or_nan(unsigned __int128 v) {
+  if (v >= ((unsigned __int128)1 << 119)) return std::nan("");
+  return std::ldexp((double)v, -kFixedFracBits);  // correctly rounded u128 -> f64
+}
+
+void upload_u32(stk_ctx* c, DevBuf<uint32_t>& buf, const std::vector<uint32_t>& v) {
+  buf.ensure(std::max<size_t>(v.size(), 1));
+  if (!v.empty())
+    CK(cudaMemcpyAsync(buf.p, v.data(), sizeof(uint32_t) * v.size(), cudaMemcpyHostToDevice,
+                       c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+// Horizontal slabs for point_in_polygon (stk_device.cuh pip_slab): edge k
+// (ring[k] -> ring[k+1]) goes to every slab its y-range, widened by
+// tol = 2e-12 * pip_lim (>= the reference's on_segment tolerance 1e-12*scale
+// for any probe with |x|, |y| <= pip_lim) and by one slab each side, meets.
+void build_slabs(stk_ctx* c) {
+  const uint32_t m = c->nv;
+  const double* r = c->ring.data();
+  const double ext = std::max(c->xmax - c->xmin, c->ymax - c->ymin);
+  c->pip_lim = 2.0 * (c->maxabs + ext) + 1.0;
+  const double tol = 2e-12 * c->pip_lim;
+  const uint32_t ns = std::min<uint32_t>(4096, std::max<uint32_t>(1, m / 2));
+  c->nslab = ns;
+  c->slab_y0 = c->ymin;
+  c->slab_inv_h = (double)ns / (c->ymax - c->ymin);
+  c->pip_ylo = c->ymin - tol;
+  c->pip_yhi = c->ymax + tol;
+  auto slab_of = [&](double y) {
+    const double f = std::floor((y - c->slab_y0) * c->slab_inv_h);
+    return (int64_t)std::max(-2.0, std::min((double)ns + 1.0, f));
+  };
+  std::vector<uint32_t> count(ns + 1, 0), start(ns + 1, 0), edge;
+  auto range = [&](uint32_t k, int64_t* s0, int64_t* s1) {
+    const uint32_t k1 = (k + 1 == m) ? 0 : k + 1;
+    const double lo = std::min(r[2 * k + 1], r[2 * k1 + 1]) - tol;
+    const double hi = std::max(r[2 * k + 1], r[2 * k1 + 1]) + tol;
+    *s0 = std::max<int64_t>(0, slab_of(lo) - 1);
+    *s1 = std::min<int64_t>(ns - 1, slab_of(hi) + 1);
+  };
+  for (uint32_t k = 0; k < m; ++k) {
+    int64_t s0, s1;
+    range(k, &s0, &s1);
+    for (int64_t q = s0; q <= s1; ++q) ++count[q];
+  }
+  for (uint32_t q = 0; q < ns; ++q) start[q + 1] = start[q] + count[q];
+  edge.resize(start[ns]);
+  std::vector<uint32_t> fill(start.begin(), start.end() - 1);
+  for (uint32_t k = 0; k < m; ++k) {
+    int64_t s0, s1;
+    range(k, &s0, &s1);
+    for (int64_t q = s0; q <= s1; ++q) edge[fill[q]++] = k;
+  }
+  upload_u32(c, c->d_slab_start, start);
+  upload_u32(c, c->d_slab_edge, edge);
+  c->slab_ok = true;
+}
+
+// Edge cells for the arc weight and the safe radius (general polygons): a
+// square grid of width w >= s_max/2 over the ring's bbox; cell (ix, iy) lists
+// segment i (ring[i-1] -> ring[i]) unless the segment is farther than
+// reach + half-diagonal from the cell center, i.e. farther than
+// reach = s_max (1 + 4e-6) + 1e-9 S from every point of the cell.  For
+// d <= s_max the reference rejects every unlisted segment.
+double seg_dist(double px, double py, double ax, double ay, double bx, double by) {
+  const double ex = bx - ax, ey = by - ay, l2 = ex * ex + ey * ey;
+  double t = 0.0;
+  if (l2 > 0.0) t = std::min(1.0, std::max(0.0, ((px - ax) * ex + (py - ay) * ey) / l2));
+  const double qx = ax + t * ex - px, qy = ay + t * ey - py;
+  return std::sqrt(qx * qx + qy * qy);
+}
+
+void build_edge_cells(stk_ctx* c) {
+  const uint32_t m = c->nv;
+  const double* r = c->ring.data();
+  const double smax = c->s_values.back();
+  const double S = c->pip_lim;
+  const double reach = smax * (1.0 + 4e-6) + 1e-9 * S;
+  const double W = c->xmax - c->xmin, H = c->ymax - c->ymin;
+  const double ew = std::max(smax / 2.0, std::max(W, H) / 512.0);
+  const int nx = std::max(1, (int)std::ceil(W / ew)), ny = std::max(1, (int)std::ceil(H / ew));
+  const double half_diag = ew * 0.70710678118654757 * (1.0 + 1e-9) + 1e-9 * S;
+  c->ec_nx = nx;
+  c->ec_ny = ny;
+  c->ec_x0 = c->xmin;
+  c->ec_y0 = c->ymin;
+  c->ec_inv_w = 1.0 / ew;
+  c->ec_dmax = smax;
+  c->ec_reach = reach * (1.0 - 1e-9);
+  const uint64_t cells = (uint64_t)nx * ny;
+  std::vector<std::vector<uint32_t>> lists(cells);
+  for (uint32_t i = 0; i < m; ++i) {
+    const uint32_t j = i == 0 ? m - 1 : i - 1;
+    const double ax = r[2 * j], ay = r[2 * j + 1], bx = r[2 * i], by = r[2 * i + 1];
+    const double lim = reach + half_diag;
+    auto cell_lo = [&](double v, double v0) { return (int)std::floor((v - v0) / ew) - 1; };
+    const int ix0 = std::max(0, cell_lo(std::min(ax, bx) - lim, c->xmin));
+    const int ix1 = std::min(nx - 1, cell_lo(std::max(ax, bx) + lim, c->xmin) + 2);
+    const int iy0 = std::max(0, cell_lo(std::min(ay, by) - lim, c->ymin));
+    const int iy1 = std::min(ny - 1, cell_lo(std::max(ay, by) + lim, c->ymin) + 2);
+    for (int iy = iy0; iy <= iy1; ++iy)
+      for (int ix = ix0; ix <= ix1; ++ix) {
+        const double cx = c->xmin + (ix + 0.5) * ew, cy = c->ymin + (iy + 0.5) * ew;
+        if (seg_dist(cx, cy, ax, ay, bx, by) <= lim) lists[(uint64_t)iy * nx + ix].push_back(i);
+      }
+  }
+  std::vector<uint32_t> start(cells + 1, 0), edge;
+  for (uint64_t q = 0; q < cells; ++q) start[q + 1] = start[q] + (uint32_t)lists[q].size();
+  edge.reserve(start[cells]);
+  for (auto& l : lists) edge.insert(edge.end(), l.begin(), l.end());
+  upload_u32(c, c->d_ec_start, start);
+  upload_u32(c, c->d_ec_edge, edge);
+  c->ec_ok = true;
+}
+
+RegionView region_view(stk_ctx* c);
+
+// A device-memory copy of a RegionView (pageable H2D: the source is consumed
+// before cudaMemcpyAsync returns).
+const RegionView* device_region(stk_ctx* c, const RegionView& rv) {
+  c->d_rv.ensure(1);
+  CK(cudaMemcpyAsync(c->d_rv.p, &rv, sizeof(RegionView), cudaMemcpyHostToDevice, c->stream));
+  return c->d_rv.p;
+}
+
 RegionView region_view(stk_ctx* c) {
+  // STK_NO_SLABS / STK_NO_EDGE_CELLS (debugging): full-ring loops instead
+  static const bool no_slabs = std::getenv("STK_NO_SLABS") != nullptr;
+  static const bool no_ec = std::getenv("STK_NO_EDGE_CELLS") != nullptr;
+  if (c->have_region && !c->fast_rect && !c->slab_ok && !no_slabs) build_slabs(c);
+  if (c->have_region && c->have_grid && !c->fast_rect && !c->ec_ok && !no_ec) build_edge_cells(c);
   RegionView r;
   r.ring = c->d_ring.p;
   r.nv = c->nv;
@@ -184,6 +330,25 @@ RegionView region_view(stk_ctx* c) {
   // on_segment tolerance (d - h > 4 box_m)
   r.sw_dmin = 1e-8 * S;
   r.sw_margin = 4.0 * r.box_m;
+  r.slab_start = c->slab_ok ? c->d_slab_start.p : nullptr;
+  r.slab_edge = c->slab_ok ? c->d_slab_edge.p : nullptr;
+  r.nslab = c->nslab;
+  r.slab_y0 = c->slab_y0;
+  r.slab_inv_h = c->slab_inv_h;
+  r.pip_lim = c->pip_lim;
+  r.pip_ylo = c->pip_ylo;
+  r.pip_yhi = c->pip_yhi;
+  r.ec_start = c->ec_ok ? c->d_ec_start.p : nullptr;
+  r.ec_edge = c->ec_ok ? c->d_ec_edge.p : nullptr;
+  r.ec_nx = c->ec_nx;
+  r.ec_ny = c->ec_ny;
+  r.ec_x0 = c->ec_x0;
+  r.ec_y0 = c->ec_y0;
+  r.ec_inv_w = c->ec_inv_w;
+  r.ec_dmax = c->ec_dmax;
+  r.ec_reach = c->ec_reach;
+  static const bool no_safe = std::getenv("STK_NO_SAFE_RADIUS") != nullptr;
+  r.no_safe = no_safe ? 1 : 0;
   return r;
 }
 
@@ -377,14 +542,16 @@ void generate(stk_ctx* c, const Batch& B, Source src, int p_first, int count, ui
   if (src == Source::Csr) {
     const uint64_t ntl = (uint64_t)(c->p1 - c->p0) + 1;  // uniform_int(p0, p1)
     const uint64_t limit = ~0ULL - (~0ULL % ntl);
-    if (c->fast_rect) {
-      csr_fast_kernel<<<count, 320, 0, c->stream>>>(B, p_first, seed0, region_view(c), ntl, limit);
-      CK(cudaGetLastError());
-  ++c->launches;
-    }
-    csr_seq_kernel<<<(count + 31) / 32, 32, 0, c->stream>>>(B, p_first, count, seed0,
-                                                            region_view(c), ntl, limit,
-                                                            c->fast_rect ? 0 : 1);
+    const RegionView rv = region_view(c);
+    if (c->fast_rect)
+      csr_fast_kernel<<<count, 320, 0, c->stream>>>(B, p_first, seed0, rv, ntl, limit);
+    else
+      csr_poly_kernel<<<count, 320, 0, c->stream>>>(B, p_first, seed0, rv, ntl, limit);
+    CK(cudaGetLastError());
+    ++c->launches;
+    // patterns a parallel kernel flagged (probability ~0): sequential, exact
+    csr_seq_kernel<<<(count + 31) / 32, 32, 0, c->stream>>>(B, p_first, count, seed0, rv, ntl,
+                                                            limit, 0);
     CK(cudaGetLastError());
   ++c->launches;
   } else if (src == Source::Bootstrap) {
@@ -420,7 +587,8 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   key_kernel<<<gp, 256, 0, c->stream>>>(B, G, 0);
   CK(cudaGetLastError());
   ++c->launches;
-  scan_kernel<<<R, 1024, 0, c->stream>>>(B.cell_count, B.cell_start, B.item_start, G.cells);
+  scan_kernel<<<R, 1024, 0, c->stream>>>(B.cell_count, B.cell_start, B.item_start, G.cells,
+                                         B.stats + 5);
   CK(cudaGetLastError());
   ++c->launches;
   scatter_kernel<<<gp, 256, 0, c->stream>>>(B, G, region_view(c), 0);
@@ -441,7 +609,8 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
     select_count_kernel<<<gs, 256, 0, c->stream>>>(B, G);
     CK(cudaGetLastError());
     ++c->launches;
-    scan_kernel<<<B.n_sel, 1024, 0, c->stream>>>(B.cell_count, B.sel_start, B.item_start, G.cells);
+    scan_kernel<<<B.n_sel, 1024, 0, c->stream>>>(B.cell_count, B.sel_start, B.item_start, G.cells,
+                                                  B.stats + 5);
     CK(cudaGetLastError());
     ++c->launches;
     select_scatter_kernel<<<gs, 256, 0, c->stream>>>(B, G);
@@ -460,7 +629,7 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   const int slots = (c->fast_rect && c->s_values.back() < 0.5 * smin_side) ? 8 : kAngleSlots;
   const size_t smem = pair_kernel_smem(P.bins, B.wide, slots);
   int per_sm = 0;
-  CK(pair_kernel_prepare(B.wide, slots, smem, &per_sm));
+  CK(pair_kernel_prepare(B.wide, slots, c->fast_rect ? 1 : 0, smem, &per_sm));
   if (per_sm < 1) throw Unsupported("distance grid too large for the pair kernel's shared histogram");
   tasks_kernel<<<1, 1, 0, c->stream>>>(B, G, (uint32_t)(c->num_sms * per_sm));
   CK(cudaGetLastError());
@@ -473,10 +642,11 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   A.G = G;
   A.bins = bin_view(c);
   A.reg = region_view(c);
+  A.reg_g = device_region(c, A.reg);
   const uint64_t ctas = (uint64_t)c->num_sms * per_sm;
   c->arcq.ensure(ctas * kPairWarps * (kArcRing + kCplxRing));
   A.B.arcq = c->arcq.p;
-  pair_kernel_launch(B.wide, slots, (unsigned)ctas, smem, c->stream, A);
+  pair_kernel_launch(B.wide, slots, c->fast_rect ? 1 : 0, (unsigned)ctas, smem, c->stream, A);
   CK(cudaGetLastError());
   ++c->launches;
   CK(cudaEventRecord(e2, c->stream));
@@ -646,11 +816,13 @@ void run_pipeline(stk_ctx* c, const double* dx, const double* dy, const int64_t*
   if (with_observed && out.obs_counts) {
     const uint32_t b = P.bins;
     for (uint32_t i = 0; i < b; ++i) {
-      const unsigned long long cnt = c->obs_raw[i], half = c->obs_raw[b + i],
+      const unsigned long long raw = c->obs_raw[i], half = c->obs_raw[b + i],
                                lo = c->obs_raw[2 * b + i], hi = c->obs_raw[3 * b + i];
+      const unsigned long long cnt = raw & ~1ULL;
       out.obs_counts[i] = cnt;
       const unsigned __int128 v = ((unsigned __int128)hi << 64 | lo) +
-                                  ((unsigned __int128)(cnt + half) << 52);
+                                  ((unsigned __int128)(cnt + half) << kFixedFracBits) +
+                                  ((raw & 1ULL) ? kInfSentinel : (unsigned __int128)0);
       if (out.obs_hi) out.obs_hi[i] = (uint64_t)(v >> 64);
       if (out.obs_lo) out.obs_lo[i] = (uint64_t)v;
     }
@@ -838,6 +1010,7 @@ int stk_set_region(stk_ctx* c, const double* ring_xy, uint32_t nv, int64_t perio
                    int64_t period_end) {
   return guarded(c, [&] {
     c->have_region = false;
+    c->slab_ok = c->ec_ok = false;
     const RegionInfo ri = check_region(ring_xy, nv, period_start, period_end);
     const std::vector<double>& r = ri.ring;
     const uint32_t m = ri.nv;
@@ -875,6 +1048,7 @@ int stk_set_grid(stk_ctx* c, const double* s_values, uint32_t cs, const int64_t*
                  uint32_t ct) {
   return guarded(c, [&] {
     c->have_grid = false;
+    c->ec_ok = false;
     check_grid(s_values, cs, t_values, ct);
     if ((uint64_t)cs * ct > (1u << 20)) throw Unsupported("more than 2^20 grid cells");
     if (cs > (uint32_t)kMaxAxis || ct > (uint32_t)kMaxAxis)
@@ -981,14 +1155,16 @@ int stk_pair_histogram(stk_ctx* c, const double* x, const double* y, const int64
     CK(cudaEventRecord(tm.t1, c->stream));
     fill_telemetry(c, tm, tel, 1);
     for (uint32_t b = 0; b < bins; ++b) {
-      const unsigned long long cnt = h[b], half = h[bins + b], lo = h[2 * bins + b],
+      const unsigned long long raw = h[b], half = h[bins + b], lo = h[2 * bins + b],
                                hi = h[3 * bins + b];
+      const unsigned long long cnt = raw & ~1ULL;  // bit 0: the bin received 1/0 (omega == 0)
       if (counts) counts[b] = cnt;
       const unsigned __int128 v = ((unsigned __int128)hi << 64 | lo) +
-                                  ((unsigned __int128)(cnt + half) << 52);
+                                  ((unsigned __int128)(cnt + half) << kFixedFracBits) +
+                                  ((raw & 1ULL) ? kInfSentinel : (unsigned __int128)0);
       if (sum_hi) sum_hi[b] = (uint64_t)(v >> 64);
       if (sum_lo) sum_lo[b] = (uint64_t)v;
-      if (hist) hist[b] = std::ldexp((double)v, -52);  // correctly rounded u128 -> f64
+      if (hist) hist[b] = fixed_or_nan(v);
     }
   });
 }
@@ -1004,7 +1180,7 @@ int stk_finalize(stk_ctx* c, uint64_t n, const uint64_t* sum_hi, const uint64_t*
       for (uint32_t ti = 0; ti < ct; ++ti) {
         const uint32_t b = si * ct + ti;
         const unsigned __int128 v = ((unsigned __int128)sum_hi[b] << 64) | sum_lo[b];
-        double acc = std::ldexp((double)v, -52);
+        double acc = fixed_or_nan(v);
         if (si > 0) acc += K[b - ct];
         if (ti > 0) acc += K[b - 1];
         if (si > 0 && ti > 0) acc -= K[b - ct - 1];
@@ -1197,8 +1373,9 @@ int stk_spatial_weights(stk_ctx* c, const double* cx, const double* cy, const do
     CK(cudaMemcpyAsync(b.p, cx, 8 * count, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(b.p + count, cy, 8 * count, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(b.p + 2 * count, d, 8 * count, cudaMemcpyHostToDevice, c->stream));
+    const RegionView rv = region_view(c);
     weights_kernel<<<(unsigned)((count + 127) / 128), 128, 0, c->stream>>>(
-        b.p, b.p + count, b.p + 2 * count, count, region_view(c), b.p + 3 * count, c->ovf.p,
+        b.p, b.p + count, b.p + 2 * count, count, rv, device_region(c, rv), b.p + 3 * count, c->ovf.p,
         c->bad.p);
     CK(cudaGetLastError());
   ++c->launches;

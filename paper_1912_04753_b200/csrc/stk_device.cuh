@@ -62,6 +62,70 @@ __device__ __forceinline__ bool point_in_polygon(double px, double py, const dou
   return inside;
 }
 
+// point_in_polygon restricted to the probe's slab (RegionView::slab_*): the
+// same expressions, per edge, as the reference, over the only edges that can
+// change its answer.  An edge can pass on_segment only if py lies in its
+// y-range widened by 1e-12*scale <= 1e-12*pip_lim, and can toggle the ray
+// cast only if (a.y > py) != (b.y > py), i.e. py lies in its y-range; the host
+// lists every edge whose y-range widened by 2e-12*pip_lim (plus one slab on
+// each side, against rounding of the slab index) meets the slab.  Probes
+// outside [pip_ylo, pip_yhi] meet no such edge: false, as the reference.
+__device__ __forceinline__ bool pip_slab(double px, double py, const RegionView& R) {
+  if (!(py >= R.pip_ylo && py <= R.pip_yhi)) return false;
+  int s = (int)floor((py - R.slab_y0) * R.slab_inv_h);
+  s = min(max(s, 0), (int)R.nslab - 1);
+  const uint32_t b = R.slab_start[s], e = R.slab_start[s + 1];
+  const uint32_t nv = R.nv;
+  const double2* ring = R.ring;
+  const double smax = fmax(fmax(R.maxabs, 1.0), fmax(fabs(px), fabs(py)));
+  const double bound = 1e-12 * smax * smax;
+  for (uint32_t k = b; k < e; ++k) {  // on_segment(p, ring[i], ring[i+1]) (geometry.cpp:84-86)
+    const uint32_t i = R.slab_edge[k];
+    const double2 a = ring[i];
+    const double2 bb = ring[(i + 1 == nv) ? 0 : i + 1];
+    const double cross = (bb.x - a.x) * (py - a.y) - (bb.y - a.y) * (px - a.x);
+    if (fabs(cross) > bound) continue;  // see point_in_polygon
+    if (on_segment(px, py, a.x, a.y, bb.x, bb.y)) return true;
+  }
+  bool inside = false;
+  for (uint32_t k = b; k < e; ++k) {  // ray cast: the reference's (a, b) = (ring[i+1], ring[i])
+    const uint32_t i = R.slab_edge[k];
+    const double2 a = ring[(i + 1 == nv) ? 0 : i + 1];
+    const double2 bb = ring[i];
+    if ((a.y > py) != (bb.y > py)) {
+      const double x_cross = a.x + (py - a.y) / (bb.y - a.y) * (bb.x - a.x);
+      if (px < x_cross) inside = !inside;
+    }
+  }
+  return inside;
+}
+
+// geom::point_in_polygon for the region: slab index when built and the probe
+// is within its validity bound, else the full restatement.
+__device__ __forceinline__ bool point_in_region(double px, double py, const RegionView& R) {
+  if (R.slab_start != nullptr && fabs(px) <= R.pip_lim && fabs(py) <= R.pip_lim)
+    return pip_slab(px, py, R);
+  return point_in_polygon(px, py, R.ring, R.nv, R.maxabs);
+}
+
+// The edge-cell list of a center (RegionView::ec_*), or nullptr (all segments)
+// when not built or d exceeds the radius the lists cover.
+__device__ __forceinline__ const uint32_t* edge_list(double cx, double cy, double d,
+                                                     const RegionView& R, uint32_t* cnt) {
+  if (R.ec_start == nullptr || !(d <= R.ec_dmax)) {
+    *cnt = R.nv;
+    return nullptr;
+  }
+  int ix = (int)floor((cx - R.ec_x0) * R.ec_inv_w);
+  int iy = (int)floor((cy - R.ec_y0) * R.ec_inv_w);
+  ix = min(max(ix, 0), R.ec_nx - 1);
+  iy = min(max(iy, 0), R.ec_ny - 1);
+  const uint32_t cell = (uint32_t)iy * (uint32_t)R.ec_nx + (uint32_t)ix;
+  const uint32_t b = R.ec_start[cell];
+  *cnt = R.ec_start[cell + 1] - b;
+  return R.ec_edge + b;
+}
+
 // atan2 with one division: |y|,|x| -> t in [-tan(pi/8), tan(pi/8)] via
 // t = mn/mx (mn <= tan(pi/8) mx) or t = (mn - mx)/(mn + mx) (+ pi/4), then
 // atan(t) = t + t*s*R(s), s = t^2, R a degree-10 fit (tools/fit_atan.py;
@@ -133,9 +197,90 @@ __device__ __forceinline__ int segment_circle_angles(double2 a, double2 b, doubl
 // Restates edge::spatial_isotropic_weight (edge_correction.cpp:42-79) for a
 // center already known to lie inside the region (the estimator validates
 // every point up front, estimator.cpp:123-127, so the reference's throw is
-// unreachable on this path).  *overflow is set if more than kMaxAngles
-// crossings occur (reported as STK_EUNSUPPORTED by the host).
-__device__ __noinline__ double spatial_weight(double cx, double cy, double d, const double2* ring,
+// unreachable on this path), for any number of crossings in bounded storage:
+// each pass re-derives every crossing angle (segment_circle_angles, same
+// arithmetic) and keeps the kMaxAngles smallest above the previous pass's
+// largest, so the passes visit the reference's sorted sequence in order.  The
+// de-duplication (v - last kept > 1e-9), the wrap rule and the arc sums then
+// run as a stream with one kept angle of delay (an arc is summed once its end
+// is known not to be the last kept angle, which the wrap rule may drop), in
+// the reference's summation order.  Skipping values equal to the previous
+// pass's largest is exact: a duplicate of a value never survives the dedupe.
+__device__ __noinline__ double spatial_weight(double cx, double cy, double d, const RegionView* Rp,
+                                              int* overflow) {
+  (void)overflow;
+  if (d <= 0.0) return 1.0;
+  const RegionView& R = *Rp;  // device memory (a kernel parameter would be copied to the stack)
+  const double2* ring = R.ring;
+  const uint32_t nv = R.nv;
+  uint32_t cnt;
+  const uint32_t* list = edge_list(cx, cy, d, R, &cnt);  // segments that can cross (§4.6)
+  double buf[kMaxAngles];
+  double lower = -1.0;  // angles are in [0, 2*pi)
+  int u = 0;            // kept angles so far
+  double first = 0.0, prev = 0.0, cur = 0.0, inside_span = 0.0;
+  auto arc = [&](double a0, double a1) {
+    const double mid = 0.5 * (a0 + a1);
+    double sn, cs;
+    sincos(mid, &sn, &cs);
+    const double px = cx + d * cs, py = cy + d * sn;
+    if (point_in_region(px, py, R)) inside_span += a1 - a0;
+  };
+  for (;;) {
+    int n = 0;
+    bool dropped = false;
+    for (uint32_t k = 0; k < cnt; ++k) {
+      const uint32_t i = list ? list[k] : k;
+      double two[2];
+      const int m = segment_circle_angles(ring[i == 0 ? nv - 1 : i - 1], ring[i], cx, cy, d, two, 0);
+      for (int q = 0; q < m; ++q) {
+        const double v = two[q];
+        if (!(v > lower)) continue;
+        if (n == kMaxAngles) {
+          if (v >= buf[n - 1]) {
+            dropped = true;
+            continue;
+          }
+          --n;  // the largest leaves; it is re-found by a later pass
+          dropped = true;
+        }
+        int b = n - 1;  // insertion (ascending)
+        while (b >= 0 && buf[b] > v) {
+          buf[b + 1] = buf[b];
+          --b;
+        }
+        buf[b + 1] = v;
+        ++n;
+      }
+    }
+    for (int a = 0; a < n; ++a) {
+      const double v = buf[a];
+      if (u == 0) {
+        first = cur = v;
+        u = 1;
+      } else if (v - cur > kAngleEps) {
+        if (u >= 2) arc(prev, cur);  // cur is not the last kept angle
+        prev = cur;
+        cur = v;
+        ++u;
+      }
+    }
+    if (!dropped || n == 0) break;
+    lower = buf[n - 1];
+  }
+  if (u > 1 && (first + kTwoPi) - cur <= kAngleEps) {  // the wrap rule drops the last kept
+    --u;
+    if (u < 2) return 1.0;
+    arc(prev, first + kTwoPi);
+    return inside_span / kTwoPi;
+  }
+  if (u < 2) return 1.0;
+  arc(prev, cur);
+  arc(cur, first + kTwoPi);
+  return inside_span / kTwoPi;
+}
+
+__device__ __noinline__ double spatial_weight_ring(double cx, double cy, double d, const double2* ring,
                                               uint32_t nv, double ring_maxabs, int* overflow) {
   if (d <= 0.0) return 1.0;
   double ang[kMaxAngles];
@@ -255,7 +400,11 @@ __device__ __forceinline__ int rect_probe_certified(double cx, double cy, double
 // rejects them too; and PIP uses point_in_rect.
 // Same arithmetic and order as the reference; returns -1 when more than `cap`
 // crossings occur (caller falls back to spatial_weight()).
-__device__ STK_WEIGHT_INLINE double spatial_weight_buf(double cx, double cy, double d,
+// Rings of at most 32 segments visited in full (the rectangle kernel's
+// deferred drain).  Kept with runtime R.rect tests: specialising them away
+// changes the pair kernel's register allocation for the worse (the hot loop
+// then reloads its neighbour from local memory).
+__device__ STK_WEIGHT_INLINE double spatial_weight_buf_rect(double cx, double cy, double d,
                                                        const RegionView& R, double* buf,
                                                        int stride, int cap) {
   if (d <= 0.0) return 1.0;
@@ -347,6 +496,107 @@ __device__ STK_WEIGHT_INLINE double spatial_weight_buf(double cx, double cy, dou
   return inside_span / kTwoPi;
 }
 
+// RECT: the region is RegionView::rect (4 segments, rectangle PIP); else a
+// general ring through the edge cells and the slab PIP.
+template <bool RECT>
+__device__ STK_WEIGHT_INLINE double spatial_weight_buf(double cx, double cy, double d,
+                                                       const RegionView& R, double* buf,
+                                                       int stride, int cap) {
+  if (d <= 0.0) return 1.0;
+  const uint32_t nv = R.nv;
+  const double2* ring = R.ring;
+  const double r2 = d * d;
+  const double reach = d * (1.0 + 1e-6);
+  uint32_t cnt = 4;
+  const uint32_t* list = RECT ? nullptr : edge_list(cx, cy, d, R, &cnt);
+  int n = 0;
+  for (uint32_t base = 0; base < cnt; base += 32) {  // 32 segments per accept mask
+  const uint32_t m = RECT ? 4u : min(32u, cnt - base);
+  uint32_t acc = 0;
+  for (uint32_t k = 0; k < m; ++k) {  // segment (ring[i-1], ring[i])
+    const uint32_t i = (!RECT && list) ? list[base + k] : base + k;
+    const double2 A = ring[i == 0 ? nv - 1 : i - 1], Bv = ring[i];
+    if (RECT) {
+      const double h = A.x == Bv.x ? fabs(A.x - cx) : fabs(A.y - cy);
+      if (h > reach) continue;
+    }
+    const double dx = Bv.x - A.x, dy = Bv.y - A.y;
+    const double fx = A.x - cx, fy = A.y - cy;
+    const double qa = dx * dx + dy * dy;
+    const double qb = 2.0 * (fx * dx + fy * dy);
+    const double qc = fx * fx + fy * fy - r2;
+    const double disc = qb * qb - 4.0 * qa * qc;
+    const double scale = qb * qb + fabs(4.0 * qa * qc);
+    if (qa != 0.0 && disc > 1e-9 * scale) acc |= 1u << k;
+  }
+  while (acc) {
+    const uint32_t k = __ffs(acc) - 1;
+    acc &= acc - 1;
+    const uint32_t i = (!RECT && list) ? list[base + k] : base + k;
+    const double2 A = ring[i == 0 ? nv - 1 : i - 1], Bv = ring[i];
+    const double dx = Bv.x - A.x, dy = Bv.y - A.y;
+    const double fx = A.x - cx, fy = A.y - cy;
+    const double qa = dx * dx + dy * dy;
+    const double qb = 2.0 * (fx * dx + fy * dy);
+    const double qc = fx * fx + fy * fy - r2;
+    const double disc = qb * qb - 4.0 * qa * qc;
+    const double sq = sqrt(disc);
+    const double t0 = (-qb - sq) / (2.0 * qa);
+    const double t1 = (-qb + sq) / (2.0 * qa);
+    if (t0 >= 0.0 && t0 <= 1.0) {
+      if (n >= cap) return -1.0;
+      buf[(2 * n) * stride] = (A.y + t0 * dy) - cy;
+      buf[(2 * n + 1) * stride] = (A.x + t0 * dx) - cx;
+      ++n;
+    }
+    if (t1 >= 0.0 && t1 <= 1.0) {
+      if (n >= cap) return -1.0;
+      buf[(2 * n) * stride] = (A.y + t1 * dy) - cy;
+      buf[(2 * n + 1) * stride] = (A.x + t1 * dx) - cx;
+      ++n;
+    }
+  }
+  }
+  if (n == 0) return 1.0;
+  for (int k = 0; k < n; ++k) {  // angle k overwrites slot k (vector k sits at 2k, 2k+1)
+    double ang = fast_atan2(buf[(2 * k) * stride], buf[(2 * k + 1) * stride]);
+    if (ang < 0.0) ang += kTwoPi;
+    buf[k * stride] = ang;
+  }
+  for (int a = 1; a < n; ++a) {  // std::sort (ascending; same sequence)
+    const double v = buf[a * stride];
+    int b = a - 1;
+    while (b >= 0 && buf[b * stride] > v) {
+      buf[(b + 1) * stride] = buf[b * stride];
+      --b;
+    }
+    buf[(b + 1) * stride] = v;
+  }
+  int u = 0;
+  for (int a = 0; a < n; ++a) {
+    const double v = buf[a * stride];
+    if (u == 0 || v - buf[(u - 1) * stride] > kAngleEps) buf[(u++) * stride] = v;
+  }
+  const double first = buf[0];
+  if (u > 1 && (first + kTwoPi) - buf[(u - 1) * stride] <= kAngleEps) --u;
+  if (u < 2) return 1.0;
+  double inside_span = 0.0;
+  for (int a = 0; a < u; ++a) {
+    const double a0 = buf[a * stride];
+    const double a1 = (a + 1 < u) ? buf[(a + 1) * stride] : first + kTwoPi;
+    const double mid = 0.5 * (a0 + a1);
+    int dec = RECT ? rect_probe_certified(cx, cy, d, mid, R) : -1;
+    if (dec < 0) {
+      double sn, cs;
+      sincos(mid, &sn, &cs);
+      const double px = cx + d * cs, py = cy + d * sn;
+      dec = (RECT ? point_in_rect(px, py, R) : point_in_region(px, py, R)) ? 1 : 0;
+    }
+    if (dec) inside_span += a1 - a0;
+  }
+  return inside_span / kTwoPi;
+}
+
 // spatial_isotropic_weight in closed form for the dominant rectangle case:
 // the center strictly inside, exactly one edge within reach d*(1+1e-6) and
 // that edge's quadratic accepted (the same expression as the reference, so
@@ -404,11 +654,24 @@ __device__ __forceinline__ double rect_single_edge_weight(double cx, double cy, 
 // for this center (the circle stays strictly inside every edge's reach by a
 // relative margin far above the rounding error of the reference's quadratic;
 // DESIGN.md §4.2).  Returns -1 when no such radius exists.
-__device__ __forceinline__ double safe_q(double cx, double cy, const double2* ring, uint32_t nv,
-                                         double ring_maxabs) {
+// With edge cells (general polygons) only the cell's segments are visited:
+// every other segment is farther than ec_reach from the point, so the true
+// nearest distance is >= min(listed nearest, ec_reach) and the radius below
+// stays a lower bound.
+__device__ __forceinline__ double safe_q(double cx, double cy, const RegionView& R) {
+  const double2* ring = R.ring;
+  const uint32_t nv = R.nv;
   double r2 = 1.0e308;
-  for (uint32_t i = 0, j = nv - 1; i < nv; j = i++) {
-    const double2 a = ring[j], b = ring[i];
+  uint32_t cnt = nv;
+  const uint32_t* list = nullptr;
+  if (!R.rect && R.ec_start != nullptr) {
+    list = edge_list(cx, cy, 0.0, R, &cnt);
+    r2 = R.ec_reach * R.ec_reach;
+  }
+  const double ring_maxabs = R.maxabs;
+  for (uint32_t k = 0; k < cnt; ++k) {
+    const uint32_t i = list ? list[k] : k;
+    const double2 a = ring[i == 0 ? nv - 1 : i - 1], b = ring[i];
     const double ex = b.x - a.x, ey = b.y - a.y;
     const double len2 = ex * ex + ey * ey;
     double t = 0.0;
@@ -426,43 +689,47 @@ __device__ __forceinline__ double safe_q(double cx, double cy, const double2* ri
 }
 
 // -------------------------------------------------- exact accumulation
-// Term 1/w (>= 1) minus 1, as 128-bit fixed point with 52 fractional bits.
-// 1/w >= 1 has ulp >= 2^-52, so the conversion is exact.
-__device__ __forceinline__ void fixed52_minus_one(double term, uint64_t* lo, uint64_t* hi) {
+// Term 1/w minus 1 as a signed 128-bit fixed-point integer with 53 fractional
+// bits (two's complement in lo/hi).  w = omega * v with v in {1, 1/2} and
+// omega <= 1 up to the reference's own rounding (its arc sum can exceed 2*pi by
+// an ulp: omega = 1 + 2^-52 happens), so 1/w >= 1/2 and its ulp is >= 2^-53:
+// the conversion is exact, and terms just below 1 give small negative values.
+__device__ __forceinline__ void fixed_term_minus_one(double term, uint64_t* lo, uint64_t* hi) {
   const uint64_t bits = __double_as_longlong(term);
-  const int e = int((bits >> 52) & 0x7FF) - 1023;            // term = 1.m * 2^e, e >= 0
-  const uint64_t mant = (bits & 0xFFFFFFFFFFFFFULL) | (1ULL << 52);  // value * 2^52 = mant << e
+  const int e = int((bits >> 52) & 0x7FF) - 1023;            // term = 1.m * 2^e, e >= -1
+  const uint64_t mant = (bits & 0xFFFFFFFFFFFFFULL) | (1ULL << 52);
+  const int sh = e + 1;                                       // term * 2^53 = mant << sh
   uint64_t l, h;
-  if (e < 0 || e >= 75) {  // cannot happen for w in (0,1]; saturate visibly
+  if (sh < 0 || sh >= 75) {  // cannot happen for w in (0, 1 + tiny]; saturate visibly
     l = ~0ULL;
     h = ~0ULL >> 1;
-  } else if (e == 0) {
+  } else if (sh == 0) {
     l = mant;
     h = 0;
-  } else if (e < 64) {
-    l = mant << e;
-    h = mant >> (64 - e);
+  } else if (sh < 64) {
+    l = mant << sh;
+    h = mant >> (64 - sh);
   } else {
     l = 0;
-    h = mant << (e - 64);
+    h = mant << (sh - 64);
   }
-  // subtract 1.0 == 2^52
-  const uint64_t one = 1ULL << 52;
+  // subtract 1.0 == 2^53 (borrows into hi: negative results wrap to two's complement)
+  const uint64_t one = 1ULL << kFixedFracBits;
   h -= (l < one) ? 1ULL : 0ULL;
   l -= one;
   *lo = l;
   *hi = h;
 }
 
-// Correctly rounded double of the 128-bit unsigned value (hi:lo) * 2^-52.
+// Correctly rounded double of the 128-bit unsigned value (hi:lo) * 2^-53.
 __device__ __forceinline__ double fixed128_to_double(uint64_t hi, uint64_t lo) {
-  if (hi == 0) return ldexp((double)lo, -52);  // u64 -> f64 conversion rounds to nearest
+  if (hi == 0) return ldexp((double)lo, -kFixedFracBits);  // u64 -> f64 rounds to nearest
   const int lz = __clzll((long long)hi);
   const int sh = 64 - lz;  // bits of hi above position 64
   uint64_t top = lz == 0 ? hi : ((hi << lz) | (lo >> sh));
   const uint64_t rest = lo << lz;  // low bits that do not fit in top
   if (rest != 0) top |= 1ULL;      // sticky bit (below the 53-bit rounding point)
-  return ldexp((double)top, sh - 52);
+  return ldexp((double)top, sh - kFixedFracBits);
 }
 
 // ------------------------------------------------------ MT19937-64

@@ -32,8 +32,7 @@ __global__ void validate_kernel(const double* x, const double* y, const int64_t*
                                 RegionView reg, unsigned long long* bad) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const bool ok = point_in_polygon(x[i], y[i], reg.ring, reg.nv) && t[i] >= reg.p0 &&
-                    t[i] <= reg.p1;
+    const bool ok = point_in_region(x[i], y[i], reg) && t[i] >= reg.p0 && t[i] <= reg.p1;
     if (!ok) atomicMin(bad, (unsigned long long)i);
   }
 }
@@ -108,8 +107,102 @@ __global__ void __launch_bounds__(320) csr_fast_kernel(Batch B, int p_first, uin
   if (threadIdx.x == 0 && s_flag) B.flags[p] = 1;
 }
 
-// Sequential exact generator (one thread per pattern): general polygons, or a
-// pattern the fast path flagged.  Follows generate_cstr line by line.
+// CSR for general polygons (rejection sampling; simulation.cpp:10-24).  A
+// candidate starting at MT output j reads outputs j, j+1 (x, y); if inside it
+// draws t from j+2 (retrying below()'s rare rejections), else the next
+// candidate starts at j+2.  Which outputs start candidates therefore depends
+// on every earlier acceptance, but acceptance *if* j starts one does not: one
+// CTA per pattern keeps a 624-output window (two twists) in shared memory,
+// tests every start of the first 312 in parallel (point_in_region, the slab
+// PIP), and one thread walks the chain of starts through the acceptance bits
+// — a few instructions per step — recording the accepted ones, which the CTA
+// then writes out.  Bit-identical to the sequential generator; a pattern whose
+// t-draw rejections overrun the window (probability ~0) is flagged for it.
+__global__ void __launch_bounds__(320) csr_poly_kernel(Batch B, int p_first, uint64_t seed0,
+                                                        RegionView reg, uint64_t ntl,
+                                                        uint64_t limit) {
+  __shared__ uint64_t st[312];
+  __shared__ uint64_t out[624];  // output j at out[j % 624]
+  __shared__ uint32_t accw[10];  // bit i: a candidate starting at base + i is inside
+  __shared__ uint32_t acc_pos[104];  // accepted starts of this chunk (relative to base)
+  __shared__ uint32_t acc_t[104];    // ... and the output index of their t draw
+  __shared__ uint32_t s_cnt;
+  __shared__ uint64_t s_pos;
+  __shared__ int s_flag;
+  const int p = p_first + blockIdx.x;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_flag = 0;
+    s_pos = 0;
+  }
+  mt_seed_smem(st, seed0 + (uint64_t)blockIdx.x);
+  for (int h = 0; h < 2; ++h) {
+    mt_twist_smem(st);
+    if (tid < 312) out[h * 312 + tid] = mt_temper(st[tid]);
+  }
+  __syncthreads();
+  const uint64_t n = B.n;
+  double* X = B.x + (uint64_t)p * n;
+  double* Y = B.y + (uint64_t)p * n;
+  int64_t* T = B.t + (uint64_t)p * n;
+  uint64_t k = 0;  // points emitted (uniform across the CTA)
+  for (uint64_t base = 0; k < n; base += 312) {
+    const uint32_t off = (uint32_t)(base % 624);
+    bool in = false;
+    if (tid < 312) {
+      const uint64_t vx = out[(off + tid) % 624], vy = out[(off + tid + 1) % 624];
+      in = point_in_region(mt_uniform(vx, reg.xmin, reg.xmax), mt_uniform(vy, reg.ymin, reg.ymax),
+                           reg);
+    }
+    const unsigned bal = __ballot_sync(FULL_MASK, in);
+    if ((tid & 31) == 0 && tid < 320) accw[tid >> 5] = bal;
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t pos = s_pos, kk = k;
+      uint32_t cnt = 0;
+      while (pos < base + 312 && kk < n) {
+        const uint32_t r = (uint32_t)(pos - base);
+        if (!((accw[r >> 5] >> (r & 31)) & 1u)) {
+          pos += 2;
+          continue;
+        }
+        uint32_t j = r + 2;  // below(): redraw while v >= limit (rng.hpp:17-25)
+        while (j < 624 && out[(off + j) % 624] >= limit) ++j;
+        if (j >= 624) {  // rejections overran the window: sequential kernel
+          s_flag = 1;
+          kk = n;
+          break;
+        }
+        acc_pos[cnt] = r;
+        acc_t[cnt] = j;
+        ++cnt;
+        ++kk;
+        pos = base + j + 1;
+      }
+      s_pos = pos;
+      s_cnt = cnt;
+    }
+    __syncthreads();
+    const uint32_t cnt = s_cnt;
+    if (tid < (int)cnt) {
+      const uint32_t r = acc_pos[tid];
+      X[k + tid] = mt_uniform(out[(off + r) % 624], reg.xmin, reg.xmax);
+      Y[k + tid] = mt_uniform(out[(off + r + 1) % 624], reg.ymin, reg.ymax);
+      T[k + tid] = reg.p0 + (int64_t)(out[(off + acc_t[tid]) % 624] % ntl);
+    }
+    k += cnt;
+    if (s_flag) break;
+    __syncthreads();
+    // the window slides by one twist: outputs base+624 .. base+935 replace base..base+311
+    mt_twist_smem(st);
+    if (tid < 312) out[off + tid] = mt_temper(st[tid]);
+    __syncthreads();
+  }
+  if (tid == 0 && s_flag) B.flags[p] = 1;
+}
+
+// Sequential exact generator (one thread per pattern): a pattern a parallel
+// kernel flagged.  Follows generate_cstr line by line.
 __global__ void csr_seq_kernel(Batch B, int p_first, int count, uint64_t seed0, RegionView reg,
                                uint64_t ntl, uint64_t limit, int force) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -142,7 +235,7 @@ __global__ void csr_seq_kernel(Batch B, int p_first, int count, uint64_t seed0, 
   while (k < n) {
     const double cx = mt_uniform(next(), reg.xmin, reg.xmax);
     const double cy = mt_uniform(next(), reg.ymin, reg.ymax);
-    if (!point_in_polygon(cx, cy, reg.ring, reg.nv)) continue;
+    if (!point_in_region(cx, cy, reg)) continue;
     uint64_t vt;
     do {
       vt = next();
@@ -275,7 +368,8 @@ __global__ void key_kernel(Batch B, GridGeom G, int p_first) {
 // Block-wide exclusive scan of two u32 streams (per-cell counts and their
 // 32-center chunk counts); one CTA of 1024 threads per pattern (blockIdx.x).
 __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* counts, uint32_t* start_all,
-                                                     uint32_t* istart_all, uint32_t cells) {
+                                                     uint32_t* istart_all, uint32_t cells,
+                                                     unsigned long long* max_cell) {
   const int p = blockIdx.x;
   const uint32_t* cnt = counts + (uint64_t)p * cells;
   uint32_t* start = start_all + (uint64_t)p * (cells + 1);
@@ -285,9 +379,11 @@ __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* counts, uint
   if (threadIdx.x == 0) carry_a = carry_b = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t amax = 0;
   for (uint32_t base = 0; base < cells; base += 1024) {
     const uint32_t c = base + threadIdx.x;
     const uint32_t a = c < cells ? cnt[c] : 0u;
+    amax = max(amax, a);
     const uint32_t b = (a + kItemCenters - 1) / kItemCenters;
     uint32_t ia = a, ib = b;  // inclusive warp scan
 #pragma unroll
@@ -336,6 +432,8 @@ __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* counts, uint
     start[cells] = carry_a;
     istart[cells] = carry_b;
   }
+  amax = __reduce_max_sync(FULL_MASK, amax);
+  if (lane == 0 && amax) atomicMax(max_cell, (unsigned long long)amax);
 }
 
 // Largest float <= v (a conservative safe radius^2 stays conservative).
@@ -355,7 +453,7 @@ __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first) {
   const int64_t t = B.t[o];
   B.pxy[d] = make_double2(x, y);
   B.idx[d] = (uint32_t)i;
-  const float sq = float_floor(safe_q(x, y, R.ring, R.nv, R.maxabs));
+  const float sq = R.no_safe ? -1.0f : float_floor(safe_q(x, y, R));
   const int64_t vt = min(t - R.p0, R.p1 - t);
   if (B.wide) {
     PtMeta<int64_t> m{t - R.p0, vt, sq, (uint32_t)i};
@@ -417,6 +515,14 @@ __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas) {
   uint64_t ti = total / (8ull * resident_ctas);
   ti = ti < (uint64_t)kTaskMinItems ? (uint64_t)kTaskMinItems : ti;
   ti = ti > (uint64_t)kTaskMaxItems ? (uint64_t)kTaskMaxItems : ti;
+  // The CTA's per-bin u32 counters take 2 per unordered pair of the task: an
+  // item (<= 32 centers) meets at most (half-stencil cells) x (largest cell)
+  // neighbours, so cap the task at 2^31 counted pairs.
+  const uint64_t stencil_cells =
+      (uint64_t)((G.rs + 1) + G.rt * (2 * G.rs + 1)) * (uint64_t)(2 * G.rs + 1);
+  const uint64_t item_pairs = 2ull * kItemCenters * stencil_cells * (B.stats[5] + 1);
+  const uint64_t cap = (1ull << 31) / item_pairs;
+  if (ti > cap) ti = cap > 0 ? cap : 1;
   const uint32_t task_items = (uint32_t)ti;
   uint32_t acc = 0;
   for (int p = 0; p < B.R; ++p) {
@@ -443,9 +549,8 @@ __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas) {
 // arc-sum section (touched once per 32 arc pairs) follows the runtime-sized
 // count section.
 struct ArcSum {
-  unsigned long long lo;  // arc-path fixed-point sum, low 64 bits
-  uint32_t hi;            // carries into bit 64
-  uint32_t pad;
+  unsigned long long lo;  // arc-path fixed-point sum (two's complement), low 64 bits
+  unsigned long long hi;  // high 64 bits
 };
 
 template <typename TT, int SLOTS>
@@ -469,20 +574,25 @@ size_t pair_kernel_smem(uint32_t bins, int wide, int slots) {
   return slots > 8 ? PairLayout<int32_t, 16>::total(bins) : PairLayout<int32_t, 8>::total(bins);
 }
 
-// Adds one arc-path ordered pair to the CTA histogram as 128-bit fixed point
-// of (1/(omega*v) - 1); bw = bin | (v == 1/2) << 31.
+// Adds one arc-path ordered pair to the CTA histogram: (1/(omega*v) - 1) as a
+// signed 128-bit fixed-point integer (53 fractional bits, two's complement,
+// carry detected on the low word); bw = bin | (v == 1/2) << 31.
 __device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, ArcSum* s_arc,
-                                             uint32_t* n_arc) {
+                                             uint2* s_ch, uint32_t* n_arc) {
   if (ws != 1.0) ++*n_arc;                           // omega != 1 (SURVEY's arc-pair definition)
   const double w = ws * ((bw >> 31) ? 0.5 : 1.0);  // edge::pair_weight (edge_correction.cpp:88-103)
   const double term = 1.0 / w;                      // PairHistogram::add(.., 1.0 / w)
-  uint64_t lo, hi;
-  fixed52_minus_one(term, &lo, &hi);
   const uint32_t bin = bw & 0x7fffffffu;
+  if (w == 0.0) {  // omega == 0: the reference adds 1/0 = inf and its bin ends NaN
+    atomicOr(&s_ch[bin].x, 1u);  // bit 0 of the (always even) count: "infinite term"
+    return;
+  }
+  uint64_t lo, hi;
+  fixed_term_minus_one(term, &lo, &hi);
   if (lo | hi) {
     const unsigned long long old = atomicAdd(&s_arc[bin].lo, (unsigned long long)lo);
     if (old + lo < old) ++hi;
-    if (hi) atomicAdd(&s_arc[bin].hi, (uint32_t)hi);
+    if (hi) atomicAdd(&s_arc[bin].hi, (unsigned long long)hi);
   }
 }
 
@@ -493,9 +603,10 @@ __device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, ArcSum* s_a
 // form's gate are weighted here; the rest (and every entry of a general
 // polygon) move to the warp's deferred ring, so the general routine runs on
 // full warps of entries that need it.
+template <bool RECT>
 __device__ __forceinline__ void drain_main(int count, int lane, const uint4* ring, uint32_t head,
                                            uint4* cring, uint32_t* ctail, unsigned lanemask_lt,
-                                           const double2* pxy, ArcSum* s_arc,
+                                           const double2* pxy, ArcSum* s_arc, uint2* s_ch,
                                            const RegionView& reg, uint32_t* n_arc) {
   const bool valid = lane < count;
   uint4 e = make_uint4(0u, 0u, 0u, 0u);
@@ -512,23 +623,31 @@ __device__ __forceinline__ void drain_main(int count, int lane, const uint4* rin
   const unsigned m = __ballot_sync(FULL_MASK, defer);
   if (defer) cring[(*ctail + __popc(m & lanemask_lt)) & (kCplxRing - 1)] = e;
   *ctail += __popc(m);
-  if (valid && !defer) add_arc_term(ws, e.y, s_arc, n_arc);
+  if (valid && !defer) add_arc_term(ws, e.y, s_arc, s_ch, n_arc);
 }
 
 // Deferred ring: the reference's general spatial_isotropic_weight.
+template <bool RECT>
 __device__ __forceinline__ void drain_general(int count, int lane, const uint4* cring,
                                               uint32_t head, double* angs, int slots,
-                                              const double2* pxy, ArcSum* s_arc,
-                                              const RegionView& reg, int* overflow,
-                                              uint32_t* n_arc) {
+                                              const double2* pxy, ArcSum* s_arc, uint2* s_ch,
+                                              const RegionView& reg, const RegionView* reg_g,
+                                              int* overflow, uint32_t* n_arc) {
   if (lane >= count) return;
   const uint4 e = cring[(head + lane) & (kCplxRing - 1)];
   const double2 c = pxy[e.x];
   const double d = sqrt(__hiloint2double((int)e.w, (int)e.z));
   double ws = -1.0;
-  if (reg.nv <= 32) ws = spatial_weight_buf(c.x, c.y, d, reg, angs + lane, 32, slots / 2);
-  if (ws < 0.0) ws = spatial_weight(c.x, c.y, d, reg.ring, reg.nv, reg.maxabs, overflow);
-  add_arc_term(ws, e.y, s_arc, n_arc);
+  if (RECT) {
+    if (reg.nv <= 32) ws = spatial_weight_buf_rect(c.x, c.y, d, reg, angs + lane, 32, slots / 2);
+  } else {
+    ws = spatial_weight_buf<false>(c.x, c.y, d, reg, angs + lane, 32, slots / 2);
+  }
+  if (ws < 0.0) {
+    if (RECT) ws = spatial_weight_ring(c.x, c.y, d, reg.ring, reg.nv, reg.maxabs, overflow);
+    else ws = spatial_weight(c.x, c.y, d, reg_g, overflow);
+  }
+  add_arc_term(ws, e.y, s_arc, s_ch, n_arc);
 }
 
 #ifndef STK_PAIR_MINB
@@ -544,7 +663,7 @@ constexpr int kKUnroll = STK_K_UNROLL;
 #ifndef STK_SPECIALIZE
 #define STK_SPECIALIZE 1  // 2: own-tile x deep variants, 1: deep only, 0: one generic loop
 #endif
-template <typename TT, int SLOTS>
+template <typename TT, int SLOTS, bool RECT>
 __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_task, s_next;
@@ -612,7 +731,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     for (uint32_t b = tid; b < bins; b += blockDim.x) {
       S.ch[b] = make_uint2(0u, 0u);
       S.arc[b].lo = 0ULL;
-      S.arc[b].hi = 0u;
+      S.arc[b].hi = 0ULL;
     }
     __syncthreads();
     const uint32_t task = s_task;
@@ -714,14 +833,15 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         if (cpending >= 32 || (done && pending == 0 && cpending > 0)) {
           const int cnt_ = (int)min(cpending, 32u);
           __syncwarp();
-          drain_general(cnt_, lane, cring, ch_, angs, slots, pxy, S.arc, A.reg, &overflow, &n_arc);
+          drain_general<RECT>(cnt_, lane, cring, ch_, angs, slots, pxy, S.arc, S.ch, A.reg, A.reg_g,
+                              &overflow, &n_arc);
           ch_ += (uint32_t)cnt_;
           continue;
         }
         if (pending >= 32 || (done && pending > 0)) {
           const int cnt_ = (int)min(pending, 32u);
           __syncwarp();
-          drain_main(cnt_, lane, arcq, qh, cring, &ct_, lanemask_lt, pxy, S.arc, A.reg, &n_arc);
+          drain_main<RECT>(cnt_, lane, arcq, qh, cring, &ct_, lanemask_lt, pxy, S.arc, S.ch, A.reg, &n_arc);
           qh += (uint32_t)cnt_;
           continue;
         }
@@ -848,7 +968,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     const uint64_t hb = (uint64_t)p * bins;
     for (uint32_t b = tid; b < bins; b += blockDim.x) {
       const uint2 chb = S.ch[b];
-      if (chb.x) atomicAdd(&B.h_cnt[hb + b], (unsigned long long)chb.x);
+      // counts are even (2 per unordered pair); bit 0 flags an infinite term
+      if (chb.x > 1u) atomicAdd(&B.h_cnt[hb + b], (unsigned long long)(chb.x & ~1u));
+      if (chb.x & 1u) atomicOr(&B.h_cnt[hb + b], 1ULL);
       if (chb.y) atomicAdd(&B.h_half[hb + b], (unsigned long long)chb.y);
       const unsigned long long lo = S.arc[b].lo;
       unsigned long long hi = S.arc[b].hi;
@@ -874,26 +996,36 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
 }
 
 // Host-side launch helpers (keep the kernel templates in this translation unit).
-static const void* pair_fn(int wide, int slots) {
-  if (wide) return slots > 8 ? (const void*)pair_kernel<int64_t, 16> : (const void*)pair_kernel<int64_t, 8>;
-  return slots > 8 ? (const void*)pair_kernel<int32_t, 16> : (const void*)pair_kernel<int32_t, 8>;
+template <typename TT, int SLOTS>
+static const void* pair_fn3(int rect) {
+  return rect ? (const void*)pair_kernel<TT, SLOTS, true> : (const void*)pair_kernel<TT, SLOTS, false>;
+}
+static const void* pair_fn(int wide, int slots, int rect) {
+  if (wide) return slots > 8 ? pair_fn3<int64_t, 16>(rect) : pair_fn3<int64_t, 8>(rect);
+  return slots > 8 ? pair_fn3<int32_t, 16>(rect) : pair_fn3<int32_t, 8>(rect);
 }
 
-cudaError_t pair_kernel_prepare(int wide, int slots, size_t smem, int* per_sm) {
-  const void* fn = pair_fn(wide, slots);
+cudaError_t pair_kernel_prepare(int wide, int slots, int rect, size_t smem, int* per_sm) {
+  const void* fn = pair_fn(wide, slots, rect);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fn, kPairWarps * 32, smem);
 }
 
-void pair_kernel_launch(int wide, int slots, unsigned ctas, size_t smem, cudaStream_t stream,
-                        const PairArgs& A) {
+template <typename TT, int SLOTS>
+static void launch3(int rect, unsigned ctas, size_t smem, cudaStream_t stream, const PairArgs& A) {
+  if (rect) pair_kernel<TT, SLOTS, true><<<ctas, kPairWarps * 32, smem, stream>>>(A);
+  else pair_kernel<TT, SLOTS, false><<<ctas, kPairWarps * 32, smem, stream>>>(A);
+}
+
+void pair_kernel_launch(int wide, int slots, int rect, unsigned ctas, size_t smem,
+                        cudaStream_t stream, const PairArgs& A) {
   if (wide) {
-    if (slots > 8) pair_kernel<int64_t, 16><<<ctas, kPairWarps * 32, smem, stream>>>(A);
-    else pair_kernel<int64_t, 8><<<ctas, kPairWarps * 32, smem, stream>>>(A);
+    if (slots > 8) launch3<int64_t, 16>(rect, ctas, smem, stream, A);
+    else launch3<int64_t, 8>(rect, ctas, smem, stream, A);
   } else {
-    if (slots > 8) pair_kernel<int32_t, 16><<<ctas, kPairWarps * 32, smem, stream>>>(A);
-    else pair_kernel<int32_t, 8><<<ctas, kPairWarps * 32, smem, stream>>>(A);
+    if (slots > 8) launch3<int32_t, 16>(rect, ctas, smem, stream, A);
+    else launch3<int32_t, 8>(rect, ctas, smem, stream, A);
   }
 }
 
@@ -913,11 +1045,14 @@ __global__ void __launch_bounds__(256) finalize_kernel(Batch B, uint32_t cs, uin
   double* K = B.K + hb;
   double* L = B.L + hb;
   for (uint32_t b = threadIdx.x; b < bins; b += blockDim.x) {
-    const unsigned long long c = B.h_cnt[hb + b] + B.h_half[hb + b];
+    const unsigned long long cnt = B.h_cnt[hb + b];
+    const unsigned long long c = (cnt & ~1ULL) + B.h_half[hb + b];
     const unsigned long long lo0 = B.h_lo[hb + b];
-    const unsigned long long lo = lo0 + (c << 52);
-    const unsigned long long hi = B.h_hi[hb + b] + (c >> 12) + (lo < lo0 ? 1ULL : 0ULL);
-    K[b] = fixed128_to_double(hi, lo);
+    const unsigned long long lo = lo0 + (c << kFixedFracBits);
+    const unsigned long long hi =
+        B.h_hi[hb + b] + (c >> (64 - kFixedFracBits)) + (lo < lo0 ? 1ULL : 0ULL);
+    // a bin that received 1/0 (omega == 0): the reference's Kahan sum is NaN
+    K[b] = (cnt & 1ULL) ? __longlong_as_double(0x7ff8000000000000LL) : fixed128_to_double(hi, lo);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -980,21 +1115,24 @@ __global__ void diff_kernel(const double* est_l, const double* upper, uint32_t b
 
 // ============================================================ utilities
 __global__ void weights_kernel(const double* cx, const double* cy, const double* d,
-                               uint64_t count, RegionView reg, double* w, int* overflow,
+                               uint64_t count, RegionView reg, const RegionView* reg_g, double* w, int* overflow,
                                unsigned long long* bad) {
   __shared__ double angs[kAngleSlots * 128];
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= count) return;
-  if (d[i] > 0.0 && !point_in_polygon(cx[i], cy[i], reg.ring, reg.nv)) {
+  if (d[i] > 0.0 && !point_in_region(cx[i], cy[i], reg)) {
     atomicMin(bad, (unsigned long long)i);
     w[i] = 0.0;
     return;
   }
   // the pair kernel's order: closed form (rectangles), then the general routines
   double ws = reg.rect ? rect_single_edge_weight(cx[i], cy[i], d[i], reg) : -1.0;
-  if (ws < 0.0 && reg.nv <= 32)
-    ws = spatial_weight_buf(cx[i], cy[i], d[i], reg, angs + threadIdx.x, 128, kAngleSlots / 2);
-  if (ws < 0.0) ws = spatial_weight(cx[i], cy[i], d[i], reg.ring, reg.nv, reg.maxabs, overflow);
+  if (ws < 0.0)
+    ws = reg.rect ? spatial_weight_buf<true>(cx[i], cy[i], d[i], reg, angs + threadIdx.x, 128,
+                                             kAngleSlots / 2)
+                  : spatial_weight_buf<false>(cx[i], cy[i], d[i], reg, angs + threadIdx.x, 128,
+                                              kAngleSlots / 2);
+  if (ws < 0.0) ws = spatial_weight(cx[i], cy[i], d[i], reg_g, overflow);
   w[i] = ws;
 }
 

@@ -13,11 +13,14 @@ struct PairArgs {
   GridGeom G;
   BinView bins;
   RegionView reg;
+  const RegionView* reg_g;  // device-memory copy of reg for the out-of-line fallback weight
 };
 
 __global__ void validate_kernel(const double* x, const double* y, const int64_t* t, uint64_t n,
                                 RegionView reg, unsigned long long* bad);
 __global__ void csr_fast_kernel(Batch B, int p_first, uint64_t seed0, RegionView reg,
+                                uint64_t ntl, uint64_t limit);
+__global__ void csr_poly_kernel(Batch B, int p_first, uint64_t seed0, RegionView reg,
                                 uint64_t ntl, uint64_t limit);
 __global__ void csr_seq_kernel(Batch B, int p_first, int count, uint64_t seed0, RegionView reg,
                                uint64_t ntl, uint64_t limit, int force);
@@ -28,14 +31,14 @@ __global__ void resample_seq_kernel(Batch B, int p_first, int count, uint64_t se
                                     int mode);
 __global__ void key_kernel(Batch B, GridGeom G, int p_first);
 __global__ void scan_kernel(const uint32_t* counts, uint32_t* start, uint32_t* istart,
-                            uint32_t cells);
+                            uint32_t cells, unsigned long long* max_cell);
 __global__ void select_count_kernel(Batch B, GridGeom G);
 __global__ void select_scatter_kernel(Batch B, GridGeom G);
 __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first);
 __global__ void items_kernel(Batch B, GridGeom G, int p_first);
 __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas);
-cudaError_t pair_kernel_prepare(int wide, int slots, size_t smem, int* per_sm);
-void pair_kernel_launch(int wide, int slots, unsigned ctas, size_t smem, cudaStream_t stream,
+cudaError_t pair_kernel_prepare(int wide, int slots, int rect, size_t smem, int* per_sm);
+void pair_kernel_launch(int wide, int slots, int rect, unsigned ctas, size_t smem, cudaStream_t stream,
                         const PairArgs& A);
 __global__ void finalize_kernel(Batch B, uint32_t cs, uint32_t ct, const double* s_values,
                                 const int64_t* t_values, double area, int64_t duration,
@@ -45,7 +48,7 @@ __global__ void envelope_kernel(Batch B, uint32_t bins, int p_first, int count, 
 __global__ void diff_kernel(const double* est_l, const double* upper, uint32_t bins,
                             double* diff);
 __global__ void weights_kernel(const double* cx, const double* cy, const double* d,
-                               uint64_t count, RegionView reg, double* w, int* overflow,
+                               uint64_t count, RegionView reg, const RegionView* reg_g, double* w, int* overflow,
                                unsigned long long* bad);
 __global__ void dfma_peak_kernel(double* out, int iters, double a, double b);
 

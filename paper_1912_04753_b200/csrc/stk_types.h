@@ -9,7 +9,10 @@ namespace stk {
 constexpr int kItemCenters = 32;    // centers per warp work item (one per lane)
 constexpr int kTaskMinItems = 4;    // warp items per CTA task: adaptive in [min, max] so the
 constexpr int kTaskMaxItems = 256;  // batch has ~8 tasks per resident CTA
-constexpr int kPairWarps = 8;       // warps per pair-kernel CTA
+#ifndef STK_PAIR_WARPS
+#define STK_PAIR_WARPS 8
+#endif
+constexpr int kPairWarps = STK_PAIR_WARPS;  // warps per pair-kernel CTA
 constexpr int kBucketTable = 1024;  // bucket table size for bin guesses
 constexpr int kAngleSlots = 16;    // per-lane crossing scratch: 2 doubles x 8 crossings
 constexpr int kRingSmem = 32;      // ring vertices staged in shared memory (bitmask path)
@@ -17,6 +20,7 @@ constexpr int kRingSmem = 32;      // ring vertices staged in shared memory (bit
 #define STK_ARC_CHUNK 12
 #endif
 constexpr int kArcChunk = STK_ARC_CHUNK;        // candidate steps between arc drains
+constexpr int kFixedFracBits = 53;  // fixed-point weighted sums: value * 2^53
 constexpr int kArcRing = 1024;      // per-warp arc ring entries (> 31 + kArcChunk * 64)
 constexpr int kCplxRing = 128;      // per-warp ring of entries deferred to the general weight (> 63)
 
@@ -32,6 +36,23 @@ struct RegionView {
   double2 rv[4];        // rect: the ring's vertices (kernel-parameter copy)
   double sw_dmin;       // rect single-edge closed form: smallest radius it accepts
   double sw_margin;     // ... and smallest d - h (outside midpoint clear of the boundary)
+  // General polygons.  Horizontal slabs: slab s lists every
+  // edge k (ring[k] -> ring[k+1]) whose y-range, widened by the on_segment
+  // tolerance, meets the slab; point_in_polygon of a probe then visits only
+  // its slab's edges.  Valid for probes with |x|, |y| <= pip_lim.
+  const uint32_t* slab_start;  // [nslab + 1]
+  const uint32_t* slab_edge;
+  uint32_t nslab;
+  double slab_y0, slab_inv_h, pip_lim, pip_ylo, pip_yhi;
+  // Edge cells: cell (ix, iy) of width 1/ec_inv_w lists every segment i
+  // (ring[i-1] -> ring[i]) within ec_reach of the cell; a circle of radius
+  // d <= ec_dmax around any point of the cell crosses no other segment
+  // (the reference rejects them).  ec_start == nullptr: not built.
+  const uint32_t* ec_start;    // [ec_nx * ec_ny + 1]
+  const uint32_t* ec_edge;
+  int ec_nx, ec_ny;
+  double ec_x0, ec_y0, ec_inv_w, ec_dmax, ec_reach;
+  int no_safe;  // debugging (STK_NO_SAFE_RADIUS): every pair takes the exact path
 };
 
 // Distance grid in the forms the kernels consume.
@@ -111,7 +132,7 @@ struct Batch {
   // exact histograms [R][bins]
   unsigned long long* h_cnt;   // in-threshold pairs
   unsigned long long* h_half;  // interior pairs with v = 1/2 (contribute 2)
-  unsigned long long* h_lo;    // arc-path sum of (1/w - 1), 128-bit fixed 52
+  unsigned long long* h_lo;    // arc-path sum of (1/w - 1), signed 128-bit fixed 53
   unsigned long long* h_hi;
   double* K;  // [R][bins]
   double* L;  // [R][bins]

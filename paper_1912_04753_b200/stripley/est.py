@@ -214,7 +214,7 @@ def pair_histogram(points, region: StudyRegion, grid: DistanceGrid, shard: int =
                    nshards: int = 1, device=None, telemetry: EstimatorTelemetry | None = None):
     """Pre-cumulative per-bin results of one pattern (or one shard of it):
     exact ``counts`` (uint64), the exact weighted sum as 128-bit fixed point
-    (``sum_hi``, ``sum_lo``; 52 fractional bits) and ``hist`` (that sum rounded
+    (``sum_hi``, ``sum_lo``; 53 fractional bits) and ``hist`` (that sum rounded
     once) — est::PairHistogram (estimator.hpp:55-81)."""
     pts, d = _prepare(points, region, grid, None, device)
     shape = (grid.cells_s(), grid.cells_t())

@@ -10,16 +10,28 @@ out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--
 path = None
 agg = {}
 src = open("paper_1912_04753_b200/csrc/stk_kernels.cu").read().splitlines()
+dev = open("paper_1912_04753_b200/csrc/stk_device.cuh").read().splitlines()
 def region(path, ln):
     if path == "stk_device.cuh":
-        return "arc weight (stk_device.cuh)"
+        for k in range(ln - 1, -1, -1):
+            line = dev[k]
+            if line.startswith("__device__"):
+                name = line.split("(")[0].split()[-1]
+                if name in ("rect_single_edge_weight",):
+                    return "arc weight: closed form"
+                if name in ("fast_atan2",):
+                    return "arc weight: atan2"
+                if name in ("fixed52_minus_one",):
+                    return "arc term (fixed point)"
+                return "arc weight: general (" + name + ")"
+        return "arc weight: other"
     if path != "stk_kernels.cu":
         return "intrinsics " + path
     # find the enclosing function by scanning upward for a marker
     for k in range(ln - 1, -1, -1):
         line = src[k]
-        if "drain_arcs(" in line and "void" in line:
-            return "arc drain"
+        if "void drain_main(" in line or "void drain_general(" in line or "void add_arc_term(" in line:
+            return "arc drain (" + line.split("(")[0].split()[-1] + ")"
         if "for (int k = kc; k < kend; ++k)" in line or "for (int k = 0; k < m; ++k)" in line or "for (uint32_t j0 = rb; j0 < re; j0 += 32)" in line:
             return "candidate/bin loop"
         if "flush the CTA histogram" in line:

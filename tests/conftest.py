@@ -20,14 +20,27 @@ def golden(name):
 
 
 def rel_err(a, b, floor=1e-300):
+    """Largest relative difference over finite entries; inf when the NaN
+    positions differ (a bin that received 1/0 is NaN in the reference)."""
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
+    if not np.array_equal(np.isnan(a), np.isnan(b)):
+        return float("inf")
+    m = ~np.isnan(a)
+    if not m.any():
+        return 0.0
+    a, b = a[m], b[m]
     return float(np.max(np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), floor)))
 
 
 def surfaces_close(a, b, rel_tol=1e-9, abs_tol=1e-12):
-    """testutil::rel_close elementwise (proj/tests/helpers.hpp:141-152)."""
+    """testutil::rel_close elementwise (proj/tests/helpers.hpp:141-152), with
+    NaN required in the same places."""
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
+    if not np.array_equal(np.isnan(a), np.isnan(b)):
+        return False
+    m = ~np.isnan(a)
+    a, b = a[m], b[m]
     tol = np.maximum(abs_tol, rel_tol * np.maximum(np.abs(a), np.abs(b)))
     return bool(np.all(np.abs(a - b) <= tol))

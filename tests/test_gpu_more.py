@@ -130,7 +130,10 @@ def _compare(api, port, x, y, t, ring, p0, p1, s, tv, tol=TOL):
 
 def test_coincident_points_pair_with_weight_one(api, port):
     """Self-exclusion is by index; coincident distinct points pair at d = 0
-    with omega = 1 (edge_correction.cpp:47)."""
+    with omega = 1 (edge_correction.cpp:47).  The circle around (50, 50)
+    through all four corners gets omega == 0 from the reference's arc rule:
+    1/0 = inf enters that bin, whose K is NaN in the reference (checked
+    against oracle/_ref when it is built here)."""
     ring, p0, p1 = square(100.0)
     x = np.array([0.0, 0.0, 50.0, 50.0, 50.0, 100.0])
     y = np.array([0.0, 0.0, 50.0, 50.0, 50.0, 100.0])
@@ -138,6 +141,12 @@ def test_coincident_points_pair_with_weight_one(api, port):
     h = _compare(api, port, x, y, t, ring, p0, p1, [1.0, 10.0, 200.0], [1, 5, 100])
     assert h["counts"][0, 0] == 4  # (0,0)x2 at u=0 and the two (50,50) points at u=0
     assert h["counts"][0, 1] == 4  # (50,50) pairs at u=2
+    assert np.isnan(h["hist"][2, 2]) and h["counts"][2, 2] == 22
+    assert h["sum_hi"][2, 2] >= 1 << 56  # the exported infinite-term mark (stk.h)
+    est, geom = api["est"], api["geom"]
+    k = est.estimate_surface((x, y, t), geom.StudyRegion(ring, p0, p1),
+                             est.DistanceGrid([1.0, 10.0, 200.0], [1, 5, 100]))
+    assert np.isnan(k.values[2, 2]) and np.isfinite(k.values[:2]).all()
 
 
 def test_points_on_boundary_corners_and_period_ends(api, port):

@@ -154,9 +154,44 @@ def test_port_vs_live_reference_random_polygons():
 
 
 def test_fixed_point_rounding():
-    # 2^52 * (1 + 2^-52) rounds to even; values with hi words round once.
+    # 53 fractional bits: 2^53 is 1.0; 2 + 2^-53 rounds to 2; hi words round once.
     assert port.__name__  # noqa
     lib = oracle._load_port()
-    assert lib.orc_fixed_to_double(0, 1 << 52) == 1.0
-    assert lib.orc_fixed_to_double(1, 0) == 2.0 ** 12
-    assert lib.orc_fixed_to_double(0, (1 << 53) + 1) == 2.0  # 2 + 2^-52 -> exact
+    assert lib.orc_fixed_to_double(0, 1 << 53) == 1.0
+    assert lib.orc_fixed_to_double(1, 0) == 2.0 ** 11
+    assert lib.orc_fixed_to_double(0, (1 << 54) + 1) == 2.0
+    assert lib.orc_fixed_to_double(0, (1 << 53) - 1) == 1.0 - 2.0 ** -53  # a term below 1
+
+
+def test_port_vs_live_reference_degenerate_weights():
+    """Reference rounding corners the port must reproduce: omega == 0 (the
+    circle through all four corners of a square: 1/0 enters the bin, whose K
+    is NaN in the reference) and omega slightly above 1 (an arc sum one ulp
+    over 2*pi at UTM-like coordinates: a term just below 1)."""
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built here")
+    from oracle import ref
+
+    ring = np.array([[0, 0], [100.0, 0], [100.0, 100.0], [0, 100.0]])
+    x = np.array([0.0, 0.0, 50.0, 50.0, 50.0, 100.0])
+    t = np.array([0, 0, 10, 10, 12, 100])
+    s, tv = np.array([1.0, 10.0, 200.0]), np.array([1, 5, 100], np.int64)
+    k_ref, _, _ = ref.estimate_surface(x, x.copy(), t, ring, 0, 100, s, tv, use_index=True)
+    h = port.estimate(x, x.copy(), t, ring, 0, 100, s, tv)
+    assert np.isnan(k_ref[2, 2]) and surfaces_close(h["k"], k_ref, 1e-12)
+    # omega = 1 + 2^-52 from the reference (found by tests/test_gpu_polygons.py)
+    a = 2.0 * np.pi * np.arange(200) / 200
+    r = 1000.0 * np.random.default_rng(4).uniform(0.4, 1.0, 200)
+    star = np.stack([1100.0 + r * np.cos(a), 1100.0 + r * np.sin(a)], axis=1) + [4.5e5, 4.2e6]
+    w = ref.spatial_weight(451257.7456706156, 4200906.479450759, 173.86844087028163, star)
+    assert w == port.spatial_weight(451257.7456706156, 4200906.479450759, 173.86844087028163,
+                                    star)
+    cx, cy = 451103.41905628354, 4200826.394927663
+    assert ref.spatial_weight(cx, cy, 173.86844087028163, star) > 1.0  # 1 + 2^-52
+    xs = np.array([cx, 451257.7456706156])
+    ys = np.array([cy, 4200906.479450759])
+    ts = np.array([227, 251])
+    s2, tv2 = np.array([150.0, 300.0]), np.array([50, 400], np.int64)
+    k_ref, _, _ = ref.estimate_surface(xs, ys, ts, star, 0, 400, s2, tv2, use_index=True)
+    h = port.estimate(xs, ys, ts, star, 0, 400, s2, tv2)
+    assert rel_err(h["k"], k_ref) <= 1e-15
