@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--sims", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-sims", type=int, default=1)
+    ap.add_argument("--cpu-sample-frac", type=float, default=1.0,
+                    help="CPU reference sample: every (1/frac)-th observed point (pairs/s is "
+                         "per pair, so a subsample keeps the metric comparable)")
     ap.add_argument("--ring", type=int, default=0,
                     help="replace the square by a regular polygon of this many vertices "
                          "(acceptance criterion 6 shape)")
@@ -136,6 +139,11 @@ def observed_points(cfg, dev=None):
 
 
 # ------------------------------------------------------------------ reference
+def subsample(x, y, t, frac):
+    k = max(1, int(round(1.0 / frac))) if frac < 1.0 else 1
+    return x[::k], y[::k], t[::k]
+
+
 def cpu_reference_step(x, y, t, cfg, s, tv, sample_sims, workers):
     """One bounded sample of the workload through the reference's rt::run_job."""
     from oracle import ref
@@ -156,7 +164,7 @@ def run_reference(args):
     cfg, s, tv, sims = workload(args.config, args.sims, args.ring)
     import oracle
 
-    x, y, t = observed_points_cpu(cfg)
+    x, y, t = subsample(*observed_points_cpu(cfg), args.cpu_sample_frac)
     workers = os.cpu_count() or 1
     kind = "reference" if oracle.ref_available() else "port"
     if kind != "reference":
@@ -173,7 +181,7 @@ def run_reference(args):
         pairs += p
         secs += dt
     value = pairs / secs
-    sample = (f"{cfg.name} observed pattern + {sample_sims} CSR realisation(s) per step "
+    sample = (f"{cfg.name} observed pattern ({len(x)} points) + {sample_sims} CSR realisation(s) per step "
               f"(of 1+{sims}), rt::run_job LocalExecutor({workers}), KDB {4 * workers} partitions, "
               f"index {'on' if cfg.name != 'C3' else 'off'}, cache off")
     line = {
@@ -368,7 +376,8 @@ def run_ours(args):
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, s, tv, sims, x, y, t, args.cpu_sample_sims)
+        cpu = cpu_baseline(cfg, s, tv, sims, *subsample(x, y, t, args.cpu_sample_frac),
+                           args.cpu_sample_sims)
 
     line = {
         "metric": "space-time in-threshold pairs evaluated per second",
@@ -417,7 +426,7 @@ def cpu_baseline(cfg, s, tv, sims, x, y, t, sample_sims):
         workers = os.cpu_count() or 1
         pairs, dt = cpu_reference_step(x, y, t, cfg, s, tv, sample_sims, workers)
         return {"value": pairs / dt, "unit": "pairs/s", "cores": workers, "kind": "reference",
-                "sample": f"{cfg.name} observed + {sample_sims} CSR realisation(s) through the "
+                "sample": f"{cfg.name} observed ({len(x)} points) + {sample_sims} CSR realisation(s) through the "
                           f"reference rt::run_job, LocalExecutor({workers}), {dt:.1f} s"}
     except Exception as e:  # the baseline is reported, never the target
         return {"value": None, "unit": "pairs/s", "cores": 0, "kind": "reference",

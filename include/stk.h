@@ -101,7 +101,11 @@ int stk_estimate_surface(stk_ctx* ctx, const double* x, const double* y, const i
 /* Per-bin (pre-cumulative) histogram of est::PairHistogram
  * (core/include/stripley/estimator.hpp:55-81) plus exact per-bin counts.
  * hist[b] is the exact sum of 1/(omega*v) rounded once; sum_hi/sum_lo (may
- * be NULL) give it as 128-bit fixed point with 53 fractional bits.
+ * be NULL) give it as 128-bit fixed point with 53 fractional bits.  A bin
+ * that received 1/0 (omega == 0: the reference adds +inf and its Kahan sum
+ * becomes NaN) has hist[b] = NaN and 2^120 added to its fixed-point sum: real
+ * sums stay below 2^110, so sums of up to 255 shard partials keep the mark,
+ * and stk_finalize turns any sum >= 2^119 into NaN.
  * Shards: the pair work of the pattern is split into nshards disjoint slices;
  * shard s computes only its slice (counts/sums add exactly across shards —
  * the single-huge-pattern multi-GPU path).  nshards = 1 for the whole. */

@@ -112,7 +112,7 @@ struct stk_ctx {
   double xmin = 0, xmax = 0, ymin = 0, ymax = 0, maxabs = 0;
   bool fast_rect = false;  // axis-aligned rectangle: every bbox draw is inside
   DevBuf<double2> d_ring;
-  // general-polygon indexes (DESIGN.md §4.6): slabs (region only) and edge
+  // general-polygon indexes (DESIGN.md §4.5): slabs (region only) and edge
   // cells (region + grid), built lazily by region_view()
   bool slab_ok = false, ec_ok = false;
   uint32_t nslab = 0;
@@ -237,7 +237,7 @@ void build_slabs(stk_ctx* c) {
 // segment i (ring[i-1] -> ring[i]) unless the segment is farther than
 // reach + half-diagonal from the cell center, i.e. farther than
 // reach = s_max (1 + 4e-6) + 1e-9 S from every point of the cell.  For
-// d <= s_max the reference rejects every unlisted segment (DESIGN.md §4.6).
+// d <= s_max the reference rejects every unlisted segment (DESIGN.md §4.5).
 double seg_dist(double px, double py, double ax, double ay, double bx, double by) {
   const double ex = bx - ax, ey = by - ay, l2 = ex * ex + ey * ey;
   double t = 0.0;
@@ -325,7 +325,7 @@ RegionView region_view(stk_ctx* c) {
   for (int i = 0; i < 4; ++i)
     r.rv[i] = (r.rect && c->ring.size() == 8) ? make_double2(c->ring[2 * i], c->ring[2 * i + 1])
                                               : make_double2(0.0, 0.0);
-  // DESIGN.md §4.5: the closed form needs the reach margin d*1e-6 far above
+  // DESIGN.md §4.4: the closed form needs the reach margin d*1e-6 far above
   // coordinate rounding (d >= 1e-8 S) and the outside probe clear of every
   // on_segment tolerance (d - h > 4 box_m)
   r.sw_dmin = 1e-8 * S;

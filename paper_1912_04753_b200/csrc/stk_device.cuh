@@ -214,7 +214,7 @@ __device__ __noinline__ double spatial_weight(double cx, double cy, double d, co
   const double2* ring = R.ring;
   const uint32_t nv = R.nv;
   uint32_t cnt;
-  const uint32_t* list = edge_list(cx, cy, d, R, &cnt);  // segments that can cross (§4.6)
+  const uint32_t* list = edge_list(cx, cy, d, R, &cnt);  // segments that can cross
   double buf[kMaxAngles];
   double lower = -1.0;  // angles are in [0, 2*pi)
   int u = 0;            // kept angles so far
@@ -610,7 +610,7 @@ __device__ STK_WEIGHT_INLINE double spatial_weight_buf(double cx, double cy, dou
 // theta_ref carries the reference's own rounding (the quadratic's
 // cancellation: <= 2^-53 * scale / (len * sqrt(disc) * d) rad), which the
 // gate qa*disc*d^2 >= 1e-10*scale^2 bounds by ~1e-11; ours, from
-// atan2(sqrt((d-h)(d+h)), h), is within ~1e-11 too (DESIGN.md §4.5).
+// atan2(sqrt((d-h)(d+h)), h), is within ~1e-11 too (DESIGN.md §4.4).
 // Returns -1 when the gate fails (the caller uses the general routine).
 __device__ __forceinline__ double rect_single_edge_weight(double cx, double cy, double d,
                                                           const RegionView& R) {
@@ -653,7 +653,7 @@ __device__ __forceinline__ double rect_single_edge_weight(double cx, double cy, 
 // Squared radius below which spatial_weight() provably returns exactly 1.0
 // for this center (the circle stays strictly inside every edge's reach by a
 // relative margin far above the rounding error of the reference's quadratic;
-// DESIGN.md §4.2).  Returns -1 when no such radius exists.
+// DESIGN.md §4.4).  Returns -1 when no such radius exists.
 // With edge cells (general polygons) only the cell's segments are visited:
 // every other segment is farther than ec_reach from the point, so the true
 // nearest distance is >= min(listed nearest, ec_reach) and the radius below

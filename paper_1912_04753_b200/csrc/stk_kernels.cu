@@ -583,7 +583,7 @@ __device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, ArcSum* s_a
   const double w = ws * ((bw >> 31) ? 0.5 : 1.0);  // edge::pair_weight (edge_correction.cpp:88-103)
   const double term = 1.0 / w;                      // PairHistogram::add(.., 1.0 / w)
   const uint32_t bin = bw & 0x7fffffffu;
-  if (w == 0.0) {  // omega == 0: the reference adds 1/0 = inf and its bin ends NaN (DESIGN.md §4.3)
+  if (w == 0.0) {  // omega == 0: the reference adds 1/0 = inf and its bin ends NaN (DESIGN.md §4.5)
     atomicOr(&s_ch[bin].x, 1u);  // bit 0 of the (always even) count: "infinite term"
     return;
   }

@@ -36,7 +36,7 @@ struct RegionView {
   double2 rv[4];        // rect: the ring's vertices (kernel-parameter copy)
   double sw_dmin;       // rect single-edge closed form: smallest radius it accepts
   double sw_margin;     // ... and smallest d - h (outside midpoint clear of the boundary)
-  // General polygons (DESIGN.md §4.6).  Horizontal slabs: slab s lists every
+  // General polygons (DESIGN.md §4.5).  Horizontal slabs: slab s lists every
   // edge k (ring[k] -> ring[k+1]) whose y-range, widened by the on_segment
   // tolerance, meets the slab; point_in_polygon of a probe then visits only
   // its slab's edges.  Valid for probes with |x|, |y| <= pip_lim.
