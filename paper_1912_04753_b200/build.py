@@ -94,5 +94,45 @@ def build_cpp_tests(force: bool = False) -> str:
     return TEST_BIN
 
 
+CLI_BIN = os.path.join(HERE, "stripley_gpu")
+CLI_SOURCES = ["stripley_cli.cpp", "stripley_io.cpp"]
+
+
+def nlohmann_include():
+    """Directory holding nlohmann/json.hpp (the JSON header the reference's
+    io.cpp uses; this image ships it in cudnn_frontend's third-party tree)."""
+    import site
+    import sysconfig
+
+    roots = {sysconfig.get_paths()["purelib"], *site.getsitepackages()}
+    for root in sorted(roots):
+        for sub in ("include/cudnn_frontend/thirdparty", "include"):
+            d = os.path.join(root, sub)
+            if os.path.exists(os.path.join(d, "nlohmann", "json.hpp")):
+                return d
+    for d in ("/usr/include", "/usr/local/include"):
+        if os.path.exists(os.path.join(d, "nlohmann", "json.hpp")):
+            return d
+    return None
+
+
+def build_cli(force: bool = False) -> str | None:
+    """The `stripley_gpu run` CLI (csrc/stripley_cli.cpp + stripley_io.cpp), linked
+    to libstk.so; None when no nlohmann/json.hpp is available."""
+    srcs = [os.path.join(CSRC, f) for f in CLI_SOURCES]
+    hdrs = [os.path.join(ROOT, "include", h) for h in ("stripley_gpu.hpp", "stripley_gpu_io.hpp")]
+    if not force and os.path.exists(CLI_BIN) and os.path.getmtime(CLI_BIN) > max(
+            os.path.getmtime(f) for f in srcs + hdrs + [LIB]):
+        return CLI_BIN
+    inc = nlohmann_include()
+    if inc is None:
+        print("warning: nlohmann/json.hpp not found; stripley_gpu CLI not built", file=sys.stderr)
+        return None
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), "-isystem",
+                    inc, *srcs, "-o", CLI_BIN, "-L", HERE, "-lstk", "-Wl,-rpath," + HERE],
+                   check=True)
+    return CLI_BIN
+
+
 if __name__ == "__main__":
     print(build_library(force="--force" in sys.argv, verbose="-v" in sys.argv))
