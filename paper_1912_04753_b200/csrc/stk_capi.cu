@@ -434,6 +434,9 @@ Plan make_plan(stk_ctx* c, uint64_t n, uint64_t patterns) {
   uint64_t R = std::max<uint64_t>(1, c->mem_budget / per);
   R = std::min<uint64_t>(R, std::max<uint64_t>(patterns, 1));
   R = std::min<uint64_t>(R, 4096);
+  // the pair kernel indexes a batch with 32-bit offsets (pattern * n + j etc.)
+  const uint64_t widest = std::max<uint64_t>({n, (uint64_t)P.G.cells + 1, P.max_items});
+  R = std::max<uint64_t>(1, std::min<uint64_t>(R, 0xffffffffull / widest));
   P.R = (int)R;
   return P;
 }

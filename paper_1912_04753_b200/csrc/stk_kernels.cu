@@ -742,34 +742,34 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       if (B.task_start[mid] <= task) lo_p = mid; else hi_p = mid - 1;
     }
     const int p = lo_p;
-    const uint64_t pb = (uint64_t)p * B.n;
-    const uint32_t* cstart = B.cell_start + (uint64_t)p * (G.cells + 1);
-    const uint32_t items_p = B.item_start[(uint64_t)p * (G.cells + 1) + G.cells];
+    // 32-bit offsets into the batch arrays (the host keeps R * n etc. < 2^32);
+    // bases stay kernel parameters instead of 64-bit registers
+    const uint32_t pb = (uint32_t)p * (uint32_t)B.n;
+    const uint32_t co = (uint32_t)p * (G.cells + 1);
+    const uint32_t items_p = B.item_start[co + G.cells];
     const uint32_t i0 = (task - B.task_start[p]) * task_items;
     const uint32_t i1 = min(i0 + task_items, items_p);
-    const uint2* items = B.items + (uint64_t)p * B.max_items;
-    const double2* pxy = B.pxy + pb;
-    const PtMeta<TT>* pmeta = reinterpret_cast<const PtMeta<TT>*>(B.pmeta) + pb;
+    const uint32_t io = (uint32_t)p * B.max_items;
+    const PtMeta<TT>* pmeta_b = reinterpret_cast<const PtMeta<TT>*>(B.pmeta);
     const bool sel_p = p < B.n_sel;
-    const uint32_t* clist = sel_p ? B.sel_start + (uint64_t)p * (G.cells + 1) : cstart;
-    const uint32_t* cposl = B.center_pos + pb;
+    const uint32_t* clist_b = sel_p ? B.sel_start : B.cell_start;
 
     for (;;) {
       uint32_t it = 0;
       if (lane == 0) it = atomicAdd(&s_next, 1u);
       it = __shfl_sync(FULL_MASK, it, 0);
       if (i0 + it >= i1) break;
-      const uint2 item = items[i0 + it];
+      const uint2 item = B.items[io + i0 + it];
       const uint32_t cell = item.x, start = item.y;
-      const uint32_t nc = min((uint32_t)kItemCenters, clist[cell + 1] - start);
+      const uint32_t nc = min((uint32_t)kItemCenters, clist_b[co + cell + 1] - start);
       // stage the item's centers (<= 32) in shared memory: the inner loop
       // broadcasts one center to the 32 neighbour lanes
       __syncwarp();
       bool cdeep = true;
       if (lane < (int)nc) {
-        const uint32_t pos = sel_p ? cposl[start + lane] : start + lane;
-        const PtMeta<TT> m = pmeta[pos];
-        cxy_w[lane] = pxy[pos];
+        const uint32_t pos = sel_p ? B.center_pos[pb + start + lane] : start + lane;
+        const PtMeta<TT> m = pmeta_b[pb + pos];
+        cxy_w[lane] = B.pxy[pb + pos];
         cm_w[lane] = m;
         cpos_w[lane] = pos;
         cdeep = (double)m.sq >= Qmax && m.vt >= Tmax;
@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       const uint32_t rest = cell / (uint32_t)G.nx;
       const int ky = (int)(rest % (uint32_t)G.ny);
       const int kt = (int)(rest / (uint32_t)G.ny);
-      const uint32_t own_end = cstart[cell + 1];
+      const uint32_t own_end = B.cell_start[co + cell + 1];
       const int RS = G.rs, RT = G.rt;
       // forward half-stencil rows (lane r holds row r): layer dt = 0 rows
       // dy = 0..RS, layers dt = 1..RT rows dy = -RS..RS; row dy = 0 of layer 0
@@ -801,9 +801,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         const int tk = kt + dt, yk = ky + dy;
         if (tk < G.nt && yk >= 0 && yk < G.ny) {
           const uint32_t row = ((uint32_t)tk * G.ny + yk) * G.nx;
-          my_rb = (dt == 0 && dy == 0) ? (sel_p ? cstart[cell] : first_pos + 1)
-                                        : cstart[row + max(kx - RS, 0)];
-          my_re = cstart[row + min(kx + RS, G.nx - 1) + 1];
+          my_rb = (dt == 0 && dy == 0) ? (sel_p ? B.cell_start[co + cell] : first_pos + 1)
+                                        : B.cell_start[co + row + max(kx - RS, 0)];
+          my_re = B.cell_start[co + row + min(kx + RS, G.nx - 1) + 1];
           if (my_rb > my_re) my_rb = my_re;
         }
       }
@@ -818,10 +818,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       uint32_t j0 = __shfl_sync(FULL_MASK, my_rb, r & 31);
       uint32_t re = __shfl_sync(FULL_MASK, my_re, r & 31);
       int kc = 0;
-      double2 nxy = make_double2(0.0, 0.0);
-      PtMeta<TT> nm{0, 0, 0.0f, 0u};
-      uint32_t jp = 0;
-      bool has = false, same_cell = false, tile_deep = false;
       for (;;) {
         const bool done = rows_left == 0;
         // the single drain site, ahead of new candidates so the ring never
@@ -833,7 +829,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         if (cpending >= 32 || (done && pending == 0 && cpending > 0)) {
           const int cnt_ = (int)min(cpending, 32u);
           __syncwarp();
-          drain_general<RECT>(cnt_, lane, cring, ch_, angs, slots, pxy, S.arc, S.ch, A.reg, A.reg_g,
+          drain_general<RECT>(cnt_, lane, cring, ch_, angs, slots, B.pxy + pb, S.arc, S.ch, A.reg, A.reg_g,
                               &overflow, &n_arc);
           ch_ += (uint32_t)cnt_;
           continue;
@@ -841,28 +837,33 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         if (pending >= 32 || (done && pending > 0)) {
           const int cnt_ = (int)min(pending, 32u);
           __syncwarp();
-          drain_main<RECT>(cnt_, lane, arcq, qh, cring, &ct_, lanemask_lt, pxy, S.arc, S.ch, A.reg, &n_arc);
+          drain_main<RECT>(cnt_, lane, arcq, qh, cring, &ct_, lanemask_lt, B.pxy + pb, S.arc, S.ch, A.reg, &n_arc);
           qh += (uint32_t)cnt_;
           continue;
         }
         if (done) break;
-        if (kc == 0) {  // new tile: this lane's neighbour into registers
-          jp = j0 + lane;
-          has = jp < re;
-          if (has) {
-            nxy = pxy[jp];
-            nm = pmeta[jp];
-          }
+        // this lane's neighbour, (re)loaded for every chunk (an L1 hit after the
+        // first): nothing of the tile stays live across the drain site above,
+        // whose register peak would otherwise push it to local memory
+        const uint32_t jp = j0 + lane;
+        const bool has = jp < re;
+        double2 nxy = make_double2(1e300, 1e300);  // no neighbour: q = inf > Qmax
+        PtMeta<TT> nm{0, 0, 0.0f, 0u};
+        if (has) {
+          nxy = B.pxy[pb + jp];
+          nm = pmeta_b[pb + jp];
+        }
+        if (kc == 0) {  // new tile
 #if STK_PREFETCH
           if (jp + 32 < re) {  // next tile of this row into L1 while this one is processed
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(pxy + jp + 32));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(pmeta + jp + 32));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(B.pxy + (pb + jp + 32)));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pmeta_b + (pb + jp + 32)));
           }
 #endif
-          same_cell = r == 0 && jp < own_end;
-          tile_deep = __all_sync(FULL_MASK, !has || ((double)nm.sq >= Qmax && nm.vt >= Tmax));
           n_cand += (unsigned long long)min(32u, re - j0) * nc;
         }
+        const bool tile_deep =
+            __all_sync(FULL_MASK, !has || ((double)nm.sq >= Qmax && nm.vt >= Tmax));
         const int kend = min(kc + kArcChunk, (int)nc);
         auto chunk = [&](auto own_tag, auto deep_tag) {
           constexpr bool OWN = decltype(own_tag)::value;
@@ -870,16 +871,27 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           // safe radius >= s_max and temporal threshold >= t_max, so all their
           // in-threshold pairs have omega == 1 and v == 1: count only
           constexpr bool DEEP = decltype(deep_tag)::value;
+          // the warp's staged centers, addressed from a per-chunk read of the
+          // thread index: a value the compiler cannot rematerialise inside
+          // the loop (it otherwise rebuilds the address every iteration)
+          uint32_t tidv;
+          asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tidv));
+          const uint32_t wo = (tidv >> 5) * 32;
+          const double2* cxy_c = S.cxy + wo;
+          const PtMeta<TT>* cm_c = S.cmeta + wo;
+          const uint32_t* cpos_c = S.cpos + wo;
+          const uint32_t jpc = j0 + (tidv & 31u);  // == jp, held in a register
+          const bool same_c = r == 0 && jpc < own_end;
 #pragma unroll kKUnroll
           for (int k = kc; k < kend; ++k) {
-            const double2 c = cxy_w[k];  // center k (broadcast)
-            const PtMeta<TT> cmk = cm_w[k];
+            const double2 c = cxy_c[k];  // center k (broadcast)
+            const PtMeta<TT> cmk = cm_c[k];
             const double dx = c.x - nxy.x, dy = c.y - nxy.y;
             const double q = dx * dx + dy * dy;  // spatial_distance^2, no FMA
             TT du = cmk.t - nm.t;
             du = du < 0 ? -du : du;              // temporal_distance
             bool owner = true;
-            if (OWN) owner = !same_cell || (sel_p ? nm.idx > cmk.idx : jp > cpos_w[k]);
+            if (OWN) owner = !same_c || (sel_p ? nm.idx > cmk.idx : jpc > cpos_c[k]);
             const bool in = has && owner && q <= Qmax && du <= Tmax;
             bool arc_i = false, arc_j = false;
             uint32_t bin = 0;
@@ -917,11 +929,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
               if (arc_i)
                 arcq[(qt + __popc(mi & lanemask_lt)) & (kArcRing - 1)] =
-                    make_uint4(cpos_w[k], bin | (half_i ? 0x80000000u : 0u), qlo, qhi);
+                    make_uint4(cpos_c[k], bin | (half_i ? 0x80000000u : 0u), qlo, qhi);
               qt += __popc(mi);
               if (arc_j)
                 arcq[(qt + __popc(mj & lanemask_lt)) & (kArcRing - 1)] =
-                    make_uint4(jp, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
+                    make_uint4(jpc, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
               qt += __popc(mj);
               n_exact += (uint32_t)arc_i + (uint32_t)arc_j;
             }
