@@ -128,12 +128,15 @@ struct stk_ctx {
   std::vector<double> s_values;
   std::vector<int64_t> t_values;
   std::vector<double> Q;
-  std::vector<uint16_t> stab, ttab;
-  float s_inv_bw = 0, t_inv_bw = 0;
+  std::vector<QBucket> qtab;
+  std::vector<TBucket<int64_t>> ttab;
+  int q_shift = 0, q_base = 0;
+  float t_inv_bw = 0;
   bool single_step = false;
   DevBuf<double> d_Q, d_s;
   DevBuf<int64_t> d_T;
-  DevBuf<uint16_t> d_stab, d_ttab;
+  DevBuf<QBucket> d_qtab;
+  DevBuf<TBucket<int64_t>> d_ttab;
 
   // batch buffers (grow-only)
   DevBuf<double> x, y;
@@ -144,6 +147,7 @@ struct stk_ctx {
   DevBuf<uint2> items;
   DevBuf<uint32_t> sel_start, center_pos;
   DevBuf<uint4> arcq;
+  DevBuf<double> angs;
   DevBuf<unsigned long long> hist, stats, bad;
   DevBuf<double> K, L, env, obs;
   DevBuf<int> flags, ovf;
@@ -356,13 +360,14 @@ BinView bin_view(stk_ctx* c) {
   BinView b;
   b.Q = c->d_Q.p;
   b.T = c->d_T.p;
-  b.s_tab = c->d_stab.p;
+  b.q_tab = c->d_qtab.p;
   b.t_tab = c->d_ttab.p;
   b.cs = (uint32_t)c->s_values.size();
   b.ct = (uint32_t)c->t_values.size();
   b.Qmax = c->Q.back();
   b.Tmax = c->t_values.back();
-  b.s_inv_bw = c->s_inv_bw;
+  b.q_shift = c->q_shift;
+  b.q_base = c->q_base;
   b.t_inv_bw = c->t_inv_bw;
   b.single_step = c->single_step ? 1 : 0;
   return b;
@@ -624,15 +629,9 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   items_kernel<<<gc, 256, 0, c->stream>>>(B, G, 0);
   CK(cudaGetLastError());
   ++c->launches;
-  // Crossing scratch: a circle of radius d <= s_max around a point of a
-  // rectangle reaches at most two edges (<= 4 crossings) when s_max is below
-  // half the shorter side; otherwise allow 8 crossings (more use the
-  // general local-memory path).
-  const double smin_side = std::min(c->xmax - c->xmin, c->ymax - c->ymin);
-  const int slots = (c->fast_rect && c->s_values.back() < 0.5 * smin_side) ? 8 : kAngleSlots;
-  const size_t smem = pair_kernel_smem(P.bins, B.wide, slots);
+  const size_t smem = pair_kernel_smem(P.bins, B.wide);
   int per_sm = 0;
-  CK(pair_kernel_prepare(B.wide, slots, c->fast_rect ? 1 : 0, smem, &per_sm));
+  CK(pair_kernel_prepare(B.wide, c->fast_rect ? 1 : 0, smem, &per_sm));
   if (per_sm < 1) throw Unsupported("distance grid too large for the pair kernel's shared histogram");
   tasks_kernel<<<1, 1, 0, c->stream>>>(B, G, (uint32_t)(c->num_sms * per_sm));
   CK(cudaGetLastError());
@@ -640,7 +639,6 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   CK(cudaEventRecord(e1, c->stream));
 
   PairArgs A;
-  A.angle_slots = slots;
   A.B = B;
   A.G = G;
   A.bins = bin_view(c);
@@ -649,7 +647,11 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   const uint64_t ctas = (uint64_t)c->num_sms * per_sm;
   c->arcq.ensure(ctas * kPairWarps * (kArcRing + kCplxRing));
   A.B.arcq = c->arcq.p;
-  pair_kernel_launch(B.wide, slots, c->fast_rect ? 1 : 0, (unsigned)ctas, smem, c->stream, A);
+  // crossing scratch of the general weight: <= 8 crossings per lane (more use
+  // the bounded-storage fallback), global and L1-resident
+  c->angs.ensure(ctas * kPairWarps * kAngleSlots * 32);
+  A.angs_g = c->angs.p;
+  pair_kernel_launch(B.wide, c->fast_rect ? 1 : 0, (unsigned)ctas, smem, c->stream, A);
   CK(cudaGetLastError());
   ++c->launches;
   CK(cudaEventRecord(e2, c->stream));
@@ -903,14 +905,14 @@ void stk_destroy(stk_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (auto e : c->evpool) cudaEventDestroy(e);
   c->d_ring.release(); c->d_Q.release(); c->d_s.release(); c->d_T.release();
-  c->d_stab.release(); c->d_ttab.release();
+  c->d_qtab.release(); c->d_ttab.release();
   c->x.release(); c->y.release(); c->t.release();
   c->pxy.release(); c->pmeta.release(); c->idx.release(); c->key.release(); c->rank.release();
   c->cell_count.release(); c->cell_start.release(); c->item_start.release();
   c->task_start.release(); c->task_counter.release(); c->items.release();
   c->hist.release(); c->stats.release(); c->bad.release(); c->K.release(); c->L.release();
   c->env.release(); c->obs.release(); c->flags.release(); c->ovf.release();
-  c->sel_start.release(); c->center_pos.release(); c->arcq.release();
+  c->sel_start.release(); c->center_pos.release(); c->arcq.release(); c->angs.release();
   c->scratch.release(); c->sx.release(); c->sy.release(); c->st.release();
   cudaStreamDestroy(c->stream);
   delete c;
@@ -1047,6 +1049,66 @@ int stk_set_region(stk_ctx* c, const double* ring_xy, uint32_t nv, int64_t perio
   });
 }
 
+namespace {
+
+// Distance buckets on q = d^2 indexed by the float bits of RN_float(q): with m
+// mantissa bits per octave (shift = 23 - m) the buckets are log-spaced, so
+// one table covers the grid's whole dynamic range.  Bucket i holds every q
+// whose float lands in it: q >= prev_float(lo_f) (RN can round up onto lo_f)
+// and q < hi_f; its entry is the first bin with Q[bin] >= that lower bound
+// (a lower bound of the true bin) and Q[bin].  Single-step when the next
+// threshold lies at or above hi_f.  Bucket 0 takes everything below.  The
+// largest m whose table is single-step everywhere wins; else m = 5 with the
+// compare loop on the device.
+bool build_q_buckets(stk_ctx* c) {
+  const std::vector<double>& Q = c->Q;
+  const int cs = (int)Q.size();
+  const double qmax = Q.back();
+  float top_f = (float)qmax;
+  if ((double)top_f < qmax) top_f = std::nextafter(top_f, std::numeric_limits<float>::infinity());
+  uint32_t top_bits;
+  std::memcpy(&top_bits, &top_f, 4);
+  auto as_float = [](uint32_t bits) {
+    float f;
+    std::memcpy(&f, &bits, 4);
+    return f;
+  };
+  auto build = [&](int m, std::vector<QBucket>* tab, int* shift, int* base) {
+    *shift = 23 - m;
+    const int64_t top = (int64_t)(top_bits >> *shift);
+    *base = (int)std::max<int64_t>(0, top - (kQBuckets - 1));
+    tab->assign(kQBuckets, QBucket{qmax, (uint32_t)(cs - 1), 0});
+    bool single = true;
+    for (int i = 0; i < kQBuckets; ++i) {
+      const uint64_t idx = (uint64_t)*base + i;
+      double lo = 0.0;
+      if (i > 0) lo = (double)std::nextafter(as_float((uint32_t)(idx << *shift)), 0.0f);
+      const uint64_t hb = (idx + 1) << *shift;
+      const double hi = hb >= 0x7f800000ull ? std::numeric_limits<double>::infinity()
+                                             : (double)as_float((uint32_t)hb);
+      int k = 0;
+      while (k < cs - 1 && Q[k] < lo) ++k;
+      (*tab)[i] = QBucket{Q[k], (uint32_t)k, 0};
+      if (lo <= qmax && k + 1 < cs && Q[k + 1] < hi) single = false;
+    }
+    return single;
+  };
+  for (int m = 8; m >= 2; --m) {
+    std::vector<QBucket> tab;
+    int shift, base;
+    if (build(m, &tab, &shift, &base)) {
+      c->qtab = std::move(tab);
+      c->q_shift = shift;
+      c->q_base = base;
+      return true;
+    }
+  }
+  build(5, &c->qtab, &c->q_shift, &c->q_base);
+  return false;
+}
+
+}  // namespace
+
 int stk_set_grid(stk_ctx* c, const double* s_values, uint32_t cs, const int64_t* t_values,
                  uint32_t ct) {
   return guarded(c, [&] {
@@ -1060,49 +1122,36 @@ int stk_set_grid(stk_ctx* c, const double* s_values, uint32_t cs, const int64_t*
     c->t_values.assign(t_values, t_values + ct);
     c->Q.resize(cs);
     for (uint32_t k = 0; k < cs; ++k) c->Q[k] = sqrt_threshold(s_values[k]);
-    // bucket tables: bucket b holds distances >= b*bw (guaranteed by a 1e-5
+    if (cs > 65535 || ct > 65535) throw Unsupported("more than 65535 bins per axis");
+    const bool q_single = build_q_buckets(c);
+    // time buckets (linear): bucket b holds u >= b*bw (guaranteed by a 1e-5
     // margin on the device-side bucket index), so the first bin at or above
-    // b*bw is a lower bound of the true bin.
-    const double smax = s_values[cs - 1];
-    const double sbw = smax / kBucketTable;
-    c->s_inv_bw = (float)((1.0 / sbw) * (1.0 - 1e-5));
-    c->stab.assign(kBucketTable, 0);
-    for (int b = 0, k = 0; b < kBucketTable; ++b) {
-      while (k < (int)cs - 1 && s_values[k] < b * sbw) ++k;
-      c->stab[b] = (uint16_t)std::min<int>(k, 65535);
-    }
+    // b*bw is a lower bound of the true bin; single-step when no bucket's
+    // range (with the margins) contains two thresholds
     const double tmax = (double)t_values[ct - 1];
     const double tbw = tmax / kBucketTable;
     c->t_inv_bw = (float)((1.0 / tbw) * (1.0 - 1e-5));
-    c->ttab.assign(kBucketTable, 0);
+    c->ttab.assign(kBucketTable, TBucket<int64_t>{0, 0});
+    bool t_single = true;
     for (int b = 0, k = 0; b < kBucketTable; ++b) {
       while (k < (int)ct - 1 && (double)t_values[k] < b * tbw) ++k;
-      c->ttab[b] = (uint16_t)std::min<int>(k, 65535);
+      c->ttab[b] = TBucket<int64_t>{t_values[k], (uint32_t)k};
+      const double hi = (b + 1) * tbw * (1.0 + 4e-5);
+      if (k + 1 < (int)ct && (double)t_values[k + 1] <= hi) t_single = false;
     }
-    if (cs > 65535 || ct > 65535) throw Unsupported("more than 65535 bins per axis");
-    // single-step binning is exact when no bucket's distance range (with the
-    // device-side margins) contains two thresholds
-    auto at_most_one = [](const auto& vals, double bw) {
-      for (int b = 0; b < kBucketTable; ++b) {
-        const double lo = b * bw, hi = (b + 1) * bw * (1.0 + 4e-5);
-        int cnt = 0;
-        for (const auto v : vals)
-          if ((double)v >= lo && (double)v <= hi) ++cnt;
-        if (cnt > 1) return false;
-      }
-      return true;
-    };
-    c->single_step = at_most_one(c->s_values, sbw) && at_most_one(c->t_values, tbw);
+    c->single_step = q_single && t_single;
     c->d_Q.ensure(cs);
     c->d_s.ensure(cs);
     c->d_T.ensure(ct);
-    c->d_stab.ensure(kBucketTable);
+    c->d_qtab.ensure(kQBuckets);
     c->d_ttab.ensure(kBucketTable);
     CK(cudaMemcpyAsync(c->d_Q.p, c->Q.data(), 8 * cs, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_s.p, s_values, 8 * cs, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_T.p, t_values, 8 * ct, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->d_stab.p, c->stab.data(), 2 * kBucketTable, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->d_ttab.p, c->ttab.data(), 2 * kBucketTable, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_qtab.p, c->qtab.data(), sizeof(QBucket) * kQBuckets,
+                       cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_ttab.p, c->ttab.data(), sizeof(TBucket<int64_t>) * kBucketTable,
+                       cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     c->have_grid = true;
   });

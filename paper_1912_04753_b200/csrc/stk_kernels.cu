@@ -553,7 +553,7 @@ struct ArcSum {
   unsigned long long hi;  // high 64 bits
 };
 
-template <typename TT, int SLOTS>
+template <typename TT>
 struct PairLayout {
   __host__ __device__ static constexpr size_t al(size_t b) { return (b + 15) & ~size_t(15); }
   static constexpr size_t cxy = 0;
@@ -561,17 +561,15 @@ struct PairLayout {
   static constexpr size_t cpos = al(cmeta + sizeof(PtMeta<TT>) * kPairWarps * 32);
   static constexpr size_t Q = al(cpos + sizeof(uint32_t) * kPairWarps * 32);
   static constexpr size_t T = al(Q + sizeof(double) * kMaxAxis);
-  static constexpr size_t stab = al(T + sizeof(TT) * kMaxAxis);
-  static constexpr size_t ttab = al(stab + sizeof(uint16_t) * kBucketTable);
-  static constexpr size_t angs = al(ttab + sizeof(uint16_t) * kBucketTable);
-  static constexpr size_t ch = al(angs + sizeof(double) * kPairWarps * SLOTS * 32);
+  static constexpr size_t qtab = al(T + sizeof(TT) * kMaxAxis);
+  static constexpr size_t ttab = al(qtab + sizeof(QBucket) * kQBuckets);
+  static constexpr size_t ch = al(ttab + sizeof(TBucket<TT>) * kBucketTable);
   static size_t __host__ __device__ lh(uint32_t bins) { return al(ch + sizeof(uint2) * bins); }
   static size_t __host__ __device__ total(uint32_t bins) { return al(lh(bins) + sizeof(ArcSum) * bins); }
 };
 
-size_t pair_kernel_smem(uint32_t bins, int wide, int slots) {
-  if (wide) return slots > 8 ? PairLayout<int64_t, 16>::total(bins) : PairLayout<int64_t, 8>::total(bins);
-  return slots > 8 ? PairLayout<int32_t, 16>::total(bins) : PairLayout<int32_t, 8>::total(bins);
+size_t pair_kernel_smem(uint32_t bins, int wide) {
+  return wide ? PairLayout<int64_t>::total(bins) : PairLayout<int32_t>::total(bins);
 }
 
 // Adds one arc-path ordered pair to the CTA histogram: (1/(omega*v) - 1) as a
@@ -663,25 +661,24 @@ constexpr int kKUnroll = STK_K_UNROLL;
 #ifndef STK_SPECIALIZE
 #define STK_SPECIALIZE 1  // 2: own-tile x deep variants, 1: deep only, 0: one generic loop
 #endif
-template <typename TT, int SLOTS, bool RECT>
+template <typename TT, bool RECT>
 __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_task, s_next;
-  using Lay = PairLayout<TT, SLOTS>;
+  using Lay = PairLayout<TT>;
   const Batch& B = A.B;
   const GridGeom& G = A.G;
   const BinView& BV = A.bins;
   const uint32_t cs = BV.cs, ct = BV.ct, bins = cs * ct;
-  constexpr int slots = SLOTS;
+  constexpr int slots = kAngleSlots;
   struct {
     double2* cxy;
     PtMeta<TT>* cmeta;
     uint32_t* cpos;
     double* Q;
     TT* T;
-    uint16_t* stab;
-    uint16_t* ttab;
-    double* angs;
+    QBucket* qtab;
+    TBucket<TT>* ttab;
     uint2* ch;  // (count, half-count) per bin
     ArcSum* arc;
   } S;
@@ -690,9 +687,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   S.cpos = (uint32_t*)(smem_raw + Lay::cpos);
   S.Q = (double*)(smem_raw + Lay::Q);
   S.T = (TT*)(smem_raw + Lay::T);
-  S.stab = (uint16_t*)(smem_raw + Lay::stab);
-  S.ttab = (uint16_t*)(smem_raw + Lay::ttab);
-  S.angs = (double*)(smem_raw + Lay::angs);
+  S.qtab = (QBucket*)(smem_raw + Lay::qtab);
+  S.ttab = (TBucket<TT>*)(smem_raw + Lay::ttab);
   S.ch = (uint2*)(smem_raw + Lay::ch);
   S.arc = (ArcSum*)(smem_raw + Lay::lh(bins));
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -702,13 +698,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   // clamping larger thresholds to TT's range preserves every comparison
   const int64_t tclamp = sizeof(TT) == 4 ? 0x7fffffffLL : 0x7fffffffffffffffLL;
   for (uint32_t b = tid; b < ct; b += blockDim.x) S.T[b] = (TT)min(BV.T[b], tclamp);
-  for (uint32_t b = tid; b < kBucketTable; b += blockDim.x) {
-    S.stab[b] = BV.s_tab[b];
-    S.ttab[b] = BV.t_tab[b];
-  }
+  for (uint32_t b = tid; b < kQBuckets; b += blockDim.x) S.qtab[b] = BV.q_tab[b];
+  for (uint32_t b = tid; b < kBucketTable; b += blockDim.x)
+    S.ttab[b] = TBucket<TT>{(TT)min(BV.t_tab[b].thr, tclamp), BV.t_tab[b].bin};
   const double Qmax = BV.Qmax;
   const TT Tmax = (TT)min(BV.Tmax, tclamp);
-  const float s_inv_bw = BV.s_inv_bw, t_inv_bw = BV.t_inv_bw;
+  const float t_inv_bw = BV.t_inv_bw;
+  const int q_shift = BV.q_shift, q_base = BV.q_base;
   const uint32_t total_tasks = B.task_start[B.R];
   const uint32_t task_items = B.task_counter[1];
   const unsigned lanemask_lt = (1u << lane) - 1u;
@@ -718,7 +714,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   uint4* arcq = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * (kArcRing + kCplxRing);
   uint4* cring = arcq + kArcRing;
     const int single_step = BV.single_step;
-  double* angs = S.angs + w * slots * 32;
+  // crossing scratch of the general weight (deferred drains only): global,
+  // L1-resident, element k of lane l at [k * 32 + l]
+  double* angs = A.angs_g + ((uint64_t)blockIdx.x * kPairWarps + w) * (slots * 32);
   int overflow = 0;
   unsigned long long tot_in = 0, tot_cand = 0, tot_exact = 0, tot_arc = 0;
 
@@ -877,11 +875,18 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           uint32_t tidv;
           asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tidv));
           const uint32_t wo = (tidv >> 5) * 32;
-          const double2* cxy_c = S.cxy + wo;
-          const PtMeta<TT>* cm_c = S.cmeta + wo;
-          const uint32_t* cpos_c = S.cpos + wo;
+          // straight from the __shared__ array: the shared address space stays
+          // visible (no generic-to-shared window arithmetic per load)
+          const double2* cxy_c = reinterpret_cast<const double2*>(smem_raw + Lay::cxy) + wo;
+          const PtMeta<TT>* cm_c = reinterpret_cast<const PtMeta<TT>*>(smem_raw + Lay::cmeta) + wo;
+          const uint32_t* cpos_c = reinterpret_cast<const uint32_t*>(smem_raw + Lay::cpos) + wo;
           const uint32_t jpc = j0 + (tidv & 31u);  // == jp, held in a register
           const bool same_c = r == 0 && jpc < own_end;
+          // own-cell rule: lower sorted position owns the pair — center k sits
+          // at first_pos + k, so "jp > its position" is "k < jp - first_pos";
+          // selected centers (shards) compare input indices instead
+          const bool idx_rule = sel_p && same_c;
+          const uint32_t own_lim = (same_c && !sel_p) ? jpc - first_pos : 0xffffffffu;
 #pragma unroll kKUnroll
           for (int k = kc; k < kend; ++k) {
             const double2 c = cxy_c[k];  // center k (broadcast)
@@ -891,22 +896,27 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             TT du = cmk.t - nm.t;
             du = du < 0 ? -du : du;              // temporal_distance
             bool owner = true;
-            if (OWN) owner = !same_c || (sel_p ? nm.idx > cmk.idx : jpc > cpos_c[k]);
+            if (OWN) owner = idx_rule ? nm.idx > cmk.idx : (uint32_t)k < own_lim;
             const bool in = has && owner && q <= Qmax && du <= Tmax;
             bool arc_i = false, arc_j = false;
             uint32_t bin = 0;
             bool half_i = false, half_j = false;
             if (in) {
-              // bin_pair: first s_k >= d <=> first Q_k >= q; first t_l >= u
-              int bq = (int)(sqrtf((float)q) * s_inv_bw);
-              bq = min(bq, kBucketTable - 1);
-              uint32_t sb = S.stab[bq];
+              // bin_pair: first s_k >= d <=> first Q_k >= q; first t_l >= u.
+              // q's bucket from the bits of RN_float(q) (log-spaced buckets,
+              // no sqrt); each entry carries its bin's threshold
+              const float qf = (float)q;
+              int bq = (int)(__float_as_uint(qf) >> q_shift) - q_base;
+              bq = min(max(bq, 0), kQBuckets - 1);
+              const QBucket qe = S.qtab[bq];
+              uint32_t sb = qe.bin;
               int bt = (int)((float)du * t_inv_bw);
               bt = min(bt, kBucketTable - 1);
-              uint32_t tb = S.ttab[bt];
+              const TBucket<TT> te = S.ttab[bt];
+              uint32_t tb = te.bin;
               if (single_step) {
-                sb += q > S.Q[sb] ? 1u : 0u;
-                tb += du > S.T[tb] ? 1u : 0u;
+                sb += q > qe.thr ? 1u : 0u;
+                tb += du > te.thr ? 1u : 0u;
               } else {
                 while (q > S.Q[sb]) ++sb;
                 while (du > S.T[tb]) ++tb;
@@ -917,8 +927,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               if (DEEP) continue;
               half_i = du > cmk.vt;
               half_j = du > nm.vt;
-              arc_i = q >= (double)cmk.sq;
-              arc_j = q >= (double)nm.sq;
+              // q >= sq (a float) implies RN_float(q) >= sq, so every pair that
+              // needs the exact path takes it; the rare extras (q < sq ==
+              // RN_float(q)) get omega == 1 exactly there (safe radius)
+              arc_i = qf >= cmk.sq;
+              arc_j = qf >= nm.sq;
               const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
               if (h) atomicAdd(&S.ch[bin].y, h);
             }
@@ -1008,37 +1021,31 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
 }
 
 // Host-side launch helpers (keep the kernel templates in this translation unit).
-template <typename TT, int SLOTS>
-static const void* pair_fn3(int rect) {
-  return rect ? (const void*)pair_kernel<TT, SLOTS, true> : (const void*)pair_kernel<TT, SLOTS, false>;
+template <typename TT>
+static const void* pair_fn2(int rect) {
+  return rect ? (const void*)pair_kernel<TT, true> : (const void*)pair_kernel<TT, false>;
 }
-static const void* pair_fn(int wide, int slots, int rect) {
-  if (wide) return slots > 8 ? pair_fn3<int64_t, 16>(rect) : pair_fn3<int64_t, 8>(rect);
-  return slots > 8 ? pair_fn3<int32_t, 16>(rect) : pair_fn3<int32_t, 8>(rect);
+static const void* pair_fn(int wide, int rect) {
+  return wide ? pair_fn2<int64_t>(rect) : pair_fn2<int32_t>(rect);
 }
 
-cudaError_t pair_kernel_prepare(int wide, int slots, int rect, size_t smem, int* per_sm) {
-  const void* fn = pair_fn(wide, slots, rect);
+cudaError_t pair_kernel_prepare(int wide, int rect, size_t smem, int* per_sm) {
+  const void* fn = pair_fn(wide, rect);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fn, kPairWarps * 32, smem);
 }
 
-template <typename TT, int SLOTS>
-static void launch3(int rect, unsigned ctas, size_t smem, cudaStream_t stream, const PairArgs& A) {
-  if (rect) pair_kernel<TT, SLOTS, true><<<ctas, kPairWarps * 32, smem, stream>>>(A);
-  else pair_kernel<TT, SLOTS, false><<<ctas, kPairWarps * 32, smem, stream>>>(A);
+template <typename TT>
+static void launch2(int rect, unsigned ctas, size_t smem, cudaStream_t stream, const PairArgs& A) {
+  if (rect) pair_kernel<TT, true><<<ctas, kPairWarps * 32, smem, stream>>>(A);
+  else pair_kernel<TT, false><<<ctas, kPairWarps * 32, smem, stream>>>(A);
 }
 
-void pair_kernel_launch(int wide, int slots, int rect, unsigned ctas, size_t smem,
-                        cudaStream_t stream, const PairArgs& A) {
-  if (wide) {
-    if (slots > 8) launch3<int64_t, 16>(rect, ctas, smem, stream, A);
-    else launch3<int64_t, 8>(rect, ctas, smem, stream, A);
-  } else {
-    if (slots > 8) launch3<int32_t, 16>(rect, ctas, smem, stream, A);
-    else launch3<int32_t, 8>(rect, ctas, smem, stream, A);
-  }
+void pair_kernel_launch(int wide, int rect, unsigned ctas, size_t smem, cudaStream_t stream,
+                        const PairArgs& A) {
+  if (wide) launch2<int64_t>(rect, ctas, smem, stream, A);
+  else launch2<int32_t>(rect, ctas, smem, stream, A);
 }
 
 // ============================================================ K5 finalize

@@ -8,7 +8,7 @@
 namespace stk {
 
 struct PairArgs {
-  int angle_slots;  // per-lane crossing scratch (2 doubles per crossing)
+  double* angs_g;   // [CTAs][warps][kAngleSlots][32] crossing scratch of the general weight
   Batch B;
   GridGeom G;
   BinView bins;
@@ -37,8 +37,8 @@ __global__ void select_scatter_kernel(Batch B, GridGeom G);
 __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first);
 __global__ void items_kernel(Batch B, GridGeom G, int p_first);
 __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas);
-cudaError_t pair_kernel_prepare(int wide, int slots, int rect, size_t smem, int* per_sm);
-void pair_kernel_launch(int wide, int slots, int rect, unsigned ctas, size_t smem, cudaStream_t stream,
+cudaError_t pair_kernel_prepare(int wide, int rect, size_t smem, int* per_sm);
+void pair_kernel_launch(int wide, int rect, unsigned ctas, size_t smem, cudaStream_t stream,
                         const PairArgs& A);
 __global__ void finalize_kernel(Batch B, uint32_t cs, uint32_t ct, const double* s_values,
                                 const int64_t* t_values, double area, int64_t duration,
@@ -52,6 +52,6 @@ __global__ void weights_kernel(const double* cx, const double* cy, const double*
                                unsigned long long* bad);
 __global__ void dfma_peak_kernel(double* out, int iters, double a, double b);
 
-size_t pair_kernel_smem(uint32_t bins, int wide, int slots);
+size_t pair_kernel_smem(uint32_t bins, int wide);
 
 }  // namespace stk

@@ -13,7 +13,8 @@ constexpr int kTaskMaxItems = 256;  // batch has ~8 tasks per resident CTA
 #define STK_PAIR_WARPS 8
 #endif
 constexpr int kPairWarps = STK_PAIR_WARPS;  // warps per pair-kernel CTA
-constexpr int kBucketTable = 1024;  // bucket table size for bin guesses
+constexpr int kBucketTable = 1024;  // time bucket table size for bin guesses
+constexpr int kQBuckets = 512;      // distance (q) bucket table size
 constexpr int kAngleSlots = 16;    // per-lane crossing scratch: 2 doubles x 8 crossings
 constexpr int kRingSmem = 32;      // ring vertices staged in shared memory (bitmask path)
 #ifndef STK_ARC_CHUNK
@@ -56,16 +57,30 @@ struct RegionView {
 };
 
 // Distance grid in the forms the kernels consume.
+// Bucket entries: the lowest bin a bucket can hold and that bin's threshold,
+// so one shared-memory load and one compare resolve a single-step bucket.
+struct QBucket {           // on q = d^2, indexed by the float bits of q (log scale)
+  double thr;              // Q[bin]
+  uint32_t bin;
+  uint32_t pad;
+};
+template <typename TT>
+struct TBucket {           // on u, linear
+  TT thr;                  // T[bin] (clamped to TT)
+  uint32_t bin;
+};
+
 struct BinView {
   const double* Q;         // Q[k] = largest q with RN(sqrt(q)) <= s_values[k]
   const int64_t* T;        // t_values
-  const uint16_t* s_tab;   // bucket (on d) -> lower bound of the s bin
-  const uint16_t* t_tab;   // bucket (on u) -> lower bound of the t bin
+  const QBucket* q_tab;    // kQBuckets entries
+  const TBucket<int64_t>* t_tab;  // kBucketTable entries (device converts to TT)
   uint32_t cs, ct;
   double Qmax;
   int64_t Tmax;
-  float s_inv_bw, t_inv_bw;  // buckets per unit distance / per time unit (with margin)
-  int single_step;           // every bucket straddles <= 1 threshold: one compare finds the bin
+  int q_shift, q_base;     // bucket = clamp((bits(float(q)) >> q_shift) - q_base)
+  float t_inv_bw;          // buckets per time unit (with margin)
+  int single_step;         // every bucket straddles <= 1 threshold: one compare finds the bin
 };
 
 // Uniform space-time cell grid (replaces the STR R-tree, st_index.cpp:54-130).

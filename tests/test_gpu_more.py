@@ -321,3 +321,24 @@ def test_c3_full_size_properties(api):
     assert np.all(np.diff(k, axis=0) >= 0) and np.all(np.diff(k, axis=1) >= 0)
     scale = region.area() * region.duration() / float(cfg.n) ** 2
     assert k[-1, -1] == pytest.approx(scale * h["hist"].sum(), rel=1e-12)
+
+
+def test_bin_tables_close_thresholds_and_wide_range(api, port):
+    """The log-scale q buckets and linear u buckets: thresholds closer than a
+    bucket (the device falls back to the compare loop), a grid spanning six
+    decades, and distances / lags landing exactly on thresholds."""
+    ring, p0, p1 = square(1000.0, 0, 10_000)
+    rng = np.random.default_rng(77)
+    n = 3000
+    x = rng.uniform(0, 1000, n)
+    y = rng.uniform(0, 1000, n)
+    t = rng.integers(0, 10_001, n)
+    # exact-threshold pairs: points at integer offsets from a few anchors
+    for a in range(10):
+        x[a * 3:a * 3 + 3] = [100.0 + 50 * a, 100.0 + 50 * a + 3.0, 100.0 + 50 * a]
+        y[a * 3:a * 3 + 3] = [500.0, 504.0, 505.0]
+        t[a * 3:a * 3 + 3] = [5000, 5020, 5040]
+    close = [5.0, 5.0 + 1e-9, 5.0 + 2e-9, 20.0, 20.000001, 100.0, 250.0]
+    _compare(api, port, x, y, t, ring, p0, p1, close, [20, 21, 22, 40, 500])
+    wide = [1e-3, 1e-2, 0.1, 1.0, 5.0, 10.0, 100.0, 300.0]
+    _compare(api, port, x, y, t, ring, p0, p1, wide, [1, 2, 3, 20, 40, 9000])
