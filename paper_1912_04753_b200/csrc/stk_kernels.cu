@@ -649,7 +649,7 @@ __device__ __forceinline__ void drain_general(int count, int lane, const uint4* 
 }
 
 #ifndef STK_PAIR_MINB
-#define STK_PAIR_MINB 4
+#define STK_PAIR_MINB 2
 #endif
 #ifndef STK_K_UNROLL
 #define STK_K_UNROLL 1

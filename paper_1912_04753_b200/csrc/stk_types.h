@@ -10,7 +10,7 @@ constexpr int kItemCenters = 32;    // centers per warp work item (one per lane)
 constexpr int kTaskMinItems = 4;    // warp items per CTA task: adaptive in [min, max] so the
 constexpr int kTaskMaxItems = 256;  // batch has ~8 tasks per resident CTA
 #ifndef STK_PAIR_WARPS
-#define STK_PAIR_WARPS 8
+#define STK_PAIR_WARPS 16
 #endif
 constexpr int kPairWarps = STK_PAIR_WARPS;  // warps per pair-kernel CTA
 constexpr int kBucketTable = 1024;  // time bucket table size for bin guesses
