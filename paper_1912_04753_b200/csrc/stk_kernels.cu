@@ -665,6 +665,12 @@ template <typename TT, bool RECT>
 __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_task, s_next;
+  // per-thread invariants the candidate loop reads once per chunk: values
+  // loaded from shared memory cannot be rematerialised by the register
+  // allocator (it otherwise rebuilds them from special registers every
+  // iteration)
+  __shared__ uint32_t s_lane[kPairWarps * 32];
+  __shared__ uint4* s_ring[kPairWarps];
   using Lay = PairLayout<TT>;
   const Batch& B = A.B;
   const GridGeom& G = A.G;
@@ -713,6 +719,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   uint32_t* cpos_w = S.cpos + w * 32;
   uint4* arcq = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * (kArcRing + kCplxRing);
   uint4* cring = arcq + kArcRing;
+  s_lane[tid] = (uint32_t)lane;
+  if (lane == 0) s_ring[w] = arcq;
     const int single_step = BV.single_step;
   // crossing scratch of the general weight (deferred drains only): global,
   // L1-resident, element k of lane l at [k * 32 + l]
@@ -875,12 +883,15 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           uint32_t tidv;
           asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tidv));
           const uint32_t wo = (tidv >> 5) * 32;
+          const uint32_t lane_c = s_lane[tidv];
+          uint4* const ring_c = s_ring[tidv >> 5];
+          const unsigned lt_c = (1u << lane_c) - 1u;
           // straight from the __shared__ array: the shared address space stays
           // visible (no generic-to-shared window arithmetic per load)
           const double2* cxy_c = reinterpret_cast<const double2*>(smem_raw + Lay::cxy) + wo;
           const PtMeta<TT>* cm_c = reinterpret_cast<const PtMeta<TT>*>(smem_raw + Lay::cmeta) + wo;
           const uint32_t* cpos_c = reinterpret_cast<const uint32_t*>(smem_raw + Lay::cpos) + wo;
-          const uint32_t jpc = j0 + (tidv & 31u);  // == jp, held in a register
+          const uint32_t jpc = j0 + lane_c;  // == jp, held in a register
           const bool same_c = r == 0 && jpc < own_end;
           // own-cell rule: lower sorted position owns the pair — center k sits
           // at first_pos + k, so "jp > its position" is "k < jp - first_pos";
@@ -897,7 +908,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             du = du < 0 ? -du : du;              // temporal_distance
             bool owner = true;
             if (OWN) owner = idx_rule ? nm.idx > cmk.idx : (uint32_t)k < own_lim;
-            const bool in = has && owner && q <= Qmax && du <= Tmax;
+            // lanes without a neighbour hold coordinates 1e300: q = +inf fails
+            const bool in = owner && q <= Qmax && du <= Tmax;
             bool arc_i = false, arc_j = false;
             uint32_t bin = 0;
             bool half_i = false, half_j = false;
@@ -941,11 +953,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             if (mi | mj) {
               const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
               if (arc_i)
-                arcq[(qt + __popc(mi & lanemask_lt)) & (kArcRing - 1)] =
+                ring_c[(qt + __popc(mi & lt_c)) & (kArcRing - 1)] =
                     make_uint4(cpos_c[k], bin | (half_i ? 0x80000000u : 0u), qlo, qhi);
               qt += __popc(mi);
               if (arc_j)
-                arcq[(qt + __popc(mj & lanemask_lt)) & (kArcRing - 1)] =
+                ring_c[(qt + __popc(mj & lt_c)) & (kArcRing - 1)] =
                     make_uint4(jpc, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
               qt += __popc(mj);
               n_exact += (uint32_t)arc_i + (uint32_t)arc_j;
