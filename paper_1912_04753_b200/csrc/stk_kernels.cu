@@ -671,6 +671,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   // iteration)
   __shared__ uint32_t s_lane[kPairWarps * 32];
   __shared__ uint4* s_ring[kPairWarps];
+  __shared__ uint2 s_lim[kPairWarps * 32];  // per-chunk owner limits (see below)
   using Lay = PairLayout<TT>;
   const Batch& B = A.B;
   const GridGeom& G = A.G;
@@ -816,7 +817,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       const unsigned nonempty = __ballot_sync(FULL_MASK, my_rb < my_re);
       uint32_t qh = 0, qt = 0;    // arc ring head / tail (monotone)
       uint32_t ch_ = 0, ct_ = 0;  // deferred ring head / tail
-      uint32_t n_in = 0, n_exact = 0, n_arc = 0;
+      uint32_t n_arc = 0;
       unsigned long long n_cand = 0;
       // flat walk over (row, tile, center chunk); one inline copy of the drain
       unsigned rows_left = nonempty;
@@ -895,9 +896,14 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           const bool same_c = r == 0 && jpc < own_end;
           // own-cell rule: lower sorted position owns the pair — center k sits
           // at first_pos + k, so "jp > its position" is "k < jp - first_pos";
-          // selected centers (shards) compare input indices instead
-          const bool idx_rule = sel_p && same_c;
-          const uint32_t own_lim = (same_c && !sel_p) ? jpc - first_pos : 0xffffffffu;
+          // selected centers (shards) compare input indices instead.  Both
+          // limits go through a volatile shared round trip so the register
+          // allocator keeps them instead of rebuilding them per iteration:
+          // owner <=> k < lim.x || center idx < lim.y
+          s_lim[tidv] = make_uint2(same_c ? (sel_p ? 0u : jpc - first_pos) : 0xffffffffu,
+                                   (sel_p && same_c) ? nm.idx : 0u);
+          const volatile uint32_t* lim_v = reinterpret_cast<volatile uint32_t*>(&s_lim[tidv]);
+          const uint2 lim = make_uint2(lim_v[0], lim_v[1]);
 #pragma unroll kKUnroll
           for (int k = kc; k < kend; ++k) {
             const double2 c = cxy_c[k];  // center k (broadcast)
@@ -907,7 +913,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             TT du = cmk.t - nm.t;
             du = du < 0 ? -du : du;              // temporal_distance
             bool owner = true;
-            if (OWN) owner = idx_rule ? nm.idx > cmk.idx : (uint32_t)k < own_lim;
+            if (OWN) owner = (uint32_t)k < lim.x || cmk.idx < lim.y;
             // lanes without a neighbour hold coordinates 1e300: q = +inf fails
             const bool in = owner && q <= Qmax && du <= Tmax;
             bool arc_i = false, arc_j = false;
@@ -935,7 +941,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               }
               bin = sb * ct + tb;
               atomicAdd(&S.ch[bin].x, 2u);
-              n_in += 2;
               if (DEEP) continue;
               half_i = du > cmk.vt;
               half_j = du > nm.vt;
@@ -960,7 +965,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
                 ring_c[(qt + __popc(mj & lt_c)) & (kArcRing - 1)] =
                     make_uint4(jpc, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
               qt += __popc(mj);
-              n_exact += (uint32_t)arc_i + (uint32_t)arc_j;
             }
           }
         };
@@ -995,8 +999,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         }
       }
       __syncwarp();
-      tot_in += n_in;
-      tot_exact += n_exact;
+      if (lane == 0) tot_exact += qt;  // every ring entry is one exact-path ordered pair
       tot_arc += n_arc;
       if (lane == 0) tot_cand += n_cand;
     }
@@ -1006,6 +1009,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     for (uint32_t b = tid; b < bins; b += blockDim.x) {
       const uint2 chb = S.ch[b];
       // counts are even (2 per unordered pair); bit 0 flags an infinite term
+      tot_in += chb.x & ~1u;  // in-threshold pairs (telemetry)
       if (chb.x > 1u) atomicAdd(&B.h_cnt[hb + b], (unsigned long long)(chb.x & ~1u));
       if (chb.x & 1u) atomicOr(&B.h_cnt[hb + b], 1ULL);
       if (chb.y) atomicAdd(&B.h_half[hb + b], (unsigned long long)chb.y);
