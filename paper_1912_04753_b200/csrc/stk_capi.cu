@@ -326,9 +326,26 @@ RegionView region_view(stk_ctx* c) {
   const double S = std::max(1.0, c->maxabs + smax);
   const double min_edge = std::max(std::min(c->xmax - c->xmin, c->ymax - c->ymin), 1e-300);
   r.box_m = 4e-12 * S * std::max(1.0, S / min_edge);
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i) {
     r.rv[i] = (r.rect && c->ring.size() == 8) ? make_double2(c->ring[2 * i], c->ring[2 * i + 1])
                                               : make_double2(0.0, 0.0);
+    r.sd_start[i] = r.sd_len[i] = 0.0;
+  }
+  if (r.rect && c->ring.size() == 8) {
+    for (int i = 0; i < 4; ++i) {  // segment (ring[i-1], ring[i]) as the reference's loop
+      const double ax = c->ring[2 * ((i + 3) & 3)], ay = c->ring[2 * ((i + 3) & 3) + 1];
+      const double bx = c->ring[2 * i], by = c->ring[2 * i + 1];
+      if (ax == bx) {  // vertical: x = xmin (side 0) or x = xmax (side 1)
+        const int sd = ax == c->xmin ? 0 : 1;
+        r.sd_start[sd] = ay;
+        r.sd_len[sd] = by - ay;
+      } else {         // horizontal: y = ymin (side 2) or y = ymax (side 3)
+        const int sd = ay == c->ymin ? 2 : 3;
+        r.sd_start[sd] = ax;
+        r.sd_len[sd] = bx - ax;
+      }
+    }
+  }
   // the closed form needs the reach margin d*1e-6 far above
   // coordinate rounding (d >= 1e-8 S) and the outside probe clear of every
   // on_segment tolerance (d - h > 4 box_m)

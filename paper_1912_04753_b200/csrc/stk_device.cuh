@@ -617,28 +617,26 @@ __device__ __forceinline__ double rect_single_edge_weight(double cx, double cy, 
   if (d <= 0.0) return 1.0;
   if (!(cx > R.xmin && cx < R.xmax && cy > R.ymin && cy < R.ymax) || d < R.sw_dmin) return -1.0;
   const double reach = d * (1.0 + 1e-6);
-  int m = 0;
-  double2 A = R.rv[0], Bv = R.rv[0];
-  double h = 0.0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const double2 a = R.rv[(i + 3) & 3], b = R.rv[i];
-    const double hi = a.x == b.x ? fabs(a.x - cx) : fabs(a.y - cy);
-    if (hi <= reach) {
-      ++m;
-      A = a;
-      Bv = b;
-      h = hi;
-    }
-  }
+  // distances to the four side lines: with the center inside, cx - xmin is
+  // exactly the reference's fabs(A.x - cx) (RN is symmetric), etc.
+  const double hl = cx - R.xmin, hr = R.xmax - cx, hb = cy - R.ymin, ht = R.ymax - cy;
+  const bool il = hl <= reach, ir = hr <= reach, ib = hb <= reach, it = ht <= reach;
+  const int m = (int)il + (int)ir + (int)ib + (int)it;
   if (m == 0) return 1.0;  // the reference accepts no edge (reach argument)
   if (m > 1) return -1.0;
+  // the one side's segment in the reference's frame: f = A - c splits into
+  // fp (across the side, = +-h) and fa (along it); B - A = (0, D) or (D, 0).
+  // The reference's qa = dx*dx + dy*dy = D*D, qb = 2(fx*dx + fy*dy) = 2(fa*D)
+  // (adding the exact zero product), qc = fx*fx + fy*fy - r^2 = h*h + fa*fa - r^2
+  // (addition commutes): bit-identical.
+  const double h = il ? hl : ir ? hr : ib ? hb : ht;
+  const int sd = il ? 0 : ir ? 1 : ib ? 2 : 3;
+  const double fa = R.sd_start[sd] - (sd < 2 ? cy : cx);
+  const double D = R.sd_len[sd];
   const double r2 = d * d;
-  const double dx = Bv.x - A.x, dy = Bv.y - A.y;
-  const double fx = A.x - cx, fy = A.y - cy;
-  const double qa = dx * dx + dy * dy;
-  const double qb = 2.0 * (fx * dx + fy * dy);
-  const double qc = fx * fx + fy * fy - r2;
+  const double qa = D * D;
+  const double qb = 2.0 * (fa * D);
+  const double qc = h * h + fa * fa - r2;
   const double disc = qb * qb - 4.0 * qa * qc;
   const double scale = qb * qb + fabs(4.0 * qa * qc);
   if (!(qa != 0.0 && disc > 1e-9 * scale)) return 1.0;  // no crossing: omega == 1

@@ -35,6 +35,10 @@ struct RegionView {
   int rect;             // 4-vertex axis-aligned rectangle (exact fast paths apply)
   double box_m;         // rect: on_segment is impossible farther than this outside the box
   double2 rv[4];        // rect: the ring's vertices (kernel-parameter copy)
+  // rect sides in the order x = xmin, x = xmax, y = ymin, y = ymax: the
+  // reference's segment (A -> B) on that side has A's along-side coordinate
+  // sd_start and B - A = sd_len (computed as the reference does)
+  double sd_start[4], sd_len[4];
   double sw_dmin;       // rect single-edge closed form: smallest radius it accepts
   double sw_margin;     // ... and smallest d - h (outside midpoint clear of the boundary)
   // General polygons.  Horizontal slabs: slab s lists every
