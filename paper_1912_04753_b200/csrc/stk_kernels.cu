@@ -553,6 +553,59 @@ struct ArcSum {
   unsigned long long hi;  // high 64 bits
 };
 
+// Explicit shared-memory accesses for the candidate loops, addressed from a
+// 32-bit base the loops receive through a volatile shared load: the compiler
+// would otherwise rebuild the dynamic window's base every iteration (an S2UR
+// of the CTA's cluster id plus 4 instructions).  volatile keeps them ordered
+// with the warp's staging stores and barriers.
+__device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_u32x4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds_u32x2(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ ulonglong2 lds_u64x2(uint32_t a) {
+  ulonglong2 v;
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void reds_add_u32(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
+template <typename TT>
+__device__ __forceinline__ PtMeta<TT> lds_meta(uint32_t a) {
+  if constexpr (sizeof(TT) == 4) {
+    const uint4 v = lds_u32x4(a);
+    return PtMeta<TT>{(TT)v.x, (TT)v.y, __uint_as_float(v.z), v.w};
+  } else {  // 24-byte records: only 8-byte aligned
+    unsigned long long t, vt;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(t) : "r"(a));
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(vt) : "r"(a + 8));
+    const uint2 w = lds_u32x2(a + 16);
+    return PtMeta<TT>{(TT)t, (TT)vt, __uint_as_float(w.x), w.y};
+  }
+}
+template <typename TT>
+__device__ __forceinline__ TBucket<TT> lds_tbucket(uint32_t a) {
+  if constexpr (sizeof(TT) == 4) {
+    const uint2 v = lds_u32x2(a);
+    return TBucket<TT>{(TT)v.x, v.y};
+  } else {
+    const ulonglong2 v = lds_u64x2(a);
+    return TBucket<TT>{(TT)v.x, (uint32_t)v.y};
+  }
+}
+
 template <typename TT>
 struct PairLayout {
   __host__ __device__ static constexpr size_t al(size_t b) { return (b + 15) & ~size_t(15); }
@@ -672,6 +725,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   __shared__ uint32_t s_lane[kPairWarps * 32];
   __shared__ uint4* s_ring[kPairWarps];
   __shared__ uint2 s_lim[kPairWarps * 32];  // per-chunk owner limits (see below)
+  __shared__ uint32_t s_base;               // shared-space address of smem_raw
   using Lay = PairLayout<TT>;
   const Batch& B = A.B;
   const GridGeom& G = A.G;
@@ -721,6 +775,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   uint4* arcq = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * (kArcRing + kCplxRing);
   uint4* cring = arcq + kArcRing;
   s_lane[tid] = (uint32_t)lane;
+  if (tid == 0) s_base = (uint32_t)__cvta_generic_to_shared(smem_raw);
   if (lane == 0) s_ring[w] = arcq;
     const int single_step = BV.single_step;
   // crossing scratch of the general weight (deferred drains only): global,
@@ -889,8 +944,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           const unsigned lt_c = (1u << lane_c) - 1u;
           // straight from the __shared__ array: the shared address space stays
           // visible (no generic-to-shared window arithmetic per load)
-          const double2* cxy_c = reinterpret_cast<const double2*>(smem_raw + Lay::cxy) + wo;
-          const PtMeta<TT>* cm_c = reinterpret_cast<const PtMeta<TT>*>(smem_raw + Lay::cmeta) + wo;
           const uint32_t* cpos_c = reinterpret_cast<const uint32_t*>(smem_raw + Lay::cpos) + wo;
           const uint32_t jpc = j0 + lane_c;  // == jp, held in a register
           const bool same_c = r == 0 && jpc < own_end;
@@ -904,10 +957,16 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
                                    (sel_p && same_c) ? nm.idx : 0u);
           const volatile uint32_t* lim_v = reinterpret_cast<volatile uint32_t*>(&s_lim[tidv]);
           const uint2 lim = make_uint2(lim_v[0], lim_v[1]);
+          const uint32_t sbase = *reinterpret_cast<volatile uint32_t*>(&s_base);
+          const uint32_t a_cxy = sbase + (uint32_t)Lay::cxy + wo * (uint32_t)sizeof(double2);
+          const uint32_t a_cm = sbase + (uint32_t)Lay::cmeta + wo * (uint32_t)sizeof(PtMeta<TT>);
+          const uint32_t a_q = sbase + (uint32_t)Lay::qtab;
+          const uint32_t a_t = sbase + (uint32_t)Lay::ttab;
+          const uint32_t a_ch = sbase + (uint32_t)Lay::ch;
 #pragma unroll kKUnroll
           for (int k = kc; k < kend; ++k) {
-            const double2 c = cxy_c[k];  // center k (broadcast)
-            const PtMeta<TT> cmk = cm_c[k];
+            const double2 c = lds_f64x2(a_cxy + k * (uint32_t)sizeof(double2));  // center k
+            const PtMeta<TT> cmk = lds_meta<TT>(a_cm + k * (uint32_t)sizeof(PtMeta<TT>));
             const double dx = c.x - nxy.x, dy = c.y - nxy.y;
             const double q = dx * dx + dy * dy;  // spatial_distance^2, no FMA
             TT du = cmk.t - nm.t;
@@ -926,11 +985,12 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               const float qf = (float)q;
               int bq = (int)(__float_as_uint(qf) >> q_shift) - q_base;
               bq = min(max(bq, 0), kQBuckets - 1);
-              const QBucket qe = S.qtab[bq];
+              const ulonglong2 qe2 = lds_u64x2(a_q + (uint32_t)bq * (uint32_t)sizeof(QBucket));
+              const QBucket qe{__longlong_as_double((long long)qe2.x), (uint32_t)qe2.y, 0u};
               uint32_t sb = qe.bin;
               int bt = (int)((float)du * t_inv_bw);
               bt = min(bt, kBucketTable - 1);
-              const TBucket<TT> te = S.ttab[bt];
+              const TBucket<TT> te = lds_tbucket<TT>(a_t + (uint32_t)bt * (uint32_t)sizeof(TBucket<TT>));
               uint32_t tb = te.bin;
               if (single_step) {
                 sb += q > qe.thr ? 1u : 0u;
@@ -940,7 +1000,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
                 while (du > S.T[tb]) ++tb;
               }
               bin = sb * ct + tb;
-              atomicAdd(&S.ch[bin].x, 2u);
+              reds_add_u32(a_ch + bin * 8u, 2u);
               if (DEEP) continue;
               half_i = du > cmk.vt;
               half_j = du > nm.vt;
@@ -950,7 +1010,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               arc_i = qf >= cmk.sq;
               arc_j = qf >= nm.sq;
               const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
-              if (h) atomicAdd(&S.ch[bin].y, h);
+              if (h) reds_add_u32(a_ch + bin * 8u + 4u, h);
             }
             if (DEEP) continue;
             const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
