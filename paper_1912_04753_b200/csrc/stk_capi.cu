@@ -479,7 +479,7 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   c->item_start.ensure(R * (P.G.cells + 1));
   c->items.ensure(R * P.max_items);
   c->task_start.ensure(R + 1);
-  c->task_counter.ensure(2);
+  c->task_counter.ensure(3);
   c->hist.ensure(R * P.bins * 4);
   c->stats.ensure(8);
   c->K.ensure(R * P.bins);

@@ -512,8 +512,18 @@ __global__ void items_kernel(Batch B, GridGeom G, int p_first) {
 __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas) {
   uint64_t total = 0;
   for (int p = 0; p < B.R; ++p) total += B.item_start[(uint64_t)p * (G.cells + 1) + G.cells];
+  // Dense cells make a few items carry most of the work (one cell holding the
+  // whole pattern in the extreme): each item is then walked as P parts,
+  // disjoint slices of its neighbour tiles taken by different warps.
+  const uint64_t maxc = B.stats[5];
+  uint64_t np = (maxc + kPartCells - 1) / kPartCells;
+  np = np < 1 ? 1 : (np > (uint64_t)kMaxParts ? (uint64_t)kMaxParts : np);
+  const uint32_t parts = (uint32_t)np;
   uint64_t ti = total / (8ull * resident_ctas);
-  ti = ti < (uint64_t)kTaskMinItems ? (uint64_t)kTaskMinItems : ti;
+  // at least one unit per warp in a task
+  uint64_t tmin = (kPairWarps + parts - 1) / parts;
+  tmin = tmin < (uint64_t)kTaskMinItems ? (uint64_t)kTaskMinItems : tmin;
+  ti = ti < tmin ? tmin : ti;
   ti = ti > (uint64_t)kTaskMaxItems ? (uint64_t)kTaskMaxItems : ti;
   // The CTA's per-bin u32 counters take 2 per unordered pair of the task: an
   // item (<= 32 centers) meets at most (half-stencil cells) x (largest cell)
@@ -533,6 +543,7 @@ __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas) {
   B.task_start[B.R] = acc;
   B.task_counter[0] = 0;
   B.task_counter[1] = task_items;
+  B.task_counter[2] = parts;
 }
 
 // ============================================================ K2 pair kernel
@@ -768,6 +779,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   const int q_shift = BV.q_shift, q_base = BV.q_base;
   const uint32_t total_tasks = B.task_start[B.R];
   const uint32_t task_items = B.task_counter[1];
+  const uint32_t parts = B.task_counter[2];  // units per item (1: whole items)
   const unsigned lanemask_lt = (1u << lane) - 1u;
   double2* cxy_w = S.cxy + w * 32;
   PtMeta<TT>* cm_w = S.cmeta + w * 32;
@@ -820,8 +832,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       uint32_t it = 0;
       if (lane == 0) it = atomicAdd(&s_next, 1u);
       it = __shfl_sync(FULL_MASK, it, 0);
-      if (i0 + it >= i1) break;
-      const uint2 item = B.items[io + i0 + it];
+      const uint32_t iu = it / parts, part = it - iu * parts;
+      if (i0 + iu >= i1) break;
+      const uint2 item = B.items[io + i0 + iu];
       const uint32_t cell = item.x, start = item.y;
       const uint32_t nc = min((uint32_t)kItemCenters, clist_b[co + cell + 1] - start);
       // stage the item's centers (<= 32) in shared memory: the inner loop
@@ -869,7 +882,28 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           if (my_rb > my_re) my_rb = my_re;
         }
       }
-      const unsigned nonempty = __ballot_sync(FULL_MASK, my_rb < my_re);
+      unsigned nonempty = __ballot_sync(FULL_MASK, my_rb < my_re);
+      // part `part` of `parts` walks tiles [T*part/parts, T*(part+1)/parts) of
+      // the item's T neighbour tiles (rows in lane order)
+      uint32_t tiles_left = 0xffffffffu, skip_tiles = 0;
+      if (parts > 1) {
+        const uint32_t tr = (my_rb < my_re) ? (my_re - my_rb + 31u) / 32u : 0u;
+        uint32_t incl = tr;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t v = __shfl_up_sync(FULL_MASK, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const uint32_t T = __shfl_sync(FULL_MASK, incl, 31);
+        const uint32_t t_lo = (uint32_t)((uint64_t)T * part / parts);
+        const uint32_t t_hi = (uint32_t)((uint64_t)T * (part + 1) / parts);
+        tiles_left = t_hi - t_lo;
+        const unsigned past = __ballot_sync(FULL_MASK, incl <= t_lo);  // rows wholly before t_lo
+        nonempty = tiles_left ? (nonempty & ~past) : 0u;
+        if (nonempty) {  // the first row of the part starts skip_tiles tiles in
+          const int r0 = __ffs(nonempty) - 1;
+          skip_tiles = t_lo - __shfl_sync(FULL_MASK, incl - tr, r0);
+        }
+      }
       uint32_t qh = 0, qt = 0;    // arc ring head / tail (monotone)
       uint32_t ch_ = 0, ct_ = 0;  // deferred ring head / tail
       uint32_t n_arc = 0;
@@ -877,7 +911,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       // flat walk over (row, tile, center chunk); one inline copy of the drain
       unsigned rows_left = nonempty;
       int r = rows_left ? __ffs(rows_left) - 1 : 32;
-      uint32_t j0 = __shfl_sync(FULL_MASK, my_rb, r & 31);
+      uint32_t j0 = __shfl_sync(FULL_MASK, my_rb, r & 31) + skip_tiles * 32u;
       uint32_t re = __shfl_sync(FULL_MASK, my_re, r & 31);
       int kc = 0;
       for (;;) {
@@ -1050,7 +1084,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         if (kc >= (int)nc) {
           kc = 0;
           j0 += 32;
-          if (j0 >= re) {
+          if (--tiles_left == 0) rows_left = 0;  // end of this item part
+          else if (j0 >= re) {
             rows_left &= rows_left - 1;
             r = rows_left ? __ffs(rows_left) - 1 : 32;
             j0 = __shfl_sync(FULL_MASK, my_rb, r & 31);

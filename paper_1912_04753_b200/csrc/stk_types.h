@@ -7,6 +7,8 @@
 namespace stk {
 
 constexpr int kItemCenters = 32;    // centers per warp work item (one per lane)
+constexpr int kPartCells = 4096;    // a cell this populous splits items into parts (>= 2)
+constexpr int kMaxParts = 32;       // ... up to this many parts per item
 constexpr int kTaskMinItems = 4;    // warp items per CTA task: adaptive in [min, max] so the
 constexpr int kTaskMaxItems = 256;  // batch has ~8 tasks per resident CTA
 #ifndef STK_PAIR_WARPS
@@ -147,7 +149,7 @@ struct Batch {
   uint32_t* sel_start;   // [n_sel][cells+1] exclusive scan of selected per cell
   uint32_t* center_pos;  // [n_sel][n] sorted positions of selected centers, by cell
   uint32_t* task_start;  // [R+1] exclusive scan of ceil(items_r / task_items)
-  uint32_t* task_counter;  // [0] dynamic task counter, [1] task_items
+  uint32_t* task_counter;  // [0] dynamic task counter, [1] task_items, [2] parts per item
   // exact histograms [R][bins]
   unsigned long long* h_cnt;   // in-threshold pairs
   unsigned long long* h_half;  // interior pairs with v = 1/2 (contribute 2)

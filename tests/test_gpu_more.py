@@ -342,3 +342,17 @@ def test_bin_tables_close_thresholds_and_wide_range(api, port):
     _compare(api, port, x, y, t, ring, p0, p1, close, [20, 21, 22, 40, 500])
     wide = [1e-3, 1e-2, 0.1, 1.0, 5.0, 10.0, 100.0, 300.0]
     _compare(api, port, x, y, t, ring, p0, p1, wide, [1, 2, 3, 20, 40, 9000])
+
+
+def test_dense_cell_item_parts(api, port):
+    """A cluster of 5,000 points inside one grid cell (> kPartCells): items
+    are walked as several parts by different warps; sums must not change."""
+    ring, p0, p1 = square(10_000.0, 0, 1000)
+    rng = np.random.default_rng(31)
+    a = rng.uniform(0, 2 * np.pi, 5000)
+    rad = 18.0 * np.sqrt(rng.uniform(0, 1, 5000))
+    x = np.concatenate([5025.0 + rad * np.cos(a), rng.uniform(0, 10_000, 2000)])
+    y = np.concatenate([5025.0 + rad * np.sin(a), rng.uniform(0, 10_000, 2000)])
+    t = np.concatenate([rng.integers(0, 40, 5000), rng.integers(0, 1001, 2000)])
+    h = _compare(api, port, x, y, t, ring, p0, p1, [5.0, 20.0, 50.0, 100.0], [10, 50, 200])
+    assert int(h["counts"].sum()) > 20_000_000
