@@ -10,7 +10,10 @@ constexpr int kItemCenters = 32;    // centers per warp work item (one per lane)
 constexpr int kPartCells = 4096;    // a cell this populous splits items into parts (>= 2)
 constexpr int kMaxParts = 32;       // ... up to this many parts per item
 constexpr int kTaskMinItems = 4;    // warp items per CTA task: adaptive in [min, max] so the
-constexpr int kTaskMaxItems = 256;  // batch has ~8 tasks per resident CTA
+#ifndef STK_TASK_MAX
+#define STK_TASK_MAX 256
+#endif
+constexpr int kTaskMaxItems = STK_TASK_MAX;  // batch has ~8 tasks per resident CTA
 #ifndef STK_PAIR_WARPS
 #define STK_PAIR_WARPS 16
 #endif
