@@ -920,7 +920,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         // holds more than 31 + kArcChunk * 64 entries: full batches while
         // any are pending, and the remainder at the end
         const uint32_t pending = qt - qh, cpending = ct_ - ch_;
-        if (pending > (uint32_t)kArcRing) overflow |= 2;  // must never happen: reported as an error
         // deferred entries first (<= 31 + 32 pending), then the main ring
         if (cpending >= 32 || (done && pending == 0 && cpending > 0)) {
           const int cnt_ = (int)min(cpending, 32u);
@@ -931,6 +930,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           continue;
         }
         if (pending >= 32 || (done && pending > 0)) {
+          // <= 31 + kArcChunk * 64 by construction; checked here, off the hot path
+          if (pending > (uint32_t)kArcRing) overflow |= 2;  // reported as an error
           const int cnt_ = (int)min(pending, 32u);
           __syncwarp();
           drain_main<RECT>(cnt_, lane, arcq, qh, cring, &ct_, lanemask_lt, B.pxy + pb, S.arc, S.ch, A.reg, &n_arc);
