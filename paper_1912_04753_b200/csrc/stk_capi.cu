@@ -121,6 +121,7 @@ struct stk_ctx {
   int ec_nx = 0, ec_ny = 0;
   double ec_x0 = 0, ec_y0 = 0, ec_inv_w = 0, ec_dmax = 0, ec_reach = 0;
   DevBuf<uint32_t> d_ec_start, d_ec_edge;
+  DevBuf<float> d_ec_dmin, d_ec_dmax;
   DevBuf<RegionView> d_rv;  // device copy of region_view() for out-of-line device code
 
   // grid (est::DistanceGrid)
@@ -257,7 +258,7 @@ void build_edge_cells(stk_ctx* c) {
   const double S = c->pip_lim;
   const double reach = smax * (1.0 + 4e-6) + 1e-9 * S;
   const double W = c->xmax - c->xmin, H = c->ymax - c->ymin;
-  const double ew = std::max(smax / 2.0, std::max(W, H) / 512.0);
+  const double ew = std::max(smax / 16.0, std::max(W, H) / 1024.0);
   const int nx = std::max(1, (int)std::ceil(W / ew)), ny = std::max(1, (int)std::ceil(H / ew));
   const double half_diag = ew * 0.70710678118654757 * (1.0 + 1e-9) + 1e-9 * S;
   c->ec_nx = nx;
@@ -268,7 +269,14 @@ void build_edge_cells(stk_ctx* c) {
   c->ec_dmax = smax;
   c->ec_reach = reach * (1.0 - 1e-9);
   const uint64_t cells = (uint64_t)nx * ny;
-  std::vector<std::vector<uint32_t>> lists(cells);
+  // per cell: (lower, upper bound of the segment's distance from the cell's
+  // points, segment)
+  struct Entry {
+    float lb, ub;
+    uint32_t seg;
+    bool operator<(const Entry& o) const { return lb < o.lb || (lb == o.lb && seg < o.seg); }
+  };
+  std::vector<std::vector<Entry>> lists(cells);
   for (uint32_t i = 0; i < m; ++i) {
     const uint32_t j = i == 0 ? m - 1 : i - 1;
     const double ax = r[2 * j], ay = r[2 * j + 1], bx = r[2 * i], by = r[2 * i + 1];
@@ -281,15 +289,44 @@ void build_edge_cells(stk_ctx* c) {
     for (int iy = iy0; iy <= iy1; ++iy)
       for (int ix = ix0; ix <= ix1; ++ix) {
         const double cx = c->xmin + (ix + 0.5) * ew, cy = c->ymin + (iy + 0.5) * ew;
-        if (seg_dist(cx, cy, ax, ay, bx, by) <= lim) lists[(uint64_t)iy * nx + ix].push_back(i);
+        const double dist = seg_dist(cx, cy, ax, ay, bx, by);
+        if (dist <= lim) {
+          // no point of the cell is nearer than dist - half_diag (rounded
+          // down), none farther than the far endpoint + half_diag (rounded up)
+          float lb = (float)std::max(0.0, (dist - half_diag) * (1.0 - 1e-9));
+          if ((double)lb > std::max(0.0, dist - half_diag)) lb = std::nextafter(lb, 0.0f);
+          const double far = std::max(std::hypot(ax - cx, ay - cy), std::hypot(bx - cx, by - cy));
+          float ub = (float)((far + half_diag) * (1.0 + 1e-9));
+          if ((double)ub < far + half_diag) ub = std::nextafter(ub, std::numeric_limits<float>::infinity());
+          lists[(uint64_t)iy * nx + ix].push_back({lb, ub, i});
+        }
       }
   }
   std::vector<uint32_t> start(cells + 1, 0), edge;
+  std::vector<float> dmin, dmax;
   for (uint64_t q = 0; q < cells; ++q) start[q + 1] = start[q] + (uint32_t)lists[q].size();
   edge.reserve(start[cells]);
-  for (auto& l : lists) edge.insert(edge.end(), l.begin(), l.end());
+  dmin.reserve(start[cells]);
+  dmax.reserve(start[cells]);
+  for (auto& l : lists) {  // nearest first: a circle of radius d stops at the first lb > reach(d)
+    std::sort(l.begin(), l.end());
+    for (const Entry& e : l) {
+      dmin.push_back(e.lb);
+      dmax.push_back(e.ub);
+      edge.push_back(e.seg);
+    }
+  }
   upload_u32(c, c->d_ec_start, start);
   upload_u32(c, c->d_ec_edge, edge);
+  c->d_ec_dmin.ensure(std::max<size_t>(dmin.size(), 1));
+  c->d_ec_dmax.ensure(std::max<size_t>(dmax.size(), 1));
+  if (!dmin.empty()) {
+    CK(cudaMemcpyAsync(c->d_ec_dmin.p, dmin.data(), sizeof(float) * dmin.size(),
+                       cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_ec_dmax.p, dmax.data(), sizeof(float) * dmax.size(),
+                       cudaMemcpyHostToDevice, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
   c->ec_ok = true;
 }
 
@@ -361,6 +398,9 @@ RegionView region_view(stk_ctx* c) {
   r.pip_yhi = c->pip_yhi;
   r.ec_start = c->ec_ok ? c->d_ec_start.p : nullptr;
   r.ec_edge = c->ec_ok ? c->d_ec_edge.p : nullptr;
+  r.ec_dmin = c->ec_ok ? c->d_ec_dmin.p : nullptr;
+  r.ec_far = c->ec_ok ? c->d_ec_dmax.p : nullptr;
+  r.ec_abs = 1e-9 * c->pip_lim;
   r.ec_nx = c->ec_nx;
   r.ec_ny = c->ec_ny;
   r.ec_x0 = c->ec_x0;

@@ -122,7 +122,21 @@ __device__ __forceinline__ const uint32_t* edge_list(double cx, double cy, doubl
   iy = min(max(iy, 0), R.ec_ny - 1);
   const uint32_t cell = (uint32_t)iy * (uint32_t)R.ec_nx + (uint32_t)ix;
   const uint32_t b = R.ec_start[cell];
-  *cnt = R.ec_start[cell + 1] - b;
+  uint32_t n = R.ec_start[cell + 1] - b;
+  if (d > 0.0) {
+    // entries are sorted by a lower bound of their distance to the cell: those
+    // beyond d (1 + 4e-6) + 1e-9 S are rejected by the reference (the
+    // edge-cell argument with d for s_max) — keep the prefix before them
+    const double lim = d * (1.0 + 4e-6) + R.ec_abs;
+    const float* dm = R.ec_dmin + b;
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if ((double)dm[mid] > lim) hi = mid; else lo = mid + 1;
+    }
+    n = lo;
+  }
+  *cnt = n;
   return R.ec_edge + b;
 }
 
@@ -215,6 +229,7 @@ __device__ __noinline__ double spatial_weight(double cx, double cy, double d, co
   const uint32_t nv = R.nv;
   uint32_t cnt;
   const uint32_t* list = edge_list(cx, cy, d, R, &cnt);  // segments that can cross
+  const double inner = d * (1.0 - 4e-6) - R.ec_abs;
   double buf[kMaxAngles];
   double lower = -1.0;  // angles are in [0, 2*pi)
   int u = 0;            // kept angles so far
@@ -230,6 +245,7 @@ __device__ __noinline__ double spatial_weight(double cx, double cy, double d, co
     int n = 0;
     bool dropped = false;
     for (uint32_t k = 0; k < cnt; ++k) {
+      if (list && (double)R.ec_far[(list - R.ec_edge) + k] < inner) continue;  // wholly inside
       const uint32_t i = list ? list[k] : k;
       double two[2];
       const int m = segment_circle_angles(ring[i == 0 ? nv - 1 : i - 1], ring[i], cx, cy, d, two, 0);
@@ -509,11 +525,15 @@ __device__ STK_WEIGHT_INLINE double spatial_weight_buf(double cx, double cy, dou
   const double reach = d * (1.0 + 1e-6);
   uint32_t cnt = 4;
   const uint32_t* list = RECT ? nullptr : edge_list(cx, cy, d, R, &cnt);
+  const double inner = d * (1.0 - 4e-6) - R.ec_abs;  // farthest point nearer: wholly inside
   int n = 0;
   for (uint32_t base = 0; base < cnt; base += 32) {  // 32 segments per accept mask
   const uint32_t m = RECT ? 4u : min(32u, cnt - base);
   uint32_t acc = 0;
   for (uint32_t k = 0; k < m; ++k) {  // segment (ring[i-1], ring[i])
+    // a segment lying inside the circle by the reach margin has both roots
+    // outside [0, 1] by far more than their error: the reference takes none
+    if (!RECT && list && (double)R.ec_far[(list - R.ec_edge) + base + k] < inner) continue;
     const uint32_t i = (!RECT && list) ? list[base + k] : base + k;
     const double2 A = ring[i == 0 ? nv - 1 : i - 1], Bv = ring[i];
     if (RECT) {
@@ -667,7 +687,10 @@ __device__ __forceinline__ double safe_q(double cx, double cy, const RegionView&
     r2 = R.ec_reach * R.ec_reach;
   }
   const double ring_maxabs = R.maxabs;
+  const float* dml = list ? R.ec_dmin + (list - R.ec_edge) : nullptr;
   for (uint32_t k = 0; k < cnt; ++k) {
+    // sorted lower bounds: nothing further down the list can come nearer
+    if (dml && (double)dml[k] * (double)dml[k] >= r2) break;
     const uint32_t i = list ? list[k] : k;
     const double2 a = ring[i == 0 ? nv - 1 : i - 1], b = ring[i];
     const double ex = b.x - a.x, ey = b.y - a.y;

@@ -60,6 +60,9 @@ struct RegionView {
   // (the reference rejects them).  ec_start == nullptr: not built.
   const uint32_t* ec_start;    // [ec_nx * ec_ny + 1]
   const uint32_t* ec_edge;
+  const float* ec_dmin;        // per list entry: lower bound of its distance to the cell (ascending)
+  const float* ec_far;         // ... and upper bound of its farthest point from the cell
+  double ec_abs;               // absolute margin of the reach test (1e-9 S)
   int ec_nx, ec_ny;
   double ec_x0, ec_y0, ec_inv_w, ec_dmax, ec_reach;
   int no_safe;  // debugging (STK_NO_SAFE_RADIUS): every pair takes the exact path
