@@ -668,6 +668,102 @@ __device__ __forceinline__ double rect_single_edge_weight(double cx, double cy, 
   return 1.0 - theta * 0.31830988618379067154;  // 1 - theta / pi
 }
 
+// spatial_isotropic_weight in closed form for a rectangle and a circle that
+// reaches several sides (corners; circles larger than the region).  For each
+// side within reach the reference's own quadratic decides accept / reject; an
+// accepted side s at distance h contributes the line crossings phi_s +- theta_s
+// (theta = atan2(sqrt((d-h)(d+h)), h); phi = 0, pi/2, pi, 3pi/2 for the right,
+// top, left, bottom side), each of which lies on the segment iff the corner on
+// its side of the foot is outside the circle.  Gates (else -1, the general
+// routine): the single-side gates of rect_single_edge_weight for every
+// accepted side, no side rejected while its line is nearer than d (a
+// tangency the reference drops), and every corner between two sides within
+// reach away from the circle by |K - c|^2 - d^2 > 1e-5 d^2 — then crossings
+// are 2.5e-6 d or more from the segment ends and from each other, far above
+// the reference's root error, and its de-duplication keeps them all.  The
+// angles are sorted and each arc's midpoint is classified by the certified
+// probe (rect_probe_certified; uncertain -> -1); no crossing at all gives 1.0
+// (the reference's rule when the circle contains the whole rectangle).
+__device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, double d,
+                                                         const RegionView& R) {
+  if (d <= 0.0) return 1.0;
+  if (!(cx > R.xmin && cx < R.xmax && cy > R.ymin && cy < R.ymax) || d < R.sw_dmin) return -1.0;
+  const double reach = d * (1.0 + 1e-6);
+  const double r2 = d * d;
+  // sides in angular order: right (x = xmax), top, left (x = xmin), bottom; the
+  // RegionView side tables are ordered left, right, bottom, top
+  const double h[4] = {R.xmax - cx, R.ymax - cy, cx - R.xmin, cy - R.ymin};
+  const int tab[4] = {1, 3, 0, 2};
+  const double along[4] = {cy, cx, cy, cx};
+  double theta[4] = {0.0, 0.0, 0.0, 0.0};
+  unsigned acc = 0, inr = 0;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    if (!(h[s] <= reach)) continue;
+    inr |= 1u << s;
+    const double fa = R.sd_start[tab[s]] - along[s];
+    const double D = R.sd_len[tab[s]];
+    const double qa = D * D;
+    const double qb = 2.0 * (fa * D);
+    const double qc = h[s] * h[s] + fa * fa - r2;
+    const double disc = qb * qb - 4.0 * qa * qc;
+    const double scale = qb * qb + fabs(4.0 * qa * qc);
+    if (!(qa != 0.0 && disc > 1e-9 * scale)) {
+      if (h[s] < d) return -1.0;  // a crossing line the reference drops as tangent
+      continue;
+    }
+    if (qa * disc * r2 < 1e-10 * scale * scale) return -1.0;
+    const double dm = d - h[s];
+    if (dm <= R.sw_margin + 1e-12 * d) return -1.0;
+    theta[s] = fast_atan2(sqrt(dm * (d + h[s])), h[s]);
+    acc |= 1u << s;
+  }
+  if (acc == 0) return 1.0;
+  // corner k sits between side k and side k+1 (counter-clockwise)
+  unsigned cin = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int k1 = (k + 1) & 3;
+    if (!((inr >> k) & 1u) || !((inr >> k1) & 1u)) continue;  // beyond reach: outside
+    const double g = h[k] * h[k] + h[k1] * h[k1] - r2;
+    if (fabs(g) <= 1e-5 * r2) return -1.0;
+    if (g < 0.0) cin |= 1u << k;
+  }
+  double ang[8];
+  int n = 0;
+  const double kHalfPi = 1.57079632679489661923;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    if (!((acc >> s) & 1u)) continue;
+    const double phi = s * kHalfPi;
+    if (!((cin >> ((s + 3) & 3)) & 1u)) {  // clockwise end, by corner (s-1, s)
+      double a = phi - theta[s];
+      if (a < 0.0) a += kTwoPi;
+      ang[n++] = a;
+    }
+    if (!((cin >> s) & 1u)) ang[n++] = phi + theta[s];  // counter-clockwise end
+  }
+  if (n == 0) return 1.0;
+  for (int a = 1; a < n; ++a) {
+    const double v = ang[a];
+    int b = a - 1;
+    while (b >= 0 && ang[b] > v) {
+      ang[b + 1] = ang[b];
+      --b;
+    }
+    ang[b + 1] = v;
+  }
+  double span = 0.0;
+  for (int a = 0; a < n; ++a) {
+    const double a0 = ang[a];
+    const double a1 = (a + 1 < n) ? ang[a + 1] : ang[0] + kTwoPi;
+    const int dec = rect_probe_certified(cx, cy, d, 0.5 * (a0 + a1), R);
+    if (dec < 0) return -1.0;
+    if (dec) span += a1 - a0;
+  }
+  return span / kTwoPi;
+}
+
 // Squared radius below which spatial_weight() provably returns exactly 1.0
 // for this center (the circle stays strictly inside every edge's reach by a
 // relative margin far above the rounding error of the reference's quadratic;

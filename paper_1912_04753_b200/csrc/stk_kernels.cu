@@ -701,7 +701,9 @@ __device__ __forceinline__ void drain_general(int count, int lane, const uint4* 
   const double d = sqrt(__hiloint2double((int)e.w, (int)e.z));
   double ws = -1.0;
   if (RECT) {
-    if (reg.nv <= 32) ws = spatial_weight_buf_rect(c.x, c.y, d, reg, angs + lane, 32, slots / 2);
+    ws = rect_multi_edge_weight(c.x, c.y, d, reg);
+    if (ws < 0.0 && reg.nv <= 32)
+      ws = spatial_weight_buf_rect(c.x, c.y, d, reg, angs + lane, 32, slots / 2);
   } else {
     ws = spatial_weight_buf<false>(c.x, c.y, d, reg, angs + lane, 32, slots / 2);
   }
@@ -1258,6 +1260,7 @@ __global__ void weights_kernel(const double* cx, const double* cy, const double*
   }
   // the pair kernel's order: closed form (rectangles), then the general routines
   double ws = reg.rect ? rect_single_edge_weight(cx[i], cy[i], d[i], reg) : -1.0;
+  if (ws < 0.0 && reg.rect) ws = rect_multi_edge_weight(cx[i], cy[i], d[i], reg);
   if (ws < 0.0)
     ws = reg.rect ? spatial_weight_buf<true>(cx[i], cy[i], d[i], reg, angs + threadIdx.x, 128,
                                              kAngleSlots / 2)
