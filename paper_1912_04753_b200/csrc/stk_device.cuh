@@ -684,6 +684,7 @@ __device__ __forceinline__ double rect_single_edge_weight(double cx, double cy, 
 // angles are sorted and each arc's midpoint is classified by the certified
 // probe (rect_probe_certified; uncertain -> -1); no crossing at all gives 1.0
 // (the reference's rule when the circle contains the whole rectangle).
+// Results below 1e-3 go to the general routine (see the end).
 __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, double d,
                                                          const RegionView& R) {
   if (d <= 0.0) return 1.0;
@@ -761,7 +762,12 @@ __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, d
     if (dec < 0) return -1.0;
     if (dec) span += a1 - a0;
   }
-  return span / kTwoPi;
+  // the reference's crossing points carry its own rounding (up to ~1e-12 rad at
+  // large coordinate offsets); a small omega would turn that into a large
+  // relative difference, so small results come from the general routine,
+  // which reproduces those crossing points
+  const double w = span / kTwoPi;
+  return w >= 1e-3 ? w : -1.0;
 }
 
 // Squared radius below which spatial_weight() provably returns exactly 1.0

@@ -135,6 +135,38 @@ def rect_stress():
     np.savez_compressed(os.path.join(OUT, "rect_stress.npz"), count=len(rects), **out)
 
 
+def rect_corner_stress():
+    """Rectangle (center, d) cases for the multi-side closed form: circles
+    through or near corners (|K - c| -/+ tiny), containing 1..4 corners, and
+    regions at large offsets."""
+    rng = np.random.default_rng(12)
+    out = {}
+    rects = [(0.0, 0.0, 1000.0, 1000.0), (500000.0, 4000000.0, 503000.0, 4001000.0),
+             (-2.0, -1.0, 2.0, 7.0)]
+    for k, (x0, y0, x1, y1) in enumerate(rects):
+        ring = np.array([[x0, y0], [x1, y0], [x1, y1], [x0, y1]], float)
+        W, H = x1 - x0, y1 - y0
+        corners = np.array([[x0, y0], [x1, y0], [x1, y1], [x0, y1]])
+        cx, cy, dd, ww = [], [], [], []
+        while len(cx) < 1500:
+            px = x0 + W * rng.uniform(0.001, 0.999)
+            py = y0 + H * rng.uniform(0.001, 0.999)
+            mode = rng.integers(3)
+            if mode == 0:    # near a corner distance
+                kd = np.hypot(*(corners[rng.integers(4)] - [px, py]))
+                d = kd * (1.0 + rng.choice([-1, 1]) * 10.0 ** rng.uniform(-14, -2))
+            elif mode == 1:  # large circles: several sides, some corners inside
+                d = rng.uniform(0.2, 1.5) * np.hypot(W, H)
+            else:            # two nearby sides
+                d = rng.uniform(0.5, 1.2) * (min(px - x0, x1 - px) + min(py - y0, y1 - py))
+            cx.append(px); cy.append(py); dd.append(d)
+            ww.append(ref.spatial_weight(px, py, d, ring))
+        out[f"{k}_ring"] = ring
+        out[f"{k}_cx"] = np.array(cx); out[f"{k}_cy"] = np.array(cy)
+        out[f"{k}_d"] = np.array(dd); out[f"{k}_w"] = np.array(ww)
+    np.savez_compressed(os.path.join(OUT, "rect_corner.npz"), count=len(rects), **out)
+
+
 def c1():
     """C1 (configs[0]) through the reference: K, per-bin counts, in_threshold."""
     cfg = configs.CONFIGS["C1"]
@@ -155,5 +187,5 @@ def mt():
 
 if __name__ == "__main__":
     oracle.build(with_ref=True)
-    sample(); polygons(); weights(); rect_stress(); c1(); mt()
+    sample(); polygons(); weights(); rect_stress(); rect_corner_stress(); c1(); mt()
     print("golden fixtures written to", OUT)

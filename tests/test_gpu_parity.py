@@ -91,6 +91,31 @@ def test_rect_closed_form_vs_reference(api):
         assert rel_err(w, w_ref) <= 1e-10, (k, rel_err(w, w_ref))
 
 
+def test_rect_multi_side_closed_form_vs_reference(api):
+    """Circles near / through rectangle corners and circles larger than the
+    region (tests/golden/rect_corner.npz, from the reference): the multi-side
+    closed form's gates must route every borderline case to the general
+    routine.  Bound: 1e-10 relative plus 1e-15 absolute — omega is a sum of
+    arc lengths formed as differences of angles near 2*pi, so a tiny inside
+    arc (omega ~ 1e-8) is known to the reference itself only to an ulp of
+    those angles (~1e-16 after / 2*pi); device and libm atan2 differ there."""
+    from paper_1912_04753_b200 import _lib
+
+    g = golden("rect_corner.npz")
+    dev, geom = api["dev"], api["geom"]
+    for k in range(int(g["count"])):
+        dev.configure(geom.StudyRegion(g[f"{k}_ring"], 0, 1))
+        cx, cy, d, w_ref = g[f"{k}_cx"], g[f"{k}_cy"], g[f"{k}_d"], g[f"{k}_w"]
+        w = np.zeros_like(w_ref)
+        dev.check(dev.lib.stk_spatial_weights(dev.h, _lib.ptr(cx), _lib.ptr(cy), _lib.ptr(d),
+                                              len(cx), _lib.ptr(w)))
+        rel = np.abs(w - w_ref) / np.maximum(np.abs(w_ref), 1e-300)
+        i = int(np.argmax(rel))
+        print("rect_corner", k, "max rel err", rel[i], "at w_ref", w_ref[i], "abs", abs(w[i] - w_ref[i]))
+        assert np.array_equal(w == 1.0, w_ref == 1.0), k
+        assert np.all(np.abs(w - w_ref) <= 1e-10 * np.abs(w_ref) + 1e-15), (k, rel[i])
+
+
 def test_edge_correction_known_answers(api):
     """proj/tests/test_edge_correction.cpp:10-29 through the device."""
     from paper_1912_04753_b200 import _lib
