@@ -397,7 +397,7 @@ def run_ours(args):
                 "realisations_per_s": patterns / (e2e_ms * 1e-3)},
         "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                      "unit": "FP64 Tinstr/s", "frac": achieved / peak if peak else None,
-                     "traffic": None,
+                     "traffic": traffic_bytes(),
                      "note": f"pair kernel: ({W_INT} x interior + {W_ARC} x arc (omega != 1) pairs) "
                              "FP64 instr / CUDA-event pair-kernel time; peak = live DFMA "
                              "microbenchmark (stk_measure_fp64_peak)",
@@ -415,6 +415,16 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def traffic_bytes():
+    """DRAM bytes (read + write) per pair-kernel launch from the committed ncu
+    capture of this workload (profiles/pair_kernel_traffic_r1.json), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "pair_kernel_traffic_r1.json")))
+        return d["dram_bytes_read"] + d["dram_bytes_write"]
+    except Exception:
+        return None
 
 
 def cpu_baseline(cfg, s, tv, sims, x, y, t, sample_sims):
