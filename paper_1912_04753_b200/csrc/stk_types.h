@@ -27,7 +27,11 @@ constexpr int kRingSmem = 32;      // ring vertices staged in shared memory (bit
 #endif
 constexpr int kArcChunk = STK_ARC_CHUNK;        // candidate steps between arc drains
 constexpr int kFixedFracBits = 53;  // fixed-point weighted sums: value * 2^53
-constexpr int kArcRing = 1024;      // per-warp arc ring entries (> 31 + kArcChunk * 64)
+#ifndef STK_ARC_RING
+#define STK_ARC_RING 1024
+#endif
+constexpr int kArcRing = STK_ARC_RING;  // per-warp arc ring entries (> 31 + kArcChunk * 64)
+static_assert(kArcRing > 31 + kArcChunk * 64, "the arc ring must hold a chunk's entries");
 constexpr int kCplxRing = 128;      // per-warp ring of entries deferred to the general weight (> 63)
 
 // Study region on the device (geom::StudyRegion, geometry.hpp:95-120).

@@ -197,3 +197,28 @@ def test_configs_generators_deterministic():
     assert x.min() >= 0 and x.max() <= c4.extent_m and t.min() >= 0 and t.max() <= c4.period_s
     s, tv = configs.grid_values(configs.CONFIGS["C5"])
     assert len(s) == 50 and len(tv) == 50 and tv[-1] == 30 * 86400
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` (the reference's own CPU path, oracle/_ref)
+    prints one JSON line with the driver's contract keys (C1: seconds)."""
+    import json
+    import subprocess
+    import sys
+
+    import oracle
+
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built here")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                        "--config", "C1", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "reference"
+    assert line["config"]["workload"].startswith("C1")
