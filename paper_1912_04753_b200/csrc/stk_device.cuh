@@ -399,9 +399,6 @@ __device__ __forceinline__ int rect_probe_certified(double cx, double cy, double
   return -1;
 }
 
-#ifndef STK_WEIGHT_INLINE
-#define STK_WEIGHT_INLINE __forceinline__
-#endif
 // spatial_isotropic_weight for rings of at most 32 vertices, organised for
 // SIMT: (1) a uniform pass over the segments marks those whose quadratic has
 // an accepted discriminant; (2) each lane walks only its accepted segments
@@ -420,7 +417,7 @@ __device__ __forceinline__ int rect_probe_certified(double cx, double cy, double
 // deferred drain).  Kept with runtime R.rect tests: specialising them away
 // changes the pair kernel's register allocation for the worse (the hot loop
 // then reloads its neighbour from local memory).
-__device__ STK_WEIGHT_INLINE double spatial_weight_buf_rect(double cx, double cy, double d,
+__device__ __forceinline__ double spatial_weight_buf_rect(double cx, double cy, double d,
                                                        const RegionView& R, double* buf,
                                                        int stride, int cap) {
   if (d <= 0.0) return 1.0;
@@ -515,7 +512,7 @@ __device__ STK_WEIGHT_INLINE double spatial_weight_buf_rect(double cx, double cy
 // RECT: the region is RegionView::rect (4 segments, rectangle PIP); else a
 // general ring through the edge cells and the slab PIP.
 template <bool RECT>
-__device__ STK_WEIGHT_INLINE double spatial_weight_buf(double cx, double cy, double d,
+__device__ __forceinline__ double spatial_weight_buf(double cx, double cy, double d,
                                                        const RegionView& R, double* buf,
                                                        int stride, int cap) {
   if (d <= 0.0) return 1.0;
