@@ -665,27 +665,62 @@ __device__ __forceinline__ double rect_single_edge_weight(double cx, double cy, 
   return 1.0 - theta * 0.31830988618379067154;  // 1 - theta / pi
 }
 
+// rect_probe_certified for the arc running counter-clockwise from crossing
+// vector va to crossing vector vb (vectors from the center, length d): its
+// midpoint direction is the chord vb - va turned clockwise by 90 degrees, for
+// every arc length in (0, 2 pi).  The chord is formed in double (the crossing
+// vectors are accurate to ~1 ulp, and crossings are >= 2.5e-6 d apart) and
+// normalised in float: direction error ~2e-7 rad, well inside the 2e-6 d
+// certification margin.
+__device__ __forceinline__ int rect_probe_chord(double cx, double cy, double d, double vax,
+                                                double vay, double vbx, double vby,
+                                                const RegionView& R) {
+  const float mx = (float)(vby - vay), my = (float)(vax - vbx);
+  const float inv = rsqrtf(fmaf(mx, mx, my * my));
+  const double px = cx + d * (double)(mx * inv), py = cy + d * (double)(my * inv);
+  const double e = d * 2e-6 + 1e-12 * (R.maxabs + d + 1.0);
+  if (px >= R.xmin + e && px < R.xmax - e && py >= R.ymin + e && py < R.ymax - e) return 1;
+  const double o = e + R.box_m;
+  if (px < R.xmin - o || px > R.xmax + o || py < R.ymin - o || py > R.ymax + o) return 0;
+  return -1;
+}
+
 // spatial_isotropic_weight in closed form for a rectangle and a circle that
 // reaches several sides (corners; circles larger than the region).  For each
 // side within reach the reference's own quadratic decides accept / reject; an
 // accepted side s at distance h contributes the line crossings phi_s +- theta_s
-// (theta = atan2(sqrt((d-h)(d+h)), h); phi = 0, pi/2, pi, 3pi/2 for the right,
-// top, left, bottom side), each of which lies on the segment iff the corner on
-// its side of the foot is outside the circle.  Gates (else -1, the general
-// routine): the single-side gates of rect_single_edge_weight for every
-// accepted side, no side rejected while its line is nearer than d (a
-// tangency the reference drops), and every corner between two sides within
-// reach away from the circle by |K - c|^2 - d^2 > 1e-5 d^2 — then crossings
-// are 2.5e-6 d or more from the segment ends and from each other, far above
-// the reference's root error, and its de-duplication keeps them all.  The
-// angles are sorted and each arc's midpoint is classified by the certified
-// probe (rect_probe_certified; uncertain -> -1); no crossing at all gives 1.0
-// (the reference's rule when the circle contains the whole rectangle).
+// (cos theta = h / d; phi = 0, pi/2, pi, 3pi/2 for the right, top, left, bottom
+// side), each of which lies on the segment iff the corner on its side of the
+// foot is outside the circle.  Gates (else -1, the general routine): the
+// single-side gates of rect_single_edge_weight for every accepted side, no side
+// rejected while its line is nearer than d (a tangency the reference drops),
+// and every corner between two sides within reach away from the circle by
+// |K - c|^2 - d^2 > 1e-5 d^2 — then crossings are 2.5e-6 d or more from the
+// segment ends and from each other, far above the reference's root error, and
+// its de-duplication keeps them all.  No crossing at all gives 1.0 (the
+// reference's rule when the circle contains the whole rectangle).
+//
+// The crossings come out in increasing angle without sorting: side s's
+// clockwise end phi - theta precedes its counter-clockwise end, and the next
+// side's clockwise end follows unless the corner between them is inside the
+// circle (then both are dropped; theta_s + theta_s1 < pi/2 exactly when that
+// corner is outside).  So ends alternate clockwise / counter-clockwise, arcs
+// from a clockwise end to the next end are outside and the others inside, and
+// each end borders one inside arc:
+//   inside span = pi/2 * (sum_cw s - sum_ccw s) + 2 pi [first end is cw]
+//                 - sum over ends of theta_s.
+// The theta sum is the argument of the product of (h_s + i w_s), w_s =
+// sqrt((d - h_s)(d + h_s)), one factor per end: one atan2 per pair instead of
+// one per side, with whole turns counted as the running product's imaginary
+// part turns non-negative again (each factor adds < pi/2).  Each arc's midpoint
+// is still classified by the certified probe (rect_probe_chord) and must match
+// the expected inside / outside pattern, else -1.
 // Results below 1e-3 go to the general routine (see the end).
 __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, double d,
                                                          const RegionView& R) {
   if (d <= 0.0) return 1.0;
   if (!(cx > R.xmin && cx < R.xmax && cy > R.ymin && cy < R.ymax) || d < R.sw_dmin) return -1.0;
+  if (!(d > 1e-30 && d < 1e30)) return -1.0;  // keeps the product of <= 8 factors of size d finite
   const double reach = d * (1.0 + 1e-6);
   const double r2 = d * d;
   // sides in angular order: right (x = xmax), top, left (x = xmin), bottom; the
@@ -693,7 +728,7 @@ __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, d
   const double h[4] = {R.xmax - cx, R.ymax - cy, cx - R.xmin, cy - R.ymin};
   const int tab[4] = {1, 3, 0, 2};
   const double along[4] = {cy, cx, cy, cx};
-  double theta[4] = {0.0, 0.0, 0.0, 0.0};
+  double w[4] = {0.0, 0.0, 0.0, 0.0};
   unsigned acc = 0, inr = 0;
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
@@ -713,7 +748,7 @@ __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, d
     if (qa * disc * r2 < 1e-10 * scale * scale) return -1.0;
     const double dm = d - h[s];
     if (dm <= R.sw_margin + 1e-12 * d) return -1.0;
-    theta[s] = fast_atan2(sqrt(dm * (d + h[s])), h[s]);
+    w[s] = sqrt(dm * (d + h[s]));
     acc |= 1u << s;
   }
   if (acc == 0) return 1.0;
@@ -727,44 +762,61 @@ __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, d
     if (fabs(g) <= 1e-5 * r2) return -1.0;
     if (g < 0.0) cin |= 1u << k;
   }
-  double ang[8];
-  int n = 0;
-  const double kHalfPi = 1.57079632679489661923;
+  double pr = 1.0, pim = 0.0;                     // running product, argument = theta sum
+  double fx = 0.0, fy = 0.0, qx = 0.0, qy = 0.0;  // first / previous crossing vector
+  int n = 0, turns = 0, ksum = 0, bad = 0;
+  bool first_cw = false, prev_cw = false;
+  auto end = [&](int s, bool cw, double vx, double vy) {
+    const double nr = pr * h[s] - pim * w[s];
+    const double ni = pr * w[s] + pim * h[s];
+    turns += (pim < 0.0) & (ni >= 0.0);
+    pr = nr;
+    pim = ni;
+    ksum += cw ? s : -s;
+    if (n == 0) {
+      first_cw = cw;
+      fx = vx;
+      fy = vy;
+    } else {  // arc previous -> this end: inside iff it ends at a clockwise end
+      bad |= (cw == prev_cw) | (rect_probe_chord(cx, cy, d, qx, qy, vx, vy, R) != (int)cw);
+    }
+    qx = vx;
+    qy = vy;
+    prev_cw = cw;
+    ++n;
+  };
+  // crossing vectors: side s's (h, -+w) turned by phi_s
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     if (!((acc >> s) & 1u)) continue;
-    const double phi = s * kHalfPi;
+    const double hs = h[s], ws = w[s];
     if (!((cin >> ((s + 3) & 3)) & 1u)) {  // clockwise end, by corner (s-1, s)
-      double a = phi - theta[s];
-      if (a < 0.0) a += kTwoPi;
-      ang[n++] = a;
+      if (s == 0) end(0, true, hs, -ws);
+      if (s == 1) end(1, true, ws, hs);
+      if (s == 2) end(2, true, -hs, ws);
+      if (s == 3) end(3, true, -ws, -hs);
     }
-    if (!((cin >> s) & 1u)) ang[n++] = phi + theta[s];  // counter-clockwise end
+    if (!((cin >> s) & 1u)) {  // counter-clockwise end, by corner (s, s+1)
+      if (s == 0) end(0, false, hs, ws);
+      if (s == 1) end(1, false, -ws, hs);
+      if (s == 2) end(2, false, -hs, -ws);
+      if (s == 3) end(3, false, ws, -hs);
+    }
   }
   if (n == 0) return 1.0;
-  for (int a = 1; a < n; ++a) {
-    const double v = ang[a];
-    int b = a - 1;
-    while (b >= 0 && ang[b] > v) {
-      ang[b + 1] = ang[b];
-      --b;
-    }
-    ang[b + 1] = v;
-  }
-  double span = 0.0;
-  for (int a = 0; a < n; ++a) {
-    const double a0 = ang[a];
-    const double a1 = (a + 1 < n) ? ang[a + 1] : ang[0] + kTwoPi;
-    const int dec = rect_probe_certified(cx, cy, d, 0.5 * (a0 + a1), R);
-    if (dec < 0) return -1.0;
-    if (dec) span += a1 - a0;
-  }
+  bad |= (first_cw == prev_cw) | (rect_probe_chord(cx, cy, d, qx, qy, fx, fy, R) != (int)first_cw);
+  if (bad) return -1.0;
+  const double kHalfPi = 1.57079632679489661923;
+  double a = fast_atan2(pim, pr);
+  if (a < 0.0) a += kTwoPi;
+  const double tsum = a + kTwoPi * turns;
+  const double span = kHalfPi * ksum + (first_cw ? kTwoPi : 0.0) - tsum;
   // the reference's crossing points carry its own rounding (up to ~1e-12 rad at
   // large coordinate offsets); a small omega would turn that into a large
   // relative difference, so small results come from the general routine,
   // which reproduces those crossing points
-  const double w = span / kTwoPi;
-  return w >= 1e-3 ? w : -1.0;
+  const double wt = span / kTwoPi;
+  return wt >= 1e-3 ? wt : -1.0;
 }
 
 // Squared radius below which spatial_weight() provably returns exactly 1.0
