@@ -712,9 +712,10 @@ __device__ __forceinline__ int rect_probe_chord(double cx, double cy, double d, 
 // The theta sum is the argument of the product of (h_s + i w_s), w_s =
 // sqrt((d - h_s)(d + h_s)), one factor per end: one atan2 per pair instead of
 // one per side, with whole turns counted as the running product's imaginary
-// part turns non-negative again (each factor adds < pi/2).  Each arc's midpoint
-// is still classified by the certified probe (rect_probe_chord) and must match
-// the expected inside / outside pattern, else -1.
+// part turns non-negative again.  Each arc's midpoint
+// other than a side's own outside arc is classified by the certified probe
+// (rect_probe_chord) and must match the expected inside / outside pattern,
+// else -1.
 // Results below 1e-3 go to the general routine (see the end).
 __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, double d,
                                                          const RegionView& R) {
@@ -762,49 +763,72 @@ __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, d
     if (fabs(g) <= 1e-5 * r2) return -1.0;
     if (g < 0.0) cin |= 1u << k;
   }
-  double pr = 1.0, pim = 0.0;                     // running product, argument = theta sum
-  double fx = 0.0, fy = 0.0, qx = 0.0, qy = 0.0;  // first / previous crossing vector
-  int n = 0, turns = 0, ksum = 0, bad = 0;
-  bool first_cw = false, prev_cw = false;
-  auto end = [&](int s, bool cw, double vx, double vy) {
-    const double nr = pr * h[s] - pim * w[s];
-    const double ni = pr * w[s] + pim * h[s];
-    turns += (pim < 0.0) & (ni >= 0.0);
-    pr = nr;
-    pim = ni;
-    ksum += cw ? s : -s;
-    if (n == 0) {
-      first_cw = cw;
-      fx = vx;
-      fy = vy;
-    } else {  // arc previous -> this end: inside iff it ends at a clockwise end
-      bad |= (cw == prev_cw) | (rect_probe_chord(cx, cy, d, qx, qy, vx, vy, R) != (int)cw);
-    }
-    qx = vx;
-    qy = vy;
-    prev_cw = cw;
-    ++n;
-  };
-  // crossing vectors: side s's (h, -+w) turned by phi_s
+  // crossing ends: slot 2s = side s's clockwise end (dropped when corner s-1
+  // is inside), slot 2s+1 its counter-clockwise end (dropped when corner s is)
+  unsigned E = 0;
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     if (!((acc >> s) & 1u)) continue;
-    const double hs = h[s], ws = w[s];
-    if (!((cin >> ((s + 3) & 3)) & 1u)) {  // clockwise end, by corner (s-1, s)
-      if (s == 0) end(0, true, hs, -ws);
-      if (s == 1) end(1, true, ws, hs);
-      if (s == 2) end(2, true, -hs, ws);
-      if (s == 3) end(3, true, -ws, -hs);
-    }
-    if (!((cin >> s) & 1u)) {  // counter-clockwise end, by corner (s, s+1)
-      if (s == 0) end(0, false, hs, ws);
-      if (s == 1) end(1, false, -ws, hs);
-      if (s == 2) end(2, false, -hs, -ws);
-      if (s == 3) end(3, false, ws, -hs);
-    }
+    E |= (((cin >> ((s + 3) & 3)) & 1u) ^ 1u) << (2 * s);
+    E |= (((cin >> s) & 1u) ^ 1u) << (2 * s + 1);
   }
-  if (n == 0) return 1.0;
-  bad |= (first_cw == prev_cw) | (rect_probe_chord(cx, cy, d, qx, qy, fx, fy, R) != (int)first_cw);
+  if (E == 0) return 1.0;
+  if (__popc(E) & 1) return -1.0;  // cannot happen (ends alternate); defensive
+  // theta sum = argument of prod_s (h_s + i w_s)^{c_s}, c_s = ends of side s;
+  // each factor adds c_s * theta_s < pi, so whole turns show as the imaginary
+  // part turning non-negative again
+  double pr = 1.0, pim = 0.0;
+  int turns = 0, ksum = 0;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const unsigned cw = (E >> (2 * s)) & 1u, ccw = (E >> (2 * s + 1)) & 1u;
+    ksum += s * ((int)cw - (int)ccw);
+    if (!(cw | ccw)) continue;
+    double zr = h[s], zi = w[s];
+    if (cw & ccw) {  // (h + i w)^2
+      zr = (h[s] - w[s]) * (h[s] + w[s]);
+      zi = 2.0 * h[s] * w[s];
+    }
+    const double nr = pr * zr - pim * zi;
+    const double ni = pr * zi + pim * zr;
+    turns += (pim < 0.0) & (ni >= 0.0);
+    pr = nr;
+    pim = ni;
+  }
+  // probes, arc by arc in angular order (per-lane loop over the set slots):
+  // the arc from end i to the next end j is inside iff j is a clockwise end;
+  // a side's own outside arc (slots 2s -> 2s+1) needs no probe: its midpoint
+  // lies beyond side s by d - h_s > sw_margin, as in the single-side form
+  auto vec = [&](int k, double& vx, double& vy) {  // crossing vector of slot k
+    const int s = k >> 1;
+    const double hs = (s & 2) ? ((s & 1) ? h[3] : h[2]) : ((s & 1) ? h[1] : h[0]);
+    double ws = (s & 2) ? ((s & 1) ? w[3] : w[2]) : ((s & 1) ? w[1] : w[0]);
+    if (!(k & 1)) ws = -ws;  // (h, -w) clockwise, (h, w) counter-clockwise, turned by phi_s
+    const double x = (s & 1) ? -ws : hs, y = (s & 1) ? hs : ws;
+    vx = (s & 2) ? -x : x;
+    vy = (s & 2) ? -y : y;
+  };
+  const int i0 = __ffs(E) - 1;
+  const bool first_cw = !(i0 & 1);
+  double x0, y0;
+  vec(i0, x0, y0);
+  double xi = x0, yi = y0;
+  int i = i0;
+  unsigned rem = E & (E - 1);
+  int bad = 0;
+  for (;;) {
+    const bool last = rem == 0;
+    const int j = last ? i0 : __ffs(rem) - 1;
+    double xj = x0, yj = y0;
+    if (!last) vec(j, xj, yj);
+    if ((i & 1) || j != i + 1)
+      bad |= rect_probe_chord(cx, cy, d, xi, yi, xj, yj, R) != (int)!(j & 1);
+    if (last) break;
+    i = j;
+    xi = xj;
+    yi = yj;
+    rem &= rem - 1;
+  }
   if (bad) return -1.0;
   const double kHalfPi = 1.57079632679489661923;
   double a = fast_atan2(pim, pr);
@@ -815,7 +839,7 @@ __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, d
   // large coordinate offsets); a small omega would turn that into a large
   // relative difference, so small results come from the general routine,
   // which reproduces those crossing points
-  const double wt = span / kTwoPi;
+  const double wt = span * 0.15915494309189533577;  // / (2 pi)
   return wt >= 1e-3 ? wt : -1.0;
 }
 
@@ -867,6 +891,13 @@ __device__ __forceinline__ double safe_q(double cx, double cy, const RegionView&
 // an ulp: omega = 1 + 2^-52 happens), so 1/w >= 1/2 and its ulp is >= 2^-53:
 // the conversion is exact, and terms just below 1 give small negative values.
 __device__ __forceinline__ void fixed_term_minus_one(double term, uint64_t* lo, uint64_t* hi) {
+  const uint64_t one = 1ULL << kFixedFracBits;
+  if (term < 2048.0) {  // term * 2^53 is an integer below 2^64: one exact conversion
+    const uint64_t v = __double2ull_rn(term * 0x1p53);
+    *lo = v - one;
+    *hi = (v < one) ? ~0ULL : 0ULL;
+    return;
+  }
   const uint64_t bits = __double_as_longlong(term);
   const int e = int((bits >> 52) & 0x7FF) - 1023;            // term = 1.m * 2^e, e >= -1
   const uint64_t mant = (bits & 0xFFFFFFFFFFFFFULL) | (1ULL << 52);
@@ -886,7 +917,6 @@ __device__ __forceinline__ void fixed_term_minus_one(double term, uint64_t* lo, 
     h = mant << (sh - 64);
   }
   // subtract 1.0 == 2^53 (borrows into hi: negative results wrap to two's complement)
-  const uint64_t one = 1ULL << kFixedFracBits;
   h -= (l < one) ? 1ULL : 0ULL;
   l -= one;
   *lo = l;
