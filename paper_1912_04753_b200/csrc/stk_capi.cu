@@ -608,10 +608,16 @@ void generate(stk_ctx* c, const Batch& B, Source src, int p_first, int count, ui
     const uint64_t ntl = (uint64_t)(c->p1 - c->p0) + 1;  // uniform_int(p0, p1)
     const uint64_t limit = ~0ULL - (~0ULL % ntl);
     const RegionView rv = region_view(c);
-    if (c->fast_rect)
-      csr_fast_kernel<<<count, 320, 0, c->stream>>>(B, p_first, seed0, rv, ntl, limit);
-    else
+    if (c->fast_rect) {
+      csr_gen_kernel<<<count, 320, 0, c->stream>>>(B, p_first, seed0, rv.xmin, rv.xmax, rv.ymin,
+                                                   rv.ymax);
+      CK(cudaGetLastError());
+      ++c->launches;
+      const dim3 gf((unsigned)((n + 255) / 256), (unsigned)count);
+      csr_finish_kernel<<<gf, 256, 0, c->stream>>>(B, p_first, rv, ntl, ~0ULL / ntl, limit);
+    } else {
       csr_poly_kernel<<<count, 320, 0, c->stream>>>(B, p_first, seed0, rv, ntl, limit);
+    }
     CK(cudaGetLastError());
     ++c->launches;
     // patterns a parallel kernel flagged (probability ~0): sequential, exact

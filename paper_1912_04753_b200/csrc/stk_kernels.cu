@@ -1,6 +1,6 @@
 // stk_kernels.cu — sm_100a kernels of the space-time K pair path.
 //
-//   K4  csr_fast_kernel / csr_seq_kernel / bootstrap_kernel / permutation_kernel
+//   K4  csr_gen_kernel + csr_finish_kernel / csr_poly_kernel / csr_seq_kernel / bootstrap_kernel / permutation_kernel
 //       device MT19937-64 point generators, bit-identical to
 //       sim::generate_cstr / generate_bootstrap / generate_permutation
 //       (proj/core/src/simulation.cpp:10-53, proj/core/include/stripley/rng.hpp:10-40)
@@ -69,42 +69,73 @@ __device__ __forceinline__ void mt_twist_smem(uint64_t* st) {
   __syncthreads();
 }
 
-// CSR fast path: point k consumes outputs 3k, 3k+1, 3k+2 (uniform x, uniform y,
-// uniform_int t) unless the bbox draw falls outside the polygon or below()
-// rejects; any such event flags the pattern for the exact sequential kernel.
-// 312 = 3 * 104, so each twist block yields exactly 104 points.
-__global__ void __launch_bounds__(320) csr_fast_kernel(Batch B, int p_first, uint64_t seed0,
-                                                        RegionView reg, uint64_t ntl,
-                                                        uint64_t limit) {
+// CSR fast path (axis-aligned rectangle: every bounding-box draw is a
+// candidate point), in two kernels.  Point k consumes MT outputs 3k, 3k+1,
+// 3k+2 (uniform x, uniform y, uniform_int t); 312 = 3 * 104, so each twist
+// yields exactly 104 points.
+//
+// csr_gen_kernel: one CTA of 312 threads per pattern runs the recurrence
+// (thread i owns state word i): seeding, then one twist of the 312-word state
+// per 104 points, in three barrier-separated phases — every y from the old
+// state (while tempering and storing the previous twist's outputs: x and y
+// as points, the t output raw), words 0..155, words 156..311.  The twist is
+// the only serial part of the generator, so nothing else runs on its critical
+// path: the t reduction and the checks are done by csr_finish_kernel over the
+// whole batch in parallel.
+__global__ void __launch_bounds__(320) csr_gen_kernel(Batch B, int p_first, uint64_t seed0,
+                                                      double xmin, double xmax, double ymin,
+                                                      double ymax) {
   __shared__ uint64_t st[312];
-  __shared__ uint64_t out[312];
-  __shared__ int s_flag;
-  const int p = p_first + blockIdx.x;
-  const uint64_t seed = seed0 + (uint64_t)blockIdx.x;
-  if (threadIdx.x == 0) s_flag = 0;
-  mt_seed_smem(st, seed);
+  const int i = threadIdx.x;
+  mt_seed_smem(st, seed0 + (uint64_t)blockIdx.x);
   const uint64_t n = B.n;
-  double* X = B.x + (uint64_t)p * n;
-  double* Y = B.y + (uint64_t)p * n;
-  int64_t* T = B.t + (uint64_t)p * n;
-  for (uint64_t base = 0; base < n; base += 104) {
-    mt_twist_smem(st);
-    if (threadIdx.x < 312) out[threadIdx.x] = mt_temper(st[threadIdx.x]);
-    __syncthreads();
-    const uint64_t k = base + threadIdx.x;
-    if (threadIdx.x < 104 && k < n) {
-      const uint64_t vx = out[3 * threadIdx.x], vy = out[3 * threadIdx.x + 1],
-                     vt = out[3 * threadIdx.x + 2];
-      const double cx = mt_uniform(vx, reg.xmin, reg.xmax);
-      const double cy = mt_uniform(vy, reg.ymin, reg.ymax);
-      if (!point_in_polygon(cx, cy, reg.ring, reg.nv) || vt >= limit) s_flag = 1;
-      X[k] = cx;
-      Y[k] = cy;
-      T[k] = reg.p0 + (int64_t)(vt % ntl);
+  const uint64_t pb = (uint64_t)(p_first + blockIdx.x) * n;
+  double* X = B.x + pb;
+  double* Y = B.y + pb;
+  uint64_t* T = reinterpret_cast<uint64_t*>(B.t + pb);
+  const uint32_t kk = (uint32_t)i / 3u, comp = (uint32_t)i % 3u;  // point i / 3, component i % 3
+  const double lo = comp == 0 ? xmin : ymin, hi = comp == 0 ? xmax : ymax;
+  double* const XY = comp == 0 ? X : Y;
+  const uint64_t ntw = (n + 103) / 104;
+  for (uint64_t tw = 0;; ++tw) {
+    uint64_t y = 0;
+    if (i < 312) {
+      if (tw > 0) {  // outputs of twist tw - 1
+        const uint64_t k = (tw - 1) * 104 + kk;
+        if (k < n) {
+          const uint64_t v = mt_temper(st[i]);
+          if (comp < 2) XY[k] = mt_uniform(v, lo, hi);
+          else T[k] = v;
+        }
+      }
+      if (i < 311) y = (st[i] & kMtUpper) | (st[i + 1] & kMtLower);
     }
+    if (tw == ntw) break;
+    __syncthreads();
+    if (i < 156) st[i] = st[i + 156] ^ mt_mag(y);
+    __syncthreads();
+    if (i >= 156 && i < 311) st[i] = st[i - 156] ^ mt_mag(y);
+    else if (i == 311) st[311] = st[155] ^ mt_mag((st[311] & kMtUpper) | (st[0] & kMtLower));
     __syncthreads();
   }
-  if (threadIdx.x == 0 && s_flag) B.flags[p] = 1;
+}
+
+// uniform_int(p0, p1) from the raw output (v % ntl by a 64-bit reciprocal m =
+// floor((2^64 - 1) / ntl): the quotient estimate is short by at most one) and
+// the fast path's preconditions: the draw inside the region and below()'s
+// rejection not triggered, else the pattern goes to the sequential kernel.
+__global__ void csr_finish_kernel(Batch B, int p_first, RegionView reg, uint64_t ntl,
+                                  uint64_t m_recip, uint64_t limit) {
+  const int p = p_first + blockIdx.y;
+  const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (k >= B.n) return;
+  const uint64_t o = (uint64_t)p * B.n + k;
+  const uint64_t vt = (uint64_t)B.t[o];
+  const uint64_t q = __umul64hi(vt, m_recip);
+  uint64_t r = vt - q * ntl;
+  if (r >= ntl) r -= ntl;
+  B.t[o] = reg.p0 + (int64_t)r;
+  if (vt >= limit || !point_in_polygon(B.x[o], B.y[o], reg.ring, reg.nv)) B.flags[p] = 1;
 }
 
 // CSR for general polygons (rejection sampling; simulation.cpp:10-24).  A

@@ -18,8 +18,10 @@ struct PairArgs {
 
 __global__ void validate_kernel(const double* x, const double* y, const int64_t* t, uint64_t n,
                                 RegionView reg, unsigned long long* bad);
-__global__ void csr_fast_kernel(Batch B, int p_first, uint64_t seed0, RegionView reg,
-                                uint64_t ntl, uint64_t limit);
+__global__ void csr_gen_kernel(Batch B, int p_first, uint64_t seed0, double xmin, double xmax,
+                               double ymin, double ymax);
+__global__ void csr_finish_kernel(Batch B, int p_first, RegionView reg, uint64_t ntl,
+                                  uint64_t m_recip, uint64_t limit);
 __global__ void csr_poly_kernel(Batch B, int p_first, uint64_t seed0, RegionView reg,
                                 uint64_t ntl, uint64_t limit);
 __global__ void csr_seq_kernel(Batch B, int p_first, int count, uint64_t seed0, RegionView reg,
