@@ -609,7 +609,7 @@ void generate(stk_ctx* c, const Batch& B, Source src, int p_first, int count, ui
     const uint64_t limit = ~0ULL - (~0ULL % ntl);
     const RegionView rv = region_view(c);
     if (c->fast_rect) {
-      csr_gen_kernel<<<count, 320, 0, c->stream>>>(B, p_first, seed0, rv.xmin, rv.xmax, rv.ymin,
+      csr_gen_kernel<<<count, kGenThreads, 0, c->stream>>>(B, p_first, seed0, rv.xmin, rv.xmax, rv.ymin,
                                                    rv.ymax);
       CK(cudaGetLastError());
       ++c->launches;

@@ -74,49 +74,74 @@ __device__ __forceinline__ void mt_twist_smem(uint64_t* st) {
 // 3k+2 (uniform x, uniform y, uniform_int t); 312 = 3 * 104, so each twist
 // yields exactly 104 points.
 //
-// csr_gen_kernel: one CTA of 312 threads per pattern runs the recurrence
-// (thread i owns state word i): seeding, then one twist of the 312-word state
-// per 104 points, in three barrier-separated phases — every y from the old
-// state (while tempering and storing the previous twist's outputs: x and y
-// as points, the t output raw), words 0..155, words 156..311.  The twist is
-// the only serial part of the generator, so nothing else runs on its critical
-// path: the t reduction and the checks are done by csr_finish_kernel over the
-// whole batch in parallel.
-__global__ void __launch_bounds__(320) csr_gen_kernel(Batch B, int p_first, uint64_t seed0,
-                                                      double xmin, double xmax, double ymin,
-                                                      double ymax) {
-  __shared__ uint64_t st[312];
+// csr_gen_kernel: one CTA per pattern runs the recurrence x[k+312] =
+// x[k+156] ^ mag((x[k] & U) | (x[k+1] & L)).  Twist warps (threads 0..159):
+// thread i < 156 owns state words i and i+156 in registers — new word i needs
+// old words i, i+1, i+156; new word i+156 needs new word i (its own) and old
+// words i+156, i+157 — so a twist is two neighbour loads, the arithmetic and
+// one barrier, the state being published to a double-buffered shared copy
+// (thread 155's second word needs new word 0, which it recomputes from old
+// words 0, 1, 156).  Temper warps (threads 160..471, one word each) temper and
+// store the previously published state during the next twist: x and y as
+// points, the t output raw.  The twist is the only serial part of the
+// generator and carries nothing else; the t reduction and the checks are done
+// by csr_finish_kernel over the whole batch in parallel.
+__global__ void __launch_bounds__(kGenThreads) csr_gen_kernel(Batch B, int p_first, uint64_t seed0,
+                                                              double xmin, double xmax,
+                                                              double ymin, double ymax) {
+  __shared__ uint64_t buf[2][312];
   const int i = threadIdx.x;
-  mt_seed_smem(st, seed0 + (uint64_t)blockIdx.x);
+  if (i == 0) {  // mersenne_twister_engine::seed
+    uint64_t v = seed0 + (uint64_t)blockIdx.x;
+    buf[0][0] = v;
+    for (int k = 1; k < 312; ++k) {
+      v = 6364136223846793005ULL * (v ^ (v >> 62)) + (uint64_t)k;
+      buf[0][k] = v;
+    }
+  }
+  __syncthreads();
   const uint64_t n = B.n;
-  const uint64_t pb = (uint64_t)(p_first + blockIdx.x) * n;
-  double* X = B.x + pb;
-  double* Y = B.y + pb;
-  uint64_t* T = reinterpret_cast<uint64_t*>(B.t + pb);
-  const uint32_t kk = (uint32_t)i / 3u, comp = (uint32_t)i % 3u;  // point i / 3, component i % 3
-  const double lo = comp == 0 ? xmin : ymin, hi = comp == 0 ? xmax : ymax;
-  double* const XY = comp == 0 ? X : Y;
   const uint64_t ntw = (n + 103) / 104;
-  for (uint64_t tw = 0;; ++tw) {
-    uint64_t y = 0;
-    if (i < 312) {
-      if (tw > 0) {  // outputs of twist tw - 1
+  if (i < 160) {  // twist warps (threads 156..159 only keep the barrier count)
+    const bool own = i < 156;
+    const int w = own ? i : 155;
+    uint64_t a = buf[0][w], c = buf[0][w + 156];
+    for (uint64_t tw = 0; tw <= ntw; ++tw) {
+      if (tw < ntw) {
+        const uint64_t* cur = buf[tw & 1];
+        uint64_t* nxt = buf[(tw + 1) & 1];
+        const uint64_t b = cur[w + 1];
+        const uint64_t e =  // old word w + 157; for w == 155 new word 0 (x[312])
+            (w < 155) ? cur[w + 157]
+                      : (cur[156] ^ mt_mag((cur[0] & kMtUpper) | (cur[1] & kMtLower)));
+        a = c ^ mt_mag((a & kMtUpper) | (b & kMtLower));
+        c = a ^ mt_mag((c & kMtUpper) | (e & kMtLower));
+        if (own) {
+          nxt[w] = a;
+          nxt[w + 156] = c;
+        }
+      }
+      __syncthreads();
+    }
+  } else {  // temper warps: word wt of the state published by twist tw - 1
+    const int wt = i - 160;
+    const bool own = wt < 312;
+    const uint32_t kk = (uint32_t)wt / 3u, comp = (uint32_t)wt % 3u;
+    const uint64_t pb = (uint64_t)(p_first + blockIdx.x) * n;
+    double* const XY = (comp == 0 ? B.x : B.y) + pb;
+    const double lo = comp == 0 ? xmin : ymin, hi = comp == 0 ? xmax : ymax;
+    uint64_t* const T = reinterpret_cast<uint64_t*>(B.t + pb);
+    for (uint64_t tw = 0; tw <= ntw; ++tw) {
+      if (own && tw > 0) {
         const uint64_t k = (tw - 1) * 104 + kk;
         if (k < n) {
-          const uint64_t v = mt_temper(st[i]);
+          const uint64_t v = mt_temper(buf[tw & 1][wt]);
           if (comp < 2) XY[k] = mt_uniform(v, lo, hi);
           else T[k] = v;
         }
       }
-      if (i < 311) y = (st[i] & kMtUpper) | (st[i + 1] & kMtLower);
+      __syncthreads();
     }
-    if (tw == ntw) break;
-    __syncthreads();
-    if (i < 156) st[i] = st[i + 156] ^ mt_mag(y);
-    __syncthreads();
-    if (i >= 156 && i < 311) st[i] = st[i - 156] ^ mt_mag(y);
-    else if (i == 311) st[311] = st[155] ^ mt_mag((st[311] & kMtUpper) | (st[0] & kMtLower));
-    __syncthreads();
   }
 }
 

@@ -18,6 +18,7 @@ struct PairArgs {
 
 __global__ void validate_kernel(const double* x, const double* y, const int64_t* t, uint64_t n,
                                 RegionView reg, unsigned long long* bad);
+constexpr int kGenThreads = 160 + 320;  // csr_gen_kernel: twist warps + temper warps
 __global__ void csr_gen_kernel(Batch B, int p_first, uint64_t seed0, double xmin, double xmax,
                                double ymin, double ymax);
 __global__ void csr_finish_kernel(Batch B, int p_first, RegionView reg, uint64_t ntl,

@@ -37,6 +37,13 @@ def test_device_mt_csr_matches_reference_stream(api, port):
         pts = sim.generate_cstr(n, region, seed)
         x, y, t = port.generate_cstr(n, ring, 0, 31_536_000, seed)
         assert np.array_equal(pts.x, x) and np.array_equal(pts.y, y) and np.array_equal(pts.t, t)
+    # t = p0 + v mod (p1 - p0 + 1) by a 64-bit reciprocal: two values, a power of
+    # two, a period wider than 32 bits, an odd size near 2^62
+    for p0, p1 in [(5, 6), (0, 1023), (-7, 2**40), (-(2**61), 2**61 + 12345)]:
+        region_p = geom.StudyRegion(ring, p0, p1)
+        pts = sim.generate_cstr(3_001, region_p, 11)
+        x, y, t = port.generate_cstr(3_001, ring, p0, p1, 11)
+        assert np.array_equal(pts.x, x) and np.array_equal(pts.t, t), (p0, p1)
     g = golden("c1.npz")
     pts = sim.generate_cstr(10_000, region, 1)
     assert np.array_equal(pts.x[:16], g["x_head"]) and np.array_equal(pts.t[:16], g["t_head"])
