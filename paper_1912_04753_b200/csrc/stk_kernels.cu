@@ -987,6 +987,21 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           continue;
         }
         if (done) break;
+        if (qh != 0) {
+          // fewer than 32 entries pending: move them to the ring's front so
+          // the ring's working set stays its first ~2 KB (L1/L2-resident)
+          // instead of cycling all kArcRing entries through DRAM.  qh is a
+          // multiple of 32 > pending, so source and destination are disjoint
+          const uint32_t pend = qt - qh;
+          uint4 e = make_uint4(0, 0, 0, 0);
+          if ((uint32_t)lane < pend) e = arcq[qh + lane];
+          __syncwarp();
+          if ((uint32_t)lane < pend) arcq[lane] = e;
+          __syncwarp();
+          if (lane == 0) tot_exact += qh;
+          qh = 0;
+          qt = pend;
+        }
         // this lane's neighbour, (re)loaded for every chunk (an L1 hit after the
         // first): nothing of the tile stays live across the drain site above,
         // whose register peak would otherwise push it to local memory
@@ -1129,6 +1144,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       }
       __syncwarp();
       if (lane == 0) tot_exact += qt;  // every ring entry is one exact-path ordered pair
+                                       // (earlier entries counted at compaction)
       tot_arc += n_arc;
       if (lane == 0) tot_cand += n_cand;
     }

@@ -1,0 +1,37 @@
+#!/bin/bash
+# One GPU-box session: parity tests, the default bench line, the other configs,
+# the ncu launch list and one full capture of the pair kernel.
+#   gpurun --timeout 2400 -- 'bash tools/gpu_round.sh [tag] [stages]'
+# stages: any of t (tests) b (bench C2) c (other configs) l (launch list) f (ncu full)
+tag=${1:-r1}
+stages=${2:-tbclf}
+out=gpurun_out
+mkdir -p $out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $out/gpu_$tag.txt 2>&1
+if [[ $stages == *t* ]]; then
+  timeout 900 python -m pytest tests -m gpu -x -q > $out/pytest_gpu_$tag.log 2>&1
+  echo "pytest rc=$?" >> $out/pytest_gpu_$tag.log
+fi
+if [[ $stages == *b* ]]; then
+  timeout 400 python bench.py > $out/bench_$tag.json 2> $out/bench_$tag.err
+  echo "bench rc=$?" >> $out/bench_$tag.err
+  timeout 400 python bench.py --impl reference --steps 2 --warmup 0 > $out/bench_ref_$tag.json 2> $out/bench_ref_$tag.err
+fi
+if [[ $stages == *c* ]]; then
+  for c in C1 C3 C4; do
+    timeout 400 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $out/bench_${c}_$tag.json 2> $out/bench_${c}_$tag.err
+  done
+  timeout 600 python bench.py --config C5 --sims 1 --steps 2 --warmup 3 --no-cpu-baseline > $out/bench_C5_$tag.json 2> $out/bench_C5_$tag.err
+fi
+if [[ $stages == *l* ]]; then
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $out/launches_$tag.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
+    > $out/ncu_launch_$tag.log 2>&1
+fi
+if [[ $stages == *f* ]]; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:pair_kernel -s 3 -c 1 \
+    -o $out/pair_kernel_$tag -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+    > $out/ncu_full_$tag.log 2>&1
+  echo "ncu rc=$?" >> $out/ncu_full_$tag.log
+fi
+echo done
