@@ -100,6 +100,7 @@ struct stk_ctx {
   std::string err;
   int num_sms = 148;
   uint64_t mem_budget = 16ull << 30;
+  int time_mul = 1;        // time cells per space-cell refinement (STK_TIME_MUL env overrides)
   int stencil_radius = 2;  // preferred cell refinement (STK_STENCIL_RADIUS env overrides)
 
   // region (geom::StudyRegion)
@@ -449,7 +450,10 @@ GridGeom make_grid_geom(stk_ctx* c, uint64_t n) {
     // implies it up to 1e-16) spans at most R cells even after FP rounding of
     // the cell index; integer time cells of width ceil(t_max / R) are exact.
     double w = smax * (1.0 + 1e-6) / R;
-    int64_t tw = std::max<int64_t>((tmax + R - 1) / R, 1);
+    // time cells may be finer than space cells (RT = R * time_mul rows of
+    // layers); the density test below uses the R-cell population
+    const int RT = std::max(1, std::min(R * c->time_mul, (32 - (R + 1)) / (2 * R + 1)));
+    int64_t tw = std::max<int64_t>((tmax + RT - 1) / RT, 1);
     int64_t nx, ny, nt;
     for (;;) {
       nx = ncell(ex, w);
@@ -458,7 +462,7 @@ GridGeom make_grid_geom(stk_ctx* c, uint64_t n) {
       if ((double)nx * (double)ny * (double)nt <= (double)cap) break;
       if (nx * ny >= nt) w *= 1.5; else tw = tw + tw / 2 + 1;
     }
-    const double per_cell = (double)n / ((double)nx * ny * nt);
+    const double per_cell = (double)n / ((double)nx * ny * nt) * (double)RT / R;
     if (R > 1 && per_cell < 8.0) continue;  // too sparse for finer cells
     g.x0 = c->xmin;
     g.y0 = c->ymin;
@@ -471,7 +475,7 @@ GridGeom make_grid_geom(stk_ctx* c, uint64_t n) {
     g.nt = (int32_t)nt;
     g.cells = (uint32_t)(nx * ny * nt);
     g.rs = R;
-    g.rt = R;
+    g.rt = RT;
     break;
   }
   return g;
@@ -953,6 +957,7 @@ int stk_create(stk_ctx** out, int device) {
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* r = std::getenv("STK_STENCIL_RADIUS")) c->stencil_radius = std::max(1, std::min(3, std::atoi(r)));
+    if (const char* r = std::getenv("STK_TIME_MUL")) c->time_mul = std::max(1, std::min(4, std::atoi(r)));
     c->stats.ensure(8);
   } catch (const std::exception& e) {
     delete c;
