@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--cpu-sample-frac", type=float, default=1.0,
                     help="CPU reference sample: every (1/frac)-th observed point (pairs/s is "
                          "per pair, so a subsample keeps the metric comparable)")
+    ap.add_argument("--n", type=int, default=0,
+                    help="profiling only: replace the config's N (the line then names the "
+                         "reduced N; not a headline measurement)")
     ap.add_argument("--ring", type=int, default=0,
                     help="replace the square by a regular polygon of this many vertices "
                          "(acceptance criterion 6 shape)")
@@ -114,10 +117,14 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def workload(cfg_name, sims_override=None, ring_vertices=0):
+def workload(cfg_name, sims_override=None, ring_vertices=0, n_override=0):
+    import dataclasses
+
     from paper_1912_04753_b200 import configs
 
     cfg = configs.CONFIGS[cfg_name]
+    if n_override:
+        cfg = dataclasses.replace(cfg, n=int(n_override))
     if ring_vertices:
         cfg = cfg.with_ring(ring_vertices)
     s, tv = configs.grid_values(cfg)
@@ -161,7 +168,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    cfg, s, tv, sims = workload(args.config, args.sims, args.ring)
+    cfg, s, tv, sims = workload(args.config, args.sims, args.ring, args.n)
     import oracle
 
     x, y, t = subsample(*observed_points_cpu(cfg), args.cpu_sample_frac)
@@ -246,7 +253,7 @@ def run_ours(args):
         group = dist.group.WORLD
     dev = devmod.get(local)
     lib = dev.lib
-    cfg, s, tv, sims = workload(args.config, args.sims, args.ring)
+    cfg, s, tv, sims = workload(args.config, args.sims, args.ring, args.n)
     region = geom.StudyRegion(cfg.ring(), 0, cfg.period_s)
     grid = est.DistanceGrid(s, tv)
     dev.configure(region, grid)

@@ -100,7 +100,8 @@ struct stk_ctx {
   std::string err;
   int num_sms = 148;
   uint64_t mem_budget = 16ull << 30;
-  int time_mul = 1;        // time cells per space-cell refinement (STK_TIME_MUL env overrides)
+  int time_radius = 0;     // time layers of the stencil, 0 = the spatial radius (STK_TIME_RADIUS env)
+  double min_cell_pop = 8.0;  // finer cells only when this populous (STK_MIN_CELL_POP env)
   int stencil_radius = 2;  // preferred cell refinement (STK_STENCIL_RADIUS env overrides)
 
   // region (geom::StudyRegion)
@@ -450,9 +451,11 @@ GridGeom make_grid_geom(stk_ctx* c, uint64_t n) {
     // implies it up to 1e-16) spans at most R cells even after FP rounding of
     // the cell index; integer time cells of width ceil(t_max / R) are exact.
     double w = smax * (1.0 + 1e-6) / R;
-    // time cells may be finer than space cells (RT = R * time_mul rows of
-    // layers); the density test below uses the R-cell population
-    const int RT = std::max(1, std::min(R * c->time_mul, (32 - (R + 1)) / (2 * R + 1)));
+    // time cells may be finer or coarser than space cells (RT layers; the
+    // half-stencil's (R + 1) + RT (2R + 1) rows must fit a warp); the density
+    // test below uses the population of cells with R time layers
+    const int RT = std::max(1, std::min(c->time_radius > 0 ? c->time_radius : R,
+                                        (32 - (R + 1)) / (2 * R + 1)));
     int64_t tw = std::max<int64_t>((tmax + RT - 1) / RT, 1);
     int64_t nx, ny, nt;
     for (;;) {
@@ -463,7 +466,7 @@ GridGeom make_grid_geom(stk_ctx* c, uint64_t n) {
       if (nx * ny >= nt) w *= 1.5; else tw = tw + tw / 2 + 1;
     }
     const double per_cell = (double)n / ((double)nx * ny * nt) * (double)RT / R;
-    if (R > 1 && per_cell < 8.0) continue;  // too sparse for finer cells
+    if (R > 1 && per_cell < c->min_cell_pop) continue;  // too sparse for finer cells
     g.x0 = c->xmin;
     g.y0 = c->ymin;
     g.inv_w = 1.0 / w;
@@ -956,8 +959,9 @@ int stk_create(stk_ctx** out, int device) {
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
-    if (const char* r = std::getenv("STK_STENCIL_RADIUS")) c->stencil_radius = std::max(1, std::min(3, std::atoi(r)));
-    if (const char* r = std::getenv("STK_TIME_MUL")) c->time_mul = std::max(1, std::min(4, std::atoi(r)));
+    if (const char* r = std::getenv("STK_STENCIL_RADIUS")) c->stencil_radius = std::max(1, std::min(4, std::atoi(r)));
+    if (const char* r = std::getenv("STK_MIN_CELL_POP")) c->min_cell_pop = std::atof(r);
+    if (const char* r = std::getenv("STK_TIME_RADIUS")) c->time_radius = std::max(0, std::min(8, std::atoi(r)));
     c->stats.ensure(8);
   } catch (const std::exception& e) {
     delete c;

@@ -417,7 +417,7 @@ __device__ __forceinline__ int rect_probe_certified(double cx, double cy, double
 // deferred drain).  Kept with runtime R.rect tests: specialising them away
 // changes the pair kernel's register allocation for the worse (the hot loop
 // then reloads its neighbour from local memory).
-__device__ __forceinline__ double spatial_weight_buf_rect(double cx, double cy, double d,
+__device__ __noinline__ double spatial_weight_buf_rect(double cx, double cy, double d,
                                                        const RegionView& R, double* buf,
                                                        int stride, int cap) {
   if (d <= 0.0) return 1.0;

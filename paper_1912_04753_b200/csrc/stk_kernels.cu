@@ -759,7 +759,7 @@ __device__ __forceinline__ void drain_general(int count, int lane, const uint4* 
   if (RECT) {
     ws = rect_multi_edge_weight(c.x, c.y, d, reg);
     if (ws < 0.0 && reg.nv <= 32)
-      ws = spatial_weight_buf_rect(c.x, c.y, d, reg, angs + lane, 32, slots / 2);
+      ws = spatial_weight_buf_rect(c.x, c.y, d, *reg_g, angs + lane, 32, slots / 2);
   } else {
     ws = spatial_weight_buf<false>(c.x, c.y, d, reg, angs + lane, 32, slots / 2);
   }
@@ -781,9 +781,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   // loaded from shared memory cannot be rematerialised by the register
   // allocator (it otherwise rebuilds them from special registers every
   // iteration)
-  __shared__ uint32_t s_lane[kPairWarps * 32];
   __shared__ uint4* s_ring[kPairWarps];
-  __shared__ uint2 s_lim[kPairWarps * 32];  // per-chunk owner limits (see below)
+  __shared__ uint2 s_lim[kPairWarps * 32];  // per-tile owner limits (see below)
+  __shared__ uint32_t s_jp[kPairWarps * 32];  // per-tile neighbour position of each lane
   __shared__ uint32_t s_base;               // shared-space address of smem_raw
   using Lay = PairLayout<TT>;
   const Batch& B = A.B;
@@ -834,7 +834,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   uint32_t* cpos_w = S.cpos + w * 32;
   uint4* arcq = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * (kArcRing + kCplxRing);
   uint4* cring = arcq + kArcRing;
-  s_lane[tid] = (uint32_t)lane;
   if (tid == 0) s_base = (uint32_t)__cvta_generic_to_shared(smem_raw);
   if (lane == 0) s_ring[w] = arcq;
     const int single_step = BV.single_step;
@@ -930,40 +929,35 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           if (my_rb > my_re) my_rb = my_re;
         }
       }
-      unsigned nonempty = __ballot_sync(FULL_MASK, my_rb < my_re);
-      // part `part` of `parts` walks tiles [T*part/parts, T*(part+1)/parts) of
-      // the item's T neighbour tiles (rows in lane order)
-      uint32_t tiles_left = 0xffffffffu, skip_tiles = 0;
-      if (parts > 1) {
-        const uint32_t tr = (my_rb < my_re) ? (my_re - my_rb + 31u) / 32u : 0u;
-        uint32_t incl = tr;
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t v = __shfl_up_sync(FULL_MASK, incl, o);
-          if (lane >= o) incl += v;
-        }
-        const uint32_t T = __shfl_sync(FULL_MASK, incl, 31);
-        const uint32_t t_lo = (uint32_t)((uint64_t)T * part / parts);
-        const uint32_t t_hi = (uint32_t)((uint64_t)T * (part + 1) / parts);
-        tiles_left = t_hi - t_lo;
-        const unsigned past = __ballot_sync(FULL_MASK, incl <= t_lo);  // rows wholly before t_lo
-        nonempty = tiles_left ? (nonempty & ~past) : 0u;
-        if (nonempty) {  // the first row of the part starts skip_tiles tiles in
-          const int r0 = __ffs(nonempty) - 1;
-          skip_tiles = t_lo - __shfl_sync(FULL_MASK, incl - tr, r0);
-        }
+      // packed neighbour walk: the item's rows, concatenated in lane (row)
+      // order, form one virtual list [0, V) — row r covers [incl_r - len_r,
+      // incl_r) and virtual index v of it sits at sorted position v + rowoff_r
+      // — and a tile is 32 consecutive virtual indices, across row ends, so
+      // the lanes stay full except in the item's last tile
+      const uint32_t len = my_re - my_rb;
+      uint32_t incl = len;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(FULL_MASK, incl, o);
+        if (lane >= o) incl += v;
       }
+      const uint32_t rowoff = my_rb - (incl - len);
+      const uint32_t V = __shfl_sync(FULL_MASK, incl, 31);
+      // part `part` of `parts` walks virtual indices [V part / parts, V (part + 1) / parts)
+#ifdef STK_PART_ALIGN
+      uint32_t v0 = (uint32_t)((uint64_t)V * part / parts) & ~31u;
+      const uint32_t v_hi = part + 1 == parts ? V : (uint32_t)((uint64_t)V * (part + 1) / parts) & ~31u;
+#else
+      uint32_t v0 = (uint32_t)((uint64_t)V * part / parts);
+      const uint32_t v_hi = (uint32_t)((uint64_t)V * (part + 1) / parts);
+#endif
       uint32_t qh = 0, qt = 0;    // arc ring head / tail (monotone)
       uint32_t ch_ = 0, ct_ = 0;  // deferred ring head / tail
       uint32_t n_arc = 0;
       unsigned long long n_cand = 0;
-      // flat walk over (row, tile, center chunk); one inline copy of the drain
-      unsigned rows_left = nonempty;
-      int r = rows_left ? __ffs(rows_left) - 1 : 32;
-      uint32_t j0 = __shfl_sync(FULL_MASK, my_rb, r & 31) + skip_tiles * 32u;
-      uint32_t re = __shfl_sync(FULL_MASK, my_re, r & 31);
+      // flat walk over (tile, center chunk); one inline copy of the drain
       int kc = 0;
       for (;;) {
-        const bool done = rows_left == 0;
+        const bool done = v0 >= v_hi;
         // the single drain site, ahead of new candidates so the ring never
         // holds more than 31 + kArcChunk * 64 entries: full batches while
         // any are pending, and the remainder at the end
@@ -1002,23 +996,54 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           qh = 0;
           qt = pend;
         }
+        uint32_t jp;
+        if (kc == 0) {  // new tile: map the lanes to their rows (usually 1-2)
+          const uint32_t v = v0 + (uint32_t)lane;
+          unsigned m = __ballot_sync(FULL_MASK, len != 0 && incl > v0 && incl - len < v0 + 32u);
+          uint32_t off = 0, row0 = 0;
+          while (m) {
+            const int rr = __ffs(m) - 1;
+            m &= m - 1;
+            const uint32_t e = __shfl_sync(FULL_MASK, incl, rr);
+            const uint32_t st = e - __shfl_sync(FULL_MASK, len, rr);
+            const uint32_t o = __shfl_sync(FULL_MASK, rowoff, rr);
+            if (v >= st && v < e) {
+              off = o;
+              row0 = rr == 0;
+            }
+          }
+          jp = v < v_hi ? v + off : 0xffffffffu;
+          s_jp[tid] = jp;
+        } else {
+          jp = *reinterpret_cast<volatile uint32_t*>(&s_jp[tid]);
+        }
         // this lane's neighbour, (re)loaded for every chunk (an L1 hit after the
         // first): nothing of the tile stays live across the drain site above,
         // whose register peak would otherwise push it to local memory
-        const uint32_t jp = j0 + lane;
-        const bool has = jp < re;
+        const bool has = jp != 0xffffffffu;
         double2 nxy = make_double2(1e300, 1e300);  // no neighbour: q = inf > Qmax
         PtMeta<TT> nm{0, 0, 0.0f, 0u};
         if (has) {
           nxy = B.pxy[pb + jp];
           nm = pmeta_b[pb + jp];
         }
-        if (kc == 0) {  // new tile
-          if (jp + 32 < re) {  // next tile of this row into L1 while this one is processed
+        if (kc == 0) {
+          if (has && jp + 32 < (uint32_t)B.n) {  // the lane's likely next neighbour into L1
             asm volatile("prefetch.global.L1 [%0];" ::"l"(B.pxy + (pb + jp + 32)));
             asm volatile("prefetch.global.L1 [%0];" ::"l"(pmeta_b + (pb + jp + 32)));
           }
-          n_cand += (unsigned long long)min(32u, re - j0) * nc;
+          // own-cell rule: lower sorted position owns the pair — center k sits
+          // at first_pos + k, so "jp > its position" is "k < jp - first_pos";
+          // selected centers (shards) compare input indices instead:
+          // owner <=> k < lim.x || center idx < lim.y.  Kept in shared memory
+          // for the tile's chunks (with jp): the register allocator cannot
+          // rebuild them inside the candidate loop
+          const uint32_t row0_end = __shfl_sync(FULL_MASK, incl, 0);  // row 0 = [0, len_0)
+          const bool same_c = v0 + (uint32_t)lane < row0_end && jp < own_end;
+          s_lim[tid] = make_uint2(same_c ? (sel_p ? 0u : jp - first_pos) : 0xffffffffu,
+                                  (sel_p && same_c) ? nm.idx : 0u);
+          n_cand += (unsigned long long)min(32u, v_hi - v0) * nc;
+          __syncwarp();
         }
         const bool tile_deep =
             __all_sync(FULL_MASK, !has || ((double)nm.sq >= Qmax && nm.vt >= Tmax));
@@ -1035,22 +1060,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           uint32_t tidv;
           asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tidv));
           const uint32_t wo = (tidv >> 5) * 32;
-          const uint32_t lane_c = s_lane[tidv];
+          const uint32_t lane_c = tidv & 31u;
           uint4* const ring_c = s_ring[tidv >> 5];
           const unsigned lt_c = (1u << lane_c) - 1u;
           // straight from the __shared__ array: the shared address space stays
           // visible (no generic-to-shared window arithmetic per load)
           const uint32_t* cpos_c = reinterpret_cast<const uint32_t*>(smem_raw + Lay::cpos) + wo;
-          const uint32_t jpc = j0 + lane_c;  // == jp, held in a register
-          const bool same_c = r == 0 && jpc < own_end;
-          // own-cell rule: lower sorted position owns the pair — center k sits
-          // at first_pos + k, so "jp > its position" is "k < jp - first_pos";
-          // selected centers (shards) compare input indices instead.  Both
-          // limits go through a volatile shared round trip so the register
-          // allocator keeps them instead of rebuilding them per iteration:
-          // owner <=> k < lim.x || center idx < lim.y
-          s_lim[tidv] = make_uint2(same_c ? (sel_p ? 0u : jpc - first_pos) : 0xffffffffu,
-                                   (sel_p && same_c) ? nm.idx : 0u);
+          const uint32_t jpc = *reinterpret_cast<volatile uint32_t*>(&s_jp[tidv]);  // == jp
           const volatile uint32_t* lim_v = reinterpret_cast<volatile uint32_t*>(&s_lim[tidv]);
           const uint2 lim = make_uint2(lim_v[0], lim_v[1]);
           const uint32_t sbase = *reinterpret_cast<volatile uint32_t*>(&s_base);
@@ -1128,18 +1144,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         // all deep; else the weighted loop (own-cell ordering in both)
         if (tile_deep && item_deep) chunk(std::true_type{}, std::true_type{});
         else chunk(std::true_type{}, std::false_type{});
-        // advance: next chunk, next tile, next non-empty row
+        // advance: next chunk, next tile
         kc = kend;
         if (kc >= (int)nc) {
           kc = 0;
-          j0 += 32;
-          if (--tiles_left == 0) rows_left = 0;  // end of this item part
-          else if (j0 >= re) {
-            rows_left &= rows_left - 1;
-            r = rows_left ? __ffs(rows_left) - 1 : 32;
-            j0 = __shfl_sync(FULL_MASK, my_rb, r & 31);
-            re = __shfl_sync(FULL_MASK, my_re, r & 31);
-          }
+          v0 += 32;
         }
       }
       __syncwarp();
