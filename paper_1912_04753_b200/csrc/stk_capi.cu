@@ -701,7 +701,8 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   ++c->launches;
   const size_t smem = pair_kernel_smem(P.bins, B.wide);
   int per_sm = 0;
-  CK(pair_kernel_prepare(B.wide, c->fast_rect ? 1 : 0, smem, &per_sm));
+  const int mode = (c->fast_rect ? 1 : 0) | (c->single_step ? 2 : 0);
+  CK(pair_kernel_prepare(B.wide, mode, smem, &per_sm));
   if (per_sm < 1) throw Unsupported("distance grid too large for the pair kernel's shared histogram");
   tasks_kernel<<<1, 1, 0, c->stream>>>(B, G, (uint32_t)(c->num_sms * per_sm));
   CK(cudaGetLastError());
@@ -721,7 +722,7 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   // the bounded-storage fallback), global and L1-resident
   c->angs.ensure(ctas * kPairWarps * kAngleSlots * 32);
   A.angs_g = c->angs.p;
-  pair_kernel_launch(B.wide, c->fast_rect ? 1 : 0, (unsigned)ctas, smem, c->stream, A);
+  pair_kernel_launch(B.wide, mode, (unsigned)ctas, smem, c->stream, A);
   CK(cudaGetLastError());
   ++c->launches;
   CK(cudaEventRecord(e2, c->stream));

@@ -773,7 +773,10 @@ __device__ __forceinline__ void drain_general(int count, int lane, const uint4* 
 #ifndef STK_PAIR_MINB
 #define STK_PAIR_MINB 2
 #endif
-template <typename TT, bool RECT>
+// SINGLE: every bin-table bucket straddles at most one threshold (the host's
+// BinView::single_step), so one compare per axis finds the bin — a template
+// flag rather than a runtime test inside the candidate loops.
+template <typename TT, bool RECT, bool SINGLE>
 __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_task, s_next;
@@ -836,7 +839,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   uint4* cring = arcq + kArcRing;
   if (tid == 0) s_base = (uint32_t)__cvta_generic_to_shared(smem_raw);
   if (lane == 0) s_ring[w] = arcq;
-    const int single_step = BV.single_step;
   // crossing scratch of the general weight (deferred drains only): global,
   // L1-resident, element k of lane l at [k * 32 + l]
   double* angs = A.angs_g + ((uint64_t)blockIdx.x * kPairWarps + w) * (slots * 32);
@@ -1104,7 +1106,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               bt = min(bt, kBucketTable - 1);
               const TBucket<TT> te = lds_tbucket<TT>(a_t + (uint32_t)bt * (uint32_t)sizeof(TBucket<TT>));
               uint32_t tb = te.bin;
-              if (single_step) {
+              if constexpr (SINGLE) {
                 sb += q > qe.thr ? 1u : 0u;
                 tb += du > te.thr ? 1u : 0u;
               } else {
@@ -1191,31 +1193,31 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
 }
 
 // Host-side launch helpers (keep the kernel templates in this translation unit).
+// mode = rect | single_step << 1.
 template <typename TT>
-static const void* pair_fn2(int rect) {
-  return rect ? (const void*)pair_kernel<TT, true> : (const void*)pair_kernel<TT, false>;
+static const void* pair_fn2(int mode) {
+  switch (mode & 3) {
+    case 0: return (const void*)pair_kernel<TT, false, false>;
+    case 1: return (const void*)pair_kernel<TT, true, false>;
+    case 2: return (const void*)pair_kernel<TT, false, true>;
+    default: return (const void*)pair_kernel<TT, true, true>;
+  }
 }
-static const void* pair_fn(int wide, int rect) {
-  return wide ? pair_fn2<int64_t>(rect) : pair_fn2<int32_t>(rect);
+static const void* pair_fn(int wide, int mode) {
+  return wide ? pair_fn2<int64_t>(mode) : pair_fn2<int32_t>(mode);
 }
 
-cudaError_t pair_kernel_prepare(int wide, int rect, size_t smem, int* per_sm) {
-  const void* fn = pair_fn(wide, rect);
+cudaError_t pair_kernel_prepare(int wide, int mode, size_t smem, int* per_sm) {
+  const void* fn = pair_fn(wide, mode);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fn, kPairWarps * 32, smem);
 }
 
-template <typename TT>
-static void launch2(int rect, unsigned ctas, size_t smem, cudaStream_t stream, const PairArgs& A) {
-  if (rect) pair_kernel<TT, true><<<ctas, kPairWarps * 32, smem, stream>>>(A);
-  else pair_kernel<TT, false><<<ctas, kPairWarps * 32, smem, stream>>>(A);
-}
-
-void pair_kernel_launch(int wide, int rect, unsigned ctas, size_t smem, cudaStream_t stream,
+void pair_kernel_launch(int wide, int mode, unsigned ctas, size_t smem, cudaStream_t stream,
                         const PairArgs& A) {
-  if (wide) launch2<int64_t>(rect, ctas, smem, stream, A);
-  else launch2<int32_t>(rect, ctas, smem, stream, A);
+  void* args[] = {const_cast<PairArgs*>(&A)};
+  cudaLaunchKernel(pair_fn(wide, mode), dim3(ctas), dim3(kPairWarps * 32), args, smem, stream);
 }
 
 // ============================================================ K5 finalize

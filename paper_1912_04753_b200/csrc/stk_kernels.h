@@ -40,8 +40,9 @@ __global__ void select_scatter_kernel(Batch B, GridGeom G);
 __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first);
 __global__ void items_kernel(Batch B, GridGeom G, int p_first);
 __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas);
-cudaError_t pair_kernel_prepare(int wide, int rect, size_t smem, int* per_sm);
-void pair_kernel_launch(int wide, int rect, unsigned ctas, size_t smem, cudaStream_t stream,
+// mode = rect | single_step << 1 (kernel template flags)
+cudaError_t pair_kernel_prepare(int wide, int mode, size_t smem, int* per_sm);
+void pair_kernel_launch(int wide, int mode, unsigned ctas, size_t smem, cudaStream_t stream,
                         const PairArgs& A);
 __global__ void finalize_kernel(Batch B, uint32_t cs, uint32_t ct, const double* s_values,
                                 const int64_t* t_values, double area, int64_t duration,
