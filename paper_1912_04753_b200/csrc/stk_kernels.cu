@@ -835,10 +835,12 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   double2* cxy_w = S.cxy + w * 32;
   PtMeta<TT>* cm_w = S.cmeta + w * 32;
   uint32_t* cpos_w = S.cpos + w * 32;
-  uint4* arcq = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * (kArcRing + kCplxRing);
-  uint4* cring = arcq + kArcRing;
+  // the warp's rings (main, then deferred); drain sites read the base back
+  // from shared memory (one load) instead of rebuilding it from special
+  // registers and the kernel parameter
+  uint4* const arcq0 = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * (kArcRing + kCplxRing);
   if (tid == 0) s_base = (uint32_t)__cvta_generic_to_shared(smem_raw);
-  if (lane == 0) s_ring[w] = arcq;
+  if (lane == 0) s_ring[w] = arcq0;
   // crossing scratch of the general weight (deferred drains only): global,
   // L1-resident, element k of lane l at [k * 32 + l]
   double* angs = A.angs_g + ((uint64_t)blockIdx.x * kPairWarps + w) * (slots * 32);
@@ -968,6 +970,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         if (cpending >= 32 || (done && pending == 0 && cpending > 0)) {
           const int cnt_ = (int)min(cpending, 32u);
           __syncwarp();
+          const uint4* cring = *reinterpret_cast<uint4* volatile*>(&s_ring[w]) + kArcRing;
           drain_general<RECT>(cnt_, lane, cring, ch_, angs, slots, B.pxy + pb, S.arc, S.ch, A.reg, A.reg_g,
                               &overflow, &n_arc);
           ch_ += (uint32_t)cnt_;
@@ -978,7 +981,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           if (pending > (uint32_t)kArcRing) overflow |= 2;  // reported as an error
           const int cnt_ = (int)min(pending, 32u);
           __syncwarp();
-          drain_main<RECT>(cnt_, lane, arcq, qh, cring, &ct_, lanemask_lt, B.pxy + pb, S.arc, S.ch, A.reg, &n_arc);
+          uint4* const arcq = *reinterpret_cast<uint4* volatile*>(&s_ring[w]);
+          drain_main<RECT>(cnt_, lane, arcq, qh, arcq + kArcRing, &ct_, lanemask_lt, B.pxy + pb, S.arc, S.ch, A.reg, &n_arc);
           qh += (uint32_t)cnt_;
           continue;
         }
@@ -989,6 +993,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           // instead of cycling all kArcRing entries through DRAM.  qh is a
           // multiple of 32 > pending, so source and destination are disjoint
           const uint32_t pend = qt - qh;
+          uint4* const arcq = *reinterpret_cast<uint4* volatile*>(&s_ring[w]);
           uint4 e = make_uint4(0, 0, 0, 0);
           if ((uint32_t)lane < pend) e = arcq[qh + lane];
           __syncwarp();
@@ -1130,13 +1135,15 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
             const unsigned mj = __ballot_sync(FULL_MASK, arc_j);
             if (mi | mj) {
+              // no wrap: a chunk starts with < 32 entries (compaction) and adds
+              // <= kArcChunk * 64, below kArcRing (static_assert in stk_types.h)
               const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
               if (arc_i)
-                ring_c[(qt + __popc(mi & lt_c)) & (kArcRing - 1)] =
+                ring_c[qt + __popc(mi & lt_c)] =
                     make_uint4(cpos_c[k], bin | (half_i ? 0x80000000u : 0u), qlo, qhi);
               qt += __popc(mi);
               if (arc_j)
-                ring_c[(qt + __popc(mj & lt_c)) & (kArcRing - 1)] =
+                ring_c[qt + __popc(mj & lt_c)] =
                     make_uint4(jpc, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
               qt += __popc(mj);
             }
