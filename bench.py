@@ -404,7 +404,8 @@ def run_ours(args):
                 "realisations_per_s": patterns / (e2e_ms * 1e-3)},
         "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                      "unit": "FP64 Tinstr/s", "frac": achieved / peak if peak else None,
-                     "traffic": traffic_bytes(),
+                     "traffic": ncu_capture(cfg.name)[0],
+                     "hw": ncu_capture(cfg.name)[1],
                      "note": f"pair kernel: ({W_INT} x interior + {W_ARC} x arc (omega != 1) pairs) "
                              "FP64 instr / CUDA-event pair-kernel time; peak = live DFMA "
                              "microbenchmark (stk_measure_fp64_peak)",
@@ -424,14 +425,18 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def traffic_bytes():
-    """DRAM bytes (read + write) per pair-kernel launch from the committed ncu
-    capture of this workload (profiles/pair_kernel_traffic_r1.json), or None."""
+def ncu_capture(cfg_name):
+    """Per-launch figures of the pair kernel from the committed ncu capture of
+    this workload (profiles/pair_kernel_ncu_r1.json, keyed by config): DRAM
+    bytes read + written and the SM issue / FP64-pipe utilisation, or None."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "pair_kernel_traffic_r1.json")))
-        return d["dram_bytes_read"] + d["dram_bytes_write"]
+        d = json.load(open(os.path.join(ROOT, "profiles", "pair_kernel_ncu_r1.json")))[cfg_name]
     except Exception:
-        return None
+        return None, None
+    hw = {"bound": "issue", "issue_active": d["issue_active"],
+          "fp64_pipe_active": d["fp64_pipe_active"], "warps_active": d["warps_active"],
+          "source": d["capture"]}
+    return d["dram_bytes_read"] + d["dram_bytes_write"], hw
 
 
 def cpu_baseline(cfg, s, tv, sims, x, y, t, sample_sims):

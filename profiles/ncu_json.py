@@ -1,0 +1,39 @@
+"""Write profiles/pair_kernel_ncu_r1.json from pair-kernel ncu captures.
+Usage: python profiles/ncu_json.py C2=profiles/pair_kernel_r1.ncu-rep [C4=...]
+(bench.py reports these per-launch figures as roofline.traffic / roofline.hw.)"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+WANT = {
+    "gpu__time_duration.sum": "duration_ms",
+    "dram__bytes_read.sum": "dram_bytes_read",
+    "dram__bytes_write.sum": "dram_bytes_write",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active",
+    "smsp__inst_executed.sum": "warp_instructions",
+}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1, "us": 1e-3, "ns": 1e-6,
+         "%": 0.01, "inst": 1}
+
+out = {}
+path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "pair_kernel_ncu_r1.json")
+for arg in sys.argv[1:]:
+    cfg, rep = arg.split("=", 1)
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    head, units, vals = rows[0], rows[1], rows[2]
+    rec = {"capture": f"profiles/{os.path.basename(rep)} (ncu --set full --clock-control none)",
+           "kernel": vals[head.index("Kernel Name")]}
+    for i, name in enumerate(head):
+        if name in WANT and WANT[name] not in rec and vals[i].strip():
+            v = float(vals[i].replace(",", "")) * SCALE.get(units[i], 1)
+            rec[WANT[name]] = round(v) if WANT[name].startswith(("dram", "warp_inst")) else round(v, 6)
+    out[cfg] = rec
+json.dump(out, open(path, "w"), indent=1)
+print(json.dumps(out, indent=1))
