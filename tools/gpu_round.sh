@@ -2,7 +2,7 @@
 # One GPU-box session: parity tests, the default bench line, the other configs,
 # the ncu launch list and one full capture of the pair kernel.
 #   gpurun --timeout 2400 -- 'bash tools/gpu_round.sh [tag] [stages]'
-# stages: any of t (tests) b (bench C2) c (other configs) l (launch list) f (ncu full)
+# stages: any of t (tests) s (smoke) b (bench C2) c (other configs) l (launch list) f (ncu full)
 tag=${1:-r1}
 stages=${2:-tbclf}
 out=gpurun_out
@@ -11,6 +11,10 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $out/gpu_$tag
 if [[ $stages == *t* ]]; then
   timeout 900 python -m pytest tests -m gpu -x -q > $out/pytest_gpu_$tag.log 2>&1
   echo "pytest rc=$?" >> $out/pytest_gpu_$tag.log
+fi
+if [[ $stages == *s* ]]; then
+  timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke_$tag.log 2>&1
+  echo "smoke rc=$?" >> $out/smoke_$tag.log
 fi
 if [[ $stages == *b* ]]; then
   timeout 400 python bench.py > $out/bench_$tag.json 2> $out/bench_$tag.err
