@@ -23,12 +23,12 @@ constexpr int kQBuckets = 512;      // distance (q) bucket table size
 constexpr int kAngleSlots = 16;    // per-lane crossing scratch: 2 doubles x 8 crossings
 constexpr int kRingSmem = 32;      // ring vertices staged in shared memory (bitmask path)
 #ifndef STK_ARC_CHUNK
-#define STK_ARC_CHUNK 12
+#define STK_ARC_CHUNK 32
 #endif
 constexpr int kArcChunk = STK_ARC_CHUNK;        // candidate steps between arc drains
 constexpr int kFixedFracBits = 53;  // fixed-point weighted sums: value * 2^53
 #ifndef STK_ARC_RING
-#define STK_ARC_RING 1024
+#define STK_ARC_RING 4096
 #endif
 constexpr int kArcRing = STK_ARC_RING;  // per-warp arc ring entries (> 31 + kArcChunk * 64)
 static_assert(kArcRing > 31 + kArcChunk * 64, "the arc ring must hold a chunk's entries");
