@@ -575,7 +575,7 @@ __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas) {
   uint64_t np = (maxc + kPartCells - 1) / kPartCells;
   np = np < 1 ? 1 : (np > (uint64_t)kMaxParts ? (uint64_t)kMaxParts : np);
   const uint32_t parts = (uint32_t)np;
-  uint64_t ti = total / (8ull * resident_ctas);
+  uint64_t ti = total / ((uint64_t)STK_TASKS_PER_CTA * resident_ctas);
   // at least one unit per warp in a task
   uint64_t tmin = (kPairWarps + parts - 1) / parts;
   tmin = tmin < (uint64_t)kTaskMinItems ? (uint64_t)kTaskMinItems : tmin;

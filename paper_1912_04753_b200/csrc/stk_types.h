@@ -10,6 +10,9 @@ constexpr int kItemCenters = 32;    // centers per warp work item (one per lane)
 constexpr int kPartCells = 4096;    // a cell this populous splits items into parts (>= 2)
 constexpr int kMaxParts = 32;       // ... up to this many parts per item
 constexpr int kTaskMinItems = 4;    // warp items per CTA task: adaptive in [min, max] so the
+#ifndef STK_TASKS_PER_CTA
+#define STK_TASKS_PER_CTA 8  // adaptive task size: about this many tasks per resident CTA
+#endif
 #ifndef STK_TASK_MAX
 #define STK_TASK_MAX 256
 #endif
