@@ -146,7 +146,7 @@ struct stk_ctx {
   DevBuf<int64_t> t;
   DevBuf<double2> pxy;
   DevBuf<unsigned char> pmeta;
-  DevBuf<uint32_t> idx, key, rank, cell_count, cell_start, item_start, task_start, task_counter;
+  DevBuf<uint32_t> key, rank, cell_count, cell_start, item_start, task_start, task_counter;
   DevBuf<uint2> items;
   DevBuf<uint32_t> sel_start, center_pos;
   DevBuf<uint4> arcq;
@@ -518,7 +518,6 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   const int wide = (c->p1 - c->p0) >= 0x7fffffffLL ? 1 : 0;
   c->pxy.ensure(R * n);
   c->pmeta.ensure(R * n * (wide ? sizeof(PtMeta<int64_t>) : sizeof(PtMeta<int32_t>)));
-  c->idx.ensure(R * n);
   c->key.ensure(R * n);
   c->rank.ensure(R * n);
   c->cell_count.ensure(R * P.G.cells);
@@ -541,7 +540,6 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   B.pxy = c->pxy.p;
   B.pmeta = c->pmeta.p;
   B.wide = wide;
-  B.idx = c->idx.p;
   B.key = c->key.p;
   B.rank = c->rank.p;
   B.cell_count = c->cell_count.p;
@@ -980,7 +978,7 @@ void stk_destroy(stk_ctx* c) {
   c->d_ring.release(); c->d_Q.release(); c->d_s.release(); c->d_T.release();
   c->d_qtab.release(); c->d_ttab.release();
   c->x.release(); c->y.release(); c->t.release();
-  c->pxy.release(); c->pmeta.release(); c->idx.release(); c->key.release(); c->rank.release();
+  c->pxy.release(); c->pmeta.release(); c->key.release(); c->rank.release();
   c->cell_count.release(); c->cell_start.release(); c->item_start.release();
   c->task_start.release(); c->task_counter.release(); c->items.release();
   c->hist.release(); c->stats.release(); c->bad.release(); c->K.release(); c->L.release();

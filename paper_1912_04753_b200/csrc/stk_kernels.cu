@@ -507,8 +507,7 @@ __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first) {
   const uint64_t d = (uint64_t)p * B.n + pos;
   const double x = B.x[o], y = B.y[o];
   const int64_t t = B.t[o];
-  B.pxy[d] = make_double2(x, y);
-  B.idx[d] = (uint32_t)i;
+  B.pxy[d] = make_double2(x, y);  // the input index travels in the meta record
   const float sq = R.no_safe ? -1.0f : float_floor(safe_q(x, y, R));
   const int64_t vt = min(t - R.p0, R.p1 - t);
   if (B.wide) {
@@ -518,6 +517,12 @@ __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first) {
     PtMeta<int32_t> m{(int32_t)(t - R.p0), (int32_t)vt, sq, (uint32_t)i};
     reinterpret_cast<PtMeta<int32_t>*>(B.pmeta)[d] = m;
   }
+}
+
+// Input index of the sorted point at batch offset o (PtMeta::idx).
+__device__ __forceinline__ uint32_t sorted_input_index(const Batch& B, uint64_t o) {
+  return B.wide ? reinterpret_cast<const PtMeta<int64_t>*>(B.pmeta)[o].idx
+                : reinterpret_cast<const PtMeta<int32_t>*>(B.pmeta)[o].idx;
 }
 
 // Center selection (patterns [0, n_sel)): count selected centers per cell.
@@ -531,7 +536,7 @@ __global__ void select_count_kernel(Batch B, GridGeom G) {
   const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (j >= B.n) return;
   const uint64_t pb = (uint64_t)p * B.n;
-  const uint32_t i = B.idx[pb + j];
+  const uint32_t i = sorted_input_index(B, pb + j);
   uint32_t r = 0xFFFFFFFFu;
   if (selected(B, i)) r = atomicAdd(&B.cell_count[(uint64_t)p * G.cells + B.key[pb + i]], 1u);
   B.rank[pb + j] = r;
@@ -544,7 +549,7 @@ __global__ void select_scatter_kernel(Batch B, GridGeom G) {
   const uint64_t pb = (uint64_t)p * B.n;
   const uint32_t r = B.rank[pb + j];
   if (r == 0xFFFFFFFFu) return;
-  const uint32_t cell = B.key[pb + B.idx[pb + j]];
+  const uint32_t cell = B.key[pb + sorted_input_index(B, pb + j)];
   B.center_pos[pb + B.sel_start[(uint64_t)p * (G.cells + 1) + cell] + r] = (uint32_t)j;
 }
 

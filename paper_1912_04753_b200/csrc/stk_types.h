@@ -144,7 +144,6 @@ struct Batch {
   double2* pxy;   // (x, y)
   void* pmeta;    // PtMeta<int32_t> (16 B) or PtMeta<int64_t> (24 B) when `wide`
   int wide;       // study period >= 2^31 time units: 64-bit relative times
-  uint32_t* idx;  // input index of each sorted point
   uint32_t* key;  // cell key per unsorted point
   uint32_t* rank; // rank within the cell per unsorted point
   uint32_t* cell_count;  // [R][cells]
