@@ -2,7 +2,7 @@
 # One GPU-box session: parity tests, the default bench line, the other configs,
 # the ncu launch list and one full capture of the pair kernel.
 #   gpurun --timeout 2400 -- 'bash tools/gpu_round.sh [tag] [stages]'
-# stages: any of t (tests) s (smoke) b (bench C2) c (other configs) l (launch list) f (ncu full)
+# stages: any of t (tests) s (smoke) b (bench C2) c (other configs) p (polygons) l (launch list) f (ncu full)
 tag=${1:-r1}
 stages=${2:-tbclf}
 out=gpurun_out
@@ -26,6 +26,11 @@ if [[ $stages == *c* ]]; then
     timeout 400 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $out/bench_${c}_$tag.json 2> $out/bench_${c}_$tag.err
   done
   timeout 600 python bench.py --config C5 --sims 1 --steps 2 --warmup 3 --no-cpu-baseline > $out/bench_C5_$tag.json 2> $out/bench_C5_$tag.err
+fi
+if [[ $stages == *p* ]]; then
+  for v in 128 512 2048; do
+    timeout 600 python bench.py --ring $v --steps 2 --warmup 2 --cpu-sample-frac 0.1 > $out/bench_ring${v}_$tag.json 2> $out/bench_ring${v}_$tag.err
+  done
 fi
 if [[ $stages == *l* ]]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
