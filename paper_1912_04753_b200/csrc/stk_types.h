@@ -7,7 +7,10 @@
 namespace stk {
 
 constexpr int kItemCenters = 32;    // centers per warp work item (one per lane)
-constexpr int kPartCells = 4096;    // a cell this populous splits items into parts (>= 2)
+#ifndef STK_PART_CELLS
+#define STK_PART_CELLS 4096
+#endif
+constexpr int kPartCells = STK_PART_CELLS;    // a cell this populous splits items into parts (>= 2)
 constexpr int kMaxParts = 32;       // ... up to this many parts per item
 constexpr int kTaskMinItems = 4;    // warp items per CTA task: adaptive in [min, max] so the
 #ifndef STK_TASKS_PER_CTA
