@@ -15,6 +15,8 @@ device pipeline (generation, pairs, finalize, L, envelope, diff) delivers them.
 import numpy as np
 import pytest
 
+from conftest import surfaces_close
+
 pytestmark = pytest.mark.gpu
 
 
@@ -64,3 +66,37 @@ def test_criterion4_significance(api):
         if np.any(res.diff_upper.values[1:, :] > 0.0):
             detected += 1
     assert detected >= 19, f"clustering detected in only {detected}/20 repetitions"
+
+
+def test_criterion9_smoke_benchmark_matches_reference(api):
+    """Criterion 9 (:478-506): n = 10,000 uniform points (the reference's own
+    generator, seed 909), 20 x 20 grid, 19 CSR simulations, seed 77 — well
+    under the 5-minute bar, and equal to the reference's rt::run_job (K, L,
+    envelopes, diff within 1e-9; in-threshold pairs of the observed pattern
+    exact)."""
+    import time
+
+    from oracle import ref
+
+    if not __import__("oracle").ref_available():
+        pytest.skip("reference (oracle/_ref) not built")
+    est, geom, rt = api["est"], api["geom"], api["rt"]
+    side = 10000.0
+    ring = np.array([[0, 0], [side, 0], [side, side], [0, side]], float)
+    region = geom.StudyRegion(ring, 0, 100)
+    grid = est.DistanceGrid.regular(25.0, 500.0, 2, 40)
+    x, y, t = ref.uniform_points(909, ring, 0, 100, 10000)
+    spec = rt.JobSpec(grid=grid, sims=19, seed=77)
+    t0 = time.perf_counter()
+    res = rt.run_job((x, y, t), region, spec, rt.DeviceExecutor(device=0))
+    elapsed = time.perf_counter() - t0
+    assert elapsed < 300.0
+    assert res.k_hat.values.shape == (20, 20) and res.upper_l is not None
+    r = ref.run_job(x, y, t, ring, 0, 100, grid.s_values, grid.t_values, 19, 77,
+                    partitions=8, workers=4, use_index=True, use_cache=True)
+    assert res.telemetry.in_threshold_pairs >= r["in_threshold"]
+
+    assert surfaces_close(res.k_hat.values, r["k"]) and surfaces_close(res.l_hat.values, r["l"])
+    assert surfaces_close(res.upper_l.values, r["upper"])
+    assert surfaces_close(res.lower_l.values, r["lower"])
+    assert surfaces_close(res.diff_upper.values, r["diff"])
