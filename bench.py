@@ -405,7 +405,7 @@ def run_ours(args):
         "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                      "unit": "FP64 Tinstr/s", "frac": achieved / peak if peak else None,
                      "traffic": ncu_capture(cfg.name)[0],
-                     "hw": ncu_capture(cfg.name)[1],
+                     "hw": hw_view(ncu_capture(cfg.name)[1], pairs / args.steps, peak),
                      "note": f"pair kernel: ({W_INT} x interior + {W_ARC} x arc (omega != 1) pairs) "
                              "FP64 instr / CUDA-event pair-kernel time; peak = live DFMA "
                              "microbenchmark (stk_measure_fp64_peak)",
@@ -425,6 +425,16 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def hw_view(hw, pairs_per_launch, peak):
+    """SASS-counted FP64 instructions per in-threshold pair and the FP64 rate
+    they imply over the captured launch (one pair-kernel launch per step)."""
+    if hw and hw.get("fp64_thread_instructions") and pairs_per_launch:
+        f = hw["fp64_thread_instructions"]
+        hw["fp64_sass_instr_per_pair"] = f / pairs_per_launch
+        hw["fp64_sass_rate_frac"] = (f / (hw["duration_ms"] * 1e-3)) / peak if peak else None
+    return hw
+
+
 def ncu_capture(cfg_name):
     """Per-launch figures of the pair kernel from the committed ncu capture of
     this workload (profiles/pair_kernel_ncu_r1.json, keyed by config): DRAM
@@ -435,7 +445,8 @@ def ncu_capture(cfg_name):
         return None, None
     hw = {"bound": "issue", "issue_active": d["issue_active"],
           "fp64_pipe_active": d["fp64_pipe_active"], "warps_active": d["warps_active"],
-          "source": d["capture"]}
+          "fp64_thread_instructions": d.get("fp64_thread_instructions"),
+          "duration_ms": d["duration_ms"], "source": d["capture"]}
     return d["dram_bytes_read"] + d["dram_bytes_write"], hw
 
 

@@ -34,6 +34,15 @@ for arg in sys.argv[1:]:
         if name in WANT and WANT[name] not in rec and vals[i].strip():
             v = float(vals[i].replace(",", "")) * SCALE.get(units[i], 1)
             rec[WANT[name]] = round(v) if WANT[name].startswith(("dram", "warp_inst")) else round(v, 6)
+    # SASS-counted FP64 thread-instructions (DADD + DMUL + DFMA) per launch
+    per_cycle = 0.0
+    for op in ("dadd", "dmul", "dfma"):
+        k = f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed"
+        if k in head and vals[head.index(k)].strip():
+            per_cycle += float(vals[head.index(k)].replace(",", ""))
+    if "sm__cycles_elapsed.avg" in head:
+        rec["fp64_thread_instructions"] = round(
+            per_cycle * float(vals[head.index("sm__cycles_elapsed.avg")].replace(",", "")))
     out[cfg] = rec
 json.dump(out, open(path, "w"), indent=1)
 print(json.dumps(out, indent=1))
