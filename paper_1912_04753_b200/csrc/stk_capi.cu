@@ -134,7 +134,7 @@ struct stk_ctx {
   std::vector<QBucket> qtab;
   std::vector<TBucket<int64_t>> ttab;
   int q_shift = 0, q_base = 0;
-  float t_inv_bw = 0;
+  int t_shift = 0;
   bool single_step = false;
   DevBuf<double> d_Q, d_s;
   DevBuf<int64_t> d_T;
@@ -427,7 +427,7 @@ BinView bin_view(stk_ctx* c) {
   b.Tmax = c->t_values.back();
   b.q_shift = c->q_shift;
   b.q_base = c->q_base;
-  b.t_inv_bw = c->t_inv_bw;
+  b.t_shift = c->t_shift;
   b.single_step = c->single_step ? 1 : 0;
   return b;
 }
@@ -1122,45 +1122,45 @@ int stk_set_region(stk_ctx* c, const double* ring_xy, uint32_t nv, int64_t perio
 
 namespace {
 
-// Distance buckets on q = d^2 indexed by the float bits of RN_float(q): with m
-// mantissa bits per octave (shift = 23 - m) the buckets are log-spaced, so
-// one table covers the grid's whole dynamic range.  Bucket i holds every q
-// whose float lands in it: q >= prev_float(lo_f) (RN can round up onto lo_f)
-// and q < hi_f; its entry is the first bin with Q[bin] >= that lower bound
-// (a lower bound of the true bin) and Q[bin].  Single-step when the next
-// threshold lies at or above hi_f.  Bucket 0 takes everything below.  The
-// largest m whose table is single-step everywhere wins; else m = 5 with the
-// compare loop on the device.
+// Distance buckets on q = d^2 indexed by the high word of q's IEEE bits (sign,
+// 11 exponent bits, top 20 mantissa bits; q >= 0 orders as an integer): with m
+// mantissa bits per octave (shift = 20 - m) the buckets are log-spaced, so one
+// table covers the grid's whole dynamic range, and bucket i holds exactly the
+// q in [D((base + i) << shift : 0), D((base + i + 1) << shift : 0)) — no
+// conversion and no rounding on the device.  Its entry is the first bin with
+// Q[bin] >= the bucket's lower bound (a lower bound of the true bin) and
+// Q[bin].  Single-step when the next threshold lies at or above the bucket's
+// upper bound.  Bucket 0 takes everything below.  The largest m whose table is
+// single-step everywhere wins; else m = 5 with the compare loop on the device.
 bool build_q_buckets(stk_ctx* c) {
   const std::vector<double>& Q = c->Q;
   const int cs = (int)Q.size();
   const double qmax = Q.back();
-  float top_f = (float)qmax;
-  if ((double)top_f < qmax) top_f = std::nextafter(top_f, std::numeric_limits<float>::infinity());
-  uint32_t top_bits;
-  std::memcpy(&top_bits, &top_f, 4);
-  auto as_float = [](uint32_t bits) {
-    float f;
-    std::memcpy(&f, &bits, 4);
-    return f;
+  uint64_t qbits;
+  std::memcpy(&qbits, &qmax, 8);
+  const uint32_t top_hi = (uint32_t)(qbits >> 32);
+  auto from_hi = [](uint64_t hi) {  // the double with high word hi and low word 0
+    if (hi >= 0x7ff00000ull) return std::numeric_limits<double>::infinity();
+    const uint64_t bits = hi << 32;
+    double d;
+    std::memcpy(&d, &bits, 8);
+    return d;
   };
   auto build = [&](int m, std::vector<QBucket>* tab, int* shift, int* base) {
-    *shift = 23 - m;
-    const int64_t top = (int64_t)(top_bits >> *shift);
+    *shift = 20 - m;
+    const int64_t top = (int64_t)(top_hi >> *shift);
     *base = (int)std::max<int64_t>(0, top - (kQBuckets - 1));
     tab->assign(kQBuckets, QBucket{qmax, (uint32_t)(cs - 1), 0});
     bool single = true;
     for (int i = 0; i < kQBuckets; ++i) {
       const uint64_t idx = (uint64_t)*base + i;
-      double lo = 0.0;
-      if (i > 0) lo = (double)std::nextafter(as_float((uint32_t)(idx << *shift)), 0.0f);
-      const uint64_t hb = (idx + 1) << *shift;
-      const double hi = hb >= 0x7f800000ull ? std::numeric_limits<double>::infinity()
-                                             : (double)as_float((uint32_t)hb);
+      const double lo = i > 0 ? from_hi(idx << *shift) : 0.0;
+      const double hi = from_hi((idx + 1) << *shift);
       int k = 0;
       while (k < cs - 1 && Q[k] < lo) ++k;
       (*tab)[i] = QBucket{Q[k], (uint32_t)k, 0};
-      if (lo <= qmax && k + 1 < cs && Q[k + 1] < hi) single = false;
+      // a second step is needed iff some in-threshold q of the bucket exceeds Q[k + 1]
+      if (lo <= qmax && k + 1 < cs && Q[k + 1] < hi && Q[k + 1] < qmax) single = false;
     }
     return single;
   };
@@ -1195,20 +1195,21 @@ int stk_set_grid(stk_ctx* c, const double* s_values, uint32_t cs, const int64_t*
     for (uint32_t k = 0; k < cs; ++k) c->Q[k] = sqrt_threshold(s_values[k]);
     if (cs > 65535 || ct > 65535) throw Unsupported("more than 65535 bins per axis");
     const bool q_single = build_q_buckets(c);
-    // time buckets (linear): bucket b holds u >= b*bw (guaranteed by a 1e-5
-    // margin on the device-side bucket index), so the first bin at or above
-    // b*bw is a lower bound of the true bin; single-step when no bucket's
-    // range (with the margins) contains two thresholds
-    const double tmax = (double)t_values[ct - 1];
-    const double tbw = tmax / kBucketTable;
-    c->t_inv_bw = (float)((1.0 / tbw) * (1.0 - 1e-5));
+    // time buckets (linear, width 2^t_shift): bucket b holds exactly the lags
+    // u in [b 2^k, (b + 1) 2^k), so the first bin at or above b 2^k is a lower
+    // bound of the true bin; single-step when the next threshold covers the
+    // bucket's last lag
+    const int64_t tmax = t_values[ct - 1];
+    int tsh = 0;
+    while ((tmax >> tsh) >= (int64_t)kBucketTable) ++tsh;
+    c->t_shift = tsh;
     c->ttab.assign(kBucketTable, TBucket<int64_t>{0, 0});
     bool t_single = true;
     for (int b = 0, k = 0; b < kBucketTable; ++b) {
-      while (k < (int)ct - 1 && (double)t_values[k] < b * tbw) ++k;
+      const int64_t lo = (int64_t)b << tsh, last = (((int64_t)b + 1) << tsh) - 1;
+      while (k < (int)ct - 1 && t_values[k] < lo) ++k;
       c->ttab[b] = TBucket<int64_t>{t_values[k], (uint32_t)k};
-      const double hi = (b + 1) * tbw * (1.0 + 4e-5);
-      if (k + 1 < (int)ct && (double)t_values[k + 1] <= hi) t_single = false;
+      if (lo <= tmax && k + 1 < (int)ct && t_values[k + 1] < std::min(last, tmax)) t_single = false;
     }
     c->single_step = q_single && t_single;
     c->d_Q.ensure(cs);

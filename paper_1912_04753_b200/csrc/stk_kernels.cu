@@ -492,10 +492,11 @@ __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* counts, uint
   if (lane == 0 && amax) atomicMax(max_cell, (unsigned long long)amax);
 }
 
-// Largest float <= v (a conservative safe radius^2 stays conservative).
-__device__ __forceinline__ float float_floor(double v) {
-  float f = __double2float_rd(v);
-  return f;
+// High word of a non-negative lower bound of v (the double with that high word
+// and a zero low word is <= v): hi32(q) < sqh then implies q < v.  0 (every
+// q takes the exact path) when v <= 0.
+__device__ __forceinline__ uint32_t safe_hi(double v) {
+  return v > 0.0 ? (uint32_t)__double2hiint(v) : 0u;
 }
 
 __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first) {
@@ -508,7 +509,7 @@ __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first) {
   const double x = B.x[o], y = B.y[o];
   const int64_t t = B.t[o];
   B.pxy[d] = make_double2(x, y);  // the input index travels in the meta record
-  const float sq = R.no_safe ? -1.0f : float_floor(safe_q(x, y, R));
+  const uint32_t sq = R.no_safe ? 0u : safe_hi(safe_q(x, y, R));
   const int64_t vt = min(t - R.p0, R.p1 - t);
   if (B.wide) {
     PtMeta<int64_t> m{t - R.p0, vt, sq, (uint32_t)i};
@@ -658,13 +659,13 @@ template <typename TT>
 __device__ __forceinline__ PtMeta<TT> lds_meta(uint32_t a) {
   if constexpr (sizeof(TT) == 4) {
     const uint4 v = lds_u32x4(a);
-    return PtMeta<TT>{(TT)v.x, (TT)v.y, __uint_as_float(v.z), v.w};
+    return PtMeta<TT>{(TT)v.x, (TT)v.y, v.z, v.w};
   } else {  // 24-byte records: only 8-byte aligned
     unsigned long long t, vt;
     asm volatile("ld.shared.u64 %0, [%1];" : "=l"(t) : "r"(a));
     asm volatile("ld.shared.u64 %0, [%1];" : "=l"(vt) : "r"(a + 8));
     const uint2 w = lds_u32x2(a + 16);
-    return PtMeta<TT>{(TT)t, (TT)vt, __uint_as_float(w.x), w.y};
+    return PtMeta<TT>{(TT)t, (TT)vt, w.x, w.y};
   }
 }
 template <typename TT>
@@ -831,8 +832,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     S.ttab[b] = TBucket<TT>{(TT)min(BV.t_tab[b].thr, tclamp), BV.t_tab[b].bin};
   const double Qmax = BV.Qmax;
   const TT Tmax = (TT)min(BV.Tmax, tclamp);
-  const float t_inv_bw = BV.t_inv_bw;
+  const int t_shift = BV.t_shift;
   const int q_shift = BV.q_shift, q_base = BV.q_base;
+  // deep: hi32(q) < sqh for every in-threshold q (q <= Qmax)
+  const uint32_t Qmax_hi = (uint32_t)__double2hiint(BV.Qmax);
   const uint32_t total_tasks = B.task_start[B.R];
   const uint32_t task_items = B.task_counter[1];
   const uint32_t parts = B.task_counter[2];  // units per item (1: whole items)
@@ -903,7 +906,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         cxy_w[lane] = B.pxy[pb + pos];
         cm_w[lane] = m;
         cpos_w[lane] = pos;
-        cdeep = (double)m.sq >= Qmax && m.vt >= Tmax;
+        cdeep = m.sqh > Qmax_hi && m.vt >= Tmax;
       }
       const bool item_deep = __all_sync(FULL_MASK, cdeep);
       __syncwarp();
@@ -1034,7 +1037,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         // whose register peak would otherwise push it to local memory
         const bool has = jp != 0xffffffffu;
         double2 nxy = make_double2(1e300, 1e300);  // no neighbour: q = inf > Qmax
-        PtMeta<TT> nm{0, 0, 0.0f, 0u};
+        PtMeta<TT> nm{0, 0, 0u, 0u};
         if (has) {
           nxy = B.pxy[pb + jp];
           nm = pmeta_b[pb + jp];
@@ -1058,7 +1061,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           __syncwarp();
         }
         const bool tile_deep =
-            __all_sync(FULL_MASK, !has || ((double)nm.sq >= Qmax && nm.vt >= Tmax));
+            __all_sync(FULL_MASK, !has || (nm.sqh > Qmax_hi && nm.vt >= Tmax));
         const int kend = min(kc + kArcChunk, (int)nc);
         auto chunk = [&](auto own_tag, auto deep_tag) {
           constexpr bool OWN = decltype(own_tag)::value;
@@ -1104,16 +1107,16 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             bool half_i = false, half_j = false;
             if (in) {
               // bin_pair: first s_k >= d <=> first Q_k >= q; first t_l >= u.
-              // q's bucket from the bits of RN_float(q) (log-spaced buckets,
-              // no sqrt); each entry carries its bin's threshold
-              const float qf = (float)q;
-              int bq = (int)(__float_as_uint(qf) >> q_shift) - q_base;
+              // q's bucket from the high word of its bits (log-spaced
+              // buckets, no sqrt, no conversion); each entry carries its
+              // bin's threshold
+              const uint32_t qh = (uint32_t)__double2hiint(q);
+              int bq = (int)(qh >> q_shift) - q_base;
               bq = min(max(bq, 0), kQBuckets - 1);
               const ulonglong2 qe2 = lds_u64x2(a_q + (uint32_t)bq * (uint32_t)sizeof(QBucket));
               const QBucket qe{__longlong_as_double((long long)qe2.x), (uint32_t)qe2.y, 0u};
               uint32_t sb = qe.bin;
-              int bt = (int)((float)du * t_inv_bw);
-              bt = min(bt, kBucketTable - 1);
+              const int bt = (int)min(du >> t_shift, (TT)(kBucketTable - 1));
               const TBucket<TT> te = lds_tbucket<TT>(a_t + (uint32_t)bt * (uint32_t)sizeof(TBucket<TT>));
               uint32_t tb = te.bin;
               if constexpr (SINGLE) {
@@ -1128,11 +1131,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               if (DEEP) continue;
               half_i = du > cmk.vt;
               half_j = du > nm.vt;
-              // q >= sq (a float) implies RN_float(q) >= sq, so every pair that
-              // needs the exact path takes it; the rare extras (q < sq ==
-              // RN_float(q)) get omega == 1 exactly there (safe radius)
-              arc_i = qf >= cmk.sq;
-              arc_j = qf >= nm.sq;
+              // hi32(q) < sqh implies q below the safe radius^2 (omega == 1);
+              // the rest take the exact path (the few with q just under the
+              // safe radius get omega == 1 exactly there)
+              arc_i = qh >= cmk.sqh;
+              arc_j = qh >= nm.sqh;
               const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
               if (h) reds_add_u32(a_ch + bin * 8u + 4u, h);
             }

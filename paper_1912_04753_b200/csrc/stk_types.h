@@ -100,8 +100,8 @@ struct BinView {
   uint32_t cs, ct;
   double Qmax;
   int64_t Tmax;
-  int q_shift, q_base;     // bucket = clamp((bits(float(q)) >> q_shift) - q_base)
-  float t_inv_bw;          // buckets per time unit (with margin)
+  int q_shift, q_base;     // bucket = clamp((hi32(q) >> q_shift) - q_base): log-spaced
+  int t_shift;             // time bucket = min(u >> t_shift, kBucketTable - 1)
   int single_step;         // every bucket straddles <= 1 threshold: one compare finds the bin
 };
 
@@ -131,7 +131,7 @@ template <typename TT>
 struct PtMeta {
   TT t;
   TT vt;
-  float sq;
+  uint32_t sqh;  // high word of a lower bound of the safe q: hi32(q) < sqh => omega == 1
   uint32_t idx;
 };
 
