@@ -129,7 +129,9 @@ def _from_limbs(h, m, l):
     m = np.asarray(m, np.int64).astype(object)
     l = np.asarray(l, np.int64).astype(object)
     v = h * (1 << 64) + m * (1 << 32) + l
-    hi = np.array([int(x) >> 64 for x in v.ravel()], dtype=np.uint64).reshape(v.shape)
+    # two's complement: a bin's total (1/w - 1) sum can be negative (omega = 1 + ulp)
+    hi = np.array([(int(x) >> 64) & ((1 << 64) - 1) for x in v.ravel()],
+                  dtype=np.uint64).reshape(v.shape)
     lo = np.array([int(x) & ((1 << 64) - 1) for x in v.ravel()], dtype=np.uint64).reshape(v.shape)
     return hi, lo
 

@@ -168,6 +168,13 @@ def test_limbs_roundtrip_exact():
     hi2, lo2 = rt._from_limbs(8 * h, 8 * m, 8 * l)
     for a, b, c, d in zip(hi, lo, hi2, lo2):
         assert (int(c) << 64 | int(d)) == 8 * (int(a) << 64 | int(b))
+    # negative totals (two's complement, e.g. a bin whose terms are all 1 - ulp):
+    # -5 on each of 3 ranks sums to -15 = (2^64 - 1) : (2^64 - 15)
+    m1 = np.array([np.uint64(2**64 - 1)], dtype=np.uint64)
+    neg = np.array([np.uint64(2**64 - 5)], dtype=np.uint64)
+    h, m, l = rt._to_limbs(m1, neg)
+    hi3, lo3 = rt._from_limbs(3 * h, 3 * m, 3 * l)
+    assert int(hi3[0]) == 2**64 - 1 and int(lo3[0]) == 2**64 - 15
 
 
 def test_device_calls_fail_loudly_without_gpu():
