@@ -342,13 +342,14 @@ def run_ours(args):
     pairs_rank = sum(t_.in_threshold_pairs for t_ in tels)
     arc_rank = sum(t_.arc_pairs for t_ in tels)  # omega != 1 (SURVEY 8(d) arc pairs)
     exact_rank = sum(t_.exact_path_pairs for t_ in tels)
+    cand_rank = sum(t_.candidate_pairs for t_ in tels)  # unordered pairs the kernel tested
     pair_ms_rank = sum(t_.pair_ms for t_ in tels)
     grid_ms_rank = sum(t_.grid_ms for t_ in tels)
     patterns_rank = sum(t_.patterns for t_ in tels)
     launches = sum(t_.kernel_launches for t_ in tels) // max(args.steps, 1)
 
     # max over ranks of time, sum over ranks of work
-    tot = np.array([pairs_rank, arc_rank, patterns_rank, exact_rank], dtype=np.float64)
+    tot = np.array([pairs_rank, arc_rank, patterns_rank, exact_rank, cand_rank], dtype=np.float64)
     tmax = np.array([ms, e2e_ms, pair_ms_rank, grid_ms_rank], dtype=np.float64)
     if world > 1:
         import torch.distributed as dist
@@ -359,7 +360,7 @@ def run_ours(args):
         dist.all_reduce(a, op=dist.ReduceOp.SUM)
         dist.all_reduce(b, op=dist.ReduceOp.MAX)
         tot, tmax = a.cpu().numpy(), b.cpu().numpy()
-    pairs, arcs, patterns, exact = tot
+    pairs, arcs, patterns, exact, cands = tot
     ms, e2e_ms, pair_ms, grid_ms = tmax
 
     if rank != 0:
@@ -397,6 +398,10 @@ def run_ours(args):
         "pairs_per_step": pairs / args.steps,
         "arc_fraction": arcs / pairs if pairs else None,
         "exact_path_fraction": exact / pairs if pairs else None,
+        # secondary, implementation-dependent: (center, neighbour)
+        # candidates the pair kernel tested, each serving both ordered pairs
+        "candidate_pairs_per_s": cands / (ms * 1e-3),
+        "candidates_per_unordered_in_threshold_pair": (2 * cands / pairs) if pairs else None,
         "e2e": {"value": e2e_value, "unit": "pairs/s",
                 "h2d_bytes_per_step": int(24 * n),
                 "d2h_bytes_per_step": int(8 * bins * (5 if world == 1 else 0) +
