@@ -701,22 +701,26 @@ size_t pair_kernel_smem(uint32_t bins, int wide) {
 // Adds one arc-path ordered pair to the CTA histogram: (1/(omega*v) - 1) as a
 // signed 128-bit fixed-point integer (53 fractional bits, two's complement,
 // carry detected on the low word); bw = bin | (v == 1/2) << 31.
-__device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, ArcSum* s_arc,
-                                             uint2* s_ch, uint32_t* n_arc) {
+// sa_arc / sa_ch: shared-space addresses of the arc-sum and count sections.
+__device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, uint32_t sa_arc,
+                                             uint32_t sa_ch, uint32_t* n_arc) {
   if (ws != 1.0) ++*n_arc;                           // omega != 1 (SURVEY's arc-pair definition)
   const double w = ws * ((bw >> 31) ? 0.5 : 1.0);  // edge::pair_weight (edge_correction.cpp:88-103)
   const double term = 1.0 / w;                      // PairHistogram::add(.., 1.0 / w)
   const uint32_t bin = bw & 0x7fffffffu;
   if (w == 0.0) {  // omega == 0: the reference adds 1/0 = inf and its bin ends NaN
-    atomicOr(&s_ch[bin].x, 1u);  // bit 0 of the (always even) count: "infinite term"
+    // bit 0 of the (always even) count: "infinite term"
+    asm volatile("red.shared.or.b32 [%0], 1;" ::"r"(sa_ch + bin * (uint32_t)sizeof(uint2)));
     return;
   }
   uint64_t lo, hi;
   fixed_term_minus_one(term, &lo, &hi);
   if (lo | hi) {
-    const unsigned long long old = atomicAdd(&s_arc[bin].lo, (unsigned long long)lo);
+    const uint32_t a = sa_arc + bin * (uint32_t)sizeof(ArcSum);
+    unsigned long long old;
+    asm volatile("atom.shared.add.u64 %0, [%1], %2;" : "=l"(old) : "r"(a), "l"(lo) : "memory");
     if (old + lo < old) ++hi;
-    if (hi) atomicAdd(&s_arc[bin].hi, (unsigned long long)hi);
+    if (hi) asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(a + 8u), "l"(hi) : "memory");
   }
 }
 
@@ -730,7 +734,7 @@ __device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, ArcSum* s_a
 template <bool RECT>
 __device__ __forceinline__ void drain_main(int count, int lane, const uint4* ring, uint32_t head,
                                            uint4* cring, uint32_t* ctail, unsigned lanemask_lt,
-                                           const double2* pxy, ArcSum* s_arc, uint2* s_ch,
+                                           const double2* pxy, uint32_t sa_arc, uint32_t sa_ch,
                                            const RegionView& reg, uint32_t* n_arc) {
   const bool valid = lane < count;
   uint4 e = make_uint4(0u, 0u, 0u, 0u);
@@ -747,14 +751,14 @@ __device__ __forceinline__ void drain_main(int count, int lane, const uint4* rin
   const unsigned m = __ballot_sync(FULL_MASK, defer);
   if (defer) cring[(*ctail + __popc(m & lanemask_lt)) & (kCplxRing - 1)] = e;
   *ctail += __popc(m);
-  if (valid && !defer) add_arc_term(ws, e.y, s_arc, s_ch, n_arc);
+  if (valid && !defer) add_arc_term(ws, e.y, sa_arc, sa_ch, n_arc);
 }
 
 // Deferred ring: the reference's general spatial_isotropic_weight.
 template <bool RECT>
 __device__ __forceinline__ void drain_general(int count, int lane, const uint4* cring,
                                               uint32_t head, double* angs, int slots,
-                                              const double2* pxy, ArcSum* s_arc, uint2* s_ch,
+                                              const double2* pxy, uint32_t sa_arc, uint32_t sa_ch,
                                               const RegionView& reg, const RegionView* reg_g,
                                               int* overflow, uint32_t* n_arc) {
   if (lane >= count) return;
@@ -773,7 +777,7 @@ __device__ __forceinline__ void drain_general(int count, int lane, const uint4* 
     if (RECT) ws = spatial_weight_ring(c.x, c.y, d, reg.ring, reg.nv, reg.maxabs, overflow);
     else ws = spatial_weight(c.x, c.y, d, reg_g, overflow);
   }
-  add_arc_term(ws, e.y, s_arc, s_ch, n_arc);
+  add_arc_term(ws, e.y, sa_arc, sa_ch, n_arc);
 }
 
 #ifndef STK_PAIR_MINB
@@ -794,6 +798,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   __shared__ uint2 s_lim[kPairWarps * 32];  // per-tile owner limits (see below)
   __shared__ uint32_t s_jp[kPairWarps * 32];  // per-tile neighbour position of each lane
   __shared__ uint32_t s_base;               // shared-space address of smem_raw
+  __shared__ uint32_t s_arc_off;            // byte offset of the arc-sum section (runtime-sized)
   using Lay = PairLayout<TT>;
   const Batch& B = A.B;
   const GridGeom& G = A.G;
@@ -847,7 +852,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   // from shared memory (one load) instead of rebuilding it from special
   // registers and the kernel parameter
   uint4* const arcq0 = B.arcq + ((uint64_t)blockIdx.x * kPairWarps + w) * (kArcRing + kCplxRing);
-  if (tid == 0) s_base = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  if (tid == 0) {
+    s_base = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    s_arc_off = (uint32_t)Lay::lh(bins);
+  }
   if (lane == 0) s_ring[w] = arcq0;
   // crossing scratch of the general weight (deferred drains only): global,
   // L1-resident, element k of lane l at [k * 32 + l]
@@ -979,8 +987,12 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           const int cnt_ = (int)min(cpending, 32u);
           __syncwarp();
           const uint4* cring = *reinterpret_cast<uint4* volatile*>(&s_ring[w]) + kArcRing;
-          drain_general<RECT>(cnt_, lane, cring, ch_, angs, slots, B.pxy + pb, S.arc, S.ch, A.reg, A.reg_g,
-                              &overflow, &n_arc);
+          // shared-space section addresses from shared memory: two loads
+          // instead of rebuilding them from the grid size at every drain
+          const uint32_t sb_ = *reinterpret_cast<volatile uint32_t*>(&s_base);
+          const uint32_t sa_arc = sb_ + *reinterpret_cast<volatile uint32_t*>(&s_arc_off);
+          drain_general<RECT>(cnt_, lane, cring, ch_, angs, slots, B.pxy + pb, sa_arc,
+                              sb_ + (uint32_t)Lay::ch, A.reg, A.reg_g, &overflow, &n_arc);
           ch_ += (uint32_t)cnt_;
           continue;
         }
@@ -990,7 +1002,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           const int cnt_ = (int)min(pending, 32u);
           __syncwarp();
           uint4* const arcq = *reinterpret_cast<uint4* volatile*>(&s_ring[w]);
-          drain_main<RECT>(cnt_, lane, arcq, qh, arcq + kArcRing, &ct_, lanemask_lt, B.pxy + pb, S.arc, S.ch, A.reg, &n_arc);
+          const uint32_t sb_ = *reinterpret_cast<volatile uint32_t*>(&s_base);
+          const uint32_t sa_arc = sb_ + *reinterpret_cast<volatile uint32_t*>(&s_arc_off);
+          drain_main<RECT>(cnt_, lane, arcq, qh, arcq + kArcRing, &ct_, lanemask_lt, B.pxy + pb, sa_arc,
+                           sb_ + (uint32_t)Lay::ch, A.reg, &n_arc);
           qh += (uint32_t)cnt_;
           continue;
         }
