@@ -36,8 +36,16 @@ def region(path, ln):
             return "candidate/bin loop"
         if "flush the CTA histogram" in line:
             return "flush"
+        if "auto chunk = [&]" in line:
+            return "chunk setup (per tile)"
+        if "new tile: map the lanes to their rows" in line:
+            return "tile start + neighbour load"
+        if "the single drain site" in line:
+            return "drain dispatch + ring compaction"
+        if "stage the item's centers" in line:
+            return "item setup (rows, centers)"
         if "__global__" in line:
-            return "kernel setup/items"
+            return "kernel prologue / task loop"
     return "other"
 for rec in csv.reader(io.StringIO(out)):
     if not rec:
