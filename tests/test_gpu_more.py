@@ -356,3 +356,30 @@ def test_dense_cell_item_parts(api, port):
     t = np.concatenate([rng.integers(0, 40, 5000), rng.integers(0, 1001, 2000)])
     h = _compare(api, port, x, y, t, ring, p0, p1, [5.0, 20.0, 50.0, 100.0], [10, 50, 200])
     assert int(h["counts"].sum()) > 20_000_000
+
+
+def test_utm_offset_clusters_integer_bucket_bins(api, port):
+    """UTM-like coordinates (a 20 km rectangle at x0 = 500 km, y0 = 4,000 km)
+    with clustered points, a distance grid spanning 10 m .. 2.5 km and a
+    lag grid in days: the integer-bit distance buckets (high word of q) and
+    power-of-two lag buckets must give the reference's bins bit for bit, and
+    points placed exactly on thresholds must land in the inclusive bin."""
+    x0, y0 = 500_000.0, 4_000_000.0
+    ring = np.array([[x0, y0], [x0 + 20_000, y0], [x0 + 20_000, y0 + 20_000], [x0, y0 + 20_000]])
+    p0, p1 = 0, 365 * 86400
+    rng = np.random.default_rng(2024)
+    cx = rng.uniform(x0 + 500, x0 + 19_500, 40)
+    cy = rng.uniform(y0 + 500, y0 + 19_500, 40)
+    ct = rng.integers(p0 + 86400, p1 - 86400, 40)
+    k = rng.integers(0, 40, 6000)
+    x = np.clip(cx[k] + rng.normal(0, 300, 6000), x0, x0 + 20_000)
+    y = np.clip(cy[k] + rng.normal(0, 300, 6000), y0, y0 + 20_000)
+    t = np.clip(ct[k] + rng.normal(0, 5 * 86400, 6000).astype(np.int64), p0, p1)
+    # exact-threshold pairs: offsets of 10, 100 and 2500 m along x, lags of 1 and 30 days
+    for j, (dx, du) in enumerate([(10.0, 86400), (100.0, 30 * 86400), (2500.0, 0)]):
+        x[2 * j], y[2 * j], t[2 * j] = x0 + 7000.0, y0 + 7000.0 + 50 * j, 100 * 86400
+        x[2 * j + 1], y[2 * j + 1], t[2 * j + 1] = x0 + 7000.0 + dx, y0 + 7000.0 + 50 * j, 100 * 86400 + du
+    s = [10.0, 25.0, 50.0, 100.0, 250.0, 500.0, 1000.0, 2500.0]
+    tv = [86400, 7 * 86400, 30 * 86400, 90 * 86400]
+    h = _compare(api, port, x, y, t, ring, p0, p1, s, tv)
+    assert int(h["counts"].sum()) > 1_000_000
