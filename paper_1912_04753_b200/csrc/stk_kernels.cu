@@ -899,8 +899,25 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       uint32_t it = 0;
       if (lane == 0) it = atomicAdd(&s_next, 1u);
       it = __shfl_sync(FULL_MASK, it, 0);
-      const uint32_t iu = it / parts, part = it - iu * parts;
-      if (i0 + iu >= i1) break;
+      // units: whole items (or `parts` slices each for dense cells), except
+      // the task's last kPairWarps items, cut into at least kTailParts slices
+      // so the warps finish the task together (task-end barrier)
+      const uint32_t n_items = i1 - i0;
+      const uint32_t n_tail = min(n_items, (uint32_t)kPairWarps);
+      const uint32_t head_units = (n_items - n_tail) * parts;
+      const uint32_t tparts = max(parts, (uint32_t)kTailParts);
+      uint32_t iu, part, np;
+      if (it < head_units) {
+        iu = it / parts;
+        part = it - iu * parts;
+        np = parts;
+      } else {
+        const uint32_t r = it - head_units;
+        iu = (n_items - n_tail) + r / tparts;
+        part = r - (r / tparts) * tparts;
+        np = tparts;
+      }
+      if (iu >= n_items) break;
       const uint2 item = B.items[io + i0 + iu];
       const uint32_t cell = item.x, start = item.y;
       const uint32_t nc = min((uint32_t)kItemCenters, clist_b[co + cell + 1] - start);
@@ -962,14 +979,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       }
       const uint32_t rowoff = my_rb - (incl - len);
       const uint32_t V = __shfl_sync(FULL_MASK, incl, 31);
-      // part `part` of `parts` walks virtual indices [V part / parts, V (part + 1) / parts)
-#ifdef STK_PART_ALIGN
-      uint32_t v0 = (uint32_t)((uint64_t)V * part / parts) & ~31u;
-      const uint32_t v_hi = part + 1 == parts ? V : (uint32_t)((uint64_t)V * (part + 1) / parts) & ~31u;
-#else
-      uint32_t v0 = (uint32_t)((uint64_t)V * part / parts);
-      const uint32_t v_hi = (uint32_t)((uint64_t)V * (part + 1) / parts);
-#endif
+      // part `part` of `np` walks virtual indices [V part / np, V (part + 1) / np)
+      uint32_t v0 = (uint32_t)((uint64_t)V * part / np);
+      const uint32_t v_hi = (uint32_t)((uint64_t)V * (part + 1) / np);
       uint32_t qh = 0, qt = 0;    // arc ring head / tail (monotone)
       uint32_t ch_ = 0, ct_ = 0;  // deferred ring head / tail
       uint32_t n_arc = 0;

@@ -12,6 +12,10 @@ constexpr int kItemCenters = 32;    // centers per warp work item (one per lane)
 #endif
 constexpr int kPartCells = STK_PART_CELLS;    // a cell this populous splits items into parts (>= 2)
 constexpr int kMaxParts = 32;       // ... up to this many parts per item
+#ifndef STK_TAIL_PARTS
+#define STK_TAIL_PARTS 4
+#endif
+constexpr int kTailParts = STK_TAIL_PARTS;  // slices of each of a task's last kPairWarps items
 constexpr int kTaskMinItems = 4;    // warp items per CTA task: adaptive in [min, max] so the
 #ifndef STK_TASKS_PER_CTA
 #define STK_TASKS_PER_CTA 8  // adaptive task size: about this many tasks per resident CTA
