@@ -900,10 +900,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       if (lane == 0) it = atomicAdd(&s_next, 1u);
       it = __shfl_sync(FULL_MASK, it, 0);
       // units: whole items (or `parts` slices each for dense cells), except
-      // the task's last kPairWarps items, cut into at least kTailParts slices
+      // the task's last kTailItems items, cut into at least kTailParts slices
       // so the warps finish the task together (task-end barrier)
       const uint32_t n_items = i1 - i0;
-      const uint32_t n_tail = min(n_items, (uint32_t)kPairWarps);
+      const uint32_t n_tail = min(n_items, (uint32_t)kTailItems);
       const uint32_t head_units = (n_items - n_tail) * parts;
       const uint32_t tparts = max(parts, (uint32_t)kTailParts);
       uint32_t iu, part, np;

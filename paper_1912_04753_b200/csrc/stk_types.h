@@ -15,7 +15,11 @@ constexpr int kMaxParts = 32;       // ... up to this many parts per item
 #ifndef STK_TAIL_PARTS
 #define STK_TAIL_PARTS 4
 #endif
-constexpr int kTailParts = STK_TAIL_PARTS;  // slices of each of a task's last kPairWarps items
+constexpr int kTailParts = STK_TAIL_PARTS;  // slices of each of a task's last kTailItems items
+#ifndef STK_TAIL_ITEMS
+#define STK_TAIL_ITEMS 32  // two per warp of a 16-warp CTA (16: C4 +0.7%, 48 with 3 slices: same as 32)
+#endif
+constexpr int kTailItems = STK_TAIL_ITEMS;
 constexpr int kTaskMinItems = 4;    // warp items per CTA task: adaptive in [min, max] so the
 #ifndef STK_TASKS_PER_CTA
 #define STK_TASKS_PER_CTA 8  // adaptive task size: about this many tasks per resident CTA
