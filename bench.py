@@ -4,9 +4,10 @@ pairs evaluated/s and K realisations/s vs roofline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
 
-A step is one whole rt::run_job of the workload (default configs[1] = C2: the
-observed Thomas pattern + 99 CSR realisations, their K/L surfaces and the
-envelopes).  ``value`` = in-threshold ordered pairs evaluated per second over
+A step is one whole rt::run_job of the workload (default C4, the largest
+BASELINE config whose full job fits one GPU and whose reference arm can be
+timed per realisation at full N: the observed 1M-point POI pattern + 99 CSR
+realisations, their K/L surfaces and the envelopes).  ``value`` = in-threshold ordered pairs evaluated per second over
 all ranks with the observed pattern already in HBM; ``e2e`` = the same through
 the host-buffer C ABI call (``stk_run_job`` / ``stk_run_job_shard``: H2D of the
 points and D2H of K, L, envelopes and diff inside the timed region).
@@ -17,8 +18,11 @@ contiguous block of realisations; two exact all-reduces (SUM of integer
 partials, MAX/MIN of envelopes) over NCCL combine them.
 
 ``--impl reference`` times the reference's own CPU implementation
-(oracle/_ref: the unmodified reference sources, rt::run_job with a
-LocalExecutor on all host threads) on a bounded sample of the same workload.
+(oracle/_ref: the unmodified reference sources, rt::run_job's own loop body
+with a LocalExecutor on all host threads).  Each step is one pattern of the
+same job at full N (the first timed step the observed pattern, then CSR
+realisations r = 0, 1, ...); the line reports the full job extrapolated from
+them: T_plan + T_obs + m * mean(T_csr).
 """
 from __future__ import annotations
 
@@ -40,6 +44,10 @@ sys.path.insert(0, ROOT)
 # Algorithmic FP64 instruction budget per in-threshold pair (frozen):
 W_INT = 22    # interior pair (omega == 1)
 W_ARC = 600   # boundary-crossing pair (4-vertex polygon arc weight)
+# FP64 thread-instruction peak: 148 SMs x 64 FP64 lanes x f_clk
+FP64_PEAK_AT_MAX = 148 * 64 * 1.965e9
+F_MAX_HZ = 1.965e9
+ISSUE_PER_CLK = 148 * 4  # warp-instructions issued per clock (4 schedulers per SM)
 GRID_BYTES_PER_POINT = 88  # K1 algorithmic bytes per point
 
 
@@ -49,10 +57,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4")
     ap.add_argument("--sims", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-sims", type=int, default=1)
+    ap.add_argument("--cpu-sample-sims", type=int, default=1,
+                    help="CSR realisations in our line's cpu_baseline sample")
     ap.add_argument("--cpu-sample-frac", type=float, default=1.0,
                     help="CPU reference sample: every (1/frac)-th observed point (pairs/s is "
                          "per pair, so a subsample keeps the metric comparable)")
@@ -151,17 +160,38 @@ def subsample(x, y, t, frac):
     return x[::k], y[::k], t[::k]
 
 
-def cpu_reference_step(x, y, t, cfg, s, tv, sample_sims, workers):
-    """One bounded sample of the workload through the reference's rt::run_job."""
+def ref_job(x, y, t, cfg, s, tv, workers):
+    """The reference's rt::run_job planned once on the observed points (timed:
+    build_plan is part of the job, runtime.cpp:200-204)."""
     from oracle import ref
 
-    partitions = 4 * workers
     t0 = time.perf_counter()
-    r = ref.run_job(x, y, t, cfg.ring(), 0, cfg.period_s, s, tv, sims=sample_sims, seed=cfg.seed,
-                    method=0, partitions=partitions, workers=workers,
-                    use_index=(cfg.name != "C3"), use_cache=False)
-    dt = time.perf_counter() - t0
-    return r["in_threshold"], dt
+    job = ref.Job(x, y, t, cfg.ring(), 0, cfg.period_s, s, tv, seed=cfg.seed, method=0,
+                  partitions=4 * workers, workers=workers, use_index=(cfg.name != "C3"),
+                  use_cache=False)
+    return job, time.perf_counter() - t0
+
+
+def ref_pattern(job, which):
+    """One pattern of the job through rt::run_job's loop body (runtime.cpp:216-239):
+    the observed pattern (which < 0) or CSR realisation `which` (seed + which),
+    generation included.  Returns (in-threshold pairs, seconds)."""
+    t0 = time.perf_counter()
+    r = job.pattern(which)
+    return r["in_threshold"], time.perf_counter() - t0
+
+
+def extrapolate(t_plan, obs, csr, sims):
+    """Full-job estimate from measured patterns: T = T_plan + T_obs + m * mean(T_csr),
+    pairs = P_obs + m * mean(P_csr).  obs, csr: (pairs, seconds)."""
+    p_obs, t_obs = obs
+    if csr:
+        p_csr = sum(p for p, _ in csr) / len(csr)
+        t_csr = sum(d for _, d in csr) / len(csr)
+    else:  # no realisation measured: the observed pattern's rate stands for them
+        p_csr, t_csr = p_obs, t_obs
+    secs = t_plan + t_obs + sims * t_csr
+    return p_obs + sims * p_csr, secs
 
 
 def run_reference(args):
@@ -173,33 +203,37 @@ def run_reference(args):
 
     x, y, t = subsample(*observed_points_cpu(cfg), args.cpu_sample_frac)
     workers = os.cpu_count() or 1
-    kind = "reference" if oracle.ref_available() else "port"
-    if kind != "reference":
+    if not oracle.ref_available():
         print(json.dumps({"impl": "reference",
                           "unavailable": "oracle/_ref (reference compiled from source) not built"}))
         return
-    sample_sims = args.cpu_sample_sims
-    for _ in range(args.warmup):
-        cpu_reference_step(x, y, t, cfg, s, tv, sample_sims, workers)
-    pairs = 0
-    secs = 0.0
-    for _ in range(args.steps):
-        p, dt = cpu_reference_step(x, y, t, cfg, s, tv, sample_sims, workers)
-        pairs += p
-        secs += dt
+    job, t_plan = ref_job(x, y, t, cfg, s, tv, workers)
+    # warm-up: realisations from the top of the seed ladder (not reused below)
+    for i in range(args.warmup):
+        ref_pattern(job, max(sims - 1 - i, 0))
+    obs = ref_pattern(job, -1)
+    csr = [ref_pattern(job, r) for r in range(max(args.steps - 1, 0))]
+    job.close()
+    pairs, secs = extrapolate(t_plan, obs, csr, sims)
     value = pairs / secs
-    sample = (f"{cfg.name} observed pattern ({len(x)} points) + {sample_sims} CSR realisation(s) per step "
-              f"(of 1+{sims}), rt::run_job LocalExecutor({workers}), KDB {4 * workers} partitions, "
+    measured = obs[1] + sum(d for _, d in csr)
+    sample = (f"{cfg.name} at full N: observed pattern ({len(x)} points, {obs[1]:.2f} s) + "
+              f"{len(csr)} CSR realisations (mean {extrapolate(0, obs, csr, 1)[1] - obs[1]:.2f} s) "
+              f"through rt::run_job's loop body, plan {t_plan:.2f} s; full job of 1+{sims} "
+              f"extrapolated as T_plan + T_obs + {sims} x mean(T_csr) = {secs:.1f} s; "
+              f"LocalExecutor({workers}), KDB {4 * workers} partitions, "
               f"index {'on' if cfg.name != 'C3' else 'off'}, cache off")
     line = {
         "impl": "reference", "metric": "space-time in-threshold pairs evaluated per second",
         "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * measured / max(args.steps, 1),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_dict(cfg, sims, world),
-        "realisations_per_s": args.steps * (1 + sample_sims) / secs,
-        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": workers, "kind": kind,
-                         "sample": sample},
+        "realisations_per_s": (1 + sims) / secs,
+        "job_seconds_extrapolated": secs,
+        "pairs_per_job": pairs,
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": workers,
+                         "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -372,7 +406,11 @@ def run_ours(args):
 
     value = pairs / (ms * 1e-3)
     e2e_value = pairs / (e2e_ms * 1e-3)
-    peak = dev.fp64_peak()
+    # SURVEY §8(d) roofline denominator at the clock observed during the timed
+    # region: 148 SMs x 64 FP64 lanes x f_clk (1.86e13 /s at 1965 MHz)
+    f_clk = (clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0) * 1e6
+    peak = FP64_PEAK_AT_MAX * f_clk / F_MAX_HZ
+    dfma = dev.fp64_peak()  # live DFMA micro-benchmark (side note)
     # roofline of the pair kernel: algorithmic FP64 instructions / pair-kernel time
     instr = (pairs - arcs) * W_INT + arcs * W_ARC
     achieved = instr / (pair_ms * 1e-3) if pair_ms > 0 else 0.0
@@ -382,6 +420,17 @@ def run_ours(args):
         hbm_peak = peaks.get("hbm_gbs")
     except Exception:
         hbm_peak = None
+    cap = ncu_capture(cfg.name, n, sims)
+    pair_rate = pairs / (pair_ms * 1e-3) if pair_ms > 0 else 0.0
+    issue = None
+    if cap and cap.get("warp_instructions") and pairs:
+        wipp = cap["warp_instructions"] / (pairs / args.steps)  # per in-threshold ordered pair
+        issue = {"bound": "issue", "warp_instr_per_pair": wipp,
+                 "achieved": wipp * pair_rate / 1e12, "peak": ISSUE_PER_CLK * f_clk / 1e12,
+                 "unit": "T warp-instr/s",
+                 "frac": wipp * pair_rate / (ISSUE_PER_CLK * f_clk),
+                 "note": "ncu warp-instructions per launch / in-threshold ordered pairs per "
+                         "launch x the live pair rate / (148 SMs x 4 schedulers x f_clk)"}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -409,12 +458,16 @@ def run_ours(args):
                 "realisations_per_s": patterns / (e2e_ms * 1e-3)},
         "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                      "unit": "FP64 Tinstr/s", "frac": achieved / peak if peak else None,
-                     "traffic": ncu_capture(cfg.name)[0],
-                     "hw": hw_view(ncu_capture(cfg.name)[1], pairs / args.steps, peak),
-                     "note": f"pair kernel: ({W_INT} x interior + {W_ARC} x arc (omega != 1) pairs) "
-                             "FP64 instr / CUDA-event pair-kernel time; peak = live DFMA "
-                             "microbenchmark (stk_measure_fp64_peak)",
+                     "traffic": cap["dram_bytes"] if cap else None,
+                     "note": f"pair kernel: ({W_INT} x interior + {W_ARC} x arc (omega != 1) "
+                             "in-threshold pairs) FP64 instr / CUDA-event pair-kernel time; "
+                             "peak = 148 SMs x 64 lanes x f_clk (SURVEY 8(d)) at the median "
+                             "SM clock of the timed region; traffic = ncu DRAM bytes per launch "
+                             "of the capture stamped with this build's source hash",
+                     "f_clk_mhz": f_clk / 1e6, "dfma_microbench_peak": dfma / 1e12,
                      "kernel_ms_per_step": pair_ms / args.steps,
+                     "issue": issue,
+                     "hw": cap,
                      "grid_build": {"bound": "hbm", "achieved": grid_gbs, "peak": hbm_peak,
                                     "unit": "GB/s", "frac": (grid_gbs / hbm_peak)
                                     if grid_gbs and hbm_peak else None,
@@ -430,32 +483,33 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def hw_view(hw, pairs_per_launch, peak):
-    """SASS-counted FP64 instructions per in-threshold pair and the FP64 rate
-    they imply over the captured launch (one pair-kernel launch per step)."""
-    if hw and hw.get("fp64_thread_instructions") and pairs_per_launch:
-        f = hw["fp64_thread_instructions"]
-        hw["fp64_sass_instr_per_pair"] = f / pairs_per_launch
-        hw["fp64_sass_rate_frac"] = (f / (hw["duration_ms"] * 1e-3)) / peak if peak else None
-    return hw
-
-
-def ncu_capture(cfg_name):
-    """Per-launch figures of the pair kernel from the committed ncu capture of
-    this workload (profiles/pair_kernel_ncu_r1.json, keyed by config): DRAM
-    bytes read + written and the SM issue / FP64-pipe utilisation, or None."""
+def ncu_capture(cfg_name, n, sims):
+    """Per-launch hardware figures of the pair kernel from the committed ncu
+    capture of this workload (profiles/pair_kernel_ncu.json, written by
+    profiles/ncu_json.py): used only when the capture's source hash equals this
+    build's (paper_1912_04753_b200.build.source_hash) and its workload matches;
+    otherwise None (a stale capture is never reported)."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "pair_kernel_ncu_r1.json")))[cfg_name]
+        from paper_1912_04753_b200 import build
+
+        d = json.load(open(os.path.join(ROOT, "profiles", "pair_kernel_ncu.json")))[cfg_name]
+        if d.get("src_hash") != build.source_hash():
+            return None
+        if d.get("n") not in (None, n) or d.get("sims") not in (None, sims):
+            return None
     except Exception:
-        return None, None
-    hw = {"bound": "issue", "issue_active": d["issue_active"],
-          "fp64_pipe_active": d["fp64_pipe_active"], "warps_active": d["warps_active"],
-          "fp64_thread_instructions": d.get("fp64_thread_instructions"),
-          "duration_ms": d["duration_ms"], "source": d["capture"]}
-    return d["dram_bytes_read"] + d["dram_bytes_write"], hw
+        return None
+    keys = ("issue_active", "fp64_pipe_active", "warps_active", "warp_instructions",
+            "fp64_thread_instructions", "duration_ms", "capture", "src_hash")
+    out = {k: d.get(k) for k in keys}
+    out["dram_bytes"] = d["dram_bytes_read"] + d["dram_bytes_write"]
+    return out
 
 
 def cpu_baseline(cfg, s, tv, sims, x, y, t, sample_sims):
+    """Our line's CPU baseline: the reference's rt::run_job loop body on all host
+    cores, observed pattern + `sample_sims` CSR realisations at full N, the full
+    job extrapolated as in the reference arm."""
     try:
         import oracle
 
@@ -463,10 +517,17 @@ def cpu_baseline(cfg, s, tv, sims, x, y, t, sample_sims):
             return {"value": None, "unit": "pairs/s", "cores": 0, "kind": "reference",
                     "sample": "oracle/_ref not built"}
         workers = os.cpu_count() or 1
-        pairs, dt = cpu_reference_step(x, y, t, cfg, s, tv, sample_sims, workers)
-        return {"value": pairs / dt, "unit": "pairs/s", "cores": workers, "kind": "reference",
-                "sample": f"{cfg.name} observed ({len(x)} points) + {sample_sims} CSR realisation(s) through the "
-                          f"reference rt::run_job, LocalExecutor({workers}), {dt:.1f} s"}
+        job, t_plan = ref_job(x, y, t, cfg, s, tv, workers)
+        obs = ref_pattern(job, -1)
+        csr = [ref_pattern(job, r) for r in range(sample_sims)]
+        job.close()
+        pairs, secs = extrapolate(t_plan, obs, csr, sims)
+        return {"value": pairs / secs, "unit": "pairs/s", "cores": workers, "kind": "reference",
+                "realisations_per_s": (1 + sims) / secs,
+                "sample": f"{cfg.name} observed ({len(x)} points, {obs[1]:.1f} s) + "
+                          f"{len(csr)} CSR realisation(s) through the reference's rt::run_job "
+                          f"loop body, LocalExecutor({workers}); full job of 1+{sims} "
+                          f"extrapolated: {secs:.1f} s"}
     except Exception as e:  # the baseline is reported, never the target
         return {"value": None, "unit": "pairs/s", "cores": 0, "kind": "reference",
                 "sample": f"failed: {e}"}

@@ -51,6 +51,7 @@ typedef struct {
   double total_ms;             /* device time of the whole call                      */
   uint64_t kernel_launches;    /* libstk kernels launched by the call                */
   uint64_t arc_pairs;          /* in-threshold ordered pairs with omega != 1          */
+  uint64_t batches;            /* pattern batches the call ran (memory budget)       */
 } stk_telemetry;
 
 /* ---- context-free validation (no device needed) ------------------------- */

@@ -139,6 +139,16 @@ def _load_ref():
                                         C.POINTER(C.c_int64)]
         lib.ref_pair_counts.restype = C.c_int
         lib.ref_pair_counts.argtypes = [_dp, _dp, _ip, _u64, _dp, _u32, _ip, _u32, _up]
+        lib.ref_pair_counts_indexed.restype = C.c_int
+        lib.ref_pair_counts_indexed.argtypes = [_dp, _dp, _ip, _u64, _dp, _u32, _ip, _u32,
+                                                C.c_int, _up, _up]
+        lib.ref_job_open.restype = C.c_void_p
+        lib.ref_job_open.argtypes = [_dp, _dp, _ip, _u64, _dp, _u32, _i64, _i64, _dp, _u32,
+                                     _ip, _u32, _u64, C.c_int, _u32, C.c_int, C.c_int, C.c_int]
+        lib.ref_job_pattern.restype = C.c_int
+        lib.ref_job_pattern.argtypes = [C.c_void_p, _i64, _dp, _dp, _up, _up]
+        lib.ref_job_close.restype = None
+        lib.ref_job_close.argtypes = [C.c_void_p]
         lib.ref_brute_force_k.restype = C.c_int
         lib.ref_brute_force_k.argtypes = [_dp, _dp, _ip, _u64, _dp, _u32, _i64, _i64,
                                           _dp, _u32, _ip, _u32, _dp]
@@ -408,6 +418,56 @@ class ref:
         _check(lib, lib.ref_pair_counts(_f64(x), _f64(y), _i64a(t), len(x), s, len(s), tv,
                                         len(tv), out))
         return out.reshape(len(s), len(tv))
+
+    @staticmethod
+    def pair_counts_indexed(x, y, t, s_values, t_values, threads=0):
+        """Per-bin counts over the reference's STR R-tree (threaded)."""
+        lib = _load_ref()
+        s, tv = _f64(s_values), _i64a(t_values)
+        out = np.zeros(len(s) * len(tv), np.uint64)
+        tot = np.zeros(1, np.uint64)
+        _check(lib, lib.ref_pair_counts_indexed(_f64(x), _f64(y), _i64a(t), len(x), s, len(s),
+                                                tv, len(tv), int(threads), out, tot))
+        return out.reshape(len(s), len(tv))
+
+    class Job:
+        """rt::run_job split per pattern (ref_job_open / ref_job_pattern): plan once on
+        the observed points, then run the observed pattern (``pattern(-1)``) or
+        realisation r (``pattern(r)``: sim::generate with seed + r) through the
+        reference's make_tasks -> LocalExecutor::run -> aggregate -> to_l."""
+
+        def __init__(self, x, y, t, ring, p0, p1, s_values, t_values, seed, method=0,
+                     partitions=1, workers=0, use_index=True, use_cache=False):
+            lib = _load_ref()
+            rr, nv = _ring(ring)
+            self._s, self._tv = _f64(s_values), _i64a(t_values)
+            self._keep = (_f64(x), _f64(y), _i64a(t), rr)
+            self._h = lib.ref_job_open(self._keep[0], self._keep[1], self._keep[2], len(x), rr,
+                                       nv, p0, p1, self._s, len(self._s), self._tv,
+                                       len(self._tv), seed, method, partitions, int(workers),
+                                       int(use_index), int(use_cache))
+            if not self._h:
+                raise OracleError(lib.ref_last_error().decode())
+
+        def pattern(self, which):
+            lib = _load_ref()
+            shp = (len(self._s), len(self._tv))
+            k = np.zeros(shp); l = np.zeros(shp)
+            pairs = np.zeros(1, np.uint64); comps = np.zeros(1, np.uint64)
+            _check(lib, lib.ref_job_pattern(self._h, int(which), k.reshape(-1), l.reshape(-1),
+                                            pairs, comps))
+            return dict(k=k, l=l, in_threshold=int(pairs[0]), comparisons=int(comps[0]))
+
+        def close(self):
+            if self._h:
+                _load_ref().ref_job_close(self._h)
+                self._h = None
+
+        def __del__(self):
+            try:
+                self.close()
+            except Exception:
+                pass
 
     @staticmethod
     def brute_force_k(x, y, t, ring, p0, p1, s_values, t_values):

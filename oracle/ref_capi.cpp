@@ -15,11 +15,19 @@
 //   ref_pair_counts      -> per-bin counts from geom::spatial_distance /
 //                           temporal_distance / est::bin_pair (the reference
 //                           exposes only the total)
+//   ref_pair_counts_indexed -> the same per-bin counts over index::STRTree::range_query
+//                           (core/src/st_index.cpp:108-130), centers split over threads
+//   ref_job_open / ref_job_pattern / ref_job_close -> rt::run_job's body split per
+//                           pattern (core/src/runtime.cpp:190-249): plan once, then the
+//                           observed pattern or realisation r (seed + r) through
+//                           make_tasks -> executor.run -> aggregate -> to_l
 //   ref_brute_force_k    -> testutil::brute_force_k (tests/helpers.hpp:95-139)
 //   ref_*_ring / ref_*_points -> the reference test generators (tests/helpers.hpp:18-90)
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -30,6 +38,7 @@
 #include "stripley/rng.hpp"
 #include "stripley/runtime.hpp"
 #include "stripley/simulation.hpp"
+#include "stripley/st_index.hpp"
 
 using namespace stripley_ref;
 
@@ -250,6 +259,134 @@ int ref_pair_counts(const double* x, const double* y, const int64_t* t, uint64_t
       }
   });
 }
+
+// Per-bin counts as above, over the reference's own STR R-tree: every center's
+// cylinder query (estimator.cpp:150-167) with centers split round-robin over
+// threads (the tree is immutable and safe for concurrent queries,
+// st_index.hpp:26-27).  Test infrastructure for patterns too large for the
+// O(n^2) loop.
+int ref_pair_counts_indexed(const double* x, const double* y, const int64_t* t, uint64_t n,
+                            const double* s_values, uint32_t cs, const int64_t* t_values,
+                            uint32_t ct, int threads, uint64_t* out_counts,
+                            uint64_t* out_in_threshold) {
+  return guarded([&] {
+    const auto grid = make_grid(s_values, cs, t_values, ct);
+    grid.validate();
+    const auto pts = make_points(x, y, t, n);
+    std::vector<index::IndexedPoint> indexed(n);
+    for (uint64_t i = 0; i < n; ++i) indexed[i] = {pts[i], static_cast<uint32_t>(i)};
+    const auto tree = index::STRTree::build(std::move(indexed), 16);
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned nt = threads > 0 ? static_cast<unsigned>(threads) : hw;
+    std::vector<std::vector<uint64_t>> part(nt, std::vector<uint64_t>(size_t(cs) * ct, 0));
+    std::vector<std::thread> pool;
+    for (unsigned w = 0; w < nt; ++w)
+      pool.emplace_back([&, w] {
+        geom::STCylinder cyl;
+        cyl.spatial_radius = grid.s_max();
+        cyl.temporal_radius = grid.t_max();
+        auto& cnt = part[w];
+        for (uint64_t i = w; i < n; i += nt) {
+          cyl.center = pts[i];
+          for (const auto& item : tree.range_query(cyl)) {
+            if (item.record_index == i) continue;
+            const double d = geom::spatial_distance(pts[i], item.pt);
+            const int64_t u = geom::temporal_distance(pts[i], item.pt);
+            const auto bin = est::bin_pair(grid, d, u);
+            if (bin) ++cnt[bin->first * ct + bin->second];
+          }
+        }
+      });
+    for (auto& th : pool) th.join();
+    uint64_t total = 0;
+    for (size_t b = 0; b < size_t(cs) * ct; ++b) {
+      uint64_t c = 0;
+      for (unsigned w = 0; w < nt; ++w) c += part[w][b];
+      out_counts[b] = c;
+      total += c;
+    }
+    if (out_in_threshold) *out_in_threshold = total;
+  });
+}
+
+// rt::run_job (core/src/runtime.cpp:190-249) split per pattern so a caller can
+// time or check one pattern at a time: ref_job_open validates and plans once
+// (build_plan on the observed points, as run_job does); ref_job_pattern(which)
+// runs the observed pattern (which < 0: make_tasks -> executor.run(false) ->
+// aggregate -> to_l) or realisation r = which (sim::generate(method, n, points,
+// region, seed + r) -> make_tasks -> executor.run(true) -> aggregate -> to_l),
+// the exact loop body of run_job.
+struct RefJob {
+  geom::StudyRegion region;
+  std::vector<geom::STPoint> points;
+  rt::JobSpec spec;
+  rt::JobPlan plan;
+  std::unique_ptr<rt::LocalExecutor> exec;
+  RefJob(geom::StudyRegion r) : region(std::move(r)) {}
+};
+
+void* ref_job_open(const double* x, const double* y, const int64_t* t, uint64_t n,
+                   const double* ring_xy, uint32_t nv, int64_t p0, int64_t p1,
+                   const double* s_values, uint32_t cs, const int64_t* t_values, uint32_t ct,
+                   uint64_t seed, int method, uint32_t partitions, int workers, int use_index,
+                   int use_cache) {
+  RefJob* job = nullptr;
+  const int rc = guarded([&] {
+    auto j = std::make_unique<RefJob>(make_region(ring_xy, nv, p0, p1));
+    j->points = make_points(x, y, t, n);
+    auto& spec = j->spec;
+    spec.grid = make_grid(s_values, cs, t_values, ct);
+    spec.method = method == 0 ? sim::Method::Cstr
+                  : method == 1 ? sim::Method::Bootstrap
+                                : sim::Method::Permutation;
+    spec.seed = seed;
+    spec.options.use_index = use_index != 0;
+    spec.options.use_cache = use_cache != 0;
+    spec.partitions = partitions;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    spec.workers = workers > 0 ? static_cast<uint32_t>(workers) : hw;
+    spec.time_unit = geom::TimeUnit::Seconds;
+    spec.grid.validate();
+    if (j->points.size() < 2) throw std::invalid_argument("K estimation needs n >= 2");
+    for (const auto& p : j->points)
+      if (!j->region.contains(p))
+        throw std::invalid_argument("point outside study region or period");
+    j->plan = rt::build_plan(j->points, j->region, spec);
+    j->exec = std::make_unique<rt::LocalExecutor>(spec.workers, j->region, spec.grid,
+                                                  spec.options);
+    j->exec->broadcast_plan(j->plan);
+    job = j.release();
+  });
+  return rc == 0 ? job : nullptr;
+}
+
+int ref_job_pattern(void* handle, int64_t which, double* out_k, double* out_l,
+                    uint64_t* out_in_threshold, uint64_t* out_comparisons) {
+  return guarded([&] {
+    auto* j = static_cast<RefJob*>(handle);
+    const auto& spec = j->spec;
+    std::vector<geom::STPoint> sim_points;
+    const bool sim_phase = which >= 0;
+    if (sim_phase)
+      sim_points = sim::generate(spec.method, j->points.size(), j->points, j->region,
+                                 spec.seed + static_cast<uint64_t>(which));
+    const auto& pts = sim_phase ? sim_points : j->points;
+    const auto tasks = rt::make_tasks(j->plan, pts, spec, nullptr);
+    const auto partials = j->exec->run(tasks, sim_phase);
+    uint64_t in_thr = 0, comps = 0;
+    for (const auto& p : partials) {
+      in_thr += p.in_threshold_pairs;
+      comps += p.pair_comparisons;
+    }
+    const auto k = rt::aggregate(partials, pts.size(), j->region, spec.grid);
+    if (out_k) flatten(k, out_k);
+    if (out_l) flatten(est::to_l(k), out_l);
+    if (out_in_threshold) *out_in_threshold = in_thr;
+    if (out_comparisons) *out_comparisons = comps;
+  });
+}
+
+void ref_job_close(void* handle) { delete static_cast<RefJob*>(handle); }
 
 int ref_brute_force_k(const double* x, const double* y, const int64_t* t, uint64_t n,
                       const double* ring_xy, uint32_t nv, int64_t p0, int64_t p1,

@@ -31,6 +31,7 @@ class StkTelemetry(C.Structure):
         ("total_ms", C.c_double),
         ("kernel_launches", C.c_uint64),
         ("arc_pairs", C.c_uint64),
+        ("batches", C.c_uint64),
     ]
 
     def as_dict(self):

@@ -25,6 +25,22 @@ NVCC_FLAGS = [
 ]
 
 
+def source_hash() -> str:
+    """Hash of everything libstk.so is built from (sources, headers, flags): the
+    stamp that ties a committed ncu capture to the build it profiled."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for f in SOURCES + HEADERS + CXX_SOURCES:
+        with open(os.path.join(CSRC, f), "rb") as fh:
+            h.update(f.encode() + b"\0" + fh.read())
+    for f in ("stk.h", "stripley_gpu.hpp"):
+        with open(os.path.join(ROOT, "include", f), "rb") as fh:
+            h.update(f.encode() + b"\0" + fh.read())
+    h.update(" ".join(NVCC_FLAGS).encode())
+    return h.hexdigest()[:16]
+
+
 def _nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
         if cand and (os.path.isabs(cand) and os.path.exists(cand) or not os.path.isabs(cand)):

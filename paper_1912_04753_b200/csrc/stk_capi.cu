@@ -758,6 +758,7 @@ void fill_telemetry(stk_ctx* c, Timers& tm, stk_telemetry* tel, uint64_t pattern
   tel->exact_path_pairs += st[2];
   tel->arc_pairs += st[4];
   tel->patterns += patterns;
+  tel->batches += tm.pair.size();
   tel->kernel_launches += c->launches;
   tel->gen_ms += elapsed(tm.gen);
   tel->grid_ms += elapsed(tm.grid);

@@ -1,6 +1,12 @@
-"""Write profiles/pair_kernel_ncu_r1.json from pair-kernel ncu captures.
-Usage: python profiles/ncu_json.py C2=profiles/pair_kernel_r1.ncu-rep [C4=...]
-(bench.py reports these per-launch figures as roofline.traffic / roofline.hw.)"""
+"""Write profiles/pair_kernel_ncu.json from pair-kernel ncu captures.
+
+Usage: python profiles/ncu_json.py --hash H C4=profiles/pair_kernel_C4_r2.ncu-rep[:n:sims] ...
+
+H is the libstk source hash of the build that was profiled
+(paper_1912_04753_b200.build.source_hash(), written next to the capture by
+tools/gpu_round.sh).  bench.py reports these per-launch figures as
+roofline.traffic / roofline.hw / roofline.issue only when H equals the hash of
+the build it runs (a stale capture is never reported)."""
 import csv
 import io
 import json
@@ -20,16 +26,28 @@ WANT = {
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1, "us": 1e-3, "ns": 1e-6,
          "%": 0.01, "inst": 1}
 
-out = {}
-path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "pair_kernel_ncu_r1.json")
-for arg in sys.argv[1:]:
+path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "pair_kernel_ncu.json")
+try:
+    out = json.load(open(path))
+except Exception:
+    out = {}
+args = sys.argv[1:]
+src_hash = None
+if args[:1] == ["--hash"]:
+    src_hash, args = args[1], args[2:]
+for arg in args:
     cfg, rep = arg.split("=", 1)
+    n = sims = None
+    if rep.count(":") == 2:
+        rep, n, sims = rep.split(":")
+        n, sims = int(n), int(sims)
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     head, units, vals = rows[0], rows[1], rows[2]
     rec = {"capture": f"profiles/{os.path.basename(rep)} (ncu --set full --clock-control none)",
-           "kernel": vals[head.index("Kernel Name")]}
+           "kernel": vals[head.index("Kernel Name")], "src_hash": src_hash, "n": n,
+           "sims": sims}
     for i, name in enumerate(head):
         if name in WANT and WANT[name] not in rec and vals[i].strip():
             v = float(vals[i].replace(",", "")) * SCALE.get(units[i], 1)

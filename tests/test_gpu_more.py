@@ -383,3 +383,47 @@ def test_utm_offset_clusters_integer_bucket_bins(api, port):
     tv = [86400, 7 * 86400, 30 * 86400, 90 * 86400]
     h = _compare(api, port, x, y, t, ring, p0, p1, s, tv)
     assert int(h["counts"].sum()) > 1_000_000
+
+
+def test_forced_multi_batch_bit_identical(api):
+    """run_pipeline's batch loop (stk_capi.cu): a job forced into >= 3 batches by
+    stk_set_memory_budget (the envelope fold across batches, per-batch seed
+    offsets of the ladder seed + r, observed pattern only in the first batch)
+    equals the single-batch job bit for bit, as do the realisations' L
+    surfaces and the in-threshold total (runtime.cpp:207-245)."""
+    import ctypes as C
+
+    from paper_1912_04753_b200 import _lib
+
+    est, geom, rt, sim, dev = api["est"], api["geom"], api["rt"], api["sim"], api["dev"]
+    ring, p0, p1 = square(5000.0, 0, 200 * 86400)
+    region = geom.StudyRegion(ring, p0, p1)
+    grid = est.DistanceGrid.regular(50.0, 500.0, 86400, 20 * 86400)
+    pts = sim.generate_cstr(20000, region, 99, device=0)
+    n, sims, seed = len(pts), 11, 123
+    shape = (grid.cells_s(), grid.cells_t())
+
+    def job():
+        outs = [np.zeros(shape) for _ in range(5)]
+        tel = _lib.StkTelemetry()
+        dev.check(dev.lib.stk_run_job(dev.h, _lib.ptr(pts.x), _lib.ptr(pts.y),
+                                      _lib.ptr(pts.t, C.c_int64), n, sims, seed, 0,
+                                      *[_lib.ptr(o) for o in outs], C.byref(tel)))
+        l_all, up, lo = sim.simulate(pts, region, grid, sim.Method.Cstr, 0, sims, seed, True,
+                                     device=0)
+        return outs, tel, l_all, up, lo
+
+    dev.configure(region, grid)
+    one, tel1, l1, u1, d1 = job()
+    assert tel1.batches == 1
+    try:
+        dev.set_memory_budget(6 << 20)  # ~4 patterns of 20k points per batch
+        many, teln, ln, un, dn = job()
+    finally:
+        dev.set_memory_budget(16 << 30)
+    assert teln.batches >= 3, teln.batches
+    for a, b in zip(one, many):
+        assert np.array_equal(a, b)
+    assert teln.in_threshold_pairs == tel1.in_threshold_pairs
+    assert np.array_equal(l1, ln) and np.array_equal(u1, un) and np.array_equal(d1, dn)
+    assert np.array_equal(many[2], ln.max(0)) and np.array_equal(many[3], ln.min(0))

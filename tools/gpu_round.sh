@@ -1,15 +1,17 @@
 #!/bin/bash
 # One GPU-box session: parity tests, the default bench line, the other configs,
-# the ncu launch list and one full capture of the pair kernel.
+# the ncu launch list and full captures of the pair kernel.
 #   gpurun --timeout 2400 -- 'bash tools/gpu_round.sh [tag] [stages]'
-# stages: any of t (tests) s (smoke) b (bench C2) c (other configs) p (polygons) l (launch list) f (ncu full)
-tag=${1:-r1}
+# stages: any of t (tests) s (smoke) b (bench default C4 + reference arm) c (other
+# configs) p (polygons) l (launch list) f (ncu full: C4 and C2)
+tag=${1:-r2}
 stages=${2:-tbclf}
 out=gpurun_out
 mkdir -p $out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $out/gpu_$tag.txt 2>&1
+python -c "from paper_1912_04753_b200 import build; print(build.source_hash())" > $out/src_hash_$tag.txt
 if [[ $stages == *t* ]]; then
-  timeout 900 python -m pytest tests -m gpu -x -q > $out/pytest_gpu_$tag.log 2>&1
+  timeout 1500 python -m pytest tests -m gpu -x -q -rs > $out/pytest_gpu_$tag.log 2>&1
   echo "pytest rc=$?" >> $out/pytest_gpu_$tag.log
 fi
 if [[ $stages == *s* ]]; then
@@ -17,19 +19,19 @@ if [[ $stages == *s* ]]; then
   echo "smoke rc=$?" >> $out/smoke_$tag.log
 fi
 if [[ $stages == *b* ]]; then
-  timeout 400 python bench.py > $out/bench_$tag.json 2> $out/bench_$tag.err
+  timeout 900 python bench.py --steps 20 --warmup 5 > $out/bench_$tag.json 2> $out/bench_$tag.err
   echo "bench rc=$?" >> $out/bench_$tag.err
-  timeout 400 python bench.py --impl reference --steps 2 --warmup 0 > $out/bench_ref_$tag.json 2> $out/bench_ref_$tag.err
+  timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $out/bench_ref_$tag.json 2> $out/bench_ref_$tag.err
 fi
 if [[ $stages == *c* ]]; then
-  for c in C1 C3 C4; do
-    timeout 400 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $out/bench_${c}_$tag.json 2> $out/bench_${c}_$tag.err
+  for c in C1 C2 C3; do
+    timeout 400 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > $out/bench_${c}_$tag.json 2> $out/bench_${c}_$tag.err
   done
-  timeout 600 python bench.py --config C5 --sims 1 --steps 2 --warmup 3 --no-cpu-baseline > $out/bench_C5_$tag.json 2> $out/bench_C5_$tag.err
+  timeout 900 python bench.py --config C5 --steps 2 --warmup 3 --no-cpu-baseline > $out/bench_C5_$tag.json 2> $out/bench_C5_$tag.err
 fi
 if [[ $stages == *p* ]]; then
   for v in 128 512 2048; do
-    timeout 600 python bench.py --ring $v --steps 2 --warmup 2 --cpu-sample-frac 0.1 > $out/bench_ring${v}_$tag.json 2> $out/bench_ring${v}_$tag.err
+    timeout 600 python bench.py --config C2 --ring $v --steps 2 --warmup 2 --cpu-sample-frac 0.1 > $out/bench_ring${v}_$tag.json 2> $out/bench_ring${v}_$tag.err
   done
 fi
 if [[ $stages == *l* ]]; then
@@ -39,8 +41,12 @@ if [[ $stages == *l* ]]; then
 fi
 if [[ $stages == *f* ]]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:pair_kernel -s 3 -c 1 \
-    -o $out/pair_kernel_$tag -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
-    > $out/ncu_full_$tag.log 2>&1
-  echo "ncu rc=$?" >> $out/ncu_full_$tag.log
+    -o $out/pair_kernel_C4_$tag -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+    > $out/ncu_full_C4_$tag.log 2>&1
+  echo "ncu rc=$?" >> $out/ncu_full_C4_$tag.log
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:pair_kernel -s 3 -c 1 \
+    -o $out/pair_kernel_C2_$tag -f python bench.py --config C2 --steps 1 --warmup 3 --no-cpu-baseline \
+    > $out/ncu_full_C2_$tag.log 2>&1
+  echo "ncu rc=$?" >> $out/ncu_full_C2_$tag.log
 fi
 echo done
