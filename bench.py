@@ -14,8 +14,10 @@ points and D2H of K, L, envelopes and diff inside the timed region).
 
 Multi-GPU (torchrun, one process per GPU): the job is split strong-scaling
 style — each rank takes a 1/N slice of the observed pattern's pair work and a
-contiguous block of realisations; two exact all-reduces (SUM of integer
-partials, MAX/MIN of envelopes) over NCCL combine them.
+contiguous block of realisations; one collective library call per step
+(stk_run_job_dist) combines them with two exact NCCL all-reduces on device
+buffers (SUM of integer limbs, MAX/MIN of envelopes) over the communicator the
+library holds.
 
 ``--impl reference`` times the reference's own CPU implementation
 (oracle/_ref: the unmodified reference sources, rt::run_job's own loop body
@@ -302,7 +304,10 @@ def run_ours(args):
     hy = torch.from_numpy(np.ascontiguousarray(y)).pin_memory()
     ht = torch.from_numpy(np.ascontiguousarray(t)).pin_memory()
     stream = torch.cuda.ExternalStream(dev.stream_handle())
-    executor = rt.DeviceExecutor(device=dev, rank=rank, world=world, group=group)
+    # N > 1 over NCCL: the executor joins a communicator inside the library (the
+    # unique id travels once over the torch.distributed group, outside timing)
+    executor = rt.DeviceExecutor(device=dev, rank=rank, world=world, group=group,
+                                 comm=(world > 1 and backend == "nccl"))
     r0, r1 = executor.sim_range(sims)
     spec = rt.JobSpec(grid=grid, sims=sims, seed=cfg.seed)
 
@@ -314,19 +319,25 @@ def run_ours(args):
 
     def step(device_resident: bool):
         tel = _lib.StkTelemetry()
-        if world == 1:
+        if world == 1 or executor.comm:
+            # one library call; at N > 1 a collective over the NCCL communicator
+            # inside the library (stk_run_job_dist: this rank's shard of the
+            # observed pattern + its block of realisations, exact device
+            # all-reduces, device finalize)
+            dist_ = executor.comm
             if device_resident:
-                rc = lib.stk_run_job_device(dev.h, dx.data_ptr(), dy.data_ptr(), dt.data_ptr(), n,
-                                            sims, cfg.seed, 0, P(out["k"]), P(out["l"]),
-                                            P(out["up"]), P(out["lo"]), P(out["diff"]),
-                                            C.byref(tel))
+                fn = lib.stk_run_job_dist_device if dist_ else lib.stk_run_job_device
+                rc = fn(dev.h, dx.data_ptr(), dy.data_ptr(), dt.data_ptr(), n, sims, cfg.seed, 0,
+                        P(out["k"]), P(out["l"]), P(out["up"]), P(out["lo"]), P(out["diff"]),
+                        C.byref(tel))
             else:
-                rc = lib.stk_run_job(dev.h, P(hx.numpy()), P(hy.numpy()),
-                                     P(ht.numpy(), C.c_int64), n, sims, cfg.seed, 0, P(out["k"]),
-                                     P(out["l"]), P(out["up"]), P(out["lo"]), P(out["diff"]),
-                                     C.byref(tel))
+                fn = lib.stk_run_job_dist if dist_ else lib.stk_run_job
+                rc = fn(dev.h, P(hx.numpy()), P(hy.numpy()), P(ht.numpy(), C.c_int64), n, sims,
+                        cfg.seed, 0, P(out["k"]), P(out["l"]), P(out["up"]), P(out["lo"]),
+                        P(out["diff"]), C.byref(tel))
             dev.check(rc)
         else:
+            # host-group emulation (STK_DIST_BACKEND=gloo: several ranks on one GPU)
             out["up"].fill(-np.inf)
             out["lo"].fill(np.inf)
             if device_resident:
@@ -453,8 +464,7 @@ def run_ours(args):
         "candidates_per_unordered_in_threshold_pair": (2 * cands / pairs) if pairs else None,
         "e2e": {"value": e2e_value, "unit": "pairs/s",
                 "h2d_bytes_per_step": int(24 * n),
-                "d2h_bytes_per_step": int(8 * bins * (5 if world == 1 else 0) +
-                                          (8 * bins * 5 if world > 1 else 0)),
+                "d2h_bytes_per_step": int(8 * bins * 5),  # K, L, upper, lower, diff
                 "realisations_per_s": patterns / (e2e_ms * 1e-3)},
         "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                      "unit": "FP64 Tinstr/s", "frac": achieved / peak if peak else None,

@@ -29,6 +29,7 @@ extern "C" {
 #define STK_EUNSUPPORTED 2 /* outside the path (cache tolerance != 0 ...) */
 #define STK_ECUDA 3        /* device / driver failure                     */
 #define STK_ESTATE 4       /* region or grid not set                      */
+#define STK_ENCCL 5        /* NCCL unavailable or a collective failed     */
 
 #define STK_METHOD_CSR 0         /* sim::Method::Cstr        */
 #define STK_METHOD_BOOTSTRAP 1   /* sim::Method::Bootstrap   */
@@ -164,6 +165,35 @@ int stk_run_job_shard_device(stk_ctx* ctx, const double* d_x, const double* d_y,
                              uint64_t* obs_sum_hi, uint64_t* obs_sum_lo, double* upper_l,
                              double* lower_l, stk_telemetry* tel);
 
+/* ---- multi-GPU: one process (or thread) per GPU, NCCL inside the context --
+ * Replaces the reference's DistributedExecutor + TCP workers
+ * (core/src/distributed.cpp:116-245, core/include/stripley/distributed.hpp):
+ * rank 0 creates an id with stk_comm_unique_id, every rank receives it by any
+ * out-of-band means and calls stk_comm_init on its own context.  libnccl.so.2
+ * is loaded on first use (STK_ENCCL when absent). */
+#define STK_NCCL_ID_BYTES 128
+int stk_comm_unique_id(unsigned char* id_out /* STK_NCCL_ID_BYTES */);
+int stk_comm_init(stk_ctx* ctx, const unsigned char* id, int nranks, int rank);
+int stk_comm_destroy(stk_ctx* ctx);
+/* Rank and size of the context's communicator (STK_ESTATE and 0 / 1 when none). */
+int stk_comm_rank(stk_ctx* ctx, int* rank, int* nranks);
+
+/* rt::run_job as a collective over the context's communicator: every rank
+ * passes the same observed points and arguments; rank g computes shard g of
+ * the observed pattern's pair work and its contiguous block of the
+ * realisations; the exact per-bin partials (integer limbs) are summed and the
+ * partial envelopes MAX/MIN-reduced with NCCL on the device, then K, L and
+ * diff are finalized on the device.  Every rank receives the full result,
+ * bit-identical to stk_run_job's at any number of ranks. */
+int stk_run_job_dist(stk_ctx* ctx, const double* x, const double* y, const int64_t* t, uint64_t n,
+                     uint32_t sims, uint64_t seed, int method, double* k_out, double* l_out,
+                     double* upper_l, double* lower_l, double* diff_upper, stk_telemetry* tel);
+/* Same with the observed pattern resident on the context's device. */
+int stk_run_job_dist_device(stk_ctx* ctx, const double* d_x, const double* d_y,
+                            const int64_t* d_t, uint64_t n, uint32_t sims, uint64_t seed,
+                            int method, double* k_out, double* l_out, double* upper_l,
+                            double* lower_l, double* diff_upper, stk_telemetry* tel);
+
 /* Raw CSR realisation points of generate_cstr(n, region, seed)
  * (core/src/simulation.cpp:10-24), generated on the device (host outputs). */
 int stk_generate_cstr(stk_ctx* ctx, uint64_t n, uint64_t seed, double* x, double* y,
@@ -180,6 +210,22 @@ int stk_generate(stk_ctx* ctx, int method, uint64_t n, const double* ox, const d
  * (STK_EINVAL "weight center outside study region" otherwise). */
 int stk_spatial_weights(stk_ctx* ctx, const double* cx, const double* cy, const double* d,
                         uint64_t count, double* w_out);
+
+/* rt::execute_task (core/include/stripley/runtime.hpp:96-99, core/src/runtime.cpp:73-117)
+ * for the reference's task interface (rt::Executor::run over TaskData): the
+ * pre-cumulative histogram of one task -- every (cylinder, point) candidate of
+ * the task, the center's own record skipped, within_cylinder with the
+ * cylinder's radii, bin_pair on the grid, 1/pair_weight summed exactly and
+ * rounded once per bin (NaN where the reference adds 1/0).  Points: px, py,
+ * pt, record index pidx (np of them); cylinders: center cx, cy, ct, center
+ * record index cidx, spatial radius crad, temporal radius ctrad (nc of them).
+ * A compatibility path (brute force over the task, like the reference's
+ * use_index = false branch): rt::run_job runs the fused device pipeline. */
+int stk_task_histogram(stk_ctx* ctx, const double* px, const double* py, const int64_t* pt,
+                       const uint32_t* pidx, uint64_t np, const double* cx, const double* cy,
+                       const int64_t* ct, const uint32_t* cidx, const double* crad,
+                       const int64_t* ctrad, uint64_t nc, double* hist, uint64_t* in_threshold,
+                       uint64_t* comparisons);
 
 /* ---- instrumentation --------------------------------------------------- */
 /* Device-measured FP64 issue peak (DFMA thread-instructions per second) at the

@@ -15,12 +15,16 @@
 // Errors: std::invalid_argument with the reference's messages; device
 // failures as std::runtime_error.  There is no CPU fallback.
 //
-// What differs, by design: rt::Executor is the device plug-in point (the
-// reference's KDB plan / TaskData decomposition is replaced by the on-device
-// grid), so run_job takes a DeviceExecutor; multi-process runs supply two
-// exact reduction hooks (see DeviceExecutor).
+// rt::Executor keeps the reference's virtuals (broadcast_plan / run /
+// collect_telemetry) and rt::LocalExecutor its constructor, so a program
+// written against runtime.hpp compiles unchanged; an executor that names a GPU
+// makes run_job take the fused device pipeline (the KDB plan / TaskData
+// decomposition is replaced by the on-device grid), and task lists given to
+// run() execute on the device.  Multi-GPU: DeviceExecutor with an NCCL
+// communicator inside the library (or two exact reduction hooks).
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <functional>
 #include <optional>
@@ -60,6 +64,19 @@ struct STEnvelope {
   std::int64_t envelope_id = 0;
 };
 
+/// geometry.hpp:62-69
+struct STCylinder {
+  STPoint center;
+  double spatial_radius = 0.0;
+  std::int64_t temporal_radius = 0;
+  TimeUnit temporal_unit = TimeUnit::Days;
+  bool operator==(const STCylinder&) const = default;
+};
+
+double spatial_distance(const STPoint& p, const STPoint& q);
+std::int64_t temporal_distance(const STPoint& p, const STPoint& q);
+bool within_cylinder(const STCylinder& cyl, const STPoint& p);
+
 /// Boundary-inclusive even-odd test (geometry.cpp:81-97), host side.
 bool point_in_polygon(const PlanarPoint& pt, const std::vector<PlanarPoint>& ring);
 
@@ -89,7 +106,29 @@ class StudyRegion {
 
 }  // namespace geom
 
+namespace index {
+/// st_index.hpp:12-19: a point plus the record index that identifies it.
+struct IndexedPoint {
+  geom::STPoint pt;
+  std::uint32_t record_index = 0;
+  bool operator==(const IndexedPoint&) const = default;
+};
+}  // namespace index
+
 namespace cache {
+/// weight_cache.hpp:13-25
+struct TableStats {
+  std::uint64_t hits = 0;
+  std::uint64_t misses = 0;
+  std::uint64_t insertions = 0;
+  TableStats& operator+=(const TableStats& o) {
+    hits += o.hits;
+    misses += o.misses;
+    insertions += o.insertions;
+    return *this;
+  }
+};
+
 /// At tolerance 0 the reference cache never changes results; the device
 /// recomputes weights per center.  Nonzero tolerances are rejected.
 class WeightCache {
@@ -206,15 +245,175 @@ struct JobSpec {
   geom::TimeUnit time_unit = geom::TimeUnit::Days;
 };
 
+/// runtime.hpp:35-38
+struct IndexedCylinder {
+  geom::STCylinder cyl;
+  std::uint32_t center_index = 0;
+};
+
+/// One unit of work (runtime.hpp:40-46): a partition's points plus every
+/// query cylinder assigned to it.
+struct TaskData {
+  std::uint32_t task_id = 0;
+  std::vector<index::IndexedPoint> points;
+  std::vector<IndexedCylinder> cylinders;
+};
+
+/// runtime.hpp:48-57
+struct PartialResult {
+  std::uint32_t task_id = 0;
+  std::uint32_t worker_id = 0;
+  std::vector<double> histogram;  // cells_s * cells_t, pre-cumulative
+  std::uint64_t pair_comparisons = 0;
+  std::uint64_t in_threshold_pairs = 0;
+  cache::TableStats spatial_cache;
+  cache::TableStats temporal_cache;
+};
+
+/// runtime.hpp:59-72, plus device counters.  On the device: one "partition"
+/// per pattern (the uniform grid replaces the KDB plan), so partition_count
+/// is 1 and cylinder_assignments counts one cylinder per point and pattern;
+/// the weight caches are replaced by per-center recomputation (stats stay 0);
+/// bytes_sent / bytes_received count host<->device and NCCL exchange bytes.
 struct RunTelemetry {
   std::uint64_t pair_comparisons = 0;
   std::uint64_t in_threshold_pairs = 0;
-  std::uint64_t exact_path_pairs = 0;
+  std::uint64_t cylinder_assignments = 0;
+  std::uint64_t partition_count = 0;
+  std::vector<std::uint64_t> partition_point_counts;
+  cache::TableStats spatial_cache;
+  cache::TableStats temporal_cache;
+  std::uint64_t bytes_sent = 0;
+  std::uint64_t bytes_received = 0;
   double plan_seconds = 0.0;
   double estimation_seconds = 0.0;
   double simulation_seconds = 0.0;
+  // device extras
+  std::uint64_t exact_path_pairs = 0;
   double device_ms = 0.0;
   double pair_kernel_ms = 0.0;
+};
+
+/// runtime.hpp:74-84.  The device's uniform space-time grid replaces the
+/// KDB partitioner (out of scope: it never changes results), so a plan has
+/// one partition holding every point and every cylinder.
+struct JobPlan {
+  PartitionerChoice choice = PartitionerChoice::Kdb;
+  std::uint32_t partitions = 1;
+  std::uint32_t locate(const geom::STPoint& p, std::uint32_t record_index) const {
+    (void)p;
+    (void)record_index;
+    return 0;
+  }
+  std::vector<std::uint32_t> assign(const geom::STCylinder& cyl) const {
+    (void)cyl;
+    return {0};
+  }
+};
+
+JobPlan build_plan(std::span<const geom::STPoint> points, const geom::StudyRegion& region,
+                   const JobSpec& spec);
+
+std::vector<TaskData> make_tasks(const JobPlan& plan, std::span<const geom::STPoint> dataset,
+                                 const JobSpec& spec, std::uint64_t* redundancy_out = nullptr);
+
+/// rt::execute_task on the device (stk_task_histogram).
+PartialResult execute_task(const TaskData& task, const geom::StudyRegion& region,
+                           const est::DistanceGrid& grid, const est::EstimatorOptions& options,
+                           cache::WeightCache* weight_cache = nullptr);
+
+/// Elementwise-sum partial histograms in task order, cumulative-sum, scale
+/// (runtime.cpp:119-136).
+est::KSurface aggregate(std::span<const PartialResult> partials, std::size_t n,
+                        const geom::StudyRegion& region, const est::DistanceGrid& grid);
+
+/// Task execution backend (runtime.hpp:106-117).  The reference's interface is
+/// kept verbatim; device() is this framework's extension: an executor that
+/// names a GPU (LocalExecutor, DeviceExecutor) lets run_job take the fused
+/// device pipeline, any other executor is driven through run() with tasks as
+/// the reference does.
+class Executor {
+ public:
+  virtual ~Executor() = default;
+  virtual void broadcast_plan(const JobPlan& plan) { (void)plan; }
+  virtual std::vector<PartialResult> run(const std::vector<TaskData>& tasks,
+                                         bool simulation_phase) = 0;
+  virtual void collect_telemetry(RunTelemetry& out) const = 0;
+  // ---- device extension
+  virtual int device() const { return -1; }
+  virtual std::uint32_t rank() const { return 0; }
+  virtual std::uint32_t world() const { return 1; }
+  /// world > 1: the context of device() holds an NCCL communicator (stk_comm_init)
+  virtual bool has_communicator() const { return false; }
+  /// world > 1 without a communicator: caller-supplied exact exchange hooks
+  virtual bool has_hooks() const { return false; }
+  virtual void allreduce_sum_u64(std::vector<std::uint64_t>& v) const { (void)v; }
+  virtual void allreduce_max_min(std::vector<double>& upper, std::vector<double>& lower) const {
+    (void)upper;
+    (void)lower;
+  }
+};
+
+/// The reference's in-process executor (runtime.hpp:119-136), on the GPU:
+/// `workers` is recorded (task t reports worker t mod workers) but the device
+/// replaces the thread pool; tasks run through execute_task on the device
+/// (STK_DEVICE, default 0).
+class LocalExecutor : public Executor {
+ public:
+  LocalExecutor(std::uint32_t workers, const geom::StudyRegion& region,
+                const est::DistanceGrid& grid, const est::EstimatorOptions& options);
+
+  std::vector<PartialResult> run(const std::vector<TaskData>& tasks,
+                                 bool simulation_phase) override;
+  void collect_telemetry(RunTelemetry& out) const override;
+  int device() const override { return device_; }
+
+ private:
+  std::uint32_t workers_;
+  const geom::StudyRegion& region_;
+  est::DistanceGrid grid_;
+  est::EstimatorOptions options_;
+  int device_;
+};
+
+/// One GPU per process.  world > 1 needs the exact exchange: either an NCCL
+/// communicator inside the library (the constructor taking the unique id of
+/// stk_comm_unique_id, distributed from rank 0 by any means) -- the
+/// DistributedExecutor replacement (distributed.cpp:116-245) -- or two
+/// caller-supplied hooks (in-place uint64 SUM of the exact limbs; in-place MAX
+/// of upper and MIN of lower).  Constructing world > 1 with neither throws.
+class DeviceExecutor : public Executor {
+ public:
+  using SumHook = std::function<void(std::vector<std::uint64_t>&)>;
+  using MaxMinHook = std::function<void(std::vector<double>&, std::vector<double>&)>;
+  explicit DeviceExecutor(int device = 0, std::uint32_t rank = 0, std::uint32_t world = 1,
+                          SumHook sum_u64 = {}, MaxMinHook max_min = {});
+  DeviceExecutor(int device, std::uint32_t rank, std::uint32_t world,
+                 const std::array<unsigned char, 128>& nccl_unique_id);
+  /// rank 0's side: a fresh NCCL unique id (stk_comm_unique_id)
+  static std::array<unsigned char, 128> nccl_unique_id();
+
+  std::vector<PartialResult> run(const std::vector<TaskData>& tasks,
+                                 bool simulation_phase) override;
+  void collect_telemetry(RunTelemetry& out) const override { (void)out; }
+  int device() const override { return device_; }
+  std::uint32_t rank() const override { return rank_; }
+  std::uint32_t world() const override { return world_; }
+  bool has_communicator() const override { return comm_; }
+  bool has_hooks() const override { return sum_ && maxmin_; }
+  void allreduce_sum_u64(std::vector<std::uint64_t>& v) const override {
+    if (sum_) sum_(v);
+  }
+  void allreduce_max_min(std::vector<double>& u, std::vector<double>& l) const override {
+    if (maxmin_) maxmin_(u, l);
+  }
+
+ private:
+  int device_;
+  std::uint32_t rank_, world_;
+  SumHook sum_;
+  MaxMinHook maxmin_;
+  bool comm_ = false;
 };
 
 struct RunResult {
@@ -227,52 +426,14 @@ struct RunResult {
   RunTelemetry telemetry;
 };
 
-/// The plug-in point of run_job (runtime.hpp:108-117 role).  One executor
-/// drives one GPU.  For one process per GPU (rank of world), the two exact
-/// exchange steps are supplied by the caller (e.g. NCCL all-reduces):
-///   allreduce_sum_u64: in-place SUM of a uint64 array across ranks
-///                      (observed pattern's exact per-bin partials, as limbs),
-///   allreduce_max_min: in-place MAX of `upper` and MIN of `lower`.
-class Executor {
- public:
-  virtual ~Executor() = default;
-  virtual int device() const = 0;
-  virtual std::uint32_t rank() const { return 0; }
-  virtual std::uint32_t world() const { return 1; }
-  virtual void allreduce_sum_u64(std::vector<std::uint64_t>& v) const { (void)v; }
-  virtual void allreduce_max_min(std::vector<double>& upper, std::vector<double>& lower) const {
-    (void)upper;
-    (void)lower;
-  }
-};
-
-class DeviceExecutor : public Executor {
- public:
-  explicit DeviceExecutor(int device = 0, std::uint32_t rank = 0, std::uint32_t world = 1,
-                          std::function<void(std::vector<std::uint64_t>&)> sum_u64 = {},
-                          std::function<void(std::vector<double>&, std::vector<double>&)>
-                              max_min = {})
-      : device_(device), rank_(rank), world_(world), sum_(std::move(sum_u64)),
-        maxmin_(std::move(max_min)) {}
-  int device() const override { return device_; }
-  std::uint32_t rank() const override { return rank_; }
-  std::uint32_t world() const override { return world_; }
-  void allreduce_sum_u64(std::vector<std::uint64_t>& v) const override {
-    if (sum_) sum_(v);
-  }
-  void allreduce_max_min(std::vector<double>& u, std::vector<double>& l) const override {
-    if (maxmin_) maxmin_(u, l);
-  }
-
- private:
-  int device_;
-  std::uint32_t rank_, world_;
-  std::function<void(std::vector<std::uint64_t>&)> sum_;
-  std::function<void(std::vector<double>&, std::vector<double>&)> maxmin_;
-};
-
+/// Full pipeline: plan, estimate, simulate, envelope (runtime.cpp:190-249).
+/// Simulation replicate r uses seed spec.seed + r.
 RunResult run_job(std::span<const geom::STPoint> points, const geom::StudyRegion& region,
                   const JobSpec& spec, Executor& executor);
+
+/// Performance ratios; both operands must be > 0 (runtime.hpp:155-157).
+double speedup_factor(double t_original, double t_optimized);
+double acceleration_factor(double t_standalone, double t_distributed);
 
 }  // namespace rt
 }  // namespace stripley

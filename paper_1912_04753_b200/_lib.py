@@ -14,7 +14,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("STK_LIB_PATH") or os.path.join(HERE, "libstk.so")
 
-STK_OK, STK_EINVAL, STK_EUNSUPPORTED, STK_ECUDA, STK_ESTATE = 0, 1, 2, 3, 4
+STK_OK, STK_EINVAL, STK_EUNSUPPORTED, STK_ECUDA, STK_ESTATE, STK_ENCCL = 0, 1, 2, 3, 4, 5
+NCCL_ID_BYTES = 128
 METHOD_CSR, METHOD_BOOTSTRAP, METHOD_PERMUTATION = 0, 1, 2
 
 
@@ -45,7 +46,9 @@ EXPORTED = [
     "stk_set_options", "stk_estimate_surface", "stk_pair_histogram", "stk_finalize",
     "stk_simulate", "stk_run_job", "stk_run_job_device", "stk_generate_cstr",
     "stk_spatial_weights", "stk_measure_fp64_peak", "stk_run_job_shard",
-    "stk_run_job_shard_device", "stk_generate",
+    "stk_run_job_shard_device", "stk_generate", "stk_comm_unique_id", "stk_comm_init",
+    "stk_comm_destroy", "stk_comm_rank", "stk_run_job_dist", "stk_run_job_dist_device",
+    "stk_task_histogram",
 ]
 
 _dp = C.POINTER(C.c_double)
@@ -79,6 +82,13 @@ _SIGS = {
     "stk_generate": (C.c_int, [_vp, C.c_int, _u64, _dp, _dp, _ip, _u64, _dp, _dp, _ip]),
     "stk_spatial_weights": (C.c_int, [_vp, _dp, _dp, _dp, _u64, _dp]),
     "stk_measure_fp64_peak": (C.c_int, [_vp, _dp]),
+    "stk_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "stk_comm_init": (C.c_int, [_vp, C.c_char_p, C.c_int, C.c_int]),
+    "stk_comm_destroy": (C.c_int, [_vp]),
+    "stk_comm_rank": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "stk_run_job_dist": (C.c_int, [_vp, _dp, _dp, _ip, _u64, _u32, _u64, C.c_int, _dp, _dp, _dp, _dp, _dp, _tp]),
+    "stk_run_job_dist_device": (C.c_int, [_vp, _vp, _vp, _vp, _u64, _u32, _u64, C.c_int, _dp, _dp, _dp, _dp, _dp, _tp]),
+    "stk_task_histogram": (C.c_int, [_vp, _dp, _dp, _ip, C.POINTER(C.c_uint32), _u64, _dp, _dp, _ip, C.POINTER(C.c_uint32), _dp, _ip, _u64, _dp, _up, _up]),
 }
 
 _lib = None

@@ -110,6 +110,22 @@ def build_cpp_tests(force: bool = False) -> str:
     return TEST_BIN
 
 
+REFPROG_BIN = os.path.join(ROOT, "tests", "cpp", "reference_program")
+
+
+def build_reference_program(force: bool = False) -> str:
+    """tests/cpp/reference_program.cpp: a program written against the reference's
+    runtime.hpp, compiled unchanged against include/stripley/ (the drop-in path)."""
+    src = os.path.join(ROOT, "tests", "cpp", "reference_program.cpp")
+    hdr = os.path.join(ROOT, "include", "stripley_gpu.hpp")
+    if not force and os.path.exists(REFPROG_BIN) and os.path.getmtime(REFPROG_BIN) > max(
+            os.path.getmtime(src), os.path.getmtime(LIB), os.path.getmtime(hdr)):
+        return REFPROG_BIN
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), src, "-o",
+                    REFPROG_BIN, "-L", HERE, "-lstk", "-Wl,-rpath," + HERE], check=True)
+    return REFPROG_BIN
+
+
 CLI_BIN = os.path.join(HERE, "stripley_gpu")
 CLI_SOURCES = ["stripley_cli.cpp", "stripley_io.cpp"]
 

@@ -10,6 +10,8 @@
 // All device work of one call is enqueued on the context stream; the host
 // synchronises once at the end (plus one tiny read-back for validation).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types and constants only: libnccl.so.2 is dlopen'ed on first use
 
 #include <algorithm>
 #include <cmath>
@@ -41,6 +43,57 @@ struct CudaFail : std::runtime_error {
 struct StateErr : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct NcclFail : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// NCCL entry points, resolved from libnccl.so.2 at the first communicator call
+// (the library loads, and single-GPU calls run, without NCCL installed; in a
+// process that already loaded torch's NCCL the soname resolves to that copy).
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  std::string load_error;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.load_error = std::string("libnccl.so.2 not found: ") + dlerror();
+      return a;
+    }
+    a.get_unique_id = (decltype(a.get_unique_id))dlsym(h, "ncclGetUniqueId");
+    a.comm_init_rank = (decltype(a.comm_init_rank))dlsym(h, "ncclCommInitRank");
+    a.comm_destroy = (decltype(a.comm_destroy))dlsym(h, "ncclCommDestroy");
+    a.all_reduce = (decltype(a.all_reduce))dlsym(h, "ncclAllReduce");
+    a.group_start = (decltype(a.group_start))dlsym(h, "ncclGroupStart");
+    a.group_end = (decltype(a.group_end))dlsym(h, "ncclGroupEnd");
+    a.error_string = (decltype(a.error_string))dlsym(h, "ncclGetErrorString");
+    if (!a.get_unique_id || !a.comm_init_rank || !a.comm_destroy || !a.all_reduce ||
+        !a.group_start || !a.group_end || !a.error_string) {
+      a.load_error = "libnccl.so.2 lacks the expected symbols";
+      a.get_unique_id = nullptr;
+    }
+    return a;
+  }();
+  if (!api.get_unique_id) throw NcclFail(api.load_error);
+  return api;
+}
+
+#define NK(expr)                                                                          \
+  do {                                                                                    \
+    ncclResult_t r_ = (expr);                                                             \
+    if (r_ != ncclSuccess) throw NcclFail(std::string(#expr) + ": " + nccl().error_string(r_)); \
+  } while (0)
 
 #define CK(expr)                                                                          \
   do {                                                                                    \
@@ -159,7 +212,33 @@ struct stk_ctx {
   DevBuf<int64_t> st;
 
   uint64_t launches = 0;  // kernels launched by the current call
-  std::vector<unsigned long long> obs_raw;
+  DevBuf<unsigned long long> obsraw;  // observed pattern's exact sums [4][bins] (h_cnt, h_half, h_lo, h_hi)
+  DevBuf<unsigned long long> limbs;   // their exact-exchange limbs [6][bins]
+
+  // multi-GPU (stk_comm_init): one communicator per context, one rank per GPU
+  ncclComm_t comm = nullptr;
+  int comm_rank = 0, nranks = 1;
+
+  // Pinned host staging of a call's outputs: device results land here and are
+  // copied to the caller's buffers only after the end-of-call checks (a failed
+  // validation writes nothing, like the reference's throw before any work).
+  unsigned char* hstage = nullptr;
+  size_t hstage_cap = 0, hstage_used = 0;
+  struct Out {
+    void* dst;
+    size_t off, bytes;
+  };
+  std::vector<Out> outs;
+  bool check_points = false;  // validate_kernel ran: read c->bad at the end of the call
+
+  // pair-kernel occupancy per (wide, mode, smem): set once, not per batch
+  struct Occ {
+    int wide, mode;
+    size_t smem;
+    int per_sm;
+  };
+  std::vector<Occ> occ;
+  bool rv_dev_valid = false;  // d_rv holds region_view() of the current region + grid
 
   std::vector<cudaEvent_t> evpool;
   size_t evnext = 0;
@@ -337,8 +416,11 @@ RegionView region_view(stk_ctx* c);
 // A device-memory copy of a RegionView (pageable H2D: the source is consumed
 // before cudaMemcpyAsync returns).
 const RegionView* device_region(stk_ctx* c, const RegionView& rv) {
-  c->d_rv.ensure(1);
-  CK(cudaMemcpyAsync(c->d_rv.p, &rv, sizeof(RegionView), cudaMemcpyHostToDevice, c->stream));
+  if (!c->rv_dev_valid) {  // refreshed after stk_set_region / stk_set_grid only
+    c->d_rv.ensure(1);
+    CK(cudaMemcpyAsync(c->d_rv.p, &rv, sizeof(RegionView), cudaMemcpyHostToDevice, c->stream));
+    c->rv_dev_valid = true;
+  }
   return c->d_rv.p;
 }
 
@@ -577,21 +659,44 @@ void require_ready(stk_ctx* c) {
   if (!c->have_grid) throw StateErr("distance grid not set (stk_set_grid)");
 }
 
-// Check region.contains(p) for the n points at (dx,dy,dt) on the device.
+// Check region.contains(p) for the n points at (dx,dy,dt) on the device.  No
+// host round trip: the first failing index lands in c->bad, which the pair
+// kernel reads to skip its work, and finish_call() raises the reference's
+// invalid_argument before any output reaches the caller.
 void validate_points(stk_ctx* c, const double* dx, const double* dy, const int64_t* dt,
                      uint64_t n) {
   c->bad.ensure(1);
-  const unsigned long long init = ~0ULL;
-  CK(cudaMemcpyAsync(c->bad.p, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(c->bad.p, 0xff, sizeof(unsigned long long), c->stream));
   const int blocks = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)c->num_sms * 16);
   validate_kernel<<<std::max(blocks, 1), 256, 0, c->stream>>>(dx, dy, dt, n, region_view(c),
                                                                c->bad.p);
   CK(cudaGetLastError());
   ++c->launches;
-  unsigned long long bad = 0;
-  CK(cudaMemcpyAsync(&bad, c->bad.p, sizeof(bad), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  if (bad != ~0ULL) throw InvalidArg("point outside study region or period");
+  c->check_points = true;
+}
+
+// Pinned staging of a call's host outputs (see stk_ctx::hstage).
+void stage_reset(stk_ctx* c, size_t bytes) {
+  c->outs.clear();
+  c->hstage_used = 0;
+  bytes += 256;
+  if (bytes > c->hstage_cap) {
+    if (c->hstage) cudaFreeHost(c->hstage);
+    c->hstage = nullptr;
+    c->hstage_cap = 0;
+    CK(cudaHostAlloc((void**)&c->hstage, bytes, cudaHostAllocDefault));
+    c->hstage_cap = bytes;
+  }
+}
+
+// Enqueue a device -> staging copy whose bytes go to host `dst` at finish_call.
+void* stage_d2h(stk_ctx* c, void* dst, const void* dsrc, size_t bytes) {
+  const size_t off = (c->hstage_used + 15) & ~size_t(15);
+  if (off + bytes > c->hstage_cap) throw CudaFail("internal error: output staging overflow");
+  CK(cudaMemcpyAsync(c->hstage + off, dsrc, bytes, cudaMemcpyDeviceToHost, c->stream));
+  c->hstage_used = off + bytes;
+  if (dst) c->outs.push_back({dst, off, bytes});
+  return c->hstage + off;
 }
 
 enum class Source { Observed, Csr, Bootstrap, Permutation };
@@ -647,6 +752,22 @@ void generate(stk_ctx* c, const Batch& B, Source src, int p_first, int count, ui
   }
 }
 
+// Resident pair-kernel CTAs per SM for (wide, mode, smem), cached per context.
+// The function's dynamic shared-memory limit is raised to the largest size
+// requested so far, so every cached configuration stays launchable.
+int pair_occupancy(stk_ctx* c, int wide, int mode, size_t smem) {
+  size_t mx = smem;
+  for (const auto& o : c->occ) {
+    if (o.wide == wide && o.mode == mode && o.smem == smem) return o.per_sm;
+    if (o.wide == wide && o.mode == mode) mx = std::max(mx, o.smem);
+  }
+  int per_sm = 0;
+  CK(pair_kernel_prepare(wide, mode, smem, mx, &per_sm));
+  if (per_sm < 1) throw Unsupported("distance grid too large for the pair kernel's shared histogram");
+  c->occ.push_back({wide, mode, smem, per_sm});
+  return per_sm;
+}
+
 // Grid build + pair kernel + finalize for patterns [0, R) of the batch.
 // Grid build + pair kernel (+ finalize) for the batch.  Center selection
 // (shard of nshards by input index, and input-index range [c0, c1)) applies to
@@ -698,10 +819,8 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   CK(cudaGetLastError());
   ++c->launches;
   const size_t smem = pair_kernel_smem(P.bins, B.wide);
-  int per_sm = 0;
   const int mode = (c->fast_rect ? 1 : 0) | (c->single_step ? 2 : 0);
-  CK(pair_kernel_prepare(B.wide, mode, smem, &per_sm));
-  if (per_sm < 1) throw Unsupported("distance grid too large for the pair kernel's shared histogram");
+  const int per_sm = pair_occupancy(c, B.wide, mode, smem);
   tasks_kernel<<<1, 1, 0, c->stream>>>(B, G, (uint32_t)(c->num_sms * per_sm));
   CK(cudaGetLastError());
   ++c->launches;
@@ -713,6 +832,7 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   A.bins = bin_view(c);
   A.reg = region_view(c);
   A.reg_g = device_region(c, A.reg);
+  A.abort_flag = c->check_points ? c->bad.p : nullptr;
   const uint64_t ctas = (uint64_t)c->num_sms * per_sm;
   c->arcq.ensure(ctas * kPairWarps * (kArcRing + kCplxRing));
   A.B.arcq = c->arcq.p;
@@ -746,12 +866,24 @@ double elapsed(const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
   return s;
 }
 
-void fill_telemetry(stk_ctx* c, Timers& tm, stk_telemetry* tel, uint64_t patterns) {
-  unsigned long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  CK(cudaMemcpyAsync(st, c->stats.p, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+// End of a call: ONE synchronisation, then the checks in the reference's order
+// (invalid points first: estimator.cpp:123-127 throws before any work), then
+// the staged outputs go to the caller's buffers and the telemetry is added.
+void finish_call(stk_ctx* c, Timers& tm, stk_telemetry* tel, uint64_t patterns) {
+  const unsigned long long* st =
+      (const unsigned long long*)stage_d2h(c, nullptr, c->stats.p, 8 * sizeof(unsigned long long));
+  const unsigned long long* bad =
+      c->check_points ? (const unsigned long long*)stage_d2h(c, nullptr, c->bad.p, 8) : nullptr;
   CK(cudaStreamSynchronize(c->stream));
+  c->check_points = false;
+  if (bad && *bad != ~0ULL) throw InvalidArg("point outside study region or period");
+  // stats[3]: bit 1 = arc ring overflow (pair kernel), bit 0 = more crossings
+  // than the rectangle weight's buffer holds; neither can happen by
+  // construction (<= 31 + kArcChunk*64 ring entries; <= 8 crossings on 4 sides)
   if (st[3] & 2) throw CudaFail("internal error: arc ring overflow in the pair kernel");
-  if (st[3]) throw Unsupported("more than 64 circle/boundary crossings in one edge weight");
+  if (st[3] & 1) throw CudaFail("internal error: crossing buffer overflow in the rectangle edge weight");
+  for (const auto& o : c->outs) std::memcpy(o.dst, c->hstage + o.off, o.bytes);
+  c->outs.clear();
   if (!tel) return;
   tel->in_threshold_pairs += st[0];
   tel->candidate_pairs += st[1];
@@ -792,7 +924,62 @@ struct JobOut {
   uint64_t* obs_counts = nullptr;  // host: exact pre-cumulative results of the observed
   uint64_t* obs_hi = nullptr;      //       pattern (or of its shard)
   uint64_t* obs_lo = nullptr;
+  // collective (stk_run_job_dist): this rank computed shard `rank` of the
+  // observed pattern's pairs and its block of the realisations; the exact
+  // all-reduces over the context's communicator combine them on the device
+  bool dist = false;
+  uint32_t sims_total = 0;   // realisations of the whole job (dist)
 };
+
+// Exact exchange of the observed partials and the partial envelopes over the
+// context's NCCL communicator, then finalize / diff on the device (the
+// reference's DistributedExecutor gather + aggregate, distributed.cpp:197-245,
+// runtime.cpp:119-136, done as two exact all-reduces: bit-identical at any
+// GPU count).
+void exchange(stk_ctx* c, const Plan& P, uint64_t n, bool have_env, uint32_t sims_total) {
+  const uint32_t bins = P.bins;
+  const unsigned g = (bins + 255) / 256;
+  unsigned long long* raw = c->obsraw.p;
+  c->limbs.ensure(6 * (uint64_t)bins);
+  pack_exact_kernel<<<g, 256, 0, c->stream>>>(raw, raw + bins, raw + 2 * bins, raw + 3 * bins,
+                                              bins, c->limbs.p);
+  CK(cudaGetLastError());
+  ++c->launches;
+  if (sims_total > 0 && !have_env) {  // no realisations on this rank: neutral elements
+    fill_kernel<<<g, 256, 0, c->stream>>>(c->env.p, bins, -INFINITY);
+    fill_kernel<<<g, 256, 0, c->stream>>>(c->env.p + bins, bins, INFINITY);
+    CK(cudaGetLastError());
+    c->launches += 2;
+  }
+  const NcclApi& api = nccl();
+  NK(api.group_start());
+  NK(api.all_reduce(c->limbs.p, c->limbs.p, 6 * (size_t)bins, ncclUint64, ncclSum, c->comm,
+                    c->stream));
+  if (sims_total > 0) {
+    NK(api.all_reduce(c->env.p, c->env.p, bins, ncclFloat64, ncclMax, c->comm, c->stream));
+    NK(api.all_reduce(c->env.p + bins, c->env.p + bins, bins, ncclFloat64, ncclMin, c->comm,
+                      c->stream));
+  }
+  NK(api.group_end());
+  unpack_exact_kernel<<<g, 256, 0, c->stream>>>(c->limbs.p, bins, raw, raw + bins,
+                                                raw + 2 * bins, raw + 3 * bins);
+  CK(cudaGetLastError());
+  ++c->launches;
+  Batch F{};
+  F.R = 1;
+  F.n = n;
+  F.h_cnt = raw;
+  F.h_half = raw + bins;
+  F.h_lo = raw + 2 * bins;
+  F.h_hi = raw + 3 * bins;
+  F.K = c->obs.p;
+  F.L = c->obs.p + bins;
+  finalize_kernel<<<1, 256, 0, c->stream>>>(F, (uint32_t)c->s_values.size(),
+                                            (uint32_t)c->t_values.size(), c->d_s.p, c->d_T.p,
+                                            c->area, c->duration, 0);
+  CK(cudaGetLastError());
+  ++c->launches;
+}
 
 void run_pipeline(stk_ctx* c, const double* dx, const double* dy, const int64_t* dt, uint64_t n,
                   bool with_observed, int method, uint64_t base_seed, uint32_t r_begin,
@@ -808,9 +995,12 @@ void run_pipeline(stk_ctx* c, const double* dx, const double* dy, const int64_t*
   const uint64_t patterns = (with_observed ? 1 : 0) + sims;
   Plan P = make_plan(c, n, patterns);
   const Source src = source_of(method);
+  const uint32_t bins = P.bins;
+  stage_reset(c, 8 * (uint64_t)bins * (5 + 4 + (out.l_all ? sims : 0)) + 128);
   CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * 8, c->stream));
-  c->env.ensure(2 * (uint64_t)P.bins);
-  c->obs.ensure(2 * (uint64_t)P.bins);
+  c->env.ensure(2 * (uint64_t)bins);
+  c->obs.ensure(2 * (uint64_t)bins);
+  c->obsraw.ensure(4 * (uint64_t)bins);
   bool env_init = true;
   uint64_t done = 0;
   uint32_t next_r = r_begin;
@@ -835,64 +1025,54 @@ void run_pipeline(stk_ctx* c, const double* dx, const double* dy, const int64_t*
               ~0ULL, true);
     cudaEvent_t f0 = c->ev(), f1 = c->ev();
     CK(cudaEventRecord(f0, c->stream));
-    if (obs_here && out.obs_counts) {
-      // raw exact sums of pattern 0 (h_cnt, h_half, h_lo, h_hi rows of pattern 0)
-      c->scratch.ensure(4 * (uint64_t)P.bins);
-      for (int f = 0; f < 4; ++f)
-        CK(cudaMemcpyAsync(c->scratch.p + (uint64_t)f * P.bins, B.h_cnt + (uint64_t)f * R * P.bins,
-                           8 * (uint64_t)P.bins, cudaMemcpyDeviceToDevice, c->stream));
-      c->obs_raw.resize(4 * (size_t)P.bins);
-      CK(cudaMemcpyAsync(c->obs_raw.data(), c->scratch.p, 32 * (uint64_t)P.bins,
-                         cudaMemcpyDeviceToHost, c->stream));
-    }
     if (obs_here) {
-      CK(cudaMemcpyAsync(c->obs.p, B.K, sizeof(double) * P.bins, cudaMemcpyDeviceToDevice, c->stream));
-      CK(cudaMemcpyAsync(c->obs.p + P.bins, B.L, sizeof(double) * P.bins, cudaMemcpyDeviceToDevice,
+      // exact sums of pattern 0 (rows of h_cnt, h_half, h_lo, h_hi), its K and L
+      for (int f = 0; f < 4; ++f)
+        CK(cudaMemcpyAsync(c->obsraw.p + (uint64_t)f * bins, B.h_cnt + (uint64_t)f * R * bins,
+                           8 * (uint64_t)bins, cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaMemcpyAsync(c->obs.p, B.K, sizeof(double) * bins, cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaMemcpyAsync(c->obs.p + bins, B.L, sizeof(double) * bins, cudaMemcpyDeviceToDevice,
                          c->stream));
     }
     if (nsim > 0) {
-      envelope_kernel<<<(P.bins + 255) / 256, 256, 0, c->stream>>>(
-          B, P.bins, p, nsim, env_init ? 1 : 0, c->env.p, c->env.p + P.bins);
+      envelope_kernel<<<(bins + 255) / 256, 256, 0, c->stream>>>(
+          B, bins, p, nsim, env_init ? 1 : 0, c->env.p, c->env.p + bins);
       CK(cudaGetLastError());
-  ++c->launches;
+      ++c->launches;
       env_init = false;
       if (out.l_all)
-        CK(cudaMemcpyAsync(out.l_all + (uint64_t)(next_r - r_begin) * P.bins,
-                           B.L + (uint64_t)p * P.bins, sizeof(double) * P.bins * nsim,
-                           cudaMemcpyDeviceToHost, c->stream));
+        stage_d2h(c, out.l_all + (uint64_t)(next_r - r_begin) * bins, B.L + (uint64_t)p * bins,
+                  sizeof(double) * bins * nsim);
     }
     CK(cudaEventRecord(f1, c->stream));
     tm.fin.push_back({f0, f1});
     next_r += (uint32_t)nsim;
     done += R;
   }
-  const uint32_t bins = P.bins;
-  if (with_observed && sims > 0 && out.diff) {
+  const uint32_t sims_job = out.dist ? out.sims_total : (uint32_t)sims;
+  const void* raw_host = nullptr;  // this rank's own observed sums, before any exchange
+  if (with_observed && out.obs_counts)
+    raw_host = stage_d2h(c, nullptr, c->obsraw.p, 32 * (uint64_t)bins);
+  if (out.dist) exchange(c, P, n, sims > 0, sims_job);
+  if (with_observed && sims_job > 0 && out.diff) {
     c->scratch.ensure(bins);
     diff_kernel<<<(bins + 255) / 256, 256, 0, c->stream>>>(c->obs.p + bins, c->env.p, bins,
                                                            c->scratch.p);
     CK(cudaGetLastError());
-  ++c->launches;
-    CK(cudaMemcpyAsync(out.diff, c->scratch.p, sizeof(double) * bins, cudaMemcpyDeviceToHost,
-                       c->stream));
+    ++c->launches;
+    stage_d2h(c, out.diff, c->scratch.p, sizeof(double) * bins);
   }
-  if (with_observed && out.k_obs)
-    CK(cudaMemcpyAsync(out.k_obs, c->obs.p, sizeof(double) * bins, cudaMemcpyDeviceToHost, c->stream));
-  if (with_observed && out.l_obs)
-    CK(cudaMemcpyAsync(out.l_obs, c->obs.p + bins, sizeof(double) * bins, cudaMemcpyDeviceToHost,
-                       c->stream));
-  if (sims > 0 && out.upper)
-    CK(cudaMemcpyAsync(out.upper, c->env.p, sizeof(double) * bins, cudaMemcpyDeviceToHost, c->stream));
-  if (sims > 0 && out.lower)
-    CK(cudaMemcpyAsync(out.lower, c->env.p + bins, sizeof(double) * bins, cudaMemcpyDeviceToHost,
-                       c->stream));
+  if (with_observed && out.k_obs) stage_d2h(c, out.k_obs, c->obs.p, sizeof(double) * bins);
+  if (with_observed && out.l_obs) stage_d2h(c, out.l_obs, c->obs.p + bins, sizeof(double) * bins);
+  if (sims_job > 0 && out.upper) stage_d2h(c, out.upper, c->env.p, sizeof(double) * bins);
+  if (sims_job > 0 && out.lower) stage_d2h(c, out.lower, c->env.p + bins, sizeof(double) * bins);
   CK(cudaEventRecord(tm.t1, c->stream));
-  fill_telemetry(c, tm, tel, patterns);
-  if (with_observed && out.obs_counts) {
-    const uint32_t b = P.bins;
-    for (uint32_t i = 0; i < b; ++i) {
-      const unsigned long long raw = c->obs_raw[i], half = c->obs_raw[b + i],
-                               lo = c->obs_raw[2 * b + i], hi = c->obs_raw[3 * b + i];
+  finish_call(c, tm, tel, patterns);
+  if (raw_host) {
+    const unsigned long long* r = (const unsigned long long*)raw_host;
+    for (uint32_t i = 0; i < bins; ++i) {
+      const unsigned long long raw = r[i], half = r[bins + i], lo = r[2 * bins + i],
+                               hi = r[3 * bins + i];
       const unsigned long long cnt = raw & ~1ULL;
       out.obs_counts[i] = cnt;
       const unsigned __int128 v = ((unsigned __int128)hi << 64 | lo) +
@@ -910,6 +1090,8 @@ int guarded(stk_ctx* c, F&& f) {
   try {
     CK(cudaSetDevice(c->device));
     c->launches = 0;
+    c->check_points = false;
+    c->outs.clear();
     f();
     c->err.clear();
     return STK_OK;
@@ -922,6 +1104,9 @@ int guarded(stk_ctx* c, F&& f) {
   } catch (const StateErr& e) {
     c->err = e.what();
     return STK_ESTATE;
+  } catch (const NcclFail& e) {
+    c->err = e.what();
+    return STK_ENCCL;
   } catch (const std::exception& e) {
     c->err = e.what();
     return STK_ECUDA;
@@ -986,6 +1171,9 @@ void stk_destroy(stk_ctx* c) {
   c->env.release(); c->obs.release(); c->flags.release(); c->ovf.release();
   c->sel_start.release(); c->center_pos.release(); c->arcq.release(); c->angs.release();
   c->scratch.release(); c->sx.release(); c->sy.release(); c->st.release();
+  c->obsraw.release(); c->limbs.release(); c->d_rv.release();
+  if (c->comm) nccl().comm_destroy(c->comm);
+  if (c->hstage) cudaFreeHost(c->hstage);
   cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1088,6 +1276,7 @@ int stk_set_region(stk_ctx* c, const double* ring_xy, uint32_t nv, int64_t perio
   return guarded(c, [&] {
     c->have_region = false;
     c->slab_ok = c->ec_ok = false;
+    c->rv_dev_valid = false;
     const RegionInfo ri = check_region(ring_xy, nv, period_start, period_end);
     const std::vector<double>& r = ri.ring;
     const uint32_t m = ri.nv;
@@ -1186,6 +1375,7 @@ int stk_set_grid(stk_ctx* c, const double* s_values, uint32_t cs, const int64_t*
   return guarded(c, [&] {
     c->have_grid = false;
     c->ec_ok = false;
+    c->rv_dev_valid = false;
     check_grid(s_values, cs, t_values, ct);
     if ((uint64_t)cs * ct > (1u << 20)) throw Unsupported("more than 2^20 grid cells");
     if (cs > (uint32_t)kMaxAxis || ct > (uint32_t)kMaxAxis)
@@ -1269,16 +1459,16 @@ int stk_pair_histogram(stk_ctx* c, const double* x, const double* y, const int64
     CK(cudaEventRecord(tm.t0, c->stream));
     Plan P = make_plan(c, n, 1);
     P.R = 1;
+    stage_reset(c, 32 * (uint64_t)P.bins + 128);
     Batch B = alloc_batch(c, P);
     CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * 8, c->stream));
     generate(c, B, Source::Observed, 0, 1, 0, c->sx.p, c->sy.p, c->st.p);
     run_batch(c, P, B, tm, nshards > 1 ? 1 : 0, shard, nshards, 0, ~0ULL, false);
     const uint32_t bins = P.bins;
-    std::vector<unsigned long long> h(4 * (size_t)bins);
-    CK(cudaMemcpyAsync(h.data(), B.h_cnt, sizeof(unsigned long long) * 4 * bins,
-                       cudaMemcpyDeviceToHost, c->stream));
+    const unsigned long long* h = (const unsigned long long*)stage_d2h(
+        c, nullptr, B.h_cnt, sizeof(unsigned long long) * 4 * bins);
     CK(cudaEventRecord(tm.t1, c->stream));
-    fill_telemetry(c, tm, tel, 1);
+    finish_call(c, tm, tel, 1);
     for (uint32_t b = 0; b < bins; ++b) {
       const unsigned long long raw = h[b], half = h[bins + b], lo = h[2 * bins + b],
                                hi = h[3 * bins + b];
@@ -1437,6 +1627,102 @@ int stk_run_job_shard_device(stk_ctx* c, const double* d_x, const double* d_y,
   });
 }
 
+int stk_comm_unique_id(unsigned char* id_out) {
+  if (!id_out) return STK_EINVAL;
+  try {
+    ncclUniqueId id;
+    NK(nccl().get_unique_id(&id));
+    std::memcpy(id_out, id.internal, NCCL_UNIQUE_ID_BYTES);
+    return STK_OK;
+  } catch (const std::exception&) {
+    return STK_ENCCL;
+  }
+}
+
+int stk_comm_init(stk_ctx* c, const unsigned char* id, int nranks, int rank) {
+  return guarded(c, [&] {
+    if (!id) throw InvalidArg("null NCCL unique id");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArg("rank out of range");
+    if (c->comm) {
+      NK(nccl().comm_destroy(c->comm));
+      c->comm = nullptr;
+    }
+    ncclUniqueId uid;
+    std::memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
+    ncclComm_t comm = nullptr;
+    NK(nccl().comm_init_rank(&comm, nranks, uid, rank));
+    c->comm = comm;
+    c->comm_rank = rank;
+    c->nranks = nranks;
+  });
+}
+
+int stk_comm_destroy(stk_ctx* c) {
+  return guarded(c, [&] {
+    if (c->comm) {
+      CK(cudaStreamSynchronize(c->stream));
+      NK(nccl().comm_destroy(c->comm));
+    }
+    c->comm = nullptr;
+    c->comm_rank = 0;
+    c->nranks = 1;
+  });
+}
+
+int stk_comm_rank(stk_ctx* c, int* rank, int* nranks) {
+  if (!c) return STK_ESTATE;
+  if (rank) *rank = c->comm ? c->comm_rank : 0;
+  if (nranks) *nranks = c->comm ? c->nranks : 1;
+  return c->comm ? STK_OK : STK_ESTATE;
+}
+
+static void run_dist_impl(stk_ctx* c, const double* dx, const double* dy, const int64_t* dt,
+                          uint64_t n, uint32_t sims, uint64_t seed, int method, double* k_out,
+                          double* l_out, double* upper_l, double* lower_l, double* diff_upper,
+                          stk_telemetry* tel) {
+  if (!c->comm) throw StateErr("no communicator (stk_comm_init)");
+  validate_points(c, dx, dy, dt, n);
+  const uint32_t G = (uint32_t)c->nranks, g = (uint32_t)c->comm_rank;
+  const uint32_t base = sims / G, extra = sims % G;  // contiguous blocks of the seed ladder
+  const uint32_t r0 = g * base + std::min(g, extra);
+  const uint32_t r1 = r0 + base + (g < extra ? 1u : 0u);
+  JobOut o;
+  o.k_obs = k_out;
+  o.l_obs = l_out;
+  o.upper = upper_l;
+  o.lower = lower_l;
+  o.diff = diff_upper;
+  o.dist = true;
+  o.sims_total = sims;
+  run_pipeline(c, dx, dy, dt, n, true, method, seed, r0, r1, o, tel, g, G);
+}
+
+int stk_run_job_dist(stk_ctx* c, const double* x, const double* y, const int64_t* t, uint64_t n,
+                     uint32_t sims, uint64_t seed, int method, double* k_out, double* l_out,
+                     double* upper_l, double* lower_l, double* diff_upper, stk_telemetry* tel) {
+  return guarded(c, [&] {
+    require_ready(c);
+    check_n(n);
+    (void)source_of(method);
+    upload_points(c, x, y, t, n);
+    run_dist_impl(c, c->sx.p, c->sy.p, c->st.p, n, sims, seed, method, k_out, l_out, upper_l,
+                  lower_l, diff_upper, tel);
+  });
+}
+
+int stk_run_job_dist_device(stk_ctx* c, const double* d_x, const double* d_y,
+                            const int64_t* d_t, uint64_t n, uint32_t sims, uint64_t seed,
+                            int method, double* k_out, double* l_out, double* upper_l,
+                            double* lower_l, double* diff_upper, stk_telemetry* tel) {
+  return guarded(c, [&] {
+    require_ready(c);
+    check_n(n);
+    (void)source_of(method);
+    run_dist_impl(c, d_x, d_y, d_t, n, sims, seed, method, k_out, l_out, upper_l, lower_l,
+                  diff_upper, tel);
+  });
+}
+
 int stk_generate_cstr(stk_ctx* c, uint64_t n, uint64_t seed, double* x, double* y, int64_t* t) {
   return guarded(c, [&] {
     if (!c->have_region) throw StateErr("study region not set (stk_set_region)");
@@ -1513,6 +1799,82 @@ int stk_spatial_weights(stk_ctx* c, const double* cx, const double* cy, const do
     b.release();
     if (bad != ~0ULL) throw InvalidArg("weight center outside study region");
     if (ovf) throw Unsupported("more than 64 circle/boundary crossings in one edge weight");
+  });
+}
+
+int stk_task_histogram(stk_ctx* c, const double* px, const double* py, const int64_t* pt,
+                       const uint32_t* pidx, uint64_t np, const double* cx, const double* cy,
+                       const int64_t* ct, const uint32_t* cidx, const double* crad,
+                       const int64_t* ctrad, uint64_t nc, double* hist, uint64_t* in_threshold,
+                       uint64_t* comparisons) {
+  return guarded(c, [&] {
+    require_ready(c);
+    const uint32_t cs = (uint32_t)c->s_values.size(), ctn = (uint32_t)c->t_values.size();
+    const uint32_t bins = cs * ctn;
+    // one device block: points (x, y, t, idx), cylinders (x, y, t, idx, r, tr), sums
+    const uint64_t pbytes = np * 28, cbytes = nc * 44, hbytes = 3ull * bins * 8 + 64;
+    DevBuf<unsigned char> buf;
+    buf.ensure(pbytes + cbytes + hbytes + 256);
+    unsigned char* q = buf.p;
+    auto put = [&](const void* src, size_t bytes, size_t align) {
+      q = (unsigned char*)(((uintptr_t)q + align - 1) & ~(uintptr_t)(align - 1));
+      if (bytes) CK(cudaMemcpyAsync(q, src, bytes, cudaMemcpyHostToDevice, c->stream));
+      unsigned char* at = q;
+      q += bytes;
+      return at;
+    };
+    TaskArgs T{};
+    T.px = (const double*)put(px, np * 8, 8);
+    T.py = (const double*)put(py, np * 8, 8);
+    T.pt = (const int64_t*)put(pt, np * 8, 8);
+    T.pidx = (const uint32_t*)put(pidx, np * 4, 4);
+    T.np = np;
+    T.cx = (const double*)put(cx, nc * 8, 8);
+    T.cy = (const double*)put(cy, nc * 8, 8);
+    T.ct = (const int64_t*)put(ct, nc * 8, 8);
+    T.crad = (const double*)put(crad, nc * 8, 8);
+    T.ctrad = (const int64_t*)put(ctrad, nc * 8, 8);
+    T.cidx = (const uint32_t*)put(cidx, nc * 4, 4);
+    T.nc = nc;
+    T.s_values = c->d_s.p;
+    T.t_values = c->d_T.p;
+    T.cs = cs;
+    T.ctn = ctn;
+    q = (unsigned char*)(((uintptr_t)q + 15) & ~(uintptr_t)15);
+    unsigned long long* acc = (unsigned long long*)q;  // h_cnt, h_lo, h_hi, stats[2], bad
+    CK(cudaMemsetAsync(acc, 0, (3ull * bins + 2) * 8, c->stream));
+    CK(cudaMemsetAsync(acc + 3ull * bins + 2, 0xff, 8, c->stream));
+    T.h_cnt = acc;
+    T.h_lo = acc + bins;
+    T.h_hi = acc + 2ull * bins;
+    T.stats = acc + 3ull * bins;
+    T.bad = acc + 3ull * bins + 2;
+    c->ovf.ensure(1);
+    CK(cudaMemsetAsync(c->ovf.p, 0, sizeof(int), c->stream));
+    T.overflow = c->ovf.p;
+    const RegionView rv = region_view(c);
+    if (nc && np) {
+      const uint64_t work = nc * np;
+      const unsigned blocks =
+          (unsigned)std::min<uint64_t>((work + 127) / 128, (uint64_t)c->num_sms * 64);
+      task_kernel<<<blocks, 128, 0, c->stream>>>(T, rv, device_region(c, rv));
+      CK(cudaGetLastError());
+      ++c->launches;
+    }
+    std::vector<unsigned long long> h(3ull * bins + 3);
+    CK(cudaMemcpyAsync(h.data(), acc, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    buf.release();
+    if (h[3ull * bins + 2] != ~0ULL) throw InvalidArg("weight center outside study region");
+    for (uint32_t b = 0; b < bins; ++b) {
+      const unsigned long long raw = h[b], lo = h[bins + b], hi = h[2ull * bins + b];
+      const unsigned long long cnt = raw >> 1;  // ordered pairs of the bin
+      const unsigned __int128 v = ((unsigned __int128)hi << 64 | lo) +
+                                  ((unsigned __int128)cnt << kFixedFracBits);
+      if (hist) hist[b] = (raw & 1ULL) ? std::nan("") : fixed_or_nan(v);
+    }
+    if (in_threshold) *in_threshold = h[3ull * bins];
+    if (comparisons) *comparisons = h[3ull * bins + 1];
   });
 }
 

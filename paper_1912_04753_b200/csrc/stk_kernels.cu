@@ -826,6 +826,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   S.ch = (uint2*)(smem_raw + Lay::ch);
   S.arc = (ArcSum*)(smem_raw + Lay::lh(bins));
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // an input point failed region.contains (validate_kernel ran on this stream
+  // first): the call raises invalid_argument, so skip the work
+  if (A.abort_flag && *A.abort_flag != ~0ULL) return;
 
   for (uint32_t b = tid; b < cs; b += blockDim.x) S.Q[b] = BV.Q[b];
   // times relative to the period start never exceed the duration, so
@@ -1249,9 +1252,10 @@ static const void* pair_fn(int wide, int mode) {
   return wide ? pair_fn2<int64_t>(mode) : pair_fn2<int32_t>(mode);
 }
 
-cudaError_t pair_kernel_prepare(int wide, int mode, size_t smem, int* per_sm) {
+cudaError_t pair_kernel_prepare(int wide, int mode, size_t smem, size_t smem_limit, int* per_sm) {
   const void* fn = pair_fn(wide, mode);
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e =
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_limit);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fn, kPairWarps * 32, smem);
 }
@@ -1346,6 +1350,48 @@ __global__ void diff_kernel(const double* est_l, const double* upper, uint32_t b
   diff[b] = e > u ? e - u : 0.0;
 }
 
+// ============================================================ multi-GPU exchange
+// The observed pattern's exact per-bin partials (h_cnt with the 1/0 flag in
+// bit 0, h_half, and the signed 128-bit arc sum h_hi:h_lo) as six u64 limbs
+// whose plain integer SUM across ranks is exact: [cnt & ~1, half, lo & 2^32-1,
+// lo >> 32, hi, cnt & 1] (limb sums of 32-bit halves cannot overflow below
+// 2^32 ranks; hi wraps mod 2^64, i.e. two's complement mod 2^128).
+__global__ void pack_exact_kernel(const unsigned long long* cnt, const unsigned long long* half,
+                                  const unsigned long long* lo, const unsigned long long* hi,
+                                  uint32_t bins, unsigned long long* limbs) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= bins) return;
+  const unsigned long long c = cnt[b], l = lo[b];
+  limbs[b] = c & ~1ULL;
+  limbs[bins + b] = half[b];
+  limbs[2 * bins + b] = l & 0xffffffffULL;
+  limbs[3 * bins + b] = l >> 32;
+  limbs[4 * bins + b] = hi[b];
+  limbs[5 * bins + b] = c & 1ULL;
+}
+
+// Inverse of pack_exact_kernel after the SUM: renormalise the limbs to
+// (h_cnt | flag, h_half, h_lo, h_hi) in the layout finalize_kernel reads.
+__global__ void unpack_exact_kernel(const unsigned long long* limbs, uint32_t bins,
+                                    unsigned long long* cnt, unsigned long long* half,
+                                    unsigned long long* lo, unsigned long long* hi) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= bins) return;
+  const unsigned long long l32 = limbs[2 * bins + b], h32 = limbs[3 * bins + b];
+  const unsigned long long a = h32 << 32;
+  const unsigned long long l = a + l32;
+  cnt[b] = limbs[b] | (limbs[5 * bins + b] ? 1ULL : 0ULL);
+  half[b] = limbs[bins + b];
+  lo[b] = l;
+  hi[b] = limbs[4 * bins + b] + (h32 >> 32) + (l < a ? 1ULL : 0ULL);
+}
+
+// Fill n doubles with v (neutral envelopes of a rank without realisations).
+__global__ void fill_kernel(double* p, uint32_t n, double v) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
 // ============================================================ utilities
 __global__ void weights_kernel(const double* cx, const double* cy, const double* d,
                                uint64_t count, RegionView reg, const RegionView* reg_g, double* w, int* overflow,
@@ -1368,6 +1414,81 @@ __global__ void weights_kernel(const double* cx, const double* cy, const double*
                                               kAngleSlots / 2);
   if (ws < 0.0) ws = spatial_weight(cx[i], cy[i], d[i], reg_g, overflow);
   w[i] = ws;
+}
+
+// rt::execute_task (runtime.cpp:73-117) for the reference's task interface
+// (rt::Executor::run over TaskData: a partition's points plus the query
+// cylinders assigned to it).  Every (cylinder, point) candidate is tested like
+// the reference's brute-force branch (:101-109): skip the center's own record,
+// within_cylinder (geometry.cpp:41-44, inclusive), bin_pair's lower_bound on
+// the actual grid arrays (estimator.cpp:84-92), pair_weight = spatial weight of
+// the cylinder's center x temporal weight (edge_correction.cpp:42-103), and
+// 1/w accumulated exactly (counts += 2 with bit 0 flagging 1/0, and the signed
+// 128-bit fixed-point sum of 1/w - 1, as the pair kernel).  A compatibility
+// path for callers of the task API: rt::run_job runs the fused pipeline.
+// stats: [0] in-threshold pairs, [1] candidate comparisons.
+__global__ void __launch_bounds__(128) task_kernel(TaskArgs T, RegionView reg,
+                                                   const RegionView* reg_g) {
+  __shared__ double angs[kAngleSlots * 128];
+  unsigned long long n_in = 0, n_cmp = 0;
+  const uint64_t total = T.nc * T.np;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < total;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = k / T.np, j = k - c * T.np;
+    if (T.pidx[j] == T.cidx[c]) continue;
+    ++n_cmp;
+    const double cx = T.cx[c], cy = T.cy[c];
+    const double dx = cx - T.px[j], dy = cy - T.py[j];
+    const double d = sqrt(dx * dx + dy * dy);  // spatial_distance, no FMA (-fmad=false)
+    const int64_t u = T.ct[c] >= T.pt[j] ? T.ct[c] - T.pt[j] : T.pt[j] - T.ct[c];
+    if (!(d <= T.crad[c] && u <= T.ctrad[c])) continue;  // within_cylinder
+    uint32_t lo = 0, hi = T.cs;                          // first s_k >= d
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (T.s_values[mid] < d) lo = mid + 1; else hi = mid;
+    }
+    if (lo == T.cs) continue;
+    const uint32_t si = lo;
+    lo = 0;
+    hi = T.ctn;                                          // first t_l >= u
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (T.t_values[mid] < u) lo = mid + 1; else hi = mid;
+    }
+    if (lo == T.ctn) continue;
+    const uint32_t bin = si * T.ctn + lo;
+    double ws = 1.0;
+    if (d > 0.0) {
+      if (!point_in_region(cx, cy, reg)) {
+        atomicMin(T.bad, (unsigned long long)c);
+        continue;
+      }
+      ws = reg.rect ? rect_single_edge_weight(cx, cy, d, reg) : -1.0;
+      if (ws < 0.0 && reg.rect) ws = rect_multi_edge_weight(cx, cy, d, reg);
+      if (ws < 0.0)
+        ws = reg.rect ? spatial_weight_buf<true>(cx, cy, d, reg, angs + threadIdx.x, 128,
+                                                 kAngleSlots / 2)
+                      : spatial_weight_buf<false>(cx, cy, d, reg, angs + threadIdx.x, 128,
+                                                  kAngleSlots / 2);
+      if (ws < 0.0) ws = spatial_weight(cx, cy, d, reg_g, T.overflow);
+    }
+    const double wt = (T.ct[c] - u >= reg.p0 && T.ct[c] + u <= reg.p1) ? 1.0 : 0.5;
+    const double w = ws * wt;
+    ++n_in;
+    if (w == 0.0) {  // the reference adds 1/0 = inf: its Kahan sum ends NaN
+      atomicOr(&T.h_cnt[bin], 1ULL);
+      atomicAdd(&T.h_cnt[bin], 2ULL);
+      continue;
+    }
+    atomicAdd(&T.h_cnt[bin], 2ULL);
+    uint64_t l, h;
+    fixed_term_minus_one(1.0 / w, &l, &h);
+    const unsigned long long old = atomicAdd(&T.h_lo[bin], (unsigned long long)l);
+    if (old + l < old) ++h;
+    if (h) atomicAdd(&T.h_hi[bin], (unsigned long long)h);
+  }
+  if (n_in) atomicAdd(&T.stats[0], n_in);
+  if (n_cmp) atomicAdd(&T.stats[1], n_cmp);
 }
 
 // FP64 issue peak: 8 independent DFMA chains per thread.

@@ -14,6 +14,7 @@ struct PairArgs {
   BinView bins;
   RegionView reg;
   const RegionView* reg_g;  // device-memory copy of reg for the out-of-line fallback weight
+  const unsigned long long* abort_flag;  // != ~0 (invalid input point found): skip all work
 };
 
 __global__ void validate_kernel(const double* x, const double* y, const int64_t* t, uint64_t n,
@@ -41,7 +42,7 @@ __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first);
 __global__ void items_kernel(Batch B, GridGeom G, int p_first);
 __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas);
 // mode = rect | single_step << 1 (kernel template flags)
-cudaError_t pair_kernel_prepare(int wide, int mode, size_t smem, int* per_sm);
+cudaError_t pair_kernel_prepare(int wide, int mode, size_t smem, size_t smem_limit, int* per_sm);
 void pair_kernel_launch(int wide, int mode, unsigned ctas, size_t smem, cudaStream_t stream,
                         const PairArgs& A);
 __global__ void finalize_kernel(Batch B, uint32_t cs, uint32_t ct, const double* s_values,
@@ -51,9 +52,37 @@ __global__ void envelope_kernel(Batch B, uint32_t bins, int p_first, int count, 
                                 double* upper, double* lower);
 __global__ void diff_kernel(const double* est_l, const double* upper, uint32_t bins,
                             double* diff);
+__global__ void pack_exact_kernel(const unsigned long long* cnt, const unsigned long long* half,
+                                  const unsigned long long* lo, const unsigned long long* hi,
+                                  uint32_t bins, unsigned long long* limbs);
+__global__ void unpack_exact_kernel(const unsigned long long* limbs, uint32_t bins,
+                                    unsigned long long* cnt, unsigned long long* half,
+                                    unsigned long long* lo, unsigned long long* hi);
+__global__ void fill_kernel(double* p, uint32_t n, double v);
 __global__ void weights_kernel(const double* cx, const double* cy, const double* d,
                                uint64_t count, RegionView reg, const RegionView* reg_g, double* w, int* overflow,
                                unsigned long long* bad);
+// rt::execute_task on the device (the reference's task interface).
+struct TaskArgs {
+  const double *px, *py;      // task points
+  const int64_t* pt;
+  const uint32_t* pidx;       // their record indices
+  uint64_t np;
+  const double *cx, *cy;      // cylinder centers
+  const int64_t* ct;
+  const uint32_t* cidx;       // center record indices
+  const double* crad;         // cylinder spatial radius
+  const int64_t* ctrad;       // cylinder temporal radius
+  uint64_t nc;
+  const double* s_values;
+  const int64_t* t_values;
+  uint32_t cs, ctn;
+  unsigned long long *h_cnt, *h_lo, *h_hi;  // [bins] exact sums (h_cnt: 2 per pair, bit 0 = 1/0)
+  unsigned long long* stats;  // [0] in-threshold [1] comparisons
+  unsigned long long* bad;    // first cylinder whose center lies outside the region
+  int* overflow;
+};
+__global__ void task_kernel(TaskArgs T, RegionView reg, const RegionView* reg_g);
 __global__ void dfma_peak_kernel(double* out, int iters, double a, double b);
 
 size_t pair_kernel_smem(uint32_t bins, int wide);

@@ -67,6 +67,23 @@ class Device:
     def set_memory_budget(self, nbytes: int):
         self.check(self.lib.stk_set_memory_budget(self.h, int(nbytes)))
 
+    # -- multi-GPU: NCCL communicator inside the library ---------------------
+    def comm_init(self, unique_id: bytes, nranks: int, rank: int):
+        """stk_comm_init: join the communicator of ``unique_id`` (from
+        :func:`nccl_unique_id` on rank 0) as ``rank`` of ``nranks``."""
+        if len(unique_id) != _lib.NCCL_ID_BYTES:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        self.check(self.lib.stk_comm_init(self.h, bytes(unique_id), int(nranks), int(rank)))
+
+    def comm_destroy(self):
+        self.check(self.lib.stk_comm_destroy(self.h))
+
+    def comm_rank(self):
+        """(rank, nranks) of the context's communicator, or None without one."""
+        r, n = C.c_int(), C.c_int()
+        rc = self.lib.stk_comm_rank(self.h, C.byref(r), C.byref(n))
+        return (r.value, n.value) if rc == _lib.STK_OK else None
+
     def fp64_peak(self) -> float:
         v = C.c_double()
         self.check(self.lib.stk_measure_fp64_peak(self.h, C.byref(v)))
@@ -82,6 +99,16 @@ class Device:
             self.close()
         except Exception:
             pass
+
+
+def nccl_unique_id() -> bytes:
+    """stk_comm_unique_id (ncclGetUniqueId through the library)."""
+    lib = _lib.load()
+    buf = C.create_string_buffer(_lib.NCCL_ID_BYTES)
+    rc = lib.stk_comm_unique_id(buf)
+    if rc != _lib.STK_OK:
+        raise _lib.StkError("stk_comm_unique_id failed: NCCL unavailable")
+    return buf.raw
 
 
 _devices: dict[int, Device] = {}

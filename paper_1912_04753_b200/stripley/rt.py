@@ -80,12 +80,17 @@ class RunResult:  # runtime.hpp:138-146
 class DeviceExecutor:
     """Executor backed by one GPU per process.
 
-    ``rank``/``world`` default to torch.distributed's when it is initialised;
-    ``group`` is the process group for the two all-reduces (NCCL on GPUs,
-    gloo in CPU tests of the sharding logic).
+    ``rank``/``world`` default to torch.distributed's when it is initialised.
+    With world > 1 on an NCCL process group (or ``comm=True``) the executor
+    joins an NCCL communicator INSIDE the library (``stk_comm_init``; the
+    unique id travels once over ``group``), and ``run_job`` is one collective
+    library call (``stk_run_job_dist``: exact device all-reduces, finalize on
+    the device).  Otherwise (a gloo group: CPU tests of the sharding logic, or
+    several ranks emulated on one GPU) the two exact exchanges run over
+    ``group`` from the host (:func:`allreduce_exact`, :func:`allreduce_envelopes`).
     """
 
-    def __init__(self, device=None, rank=None, world=None, group=None):
+    def __init__(self, device=None, rank=None, world=None, group=None, comm=None):
         self.device = device
         self.group = group
         if rank is None or world is None:
@@ -98,6 +103,33 @@ class DeviceExecutor:
             except Exception:
                 pass
         self.rank, self.world = int(rank), int(world)
+        if not (0 <= self.rank < self.world):
+            raise ValueError("rank must be < world")
+        self.comm = False
+        if comm is None:
+            comm = self.world > 1 and _group_backend(group) == "nccl"
+        if comm:
+            self._init_comm()
+
+    def _dev(self):
+        return self.device if isinstance(self.device, _device.Device) else _device.get(self.device)
+
+    @property
+    def device_index(self) -> int:
+        return self._dev().index
+
+    def _init_comm(self):
+        d = self._dev()
+        if self.world == 1:
+            uid = _device.nccl_unique_id()
+        else:
+            import torch.distributed as dist
+
+            box = [_device.nccl_unique_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(box, src=0, group=self.group)
+            uid = box[0]
+        d.comm_init(uid, self.world, self.rank)
+        self.comm = True
 
     # ----------------------------------------------------------- sharding
     def sim_range(self, sims: int) -> tuple[int, int]:
@@ -105,10 +137,28 @@ class DeviceExecutor:
         return shard_range(sims, self.rank, self.world)
 
     def allreduce_exact(self, counts, hi, lo):
-        return allreduce_exact(counts, hi, lo, self.group)
+        return allreduce_exact(counts, hi, lo, self.group, self._torch_device())
 
     def allreduce_envelopes(self, upper, lower):
-        return allreduce_envelopes(upper, lower, self.group)
+        return allreduce_envelopes(upper, lower, self.group, self._torch_device())
+
+    def _torch_device(self):
+        import torch
+
+        if _group_backend(self.group) == "nccl":
+            return torch.device("cuda", self.device_index)
+        return torch.device("cpu")
+
+
+def _group_backend(group):
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            return dist.get_backend(group)
+    except Exception:
+        pass
+    return None
 
 
 def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
@@ -117,52 +167,51 @@ def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
     return begin, begin + base + (1 if rank < extra else 0)
 
 
-def _to_limbs(hi, lo):
+_M32 = np.uint64(0xFFFFFFFF)
+
+
+def pack_limbs(counts, hi, lo):
+    """Exact per-bin partials -> int64 limbs whose plain integer SUM across
+    ranks is exact: [counts, lo & (2^32-1), lo >> 32, hi] (32-bit halves cannot
+    overflow below 2^31 ranks; hi is the signed high word of the two's
+    complement 128-bit sum).  The same algebra as the device's
+    pack_exact_kernel / unpack_exact_kernel (stk_kernels.cu)."""
     lo = np.asarray(lo, np.uint64)
-    return (np.asarray(hi, np.uint64).astype(np.int64), (lo >> np.uint64(32)).astype(np.int64),
-            (lo & np.uint64(0xFFFFFFFF)).astype(np.int64))
+    return np.stack([np.asarray(counts, np.uint64), lo & _M32, lo >> np.uint64(32),
+                     np.asarray(hi, np.uint64)]).view(np.int64)
 
 
-def _from_limbs(h, m, l):
-    """Renormalise summed limbs (hi*2^64 + m*2^32 + l) to (hi, lo) uint64."""
-    h = np.asarray(h, np.int64).astype(object)
-    m = np.asarray(m, np.int64).astype(object)
-    l = np.asarray(l, np.int64).astype(object)
-    v = h * (1 << 64) + m * (1 << 32) + l
-    # two's complement: a bin's total (1/w - 1) sum can be negative (omega = 1 + ulp)
-    hi = np.array([(int(x) >> 64) & ((1 << 64) - 1) for x in v.ravel()],
-                  dtype=np.uint64).reshape(v.shape)
-    lo = np.array([int(x) & ((1 << 64) - 1) for x in v.ravel()], dtype=np.uint64).reshape(v.shape)
-    return hi, lo
+def unpack_limbs(limbs):
+    """Inverse of :func:`pack_limbs` after the SUM (vectorised, wrapping
+    uint64 arithmetic = arithmetic mod 2^128)."""
+    u = np.asarray(limbs, np.int64).view(np.uint64)
+    counts, l32, h32, hi = u[0], u[1], u[2], u[3]
+    with np.errstate(over="ignore"):
+        a = h32 << np.uint64(32)
+        lo = a + l32
+        hi = hi + (h32 >> np.uint64(32)) + (lo < a).astype(np.uint64)
+    return counts, hi, lo
 
 
-def allreduce_exact(counts, hi, lo, group=None):
+def allreduce_exact(counts, hi, lo, group=None, device=None):
     """Sum exact per-bin partials across ranks: counts (u64) and the 128-bit
-    fixed-point sums split into int64 limbs so an integer all-reduce carries
-    every bit (bit-identical at any world size)."""
+    fixed-point sums as integer limbs, so the SUM carries every bit
+    (bit-identical at any world size)."""
     import torch
     import torch.distributed as dist
 
-    limbs = _to_limbs(hi, lo)
-    stack = np.stack([np.asarray(counts, np.uint64).astype(np.int64), *limbs])
-    backend = dist.get_backend(group)
-    dev = "cuda" if backend == "nccl" else "cpu"
-    ten = torch.from_numpy(stack).to(dev)
+    ten = torch.from_numpy(pack_limbs(counts, hi, lo)).to(device or "cpu")
     dist.all_reduce(ten, op=dist.ReduceOp.SUM, group=group)
-    out = ten.cpu().numpy()
-    hi2, lo2 = _from_limbs(out[1], out[2], out[3])
-    return out[0].astype(np.uint64), hi2, lo2
+    return unpack_limbs(ten.cpu().numpy())
 
 
-def allreduce_envelopes(upper, lower, group=None):
+def allreduce_envelopes(upper, lower, group=None, device=None):
     """Pointwise MAX of upper / MIN of lower across ranks (exact, order-free)."""
     import torch
     import torch.distributed as dist
 
-    backend = dist.get_backend(group)
-    dev = "cuda" if backend == "nccl" else "cpu"
-    u = torch.from_numpy(np.ascontiguousarray(upper)).to(dev)
-    l = torch.from_numpy(np.ascontiguousarray(lower)).to(dev)
+    u = torch.from_numpy(np.ascontiguousarray(upper)).to(device or "cpu")
+    l = torch.from_numpy(np.ascontiguousarray(lower)).to(device or "cpu")
     dist.all_reduce(u, op=dist.ReduceOp.MAX, group=group)
     dist.all_reduce(l, op=dist.ReduceOp.MIN, group=group)
     return u.cpu().numpy(), l.cpu().numpy()
@@ -178,7 +227,7 @@ def run_job(points, region: StudyRegion, spec: JobSpec, executor: DeviceExecutor
     shape = (grid.cells_s(), grid.cells_t())
     tel = RunTelemetry()
     t0 = time.perf_counter()
-    if executor.world == 1:
+    if executor.world == 1 and not executor.comm:
         k = np.zeros(shape); l = np.zeros(shape)
         up = np.zeros(shape); lo = np.zeros(shape); diff = np.zeros(shape)
         st = _lib.StkTelemetry()
@@ -200,8 +249,33 @@ def run_job(points, region: StudyRegion, spec: JobSpec, executor: DeviceExecutor
             res.diff_upper = KSurface(grid, diff, SurfaceKind.Diff)
         return res
 
-    # --- multi-process: one call per rank (its slice of the observed pattern's
-    # pair work + its block of realisations), then the two exact all-reduces.
+    if executor.comm:
+        # one collective library call: shard + realisation block, exact NCCL
+        # exchange and finalize on the device; every rank gets the result
+        k = np.zeros(shape); l = np.zeros(shape)
+        up = np.zeros(shape); lo = np.zeros(shape); diff = np.zeros(shape)
+        st = _lib.StkTelemetry()
+        d.check(d.lib.stk_run_job_dist(d.h, _lib.ptr(pts.x), _lib.ptr(pts.y),
+                                       _lib.ptr(pts.t, C.c_int64), n, int(spec.sims),
+                                       int(spec.seed), int(spec.method), _lib.ptr(k), _lib.ptr(l),
+                                       _lib.ptr(up), _lib.ptr(lo), _lib.ptr(diff), C.byref(st)))
+        tel.pair_comparisons = int(st.candidate_pairs)
+        tel.in_threshold_pairs = int(st.in_threshold_pairs)
+        tel.exact_path_pairs = int(st.exact_path_pairs)
+        tel.device_ms = float(st.total_ms)
+        tel.pair_ms = float(st.pair_ms)
+        tel.estimation_seconds = time.perf_counter() - t0
+        res = RunResult(KSurface(grid, k, SurfaceKind.K), KSurface(grid, l, SurfaceKind.L),
+                        theoretical_surface(grid), telemetry=tel)
+        if spec.sims > 0:
+            res.upper_l = KSurface(grid, up, SurfaceKind.L)
+            res.lower_l = KSurface(grid, lo, SurfaceKind.L)
+            res.diff_upper = KSurface(grid, diff, SurfaceKind.Diff)
+        return res
+
+    # --- multi-process over a host group: one call per rank (its slice of the
+    # observed pattern's pair work + its block of realisations), then the two
+    # exact all-reduces.
     r0, r1 = executor.sim_range(spec.sims)
     counts = np.zeros(shape, np.uint64)
     hi = np.zeros(shape, np.uint64)

@@ -427,3 +427,96 @@ def test_forced_multi_batch_bit_identical(api):
     assert teln.in_threshold_pairs == tel1.in_threshold_pairs
     assert np.array_equal(l1, ln) and np.array_equal(u1, un) and np.array_equal(d1, dn)
     assert np.array_equal(many[2], ln.max(0)) and np.array_equal(many[3], ln.min(0))
+
+
+def test_reference_program_compiles_and_runs_unchanged():
+    """A program written against the reference's runtime.hpp (LocalExecutor,
+    a user Executor plug-in with the three virtuals, run_job, RunTelemetry,
+    speedup_factor) built against include/stripley/ reproduces the golden
+    sample (proj/data/sample_result.json) through both executors and through
+    LocalExecutor::run + aggregate on the device."""
+    from paper_1912_04753_b200.build import build_reference_program
+
+    exe = build_reference_program()
+    g = golden("sample_result.npz")
+    with tempfile.TemporaryDirectory() as d:
+        pts, ring, grid = (os.path.join(d, f) for f in ("p.bin", "r.bin", "g.bin"))
+        n = len(g["x"])
+        _write(pts, np.uint64(n), g["x"], g["y"], g["t"].astype(np.int64))
+        _write(ring, np.uint64(g["ring"].size), g["ring"].reshape(-1))
+        _write(grid, np.uint64(len(g["s"])), g["s"], np.uint64(len(g["tv"])), g["tv"].astype(np.int64))
+        r = subprocess.run([exe, pts, ring, "0", "365", grid, str(int(g["sims"])),
+                            str(int(g["seed"]))], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    out = json.loads(r.stdout)
+    shape = g["k"].shape
+    for key, gk in (("k", "k"), ("l", "l"), ("upper", "upper"), ("lower", "lower"),
+                    ("diff", "diff"), ("k_plugin", "k"), ("upper_plugin", "upper")):
+        assert surfaces_close(np.array(out[key]).reshape(shape), g[gk], TOL), key
+    obs = golden("sample_result.npz")["counts_observed"]
+    assert surfaces_close(np.array(out["k_tasks"]).reshape(shape), g["k"], TOL)
+    assert out["in_threshold"] == int(g["in_threshold_total"])
+    assert out["in_threshold_plugin"] == int(g["in_threshold_total"])
+    assert out["partition_count"] == 1
+    assert out["cylinder_assignments"] == n * (1 + int(g["sims"]))
+    assert out["plugin_bytes_sent"] == 1 + int(g["sims"])  # tasks the plug-in ran
+    assert out["plugin_bytes_received"] == 1              # plans broadcast
+    assert out["ratio"] == 4.0
+    assert int(obs.sum()) > 0
+
+
+def test_nccl_world1_collective_bit_identical(api):
+    """The in-library NCCL path (stk_comm_init + stk_run_job_dist: the exact
+    limb SUM and MAX/MIN all-reduces and the device finalize) at world 1 gives
+    stk_run_job's results bit for bit; the C++ DeviceExecutor rejects world > 1
+    without a communicator or hooks."""
+    est, geom, rt = api["est"], api["geom"], api["rt"]
+    g = golden("sample_result.npz")
+    region = geom.StudyRegion(g["ring"], 0, 365)
+    grid = est.DistanceGrid(g["s"], g["tv"])
+    pts = (g["x"], g["y"], g["t"])
+    spec = rt.JobSpec(grid=grid, sims=int(g["sims"]), seed=int(g["seed"]))
+    plain = rt.run_job(pts, region, spec, rt.DeviceExecutor(device=0, comm=False))
+    ex = rt.DeviceExecutor(device=0, comm=True)
+    assert ex.comm and api["dev"].comm_rank() == (0, 1)
+    try:
+        coll = rt.run_job(pts, region, spec, ex)
+    finally:
+        api["dev"].comm_destroy()
+    for a, b in ((plain.k_hat, coll.k_hat), (plain.l_hat, coll.l_hat),
+                 (plain.upper_l, coll.upper_l), (plain.lower_l, coll.lower_l),
+                 (plain.diff_upper, coll.diff_upper)):
+        assert np.array_equal(a.values, b.values)
+    assert coll.telemetry.in_threshold_pairs == plain.telemetry.in_threshold_pairs
+    assert surfaces_close(coll.k_hat.values, g["k"], TOL)
+    assert surfaces_close(coll.upper_l.values, g["upper"], TOL)
+
+
+def test_invalid_point_raises_without_writing_outputs(api):
+    """Validation runs on the device without a mid-call round trip; a point
+    outside the region still raises the reference's invalid_argument
+    (estimator.cpp:123-127) and leaves the caller's buffers untouched."""
+    import ctypes as C
+
+    from paper_1912_04753_b200 import _lib
+
+    dev, est, geom = api["dev"], api["est"], api["geom"]
+    ring, p0, p1 = square(1000.0, 0, 100)
+    region = geom.StudyRegion(ring, p0, p1)
+    grid = est.DistanceGrid([50.0, 100.0], [5, 10])
+    dev.configure(region, grid)
+    rng = np.random.default_rng(4)
+    x = rng.uniform(0, 1000, 500); y = rng.uniform(0, 1000, 500); t = rng.integers(0, 101, 500)
+    x[123] = 1500.0
+    k = np.full((2, 2), 7.0)
+    rc = dev.lib.stk_run_job(dev.h, _lib.ptr(x), _lib.ptr(y), _lib.ptr(t, C.c_int64), 500, 3, 1,
+                             0, _lib.ptr(k), None, None, None, None, None)
+    assert rc == _lib.STK_EINVAL
+    assert dev.lib.stk_last_error(dev.h).decode() == "point outside study region or period"
+    assert np.all(k == 7.0)
+    t[5] = 101
+    x[123] = 500.0
+    with pytest.raises(ValueError, match="point outside study region or period"):
+        est.estimate_surface((x, y, t), region, grid)
+    t[5] = 100  # the context recovers: the next call is valid
+    est.estimate_surface((x, y, t), region, grid)

@@ -160,21 +160,31 @@ def test_shard_ranges_partition():
 
 
 def test_limbs_roundtrip_exact():
+    """pack_limbs / unpack_limbs (the algebra of the device's pack/unpack
+    kernels): summing limbs of W partials equals the 128-bit sum mod 2^128."""
     rng = np.random.default_rng(3)
     hi = rng.integers(0, 2**40, 50, dtype=np.uint64)
     lo = rng.integers(0, 2**63, 50, dtype=np.uint64) * np.uint64(2) + np.uint64(1)
-    h, m, l = rt._to_limbs(hi, lo)
-    # summing 8 copies in limb space equals 8x the 128-bit value
-    hi2, lo2 = rt._from_limbs(8 * h, 8 * m, 8 * l)
+    cnt = rng.integers(0, 2**50, 50, dtype=np.uint64)
+    limbs = rt.pack_limbs(cnt, hi, lo)
+    c2, hi2, lo2 = rt.unpack_limbs(8 * limbs)
+    assert np.array_equal(c2, 8 * cnt)
     for a, b, c, d in zip(hi, lo, hi2, lo2):
         assert (int(c) << 64 | int(d)) == 8 * (int(a) << 64 | int(b))
     # negative totals (two's complement, e.g. a bin whose terms are all 1 - ulp):
     # -5 on each of 3 ranks sums to -15 = (2^64 - 1) : (2^64 - 15)
     m1 = np.array([np.uint64(2**64 - 1)], dtype=np.uint64)
     neg = np.array([np.uint64(2**64 - 5)], dtype=np.uint64)
-    h, m, l = rt._to_limbs(m1, neg)
-    hi3, lo3 = rt._from_limbs(3 * h, 3 * m, 3 * l)
+    limbs = rt.pack_limbs(np.zeros(1, np.uint64), m1, neg)
+    _, hi3, lo3 = rt.unpack_limbs(3 * limbs)
     assert int(hi3[0]) == 2**64 - 1 and int(lo3[0]) == 2**64 - 15
+    # mixed signs across ranks: +7, -2, -9 -> -4
+    vals = [7, -2, -9]
+    parts = [rt.pack_limbs(np.zeros(1, np.uint64),
+                           np.array([np.uint64((v >> 64) & (2**64 - 1))], np.uint64),
+                           np.array([np.uint64(v & (2**64 - 1))], np.uint64)) for v in vals]
+    _, h4, l4 = rt.unpack_limbs(sum(parts))
+    assert (int(h4[0]) << 64 | int(l4[0])) == (-4) % 2**128
 
 
 def test_device_calls_fail_loudly_without_gpu():
