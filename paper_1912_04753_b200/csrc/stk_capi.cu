@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -102,12 +103,17 @@ const NcclApi& nccl() {
       throw CudaFail(std::string(#expr) + ": " + cudaGetErrorString(e_));                 \
   } while (0)
 
+// Bumped by every device (re)allocation: a captured CUDA graph holds raw
+// buffer addresses and is replayed only while this is unchanged.
+uint64_t g_alloc_gen = 0;
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t cap = 0;  // elements
   void ensure(size_t n) {
     if (n <= cap) return;
+    ++g_alloc_gen;
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
@@ -146,6 +152,10 @@ bool segments_properly_intersect(const double* a, const double* b, const double*
 }
 
 }  // namespace
+
+namespace {
+struct GraphCache;  // captured pipeline of the last repeated job (run_pipeline)
+}
 
 struct stk_ctx {
   int device = 0;
@@ -225,7 +235,9 @@ struct stk_ctx {
   unsigned char* hstage = nullptr;
   size_t hstage_cap = 0, hstage_used = 0;
   struct Out {
-    void* dst;
+    void* dst;        // resolved host destination (field < 0) ...
+    int field;        // ... or a JobOut field (bound per call: graphs replay the layout)
+    uint64_t elem;    // element offset into that field
     size_t off, bytes;
   };
   std::vector<Out> outs;
@@ -239,6 +251,7 @@ struct stk_ctx {
   };
   std::vector<Occ> occ;
   bool rv_dev_valid = false;  // d_rv holds region_view() of the current region + grid
+  std::unique_ptr<GraphCache> graph;
 
   std::vector<cudaEvent_t> evpool;
   size_t evnext = 0;
@@ -690,12 +703,13 @@ void stage_reset(stk_ctx* c, size_t bytes) {
 }
 
 // Enqueue a device -> staging copy whose bytes go to host `dst` at finish_call.
-void* stage_d2h(stk_ctx* c, void* dst, const void* dsrc, size_t bytes) {
+void* stage_d2h(stk_ctx* c, void* dst, const void* dsrc, size_t bytes, int field = -1,
+                uint64_t elem = 0) {
   const size_t off = (c->hstage_used + 15) & ~size_t(15);
   if (off + bytes > c->hstage_cap) throw CudaFail("internal error: output staging overflow");
   CK(cudaMemcpyAsync(c->hstage + off, dsrc, bytes, cudaMemcpyDeviceToHost, c->stream));
   c->hstage_used = off + bytes;
-  if (dst) c->outs.push_back({dst, off, bytes});
+  if (dst || field >= 0) c->outs.push_back({dst, field, elem, off, bytes});
   return c->hstage + off;
 }
 
@@ -866,10 +880,45 @@ double elapsed(const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
   return s;
 }
 
+// The pipeline shared by estimate / simulate / run_job: an optional observed
+// pattern (device pointers) followed by realisations [r_begin, r_end).
+struct JobOut {
+  double* k_obs = nullptr;   // host
+  double* l_obs = nullptr;   // host
+  double* l_all = nullptr;   // host (r_end - r_begin) * bins
+  double* upper = nullptr;   // host
+  double* lower = nullptr;   // host
+  double* diff = nullptr;    // host
+  uint64_t* obs_counts = nullptr;  // host: exact pre-cumulative results of the observed
+  uint64_t* obs_hi = nullptr;      //       pattern (or of its shard)
+  uint64_t* obs_lo = nullptr;
+  // collective (stk_run_job_dist): this rank computed shard `rank` of the
+  // observed pattern's pairs and its block of the realisations; the exact
+  // all-reduces over the context's communicator combine them on the device
+  bool dist = false;
+  uint32_t sims_total = 0;   // realisations of the whole job (dist)
+  bool validate = false;     // run validate_kernel on the observed points first
+};
+
+enum JobField { F_K = 0, F_L, F_LALL, F_UP, F_LO, F_DIFF };
+double* field_ptr(const JobOut& o, int f) {
+  switch (f) {
+    case F_K: return o.k_obs;
+    case F_L: return o.l_obs;
+    case F_LALL: return o.l_all;
+    case F_UP: return o.upper;
+    case F_LO: return o.lower;
+    default: return o.diff;
+  }
+}
+
+
+
 // End of a call: ONE synchronisation, then the checks in the reference's order
 // (invalid points first: estimator.cpp:123-127 throws before any work), then
 // the staged outputs go to the caller's buffers and the telemetry is added.
-void finish_call(stk_ctx* c, Timers& tm, stk_telemetry* tel, uint64_t patterns) {
+void finish_call(stk_ctx* c, Timers& tm, stk_telemetry* tel, uint64_t patterns,
+                 const JobOut* jo = nullptr) {
   const unsigned long long* st =
       (const unsigned long long*)stage_d2h(c, nullptr, c->stats.p, 8 * sizeof(unsigned long long));
   const unsigned long long* bad =
@@ -882,7 +931,10 @@ void finish_call(stk_ctx* c, Timers& tm, stk_telemetry* tel, uint64_t patterns) 
   // construction (<= 31 + kArcChunk*64 ring entries; <= 8 crossings on 4 sides)
   if (st[3] & 2) throw CudaFail("internal error: arc ring overflow in the pair kernel");
   if (st[3] & 1) throw CudaFail("internal error: crossing buffer overflow in the rectangle edge weight");
-  for (const auto& o : c->outs) std::memcpy(o.dst, c->hstage + o.off, o.bytes);
+  for (const auto& o : c->outs) {
+    void* dst = o.field >= 0 ? (void*)(field_ptr(*jo, o.field) + o.elem) : o.dst;
+    if (dst) std::memcpy(dst, c->hstage + o.off, o.bytes);
+  }
   c->outs.clear();
   if (!tel) return;
   tel->in_threshold_pairs += st[0];
@@ -911,25 +963,6 @@ Source source_of(int method) {
   }
   throw InvalidArg("unknown simulation method");
 }
-
-// The pipeline shared by estimate / simulate / run_job: an optional observed
-// pattern (device pointers) followed by realisations [r_begin, r_end).
-struct JobOut {
-  double* k_obs = nullptr;   // host
-  double* l_obs = nullptr;   // host
-  double* l_all = nullptr;   // host (r_end - r_begin) * bins
-  double* upper = nullptr;   // host
-  double* lower = nullptr;   // host
-  double* diff = nullptr;    // host
-  uint64_t* obs_counts = nullptr;  // host: exact pre-cumulative results of the observed
-  uint64_t* obs_hi = nullptr;      //       pattern (or of its shard)
-  uint64_t* obs_lo = nullptr;
-  // collective (stk_run_job_dist): this rank computed shard `rank` of the
-  // observed pattern's pairs and its block of the realisations; the exact
-  // all-reduces over the context's communicator combine them on the device
-  bool dist = false;
-  uint32_t sims_total = 0;   // realisations of the whole job (dist)
-};
 
 // Exact exchange of the observed partials and the partial envelopes over the
 // context's NCCL communicator, then finalize / diff on the device (the
@@ -981,26 +1014,38 @@ void exchange(stk_ctx* c, const Plan& P, uint64_t n, bool have_env, uint32_t sim
   ++c->launches;
 }
 
-void run_pipeline(stk_ctx* c, const double* dx, const double* dy, const int64_t* dt, uint64_t n,
-                  bool with_observed, int method, uint64_t base_seed, uint32_t r_begin,
-                  uint32_t r_end, const JobOut& out, stk_telemetry* tel,
-                  uint32_t obs_shard = 0, uint32_t obs_nshards = 1) {
-  require_ready(c);
-  c->evnext = 0;
+// What one enqueue of the pipeline leaves for the host epilogue (kept with a
+// captured graph so a replay needs no re-enqueue).
+struct PipeInfo {
   Timers tm;
+  uint64_t patterns = 0;
+  uint64_t launches = 0;
+  const void* raw_host = nullptr;  // staged observed sums (obs_counts requested)
+  uint32_t bins = 0;
+  bool validated = false;
+  std::vector<stk_ctx::Out> outs;
+};
+
+// Enqueue the whole pipeline on the context stream (no host synchronisation).
+PipeInfo enqueue_pipeline(stk_ctx* c, const double* dx, const double* dy, const int64_t* dt,
+                          uint64_t n, bool with_observed, int method, uint64_t base_seed,
+                          uint32_t r_begin, uint32_t r_end, const JobOut& out,
+                          uint32_t obs_shard, uint32_t obs_nshards, const Plan& P) {
+  PipeInfo info;
+  c->evnext = 0;
+  Timers& tm = info.tm;
   tm.t0 = c->ev();
   tm.t1 = c->ev();
   CK(cudaEventRecord(tm.t0, c->stream));
   const uint64_t sims = r_end > r_begin ? r_end - r_begin : 0;
   const uint64_t patterns = (with_observed ? 1 : 0) + sims;
-  Plan P = make_plan(c, n, patterns);
+  info.patterns = patterns;
   const Source src = source_of(method);
   const uint32_t bins = P.bins;
-  stage_reset(c, 8 * (uint64_t)bins * (5 + 4 + (out.l_all ? sims : 0)) + 128);
+  info.bins = bins;
+  if (out.validate) validate_points(c, dx, dy, dt, n);
+  info.validated = c->check_points;
   CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * 8, c->stream));
-  c->env.ensure(2 * (uint64_t)bins);
-  c->obs.ensure(2 * (uint64_t)bins);
-  c->obsraw.ensure(4 * (uint64_t)bins);
   bool env_init = true;
   uint64_t done = 0;
   uint32_t next_r = r_begin;
@@ -1041,8 +1086,8 @@ void run_pipeline(stk_ctx* c, const double* dx, const double* dy, const int64_t*
       ++c->launches;
       env_init = false;
       if (out.l_all)
-        stage_d2h(c, out.l_all + (uint64_t)(next_r - r_begin) * bins, B.L + (uint64_t)p * bins,
-                  sizeof(double) * bins * nsim);
+        stage_d2h(c, nullptr, B.L + (uint64_t)p * bins, sizeof(double) * bins * nsim, F_LALL,
+                  (uint64_t)(next_r - r_begin) * bins);
     }
     CK(cudaEventRecord(f1, c->stream));
     tm.fin.push_back({f0, f1});
@@ -1050,26 +1095,150 @@ void run_pipeline(stk_ctx* c, const double* dx, const double* dy, const int64_t*
     done += R;
   }
   const uint32_t sims_job = out.dist ? out.sims_total : (uint32_t)sims;
-  const void* raw_host = nullptr;  // this rank's own observed sums, before any exchange
-  if (with_observed && out.obs_counts)
-    raw_host = stage_d2h(c, nullptr, c->obsraw.p, 32 * (uint64_t)bins);
+  if (with_observed && out.obs_counts)  // this rank's own observed sums, before any exchange
+    info.raw_host = stage_d2h(c, nullptr, c->obsraw.p, 32 * (uint64_t)bins);
   if (out.dist) exchange(c, P, n, sims > 0, sims_job);
   if (with_observed && sims_job > 0 && out.diff) {
-    c->scratch.ensure(bins);
     diff_kernel<<<(bins + 255) / 256, 256, 0, c->stream>>>(c->obs.p + bins, c->env.p, bins,
                                                            c->scratch.p);
     CK(cudaGetLastError());
     ++c->launches;
-    stage_d2h(c, out.diff, c->scratch.p, sizeof(double) * bins);
+    stage_d2h(c, nullptr, c->scratch.p, sizeof(double) * bins, F_DIFF);
   }
-  if (with_observed && out.k_obs) stage_d2h(c, out.k_obs, c->obs.p, sizeof(double) * bins);
-  if (with_observed && out.l_obs) stage_d2h(c, out.l_obs, c->obs.p + bins, sizeof(double) * bins);
-  if (sims_job > 0 && out.upper) stage_d2h(c, out.upper, c->env.p, sizeof(double) * bins);
-  if (sims_job > 0 && out.lower) stage_d2h(c, out.lower, c->env.p + bins, sizeof(double) * bins);
+  if (with_observed && out.k_obs) stage_d2h(c, nullptr, c->obs.p, sizeof(double) * bins, F_K);
+  if (with_observed && out.l_obs)
+    stage_d2h(c, nullptr, c->obs.p + bins, sizeof(double) * bins, F_L);
+  if (sims_job > 0 && out.upper) stage_d2h(c, nullptr, c->env.p, sizeof(double) * bins, F_UP);
+  if (sims_job > 0 && out.lower)
+    stage_d2h(c, nullptr, c->env.p + bins, sizeof(double) * bins, F_LO);
   CK(cudaEventRecord(tm.t1, c->stream));
-  finish_call(c, tm, tel, patterns);
-  if (raw_host) {
-    const unsigned long long* r = (const unsigned long long*)raw_host;
+  info.launches = c->launches;
+  info.outs = c->outs;
+  return info;
+}
+
+// Everything a captured pipeline depends on besides the context's region /
+// grid / budget (whose setters drop the graph): a replay needs all equal.
+struct PipeKey {
+  const void *dx = nullptr, *dy = nullptr, *dt = nullptr;
+  uint64_t n = 0, seed = 0, gen = 0;
+  int method = 0;
+  uint32_t r_begin = 0, r_end = 0, shard = 0, nshards = 0;
+  unsigned flags = 0;
+  const void* hstage = nullptr;
+  bool operator==(const PipeKey& o) const {
+    return dx == o.dx && dy == o.dy && dt == o.dt && n == o.n && seed == o.seed &&
+           gen == o.gen && method == o.method && r_begin == o.r_begin && r_end == o.r_end &&
+           shard == o.shard && nshards == o.nshards && flags == o.flags && hstage == o.hstage;
+  }
+};
+
+struct GraphCache {
+  cudaGraphExec_t exec = nullptr;
+  PipeKey key, last;  // key of the captured graph; key of the last plain call
+  PipeInfo info;
+  ~GraphCache() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
+void drop_graph(stk_ctx* c) { c->graph.reset(); }
+
+// The pipeline shared by estimate / simulate / run_job: an optional observed
+// pattern (device pointers) followed by realisations [r_begin, r_end).
+// Small single-batch jobs repeated with identical arguments (a service loop,
+// the bench, one rank's share of C2 at 8 GPUs) are captured as one CUDA graph
+// on the second identical call and replayed after that: one launch and one
+// synchronisation per call instead of ~30 API calls.
+void run_pipeline(stk_ctx* c, const double* dx, const double* dy, const int64_t* dt, uint64_t n,
+                  bool with_observed, int method, uint64_t base_seed, uint32_t r_begin,
+                  uint32_t r_end, const JobOut& out, stk_telemetry* tel,
+                  uint32_t obs_shard = 0, uint32_t obs_nshards = 1) {
+  require_ready(c);
+  const uint64_t sims = r_end > r_begin ? r_end - r_begin : 0;
+  const uint64_t patterns = (with_observed ? 1 : 0) + sims;
+  const Plan P = make_plan(c, n, patterns);
+  const uint32_t bins = P.bins;
+  stage_reset(c, 8 * (uint64_t)bins * (5 + 4 + (out.l_all ? sims : 0)) + 128);
+  c->env.ensure(2 * (uint64_t)bins);
+  c->obs.ensure(2 * (uint64_t)bins);
+  c->obsraw.ensure(4 * (uint64_t)bins);
+  c->scratch.ensure(bins);
+  static const bool no_graph = std::getenv("STK_NO_GRAPH") != nullptr;
+  const bool graphable = !no_graph && !out.dist && patterns <= (uint64_t)P.R &&
+                         n * patterns <= (32ull << 20);
+  PipeKey key;
+  if (graphable) {
+    key.dx = dx; key.dy = dy; key.dt = dt; key.n = n; key.seed = base_seed;
+    key.method = method; key.r_begin = r_begin; key.r_end = r_end;
+    key.shard = obs_shard; key.nshards = obs_nshards; key.hstage = c->hstage;
+    key.flags = (with_observed ? 1u : 0u) | (out.validate ? 2u : 0u) | (out.k_obs ? 4u : 0u) |
+                (out.l_obs ? 8u : 0u) | (out.l_all ? 16u : 0u) | (out.upper ? 32u : 0u) |
+                (out.lower ? 64u : 0u) | (out.diff ? 128u : 0u) | (out.obs_counts ? 256u : 0u);
+    key.gen = g_alloc_gen;
+  }
+  PipeInfo info;
+  bool replayed = false;
+  if (graphable && !c->graph) c->graph = std::make_unique<GraphCache>();
+  GraphCache* gc = c->graph.get();
+  if (graphable && gc->exec && gc->key == key) {
+    CK(cudaGraphLaunch(gc->exec, c->stream));
+    info = gc->info;
+    replayed = true;
+  } else if (graphable && gc->last == key) {
+    // second identical call: capture (nothing allocates: same sizes as the last call)
+    if (gc->exec) cudaGraphExecDestroy(gc->exec);
+    gc->exec = nullptr;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+    cudaGraph_t graph = nullptr;
+    try {
+      info = enqueue_pipeline(c, dx, dy, dt, n, with_observed, method, base_seed, r_begin, r_end,
+                              out, obs_shard, obs_nshards, P);
+    } catch (...) {
+      cudaStreamEndCapture(c->stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    CK(cudaStreamEndCapture(c->stream, &graph));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess || g_alloc_gen != key.gen) {  // not replayable: run it plainly
+      (void)cudaGetLastError();
+      if (exec) cudaGraphExecDestroy(exec);
+      c->launches = 0;
+      c->outs.clear();
+      c->hstage_used = 0;
+      info = enqueue_pipeline(c, dx, dy, dt, n, with_observed, method, base_seed, r_begin, r_end,
+                              out, obs_shard, obs_nshards, P);
+    } else {
+      gc->exec = exec;
+      gc->key = key;
+      gc->info = info;
+      CK(cudaGraphLaunch(exec, c->stream));
+      replayed = true;
+    }
+  } else {
+    info = enqueue_pipeline(c, dx, dy, dt, n, with_observed, method, base_seed, r_begin, r_end,
+                            out, obs_shard, obs_nshards, P);
+    if (graphable) {
+      gc->last = key;
+      gc->last.gen = g_alloc_gen;  // as left by this call's allocations
+    }
+  }
+  if (replayed) {
+    c->launches = info.launches;
+    c->outs = info.outs;
+    c->check_points = info.validated;
+    c->hstage_used = 0;
+    for (const auto& o : info.outs) c->hstage_used = std::max(c->hstage_used, o.off + o.bytes);
+    if (info.raw_host)
+      c->hstage_used = std::max(c->hstage_used, (size_t)((const unsigned char*)info.raw_host -
+                                                         c->hstage) + 32 * (size_t)bins);
+  }
+  finish_call(c, info.tm, tel, info.patterns, &out);
+  if (info.raw_host) {
+    const unsigned long long* r = (const unsigned long long*)info.raw_host;
     for (uint32_t i = 0; i < bins; ++i) {
       const unsigned long long raw = r[i], half = r[bins + i], lo = r[2 * bins + i],
                                hi = r[3 * bins + i];
@@ -1171,6 +1340,7 @@ void stk_destroy(stk_ctx* c) {
   c->env.release(); c->obs.release(); c->flags.release(); c->ovf.release();
   c->sel_start.release(); c->center_pos.release(); c->arcq.release(); c->angs.release();
   c->scratch.release(); c->sx.release(); c->sy.release(); c->st.release();
+  c->graph.reset();
   c->obsraw.release(); c->limbs.release(); c->d_rv.release();
   if (c->comm) nccl().comm_destroy(c->comm);
   if (c->hstage) cudaFreeHost(c->hstage);
@@ -1186,6 +1356,7 @@ int stk_set_memory_budget(stk_ctx* c, uint64_t bytes) {
   return guarded(c, [&] {
     if (bytes < (1ull << 20)) throw InvalidArg("memory budget must be >= 1 MiB");
     c->mem_budget = bytes;
+    drop_graph(c);
   });
 }
 
@@ -1277,6 +1448,7 @@ int stk_set_region(stk_ctx* c, const double* ring_xy, uint32_t nv, int64_t perio
     c->have_region = false;
     c->slab_ok = c->ec_ok = false;
     c->rv_dev_valid = false;
+    drop_graph(c);
     const RegionInfo ri = check_region(ring_xy, nv, period_start, period_end);
     const std::vector<double>& r = ri.ring;
     const uint32_t m = ri.nv;
@@ -1376,6 +1548,7 @@ int stk_set_grid(stk_ctx* c, const double* s_values, uint32_t cs, const int64_t*
     c->have_grid = false;
     c->ec_ok = false;
     c->rv_dev_valid = false;
+    drop_graph(c);
     check_grid(s_values, cs, t_values, ct);
     if ((uint64_t)cs * ct > (1u << 20)) throw Unsupported("more than 2^20 grid cells");
     if (cs > (uint32_t)kMaxAxis || ct > (uint32_t)kMaxAxis)
@@ -1436,9 +1609,9 @@ int stk_estimate_surface(stk_ctx* c, const double* x, const double* y, const int
     require_ready(c);
     check_n(n);
     upload_points(c, x, y, t, n);
-    validate_points(c, c->sx.p, c->sy.p, c->st.p, n);
     JobOut o;
     o.k_obs = k_out;
+    o.validate = true;
     run_pipeline(c, c->sx.p, c->sy.p, c->st.p, n, true, STK_METHOD_CSR, 0, 0, 0, o, tel);
   });
 }
@@ -1524,13 +1697,13 @@ int stk_simulate(stk_ctx* c, const double* x, const double* y, const int64_t* t,
     if (src != Source::Csr) {
       if (!x || !y || !t) throw InvalidArg("bootstrap/permutation need the observed points");
       upload_points(c, x, y, t, n);
-      validate_points(c, c->sx.p, c->sy.p, c->st.p, n);
       dx = c->sx.p;
       dy = c->sy.p;
       dt = c->st.p;
     }
     if (r_end < r_begin) throw InvalidArg("r_end < r_begin");
     JobOut o;
+    o.validate = src != Source::Csr;  // the observed points feed bootstrap / permutation
     o.l_all = l_all;
     o.upper = upper_l;
     o.lower = lower_l;
@@ -1542,8 +1715,8 @@ static int run_job_impl(stk_ctx* c, const double* dx, const double* dy, const in
                         uint64_t n, uint32_t sims, uint64_t seed, int method, double* k_out,
                         double* l_out, double* upper_l, double* lower_l, double* diff_upper,
                         stk_telemetry* tel) {
-  validate_points(c, dx, dy, dt, n);
   JobOut o;
+  o.validate = true;
   o.k_obs = k_out;
   o.l_obs = l_out;
   o.upper = upper_l;
@@ -1587,8 +1760,8 @@ static void run_shard_impl(stk_ctx* c, const double* dx, const double* dy, const
   if (obs_nshards == 0 || obs_shard >= obs_nshards) throw InvalidArg("shard index out of range");
   if (r_end < r_begin) throw InvalidArg("r_end < r_begin");
   if (!obs_counts) throw InvalidArg("obs_counts is required");
-  validate_points(c, dx, dy, dt, n);
   JobOut o;
+  o.validate = true;
   o.upper = upper_l;
   o.lower = lower_l;
   o.obs_counts = obs_counts;
@@ -1681,7 +1854,6 @@ static void run_dist_impl(stk_ctx* c, const double* dx, const double* dy, const 
                           double* l_out, double* upper_l, double* lower_l, double* diff_upper,
                           stk_telemetry* tel) {
   if (!c->comm) throw StateErr("no communicator (stk_comm_init)");
-  validate_points(c, dx, dy, dt, n);
   const uint32_t G = (uint32_t)c->nranks, g = (uint32_t)c->comm_rank;
   const uint32_t base = sims / G, extra = sims % G;  // contiguous blocks of the seed ladder
   const uint32_t r0 = g * base + std::min(g, extra);
@@ -1694,6 +1866,7 @@ static void run_dist_impl(stk_ctx* c, const double* dx, const double* dy, const 
   o.diff = diff_upper;
   o.dist = true;
   o.sims_total = sims;
+  o.validate = true;
   run_pipeline(c, dx, dy, dt, n, true, method, seed, r0, r1, o, tel, g, G);
 }
 
