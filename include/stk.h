@@ -35,6 +35,9 @@ extern "C" {
 #define STK_METHOD_BOOTSTRAP 1   /* sim::Method::Bootstrap   */
 #define STK_METHOD_PERMUTATION 2 /* sim::Method::Permutation */
 
+#define STK_RNG_MT19937_64 0 /* the reference's rng::Engine stream: bit-exact realisations */
+#define STK_RNG_PHILOX 1     /* opt-in Philox4x32-10, counter-based: statistical parity only */
+
 typedef struct stk_ctx stk_ctx;
 
 /* Superset of est::EstimatorTelemetry (core/include/stripley/estimator.hpp:47-51)
@@ -93,6 +96,15 @@ int stk_set_grid(stk_ctx* ctx, const double* s_values, uint32_t cs, const int64_
  * STK_EUNSUPPORTED. */
 int stk_set_options(stk_ctx* ctx, int use_index, int use_cache, double coord_tolerance,
                     double dist_tolerance);
+
+/* Realisation generator for CSR and bootstrap (default STK_RNG_MT19937_64,
+ * the reference's std::mt19937_64 stream of rng.hpp:39 and simulation.cpp:10-35,
+ * bit for bit).  STK_RNG_PHILOX: Philox4x32-10 keyed by the realisation seed,
+ * one counter per point -- fully parallel generation, same distributions and
+ * seed ladder, results that agree with the reference statistically
+ * (calibration), not bitwise.  Permutation stays on the sequential stream
+ * (STK_EUNSUPPORTED with Philox). */
+int stk_set_rng(stk_ctx* ctx, int rng);
 
 /* ---- the hot path ----------------------------------------------------- */
 /* est::estimate_surface (core/include/stripley/estimator.hpp:107-111,
@@ -228,6 +240,10 @@ int stk_task_histogram(stk_ctx* ctx, const double* px, const double* py, const i
                        uint64_t* comparisons);
 
 /* ---- instrumentation --------------------------------------------------- */
+/* Raw Philox4x32-10 blocks computed on the device (known-answer tests):
+ * out[4i..4i+3] = philox(ctr[4i..4i+3], key[2i..2i+1]). */
+int stk_philox4x32(stk_ctx* ctx, const uint32_t* ctr, const uint32_t* key, uint32_t n,
+                   uint32_t* out);
 /* Device-measured FP64 issue peak (DFMA thread-instructions per second) at the
  * current clocks: the denominator of the pair kernel's roofline. */
 int stk_measure_fp64_peak(stk_ctx* ctx, double* instr_per_s);

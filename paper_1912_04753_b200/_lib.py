@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("STK_LIB_PATH") or os.path.join(HERE, "libstk.so")
 
 STK_OK, STK_EINVAL, STK_EUNSUPPORTED, STK_ECUDA, STK_ESTATE, STK_ENCCL = 0, 1, 2, 3, 4, 5
 NCCL_ID_BYTES = 128
+RNG_MT19937_64, RNG_PHILOX = 0, 1
 METHOD_CSR, METHOD_BOOTSTRAP, METHOD_PERMUTATION = 0, 1, 2
 
 
@@ -48,7 +49,7 @@ EXPORTED = [
     "stk_spatial_weights", "stk_measure_fp64_peak", "stk_run_job_shard",
     "stk_run_job_shard_device", "stk_generate", "stk_comm_unique_id", "stk_comm_init",
     "stk_comm_destroy", "stk_comm_rank", "stk_run_job_dist", "stk_run_job_dist_device",
-    "stk_task_histogram",
+    "stk_task_histogram", "stk_set_rng", "stk_philox4x32",
 ]
 
 _dp = C.POINTER(C.c_double)
@@ -88,6 +89,8 @@ _SIGS = {
     "stk_comm_rank": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "stk_run_job_dist": (C.c_int, [_vp, _dp, _dp, _ip, _u64, _u32, _u64, C.c_int, _dp, _dp, _dp, _dp, _dp, _tp]),
     "stk_run_job_dist_device": (C.c_int, [_vp, _vp, _vp, _vp, _u64, _u32, _u64, C.c_int, _dp, _dp, _dp, _dp, _dp, _tp]),
+    "stk_set_rng": (C.c_int, [_vp, C.c_int]),
+    "stk_philox4x32": (C.c_int, [_vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), _u32, C.POINTER(C.c_uint32)]),
     "stk_task_histogram": (C.c_int, [_vp, _dp, _dp, _ip, C.POINTER(C.c_uint32), _u64, _dp, _dp, _ip, C.POINTER(C.c_uint32), _dp, _ip, _u64, _dp, _up, _up]),
 }
 

@@ -166,6 +166,7 @@ struct stk_ctx {
   int time_radius = 0;     // time layers of the stencil, 0 = the spatial radius (STK_TIME_RADIUS env)
   double min_cell_pop = 8.0;  // finer cells only when this populous (STK_MIN_CELL_POP env)
   int stencil_radius = 2;  // preferred cell refinement (STK_STENCIL_RADIUS env overrides)
+  int rng = STK_RNG_MT19937_64;  // realisation generator (stk_set_rng)
 
   // region (geom::StudyRegion)
   bool have_region = false;
@@ -728,6 +729,21 @@ void generate(stk_ctx* c, const Batch& B, Source src, int p_first, int count, ui
     return;
   }
   CK(cudaMemsetAsync(B.flags + p_first, 0, sizeof(int) * count, c->stream));
+  if (c->rng == STK_RNG_PHILOX) {  // opt-in counter-based generator (statistical parity)
+    const dim3 gp((unsigned)((n + 255) / 256), (unsigned)count);
+    if (src == Source::Csr) {
+      const uint64_t ntl = (uint64_t)(c->p1 - c->p0) + 1;
+      csr_philox_kernel<<<gp, 256, 0, c->stream>>>(B, p_first, seed0, region_view(c), ntl);
+    } else if (src == Source::Bootstrap) {
+      bootstrap_philox_kernel<<<gp, 256, 0, c->stream>>>(B, p_first, seed0, ox, oy, ot);
+    } else {
+      throw Unsupported("permutation draws Fisher-Yates on the reference's sequential stream; "
+                        "the Philox generator covers CSR and bootstrap");
+    }
+    CK(cudaGetLastError());
+    ++c->launches;
+    return;
+  }
   if (src == Source::Csr) {
     const uint64_t ntl = (uint64_t)(c->p1 - c->p0) + 1;  // uniform_int(p0, p1)
     const uint64_t limit = ~0ULL - (~0ULL % ntl);
@@ -931,6 +947,9 @@ void finish_call(stk_ctx* c, Timers& tm, stk_telemetry* tel, uint64_t patterns,
   // construction (<= 31 + kArcChunk*64 ring entries; <= 8 crossings on 4 sides)
   if (st[3] & 2) throw CudaFail("internal error: arc ring overflow in the pair kernel");
   if (st[3] & 1) throw CudaFail("internal error: crossing buffer overflow in the rectangle edge weight");
+  if (st[3] & 4)
+    throw Unsupported("Philox CSR: 4096 rejections for one point (the region covers too small a "
+                      "share of its bounding box)");
   for (const auto& o : c->outs) {
     void* dst = o.field >= 0 ? (void*)(field_ptr(*jo, o.field) + o.elem) : o.dst;
     if (dst) std::memcpy(dst, c->hstage + o.off, o.bytes);
@@ -2048,6 +2067,31 @@ int stk_task_histogram(stk_ctx* c, const double* px, const double* py, const int
     }
     if (in_threshold) *in_threshold = h[3ull * bins];
     if (comparisons) *comparisons = h[3ull * bins + 1];
+  });
+}
+
+int stk_set_rng(stk_ctx* c, int rng) {
+  return guarded(c, [&] {
+    if (rng != STK_RNG_MT19937_64 && rng != STK_RNG_PHILOX) throw InvalidArg("unknown rng");
+    c->rng = rng;
+    drop_graph(c);
+  });
+}
+
+int stk_philox4x32(stk_ctx* c, const uint32_t* ctr, const uint32_t* key, uint32_t n,
+                   uint32_t* out) {
+  return guarded(c, [&] {
+    if (n == 0) return;
+    DevBuf<uint32_t> b;
+    b.ensure(10ull * n);
+    CK(cudaMemcpyAsync(b.p, ctr, 16ull * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(b.p + 4ull * n, key, 8ull * n, cudaMemcpyHostToDevice, c->stream));
+    philox_kat_kernel<<<(n + 127) / 128, 128, 0, c->stream>>>(b.p, b.p + 4ull * n, n,
+                                                               b.p + 6ull * n);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, b.p + 6ull * n, 16ull * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    b.release();
   });
 }
 

@@ -163,6 +163,93 @@ __global__ void csr_finish_kernel(Batch B, int p_first, RegionView reg, uint64_t
   if (vt >= limit || !point_in_polygon(B.x[o], B.y[o], reg.ring, reg.nv)) B.flags[p] = 1;
 }
 
+// ---------------------------------------------------------- Philox (opt-in)
+// Philox4x32-10 (Salmon et al., SC'11; the counter-based generator of
+// cuRAND / Random123): 10 rounds of two 32x32 -> 64 multiplies, Weyl key
+// schedule.  Counter-based: every point draws from its own counter, so a
+// realisation is generated fully in parallel.  NOT the reference's stream
+// (std::mt19937_64): results agree with the reference statistically only
+// (criterion-3 calibration, tests/test_gpu_philox.py).
+__device__ __forceinline__ uint4 philox4x32_10(uint4 ctr, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * ctr.x, hi0 = __umulhi(0xD2511F53u, ctr.x);
+    const uint32_t lo1 = 0xCD9E8D57u * ctr.z, hi1 = __umulhi(0xCD9E8D57u, ctr.z);
+    ctr = make_uint4(hi1 ^ ctr.y ^ k0, lo1, hi0 ^ ctr.w ^ k1, lo0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return ctr;
+}
+
+// Two 64-bit words of block (k, j) of realisation seed s: key = s, counter =
+// (k lo, k hi, j, 0); word a = x << 32 | y, word b = z << 32 | w.
+__device__ __forceinline__ void philox_u64x2(uint64_t s, uint64_t k, uint32_t j, uint64_t* a,
+                                             uint64_t* b) {
+  const uint4 v = philox4x32_10(make_uint4((uint32_t)k, (uint32_t)(k >> 32), j, 0u),
+                                (uint32_t)s, (uint32_t)(s >> 32));
+  *a = ((uint64_t)v.x << 32) | v.y;
+  *b = ((uint64_t)v.z << 32) | v.w;
+}
+
+// CSR with Philox (opt-in, STK_RNG_PHILOX): point k of realisation seed
+// seed0 + blockIdx.y, attempt a: x, y = bbox uniform from block (k, 2a) with
+// the reference's real01 / uniform formulas (rng.hpp:28-31), kept if inside
+// the region (point_in_polygon, simulation.cpp:10-24's rejection), t =
+// p0 + floor(u * ntl / 2^64) from block (k, 2a + 1).  Up to 4096 attempts per
+// point (flag the realisation otherwise: the host raises).
+__global__ void csr_philox_kernel(Batch B, int p_first, uint64_t seed0, RegionView reg,
+                                  uint64_t ntl) {
+  const int p = p_first + blockIdx.y;
+  const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (k >= B.n) return;
+  const uint64_t s = seed0 + (uint64_t)blockIdx.y;
+  const uint64_t o = (uint64_t)p * B.n + k;
+  for (uint32_t a = 0; a < 4096; ++a) {
+    uint64_t ux, uy, ut, spare;
+    philox_u64x2(s, k, 2 * a, &ux, &uy);
+    const double x = mt_uniform(ux, reg.xmin, reg.xmax);
+    const double y = mt_uniform(uy, reg.ymin, reg.ymax);
+    if (!reg.rect && !point_in_region(x, y, reg)) continue;
+    philox_u64x2(s, k, 2 * a + 1, &ut, &spare);
+    B.x[o] = x;
+    B.y[o] = y;
+    B.t[o] = reg.p0 + (int64_t)__umul64hi(ut, ntl);
+    return;
+  }
+  atomicOr(&B.stats[3], 4ULL);  // reported by the host: region too small in its bbox
+}
+
+// Bootstrap with Philox (opt-in): draw i of realisation seed picks observed
+// point floor(u * n / 2^64), u from block (i, 0).
+__global__ void bootstrap_philox_kernel(Batch B, int p_first, uint64_t seed0, const double* ox,
+                                        const double* oy, const int64_t* ot) {
+  const int p = p_first + blockIdx.y;
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= B.n) return;
+  uint64_t u, spare;
+  philox_u64x2(seed0 + (uint64_t)blockIdx.y, i, 0u, &u, &spare);
+  const uint64_t j = __umul64hi(u, B.n);
+  const uint64_t o = (uint64_t)p * B.n + i;
+  B.x[o] = ox[j];
+  B.y[o] = oy[j];
+  B.t[o] = ot[j];
+}
+
+// Raw Philox4x32-10 blocks for the known-answer test: out[4i..4i+3] =
+// philox(ctr[i], key[i]).
+__global__ void philox_kat_kernel(const uint32_t* ctr, const uint32_t* key, uint32_t n,
+                                  uint32_t* out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint4 v = philox4x32_10(make_uint4(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2],
+                                           ctr[4 * i + 3]), key[2 * i], key[2 * i + 1]);
+  out[4 * i] = v.x;
+  out[4 * i + 1] = v.y;
+  out[4 * i + 2] = v.z;
+  out[4 * i + 3] = v.w;
+}
+
 // CSR for general polygons (rejection sampling; simulation.cpp:10-24).  A
 // candidate starting at MT output j reads outputs j, j+1 (x, y); if inside it
 // draws t from j+2 (retrying below()'s rare rejections), else the next

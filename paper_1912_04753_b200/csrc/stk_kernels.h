@@ -28,6 +28,12 @@ __global__ void csr_poly_kernel(Batch B, int p_first, uint64_t seed0, RegionView
                                 uint64_t ntl, uint64_t limit);
 __global__ void csr_seq_kernel(Batch B, int p_first, int count, uint64_t seed0, RegionView reg,
                                uint64_t ntl, uint64_t limit, int force);
+__global__ void csr_philox_kernel(Batch B, int p_first, uint64_t seed0, RegionView reg,
+                                  uint64_t ntl);
+__global__ void bootstrap_philox_kernel(Batch B, int p_first, uint64_t seed0, const double* ox,
+                                        const double* oy, const int64_t* ot);
+__global__ void philox_kat_kernel(const uint32_t* ctr, const uint32_t* key, uint32_t n,
+                                  uint32_t* out);
 __global__ void bootstrap_kernel(Batch B, int p_first, uint64_t seed0, const double* ox,
                                  const double* oy, const int64_t* ot, uint64_t limit);
 __global__ void resample_seq_kernel(Batch B, int p_first, int count, uint64_t seed0,

@@ -67,6 +67,23 @@ class Device:
     def set_memory_budget(self, nbytes: int):
         self.check(self.lib.stk_set_memory_budget(self.h, int(nbytes)))
 
+    def set_rng(self, rng: str):
+        """Realisation generator: "mt19937_64" (default; the reference's stream,
+        bit-exact) or "philox" (opt-in Philox4x32-10, statistical parity)."""
+        code = {"mt19937_64": _lib.RNG_MT19937_64, "philox": _lib.RNG_PHILOX}[rng]
+        self.check(self.lib.stk_set_rng(self.h, code))
+
+    def philox4x32(self, ctr, key):
+        """Raw device Philox4x32-10 blocks (known-answer tests)."""
+        ctr = np.ascontiguousarray(ctr, np.uint32).reshape(-1, 4)
+        key = np.ascontiguousarray(key, np.uint32).reshape(-1, 2)
+        out = np.zeros_like(ctr)
+        u32p = C.POINTER(C.c_uint32)
+        self.check(self.lib.stk_philox4x32(self.h, ctr.ctypes.data_as(u32p),
+                                           key.ctypes.data_as(u32p), len(ctr),
+                                           out.ctypes.data_as(u32p)))
+        return out
+
     # -- multi-GPU: NCCL communicator inside the library ---------------------
     def comm_init(self, unique_id: bytes, nranks: int, rank: int):
         """stk_comm_init: join the communicator of ``unique_id`` (from
