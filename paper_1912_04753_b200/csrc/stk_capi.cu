@@ -663,6 +663,13 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   return B;
 }
 
+// Timing events of the pipeline.  cudaEventRecordExternal makes a record
+// inside stream capture a real event-record node of the graph (a plain record
+// there only expresses a dependency), so graph replays keep device timings.
+cudaError_t rec_event(cudaEvent_t e, cudaStream_t s) {
+  return cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+}
+
 struct Timers {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gen, grid, pair, fin;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -807,7 +814,7 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   const GridGeom& G = P.G;
   const int R = B.R;
   cudaEvent_t e0 = c->ev(), e1 = c->ev(), e2 = c->ev();
-  CK(cudaEventRecord(e0, c->stream));
+  CK(rec_event(e0, c->stream));
   CK(cudaMemsetAsync(B.cell_count, 0, sizeof(uint32_t) * (uint64_t)R * G.cells, c->stream));
   CK(cudaMemsetAsync(B.h_cnt, 0, sizeof(unsigned long long) * (uint64_t)R * P.bins * 4, c->stream));
   dim3 gp((unsigned)((B.n + 255) / 256), (unsigned)R);
@@ -854,7 +861,7 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   tasks_kernel<<<1, 1, 0, c->stream>>>(B, G, (uint32_t)(c->num_sms * per_sm));
   CK(cudaGetLastError());
   ++c->launches;
-  CK(cudaEventRecord(e1, c->stream));
+  CK(rec_event(e1, c->stream));
 
   PairArgs A;
   A.B = B;
@@ -873,7 +880,7 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   pair_kernel_launch(B.wide, mode, (unsigned)ctas, smem, c->stream, A);
   CK(cudaGetLastError());
   ++c->launches;
-  CK(cudaEventRecord(e2, c->stream));
+  CK(rec_event(e2, c->stream));
   tm.grid.push_back({e0, e1});
   tm.pair.push_back({e1, e2});
   if (finalize) {
@@ -882,7 +889,7 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
                                               c->area, c->duration, 0);
     CK(cudaGetLastError());
   ++c->launches;
-    CK(cudaEventRecord(e3, c->stream));
+    CK(rec_event(e3, c->stream));
     tm.fin.push_back({e2, e3});
   }
 }
@@ -892,6 +899,7 @@ double elapsed(const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
   for (auto& pr : v) {
     float ms = 0;
     if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) s += ms;
+    else (void)cudaGetLastError();  // never leave a sticky error for the next CK
   }
   return s;
 }
@@ -969,8 +977,8 @@ void finish_call(stk_ctx* c, Timers& tm, stk_telemetry* tel, uint64_t patterns,
   tel->finalize_ms += elapsed(tm.fin);
   if (tm.t0 && tm.t1) {
     float ms = 0;
-    cudaEventElapsedTime(&ms, tm.t0, tm.t1);
-    tel->total_ms += ms;
+    if (cudaEventElapsedTime(&ms, tm.t0, tm.t1) == cudaSuccess) tel->total_ms += ms;
+    else (void)cudaGetLastError();
   }
 }
 
@@ -1055,7 +1063,7 @@ PipeInfo enqueue_pipeline(stk_ctx* c, const double* dx, const double* dy, const 
   Timers& tm = info.tm;
   tm.t0 = c->ev();
   tm.t1 = c->ev();
-  CK(cudaEventRecord(tm.t0, c->stream));
+  CK(rec_event(tm.t0, c->stream));
   const uint64_t sims = r_end > r_begin ? r_end - r_begin : 0;
   const uint64_t patterns = (with_observed ? 1 : 0) + sims;
   info.patterns = patterns;
@@ -1075,7 +1083,7 @@ PipeInfo enqueue_pipeline(stk_ctx* c, const double* dx, const double* dy, const 
     Batch B = alloc_batch(c, PB);
     int p = 0;
     cudaEvent_t g0 = c->ev(), g1 = c->ev();
-    CK(cudaEventRecord(g0, c->stream));
+    CK(rec_event(g0, c->stream));
     const bool obs_here = with_observed && done == 0;
     if (obs_here) {
       generate(c, B, Source::Observed, 0, 1, 0, dx, dy, dt);
@@ -1083,12 +1091,12 @@ PipeInfo enqueue_pipeline(stk_ctx* c, const double* dx, const double* dy, const 
     }
     const int nsim = (int)(R - (obs_here ? 1 : 0));
     generate(c, B, src, p, nsim, base_seed + next_r, dx, dy, dt);
-    CK(cudaEventRecord(g1, c->stream));
+    CK(rec_event(g1, c->stream));
     tm.gen.push_back({g0, g1});
     run_batch(c, PB, B, tm, (obs_here && obs_nshards > 1) ? 1 : 0, obs_shard, obs_nshards, 0,
               ~0ULL, true);
     cudaEvent_t f0 = c->ev(), f1 = c->ev();
-    CK(cudaEventRecord(f0, c->stream));
+    CK(rec_event(f0, c->stream));
     if (obs_here) {
       // exact sums of pattern 0 (rows of h_cnt, h_half, h_lo, h_hi), its K and L
       for (int f = 0; f < 4; ++f)
@@ -1108,7 +1116,7 @@ PipeInfo enqueue_pipeline(stk_ctx* c, const double* dx, const double* dy, const 
         stage_d2h(c, nullptr, B.L + (uint64_t)p * bins, sizeof(double) * bins * nsim, F_LALL,
                   (uint64_t)(next_r - r_begin) * bins);
     }
-    CK(cudaEventRecord(f1, c->stream));
+    CK(rec_event(f1, c->stream));
     tm.fin.push_back({f0, f1});
     next_r += (uint32_t)nsim;
     done += R;
@@ -1130,7 +1138,7 @@ PipeInfo enqueue_pipeline(stk_ctx* c, const double* dx, const double* dy, const 
   if (sims_job > 0 && out.upper) stage_d2h(c, nullptr, c->env.p, sizeof(double) * bins, F_UP);
   if (sims_job > 0 && out.lower)
     stage_d2h(c, nullptr, c->env.p + bins, sizeof(double) * bins, F_LO);
-  CK(cudaEventRecord(tm.t1, c->stream));
+  CK(rec_event(tm.t1, c->stream));
   info.launches = c->launches;
   info.outs = c->outs;
   return info;
