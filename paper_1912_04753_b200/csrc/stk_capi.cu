@@ -667,7 +667,12 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
 // inside stream capture a real event-record node of the graph (a plain record
 // there only expresses a dependency), so graph replays keep device timings.
 cudaError_t rec_event(cudaEvent_t e, cudaStream_t s) {
-  return cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  const cudaError_t q = cudaStreamIsCapturing(s, &st);
+  if (q != cudaSuccess) return q;
+  return st == cudaStreamCaptureStatusActive
+             ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+             : cudaEventRecord(e, s);
 }
 
 struct Timers {

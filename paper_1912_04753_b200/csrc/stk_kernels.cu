@@ -498,14 +498,30 @@ __device__ __forceinline__ uint32_t cell_key(double x, double y, int64_t t, cons
   return (uint32_t)(((int64_t)kt * G.ny + ky) * G.nx + kx);
 }
 
+// Cell key and rank within the cell (counting sort, pass 1).  Lanes of a warp
+// that fall in the same cell share ONE atomic (__match_any_sync groups them;
+// the leader adds the group size, each lane takes base + its position in the
+// group): clustered patterns put hundreds of a warp's points in few cells,
+// where per-point atomics on one counter serialise.  The order inside a cell
+// stays arbitrary, as before (results never depend on it).
 __global__ void key_kernel(Batch B, GridGeom G, int p_first) {
   const int p = p_first + blockIdx.y;
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (i >= B.n) return;
+  const bool valid = i < B.n;
   const uint64_t o = (uint64_t)p * B.n + i;
-  const uint32_t k = cell_key(B.x[o], B.y[o], B.t[o], G);
-  B.key[o] = k;
-  B.rank[o] = atomicAdd(&B.cell_count[(uint64_t)p * G.cells + k], 1u);
+  uint32_t k = 0xffffffffu;
+  if (valid) {
+    k = cell_key(B.x[o], B.y[o], B.t[o], G);
+    B.key[o] = k;
+  }
+  const unsigned peers = __match_any_sync(FULL_MASK, k);
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(peers) - 1;
+  uint32_t base = 0;
+  if (valid && lane == leader)
+    base = atomicAdd(&B.cell_count[(uint64_t)p * G.cells + k], (uint32_t)__popc(peers));
+  base = __shfl_sync(FULL_MASK, base, leader);
+  if (valid) B.rank[o] = base + (uint32_t)__popc(peers & ((1u << lane) - 1u));
 }
 
 // Block-wide exclusive scan of two u32 streams (per-cell counts and their
@@ -1177,6 +1193,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           n_cand += (unsigned long long)min(32u, v_hi - v0) * nc;
           __syncwarp();
         }
+        // some lane's neighbour lies in the item's own cell: the ordering rule applies
+        const bool tile_own =
+            __any_sync(FULL_MASK, *reinterpret_cast<volatile uint32_t*>(&s_lim[tid].x) != 0xffffffffu);
         const bool tile_deep =
             __all_sync(FULL_MASK, !has || (nm.sqh > Qmax_hi && nm.vt >= Tmax));
         const int kend = min(kc + kArcChunk, (int)nc);
@@ -1227,13 +1246,15 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               // q's bucket from the high word of its bits (log-spaced
               // buckets, no sqrt, no conversion); each entry carries its
               // bin's threshold
+              // q <= Qmax and du <= Tmax here, so the buckets stay below the
+              // tables' tops by construction (host: base = top - (kQBuckets - 1),
+              // Tmax >> t_shift < kBucketTable): only q's lower clamp remains
               const uint32_t qh = (uint32_t)__double2hiint(q);
-              int bq = (int)(qh >> q_shift) - q_base;
-              bq = min(max(bq, 0), kQBuckets - 1);
+              const int bq = max((int)(qh >> q_shift) - q_base, 0);
               const ulonglong2 qe2 = lds_u64x2(a_q + (uint32_t)bq * (uint32_t)sizeof(QBucket));
               const QBucket qe{__longlong_as_double((long long)qe2.x), (uint32_t)qe2.y, 0u};
               uint32_t sb = qe.bin;
-              const int bt = (int)min(du >> t_shift, (TT)(kBucketTable - 1));
+              const int bt = (int)(du >> t_shift);
               const TBucket<TT> te = lds_tbucket<TT>(a_t + (uint32_t)bt * (uint32_t)sizeof(TBucket<TT>));
               uint32_t tb = te.bin;
               if constexpr (SINGLE) {
@@ -1257,9 +1278,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               if (h) reds_add_u32(a_ch + bin * 8u + 4u, h);
             }
             if (DEEP) continue;
-            const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
-            const unsigned mj = __ballot_sync(FULL_MASK, arc_j);
-            if (mi | mj) {
+            if (__any_sync(FULL_MASK, arc_i || arc_j)) {  // one vote on the common path
+              const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
+              const unsigned mj = __ballot_sync(FULL_MASK, arc_j);
               // no wrap: a chunk starts with < 32 entries (compaction) and adds
               // <= kArcChunk * 64, below kArcRing (static_assert in stk_types.h)
               const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
@@ -1275,9 +1296,16 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           }
         };
         // count-only loop when the item's centers and the tile's neighbours are
-        // all deep; else the weighted loop (own-cell ordering in both)
-        if (tile_deep && item_deep) chunk(std::true_type{}, std::true_type{});
-        else chunk(std::true_type{}, std::false_type{});
+        // all deep; else the weighted loop.  The own-cell ordering test only
+        // where some lane's neighbour shares the item's cell (tile_own).
+        const bool tile_deep_item = tile_deep && item_deep;
+        if (tile_own) {
+          if (tile_deep_item) chunk(std::true_type{}, std::true_type{});
+          else chunk(std::true_type{}, std::false_type{});
+        } else {
+          if (tile_deep_item) chunk(std::false_type{}, std::true_type{});
+          else chunk(std::false_type{}, std::false_type{});
+        }
         // advance: next chunk, next tile
         kc = kend;
         if (kc >= (int)nc) {
