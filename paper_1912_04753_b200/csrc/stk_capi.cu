@@ -960,6 +960,9 @@ void finish_call(stk_ctx* c, Timers& tm, stk_telemetry* tel, uint64_t patterns,
   // construction (<= 31 + kArcChunk*64 ring entries; <= 8 crossings on 4 sides)
   if (st[3] & 2) throw CudaFail("internal error: arc ring overflow in the pair kernel");
   if (st[3] & 1) throw CudaFail("internal error: crossing buffer overflow in the rectangle edge weight");
+  if (st[3] & 8)
+    throw Unsupported("a grid cell's stencil holds more points than the pair kernel's 32-bit "
+                      "per-task counters can take (about 3e7 in one cell)");
   if (st[3] & 4)
     throw Unsupported("Philox CSR: 4096 rejections for one point (the region covers too small a "
                       "share of its bounding box)");

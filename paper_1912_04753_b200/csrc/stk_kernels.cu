@@ -697,6 +697,7 @@ __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas) {
       (uint64_t)((G.rs + 1) + G.rt * (2 * G.rs + 1)) * (uint64_t)(2 * G.rs + 1);
   const uint64_t item_pairs = 2ull * kItemCenters * stencil_cells * (B.stats[5] + 1);
   const uint64_t cap = (1ull << 31) / item_pairs;
+  if (cap == 0) atomicOr(&B.stats[3], 8ULL);  // even one item could wrap a counter: the host raises
   if (ti > cap) ti = cap > 0 ? cap : 1;
   const uint32_t task_items = (uint32_t)ti;
   uint32_t acc = 0;
