@@ -734,10 +734,13 @@ void generate(stk_ctx* c, const Batch& B, Source src, int p_first, int count, ui
               const double* ox, const double* oy, const int64_t* ot) {
   if (count <= 0) return;
   const uint64_t n = B.n;
-  if (src == Source::Observed) {
-    CK(cudaMemcpyAsync(B.x + (uint64_t)p_first * n, ox, n * 8, cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemcpyAsync(B.y + (uint64_t)p_first * n, oy, n * 8, cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemcpyAsync(B.t + (uint64_t)p_first * n, ot, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (src == Source::Observed) {  // one kernel for the three arrays (one graph node)
+    const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)c->num_sms * 8);
+    copy_points_kernel<<<std::max(blocks, 1u), 256, 0, c->stream>>>(
+        B.x + (uint64_t)p_first * n, B.y + (uint64_t)p_first * n, B.t + (uint64_t)p_first * n,
+        ox, oy, ot, n);
+    CK(cudaGetLastError());
+    ++c->launches;
     return;
   }
   CK(cudaMemsetAsync(B.flags + p_first, 0, sizeof(int) * count, c->stream));
@@ -815,7 +818,8 @@ int pair_occupancy(stk_ctx* c, int wide, int mode, size_t smem) {
 // (shard of nshards by input index, and input-index range [c0, c1)) applies to
 // patterns [0, n_sel).
 void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint32_t shard,
-               uint32_t nshards, uint64_t c0, uint64_t c1, bool finalize) {
+               uint32_t nshards, uint64_t c0, uint64_t c1, bool finalize,
+               unsigned long long* obs_raw = nullptr, double* obs_kl = nullptr) {
   const GridGeom& G = P.G;
   const int R = B.R;
   cudaEvent_t e0 = c->ev(), e1 = c->ev(), e2 = c->ev();
@@ -891,7 +895,7 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   if (finalize) {
     cudaEvent_t e3 = c->ev();
     finalize_kernel<<<R, 256, 0, c->stream>>>(B, A.bins.cs, A.bins.ct, c->d_s.p, c->d_T.p,
-                                              c->area, c->duration, 0);
+                                              c->area, c->duration, 0, obs_raw, obs_kl);
     CK(cudaGetLastError());
   ++c->launches;
     CK(rec_event(e3, c->stream));
@@ -1044,7 +1048,7 @@ void exchange(stk_ctx* c, const Plan& P, uint64_t n, bool have_env, uint32_t sim
   F.L = c->obs.p + bins;
   finalize_kernel<<<1, 256, 0, c->stream>>>(F, (uint32_t)c->s_values.size(),
                                             (uint32_t)c->t_values.size(), c->d_s.p, c->d_T.p,
-                                            c->area, c->duration, 0);
+                                            c->area, c->duration, 0, nullptr, nullptr);
   CK(cudaGetLastError());
   ++c->launches;
 }
@@ -1101,19 +1105,11 @@ PipeInfo enqueue_pipeline(stk_ctx* c, const double* dx, const double* dy, const 
     generate(c, B, src, p, nsim, base_seed + next_r, dx, dy, dt);
     CK(rec_event(g1, c->stream));
     tm.gen.push_back({g0, g1});
+    // finalize also keeps the observed pattern's exact sums and its K, L
     run_batch(c, PB, B, tm, (obs_here && obs_nshards > 1) ? 1 : 0, obs_shard, obs_nshards, 0,
-              ~0ULL, true);
+              ~0ULL, true, obs_here ? c->obsraw.p : nullptr, obs_here ? c->obs.p : nullptr);
     cudaEvent_t f0 = c->ev(), f1 = c->ev();
     CK(rec_event(f0, c->stream));
-    if (obs_here) {
-      // exact sums of pattern 0 (rows of h_cnt, h_half, h_lo, h_hi), its K and L
-      for (int f = 0; f < 4; ++f)
-        CK(cudaMemcpyAsync(c->obsraw.p + (uint64_t)f * bins, B.h_cnt + (uint64_t)f * R * bins,
-                           8 * (uint64_t)bins, cudaMemcpyDeviceToDevice, c->stream));
-      CK(cudaMemcpyAsync(c->obs.p, B.K, sizeof(double) * bins, cudaMemcpyDeviceToDevice, c->stream));
-      CK(cudaMemcpyAsync(c->obs.p + bins, B.L, sizeof(double) * bins, cudaMemcpyDeviceToDevice,
-                         c->stream));
-    }
     if (nsim > 0) {
       envelope_kernel<<<(bins + 255) / 256, 256, 0, c->stream>>>(
           B, bins, p, nsim, env_init ? 1 : 0, c->env.p, c->env.p + bins);

@@ -884,6 +884,10 @@ __device__ __forceinline__ void drain_general(int count, int lane, const uint4* 
   add_arc_term(ws, e.y, sa_arc, sa_ch, n_arc);
 }
 
+#ifndef STK_DEEP_UNROLL
+#define STK_DEEP_UNROLL 1
+#endif
+constexpr int kDeepUnroll = STK_DEEP_UNROLL;
 #ifndef STK_PAIR_MINB
 #define STK_PAIR_MINB 2
 #endif
@@ -1227,8 +1231,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           const uint32_t a_q = sbase + (uint32_t)Lay::qtab;
           const uint32_t a_t = sbase + (uint32_t)Lay::ttab;
           const uint32_t a_ch = sbase + (uint32_t)Lay::ch;
-#pragma unroll 1  // unrolling costs registers and I-cache (measured: 2x -> +25%)
-          for (int k = kc; k < kend; ++k) {
+          auto pair_step = [&](int k) {
             const double2 c = lds_f64x2(a_cxy + k * (uint32_t)sizeof(double2));  // center k
             const PtMeta<TT> cmk = lds_meta<TT>(a_cm + k * (uint32_t)sizeof(PtMeta<TT>));
             const double dx = c.x - nxy.x, dy = c.y - nxy.y;
@@ -1267,7 +1270,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               }
               bin = sb * ct + tb;
               reds_add_u32(a_ch + bin * 8u, 2u);
-              if (DEEP) continue;
+              if (DEEP) return;
               half_i = du > cmk.vt;
               half_j = du > nm.vt;
               // hi32(q) < sqh implies q below the safe radius^2 (omega == 1);
@@ -1278,7 +1281,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
               if (h) reds_add_u32(a_ch + bin * 8u + 4u, h);
             }
-            if (DEEP) continue;
+            if (DEEP) return;
             if (__any_sync(FULL_MASK, arc_i || arc_j)) {  // one vote on the common path
               const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
               const unsigned mj = __ballot_sync(FULL_MASK, arc_j);
@@ -1294,6 +1297,15 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
                     make_uint4(jpc, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
               qt += __popc(mj);
             }
+          };
+          // the count-only loop is short and register-light: STK_DEEP_UNROLL
+          // iterations per trip overlap their FP64 chains (experiment knob)
+          if constexpr (DEEP) {
+#pragma unroll kDeepUnroll
+            for (int k = kc; k < kend; ++k) pair_step(k);
+          } else {
+#pragma unroll 1  // unrolling costs registers and I-cache (measured: 2x -> +25%)
+            for (int k = kc; k < kend; ++k) pair_step(k);
           }
         };
         // count-only loop when the item's centers and the tile's neighbours are
@@ -1391,7 +1403,9 @@ void pair_kernel_launch(int wide, int mode, unsigned ctas, size_t smem, cudaStre
 __global__ void __launch_bounds__(256) finalize_kernel(Batch B, uint32_t cs, uint32_t ct,
                                                         const double* s_values,
                                                         const int64_t* t_values, double area,
-                                                        int64_t duration, int p_first) {
+                                                        int64_t duration, int p_first,
+                                                        unsigned long long* obs_raw,
+                                                        double* obs_kl) {
   const int p = p_first + blockIdx.x;
   const uint32_t bins = cs * ct;
   const uint64_t hb = (uint64_t)p * bins;
@@ -1401,6 +1415,12 @@ __global__ void __launch_bounds__(256) finalize_kernel(Batch B, uint32_t cs, uin
     const unsigned long long cnt = B.h_cnt[hb + b];
     const unsigned long long c = (cnt & ~1ULL) + B.h_half[hb + b];
     const unsigned long long lo0 = B.h_lo[hb + b];
+    if (obs_raw && p == 0) {  // the observed pattern's exact sums, kept for the exchange / export
+      obs_raw[b] = cnt;
+      obs_raw[bins + b] = B.h_half[hb + b];
+      obs_raw[2 * bins + b] = lo0;
+      obs_raw[3 * bins + b] = B.h_hi[hb + b];
+    }
     const unsigned long long lo = lo0 + (c << kFixedFracBits);
     const unsigned long long hi =
         B.h_hi[hb + b] + (c >> (64 - kFixedFracBits)) + (lo < lo0 ? 1ULL : 0ULL);
@@ -1428,7 +1448,12 @@ __global__ void __launch_bounds__(256) finalize_kernel(Batch B, uint32_t cs, uin
     const double k = K[b] * scale;
     K[b] = k;
     const uint32_t si = b / ct, ti = b % ct;
-    L[b] = sqrt(k / (kTwoPi * (double)t_values[ti])) - s_values[si];
+    const double l = sqrt(k / (kTwoPi * (double)t_values[ti])) - s_values[si];
+    L[b] = l;
+    if (obs_kl && p == 0) {
+      obs_kl[b] = k;
+      obs_kl[bins + b] = l;
+    }
   }
 }
 
@@ -1500,6 +1525,17 @@ __global__ void unpack_exact_kernel(const unsigned long long* limbs, uint32_t bi
   half[b] = limbs[bins + b];
   lo[b] = l;
   hi[b] = limbs[4 * bins + b] + (h32 >> 32) + (l < a ? 1ULL : 0ULL);
+}
+
+// The observed pattern into its batch slot (x, y, t in one pass).
+__global__ void copy_points_kernel(double* x, double* y, int64_t* t, const double* ox,
+                                   const double* oy, const int64_t* ot, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    x[i] = ox[i];
+    y[i] = oy[i];
+    t[i] = ot[i];
+  }
 }
 
 // Fill n doubles with v (neutral envelopes of a rank without realisations).

@@ -53,7 +53,7 @@ void pair_kernel_launch(int wide, int mode, unsigned ctas, size_t smem, cudaStre
                         const PairArgs& A);
 __global__ void finalize_kernel(Batch B, uint32_t cs, uint32_t ct, const double* s_values,
                                 const int64_t* t_values, double area, int64_t duration,
-                                int p_first);
+                                int p_first, unsigned long long* obs_raw, double* obs_kl);
 __global__ void envelope_kernel(Batch B, uint32_t bins, int p_first, int count, int init,
                                 double* upper, double* lower);
 __global__ void diff_kernel(const double* est_l, const double* upper, uint32_t bins,
@@ -65,6 +65,8 @@ __global__ void unpack_exact_kernel(const unsigned long long* limbs, uint32_t bi
                                     unsigned long long* cnt, unsigned long long* half,
                                     unsigned long long* lo, unsigned long long* hi);
 __global__ void fill_kernel(double* p, uint32_t n, double v);
+__global__ void copy_points_kernel(double* x, double* y, int64_t* t, const double* ox,
+                                   const double* oy, const int64_t* ot, uint64_t n);
 __global__ void weights_kernel(const double* cx, const double* cy, const double* d,
                                uint64_t count, RegionView reg, const RegionView* reg_g, double* w, int* overflow,
                                unsigned long long* bad);
