@@ -219,6 +219,8 @@ struct stk_ctx {
   DevBuf<double> K, L, env, obs;
   DevBuf<int> flags, ovf;
   DevBuf<double> scratch;
+  DevBuf<uint32_t> perm;  // parallel permutation scratch (draws, lists, scans)
+  DevBuf<unsigned long long> perm_mx;
   DevBuf<double> sx, sy;  // host-upload staging of the observed pattern
   DevBuf<int64_t> st;
 
@@ -790,10 +792,39 @@ void generate(stk_ctx* c, const Batch& B, Source src, int p_first, int count, ui
     CK(cudaGetLastError());
   ++c->launches;
   } else {
+    // permutation: parallel Fisher-Yates (stk_kernels.cu perm_*), bit-exact; a
+    // realisation whose stream hits a below() rejection reruns sequentially
+    static const bool seq = std::getenv("STK_SEQ_PERMUTATION") != nullptr;
+    if (seq) {
+      resample_seq_kernel<<<(count + 31) / 32, 32, 0, c->stream>>>(B, p_first, count, seed0, ox,
+                                                                   oy, ot, 2);
+      CK(cudaGetLastError());
+      ++c->launches;
+      return;
+    }
+    const uint64_t cn = (uint64_t)count * n, cn1 = (uint64_t)count * (n + 1);
+    c->perm.ensure(4 * cn + 2 * cn1 + 2);
+    uint32_t* J = c->perm.p;
+    uint32_t* cnt = J + cn;
+    uint32_t* rank = cnt + cn;
+    uint32_t* list = rank + cn;
+    uint32_t* start = list + cn;
+    uint32_t* istart = start + cn1;
+    unsigned long long* mx = (unsigned long long*)(istart + cn1 + (cn1 & 1));
+    c->perm_mx.ensure(1);
+    perm_draw_kernel<<<count, 320, 0, c->stream>>>(B, p_first, seed0, J);
+    CK(cudaMemsetAsync(cnt, 0, 4 * cn, c->stream));
+    const dim3 g((unsigned)((n + 255) / 256), (unsigned)count);
+    perm_count_kernel<<<g, 256, 0, c->stream>>>(n, J, cnt, rank);
+    scan_kernel<<<count, 1024, 0, c->stream>>>(cnt, start, istart, (uint32_t)n, c->perm_mx.p);
+    perm_scatter_kernel<<<g, 256, 0, c->stream>>>(n, J, start, rank, list);
+    perm_sort_kernel<<<g, 256, 0, c->stream>>>(n, start, list);
+    perm_final_kernel<<<g, 256, 0, c->stream>>>(B, p_first, ox, oy, ot, J, start, list);
     resample_seq_kernel<<<(count + 31) / 32, 32, 0, c->stream>>>(B, p_first, count, seed0, ox,
-                                                                 oy, ot, 2);
+                                                                 oy, ot, 3);
     CK(cudaGetLastError());
-  ++c->launches;
+    c->launches += 7;
+    (void)mx;
   }
 }
 
@@ -1373,6 +1404,7 @@ void stk_destroy(stk_ctx* c) {
   c->scratch.release(); c->sx.release(); c->sy.release(); c->st.release();
   c->graph.reset();
   c->obsraw.release(); c->limbs.release(); c->d_rv.release();
+  c->perm.release(); c->perm_mx.release();
   if (c->comm) nccl().comm_destroy(c->comm);
   if (c->hstage) cudaFreeHost(c->hstage);
   cudaStreamDestroy(c->stream);

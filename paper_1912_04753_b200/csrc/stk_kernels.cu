@@ -236,6 +236,120 @@ __global__ void bootstrap_philox_kernel(Batch B, int p_first, uint64_t seed0, co
   B.t[o] = ot[j];
 }
 
+// ---------------------------------------------------------- permutation (parallel)
+// sim::generate_permutation (simulation.cpp:37-53) bit for bit, in parallel:
+// Fisher-Yates swaps times[i] <-> times[below(i + 1)] for i = n-1 .. 1, step
+// s = n-1-i drawing MT output s (below() rejects an output v only when
+// v >= 2^64 - (2^64 mod (i+1)): probability < 2^-32 per draw; any rejection
+// flags the realisation for the sequential kernel).  With J_i the swap
+// targets (J_i <= i), position p is final after step p, so
+//   final[p] = src(next step after p targeting J_p)   (J_p < p; T[J_p] if none)
+//            = src(p)                                  (J_p == p)
+//   final[0] = src(first step targeting 0)             (T[0] if none)
+//   src(i)   = src(first step i' > i targeting i), or T[i] if none
+// (src(i): the value at position i just before step i).  Steps targeting a
+// position are gathered by a counting sort on J (count, scan, scatter, sort
+// each short list); the chains src(i) -> ... increase and are short (expected
+// O(log n)).  Checked against the sequential definition (tests).
+__global__ void __launch_bounds__(320) perm_draw_kernel(Batch B, int p_first, uint64_t seed0,
+                                                         uint32_t* J) {
+  __shared__ uint64_t st[312];
+  __shared__ int s_flag;
+  const int p = p_first + blockIdx.x;
+  if (threadIdx.x == 0) s_flag = 0;
+  mt_seed_smem(st, seed0 + (uint64_t)blockIdx.x);
+  const uint64_t n = B.n;
+  uint32_t* Jp = J + (uint64_t)blockIdx.x * n;
+  for (uint64_t base = 0; base + 1 < n; base += 312) {
+    mt_twist_smem(st);
+    const uint64_t s = base + threadIdx.x;
+    if (threadIdx.x < 312 && s + 1 < n) {
+      const uint64_t v = mt_temper(st[threadIdx.x]);
+      const uint64_t i = n - 1 - s, m = i + 1;
+      if (v >= 0xFFFFFFFF00000000ULL && v >= ~0ULL - (~0ULL % m)) s_flag = 1;  // below() rejects
+      Jp[i] = (uint32_t)(v % m);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) B.flags[p] = s_flag;
+}
+
+// steps targeting each position: counts (positions 0 .. n-1) and ranks
+__global__ void perm_count_kernel(uint64_t n, const uint32_t* J, uint32_t* cnt, uint32_t* rank) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t o = (uint64_t)blockIdx.y * n;
+  if (i == 0 || i >= n) return;
+  rank[o + i] = atomicAdd(&cnt[o + J[o + i]], 1u);
+}
+
+__global__ void perm_scatter_kernel(uint64_t n, const uint32_t* J, const uint32_t* start,
+                                    const uint32_t* rank, uint32_t* list) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t o = (uint64_t)blockIdx.y * n;
+  if (i == 0 || i >= n) return;
+  list[o + start[(uint64_t)blockIdx.y * (n + 1) + J[o + i]] + rank[o + i]] = (uint32_t)i;
+}
+
+// ascending order inside each position's (short) list of steps
+__global__ void perm_sort_kernel(uint64_t n, const uint32_t* start, uint32_t* list) {
+  const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const uint32_t* st = start + (uint64_t)blockIdx.y * (n + 1);
+  uint32_t* l = list + (uint64_t)blockIdx.y * n;
+  const uint32_t a = st[q], b = st[q + 1];
+  for (uint32_t k = a + 1; k < b; ++k) {
+    const uint32_t v = l[k];
+    uint32_t m = k;
+    while (m > a && l[m - 1] > v) {
+      l[m] = l[m - 1];
+      --m;
+    }
+    l[m] = v;
+  }
+}
+
+// First step > after in position q's sorted list, or ~0u.
+__device__ __forceinline__ uint32_t perm_next(const uint32_t* start, const uint32_t* list,
+                                              uint32_t q, uint32_t after) {
+  for (uint32_t k = start[q], e = start[q + 1]; k < e; ++k)
+    if (list[k] > after) return list[k];
+  return ~0u;
+}
+
+__global__ void perm_final_kernel(Batch B, int p_first, const double* ox, const double* oy,
+                                  const int64_t* ot, const uint32_t* J, const uint32_t* start,
+                                  const uint32_t* list) {
+  const uint64_t n = B.n;
+  const uint64_t pos = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (pos >= n) return;
+  const int p = p_first + blockIdx.y;
+  const uint32_t* Jp = J + (uint64_t)blockIdx.y * n;
+  const uint32_t* st = start + (uint64_t)blockIdx.y * (n + 1);
+  const uint32_t* l = list + (uint64_t)blockIdx.y * n;
+  auto src = [&](uint32_t i) {  // value at position i just before step i
+    uint32_t k = i;
+    for (uint32_t nx = perm_next(st, l, k, k); nx != ~0u; nx = perm_next(st, l, k, k)) k = nx;
+    return ot[k];
+  };
+  int64_t v;
+  if (pos == 0) {
+    const uint32_t f = perm_next(st, l, 0u, 0u);
+    v = f == ~0u ? ot[0] : src(f);
+  } else {
+    const uint32_t q = Jp[pos];
+    if (q == (uint32_t)pos) {
+      v = src((uint32_t)pos);
+    } else {
+      const uint32_t nx = perm_next(st, l, q, (uint32_t)pos);
+      v = nx == ~0u ? ot[q] : src(nx);
+    }
+  }
+  const uint64_t o = (uint64_t)p * n + pos;
+  B.x[o] = ox[pos];
+  B.y[o] = oy[pos];
+  B.t[o] = v;
+}
+
 // Raw Philox4x32-10 blocks for the known-answer test: out[4i..4i+3] =
 // philox(ctr[i], key[i]).
 __global__ void philox_kat_kernel(const uint32_t* ctr, const uint32_t* key, uint32_t n,
@@ -428,7 +542,7 @@ __global__ void resample_seq_kernel(Batch B, int p_first, int count, uint64_t se
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= count) return;
   const int p = p_first + j;
-  if (mode == 1 && !B.flags[p]) return;
+  if ((mode == 1 || mode == 3) && !B.flags[p]) return;  // fallback of a flagged parallel run
   uint64_t st[312];
   uint64_t v = seed0 + (uint64_t)j;
   st[0] = v;
@@ -468,7 +582,7 @@ __global__ void resample_seq_kernel(Batch B, int p_first, int count, uint64_t se
       T[i] = ot[jx];
     }
     B.flags[p] = 0;
-  } else {
+  } else {  // mode 2 (always) / 3 (flagged): the sequential Fisher-Yates
     for (uint64_t i = 0; i < n; ++i) {
       X[i] = ox[i];
       Y[i] = oy[i];

@@ -32,6 +32,14 @@ __global__ void csr_philox_kernel(Batch B, int p_first, uint64_t seed0, RegionVi
                                   uint64_t ntl);
 __global__ void bootstrap_philox_kernel(Batch B, int p_first, uint64_t seed0, const double* ox,
                                         const double* oy, const int64_t* ot);
+__global__ void perm_draw_kernel(Batch B, int p_first, uint64_t seed0, uint32_t* J);
+__global__ void perm_count_kernel(uint64_t n, const uint32_t* J, uint32_t* cnt, uint32_t* rank);
+__global__ void perm_scatter_kernel(uint64_t n, const uint32_t* J, const uint32_t* start,
+                                    const uint32_t* rank, uint32_t* list);
+__global__ void perm_sort_kernel(uint64_t n, const uint32_t* start, uint32_t* list);
+__global__ void perm_final_kernel(Batch B, int p_first, const double* ox, const double* oy,
+                                  const int64_t* ot, const uint32_t* J, const uint32_t* start,
+                                  const uint32_t* list);
 __global__ void philox_kat_kernel(const uint32_t* ctr, const uint32_t* key, uint32_t n,
                                   uint32_t* out);
 __global__ void bootstrap_kernel(Batch B, int p_first, uint64_t seed0, const double* ox,
