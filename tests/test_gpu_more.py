@@ -557,3 +557,48 @@ def test_repeated_job_graph_replay_bit_identical(api):
     other, to = call(6)
     assert not np.array_equal(other[2], first[2])  # different realisations: other envelopes
     assert to.in_threshold_pairs != t1.in_threshold_pairs
+
+
+def test_parallel_permutation_bit_exact_large(api, port):
+    """The parallel Fisher-Yates (perm_* kernels: swap targets from the MT
+    stream in parallel, counting sort of the targets, short increasing
+    chains) reproduces generate_permutation's sequential swaps
+    (simulation.cpp:37-53) bit for bit at n = 200,000, and equals the
+    sequential device kernel (STK_SEQ_PERMUTATION) run in a fresh process."""
+    import ctypes as C
+
+    from paper_1912_04753_b200 import _lib
+
+    dev, geom = api["dev"], api["geom"]
+    dev.configure(geom.StudyRegion([[0, 0], [1000, 0], [1000, 1000], [0, 1000]], 0, 10**9))
+    rng = np.random.default_rng(12)
+    n = 200_000
+    x = rng.uniform(0, 1000, n); y = rng.uniform(0, 1000, n); t = rng.integers(0, 10**9, n)
+    for seed in (3, 2**63 + 5):
+        ox, oy, ot = np.zeros(n), np.zeros(n), np.zeros(n, np.int64)
+        dev.check(dev.lib.stk_generate(dev.h, 2, n, _lib.ptr(x), _lib.ptr(y),
+                                       _lib.ptr(t, C.c_int64), seed, _lib.ptr(ox), _lib.ptr(oy),
+                                       _lib.ptr(ot, C.c_int64)))
+        rx, ry, rt_ = port.generate_permutation(x, y, t, seed)
+        assert np.array_equal(ox, rx) and np.array_equal(oy, ry) and np.array_equal(ot, rt_)
+    code = (
+        "import sys, numpy as np, ctypes as C; sys.path.insert(0, %r)\n"
+        "from paper_1912_04753_b200 import _lib\n"
+        "from paper_1912_04753_b200.stripley import device, geom\n"
+        "d = device.get(0)\n"
+        "d.configure(geom.StudyRegion([[0, 0], [1000, 0], [1000, 1000], [0, 1000]], 0, 10**9))\n"
+        "r = np.random.default_rng(12); n = 200000\n"
+        "x = r.uniform(0, 1000, n); y = r.uniform(0, 1000, n); t = r.integers(0, 10**9, n)\n"
+        "o = [np.zeros(n), np.zeros(n), np.zeros(n, np.int64)]\n"
+        "d.check(d.lib.stk_generate(d.h, 2, n, _lib.ptr(x), _lib.ptr(y), _lib.ptr(t, C.c_int64),"
+        " 3, _lib.ptr(o[0]), _lib.ptr(o[1]), _lib.ptr(o[2], C.c_int64)))\n"
+        "np.save(sys.argv[1], o[2])\n" % ROOT)
+    with tempfile.TemporaryDirectory() as dd:
+        out = os.path.join(dd, "t.npy")
+        env = dict(os.environ, STK_SEQ_PERMUTATION="1")
+        r = subprocess.run(["python", "-c", code, out], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr
+        seq = np.load(out)
+    rx, ry, rt_ = port.generate_permutation(x, y, t, 3)
+    assert np.array_equal(seq, rt_)
