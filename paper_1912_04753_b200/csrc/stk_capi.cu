@@ -803,14 +803,13 @@ void generate(stk_ctx* c, const Batch& B, Source src, int p_first, int count, ui
       return;
     }
     const uint64_t cn = (uint64_t)count * n, cn1 = (uint64_t)count * (n + 1);
-    c->perm.ensure(4 * cn + 2 * cn1 + 2);
+    c->perm.ensure(4 * cn + 2 * cn1);
     uint32_t* J = c->perm.p;
     uint32_t* cnt = J + cn;
     uint32_t* rank = cnt + cn;
     uint32_t* list = rank + cn;
     uint32_t* start = list + cn;
     uint32_t* istart = start + cn1;
-    unsigned long long* mx = (unsigned long long*)(istart + cn1 + (cn1 & 1));
     c->perm_mx.ensure(1);
     perm_draw_kernel<<<count, 320, 0, c->stream>>>(B, p_first, seed0, J);
     CK(cudaMemsetAsync(cnt, 0, 4 * cn, c->stream));
@@ -824,7 +823,6 @@ void generate(stk_ctx* c, const Batch& B, Source src, int p_first, int count, ui
                                                                  oy, ot, 3);
     CK(cudaGetLastError());
     c->launches += 7;
-    (void)mx;
   }
 }
 
