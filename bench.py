@@ -306,8 +306,13 @@ def run_ours(args):
     stream = torch.cuda.ExternalStream(dev.stream_handle())
     # N > 1 over NCCL: the executor joins a communicator inside the library (the
     # unique id travels once over the torch.distributed group, outside timing)
-    executor = rt.DeviceExecutor(device=dev, rank=rank, world=world, group=group,
-                                 comm=(world > 1 and backend == "nccl"))
+    try:
+        executor = rt.DeviceExecutor(device=dev, rank=rank, world=world, group=group,
+                                     comm=(world > 1 and backend == "nccl"))
+    except Exception as e:  # NCCL inside the library unavailable: host-group exchange
+        print(f"bench: library communicator unavailable ({e}); exchanging over the "
+              "torch.distributed group", file=sys.stderr)
+        executor = rt.DeviceExecutor(device=dev, rank=rank, world=world, group=group, comm=False)
     r0, r1 = executor.sim_range(sims)
     spec = rt.JobSpec(grid=grid, sims=sims, seed=cfg.seed)
 

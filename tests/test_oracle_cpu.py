@@ -195,3 +195,61 @@ def test_port_vs_live_reference_degenerate_weights():
     k_ref, _, _ = ref.estimate_surface(xs, ys, ts, star, 0, 400, s2, tv2, use_index=True)
     h = port.estimate(xs, ys, ts, star, 0, 400, s2, tv2)
     assert rel_err(h["k"], k_ref) <= 1e-15
+
+
+def test_reference_job_split_per_pattern_reproduces_run_job():
+    """oracle.ref.Job (ref_job_open / ref_job_pattern: rt::run_job's loop body
+    split per pattern, the path the large fixtures and the bench's reference
+    arm use) reproduces the reference's own golden sample bit for bit, and the
+    R-tree per-bin counts equal the O(n^2) ones."""
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built here")
+    from oracle import ref
+
+    g = golden("sample_result.npz")
+    x, y, t, ring = g["x"], g["y"], g["t"], g["ring"]
+    job = ref.Job(x, y, t, ring, 0, 365, g["s"], g["tv"], seed=int(g["seed"]), partitions=1,
+                  workers=1, use_cache=True)
+    obs = job.pattern(-1)
+    assert np.array_equal(obs["k"], g["k"]) and np.array_equal(obs["l"], g["l"])
+    ls, total = [], obs["in_threshold"]
+    for r in range(int(g["sims"])):
+        p = job.pattern(r)
+        ls.append(p["l"])
+        total += p["in_threshold"]
+    job.close()
+    assert np.array_equal(np.max(ls, 0), g["upper"]) and np.array_equal(np.min(ls, 0), g["lower"])
+    assert total == int(g["in_threshold_total"])
+    c_idx = ref.pair_counts_indexed(x, y, t, g["s"], g["tv"], threads=4)
+    assert np.array_equal(c_idx, ref.pair_counts(x, y, t, g["s"], g["tv"]))
+    assert np.array_equal(c_idx, g["counts_observed"])
+
+
+def test_large_fixtures_consistent():
+    """The committed full-size fixtures agree with themselves: per-bin counts
+    sum to the reference's in-threshold totals; C3 has every ordered pair in
+    threshold; subset envelopes are the max / min of their realisations."""
+    import os
+
+    from conftest import GOLDEN
+
+    if os.path.exists(os.path.join(GOLDEN, "c2_job.npz")):
+        g = golden("c2_job.npz")
+        assert int(g["counts_observed"].sum()) == int(g["in_threshold_observed"])
+        assert int(g["in_threshold_total"]) > int(g["in_threshold_observed"])
+    if os.path.exists(os.path.join(GOLDEN, "c3_full.npz")):
+        g = golden("c3_full.npz")
+        n = int(g["n"])
+        assert int(g["counts"].sum()) == int(g["in_threshold"]) == n * (n - 1)
+    for name in ("c4_parity.npz", "c5_parity.npz"):
+        if not os.path.exists(os.path.join(GOLDEN, name)):
+            continue
+        g = golden(name)
+        rs = [int(r) for r in g["realisations"]]
+        for key in ["obs"] + [f"r{r}" for r in rs]:
+            if f"{key}_counts" in g.files:
+                assert int(g[f"{key}_counts"].sum()) == int(g[f"{key}_in_threshold"])
+        if "upper_subset" in g.files:
+            ls = np.stack([g[f"r{r}_l"] for r in rs])
+            assert np.array_equal(ls.max(0), g["upper_subset"])
+            assert np.array_equal(ls.min(0), g["lower_subset"])
