@@ -87,6 +87,28 @@ static int selftest() {
   for (const auto& s : sims)
     for (std::size_t i = 0; i < 2; ++i)
       for (std::size_t j = 0; j < 2; ++j) EXPECT(lo.values[i][j] <= s.values[i][j] && s.values[i][j] <= up.values[i][j]);
+  // executors (runtime.hpp:106-136): LocalExecutor, the NCCL-communicator
+  // DeviceExecutor at world 1 (stk_run_job_dist: exact device exchange) and a
+  // world > 1 executor without communicator or hooks (rejected)
+  {
+    rt::JobSpec spec;
+    spec.grid = est::DistanceGrid{{250.0, 500.0, 1000.0}, {10, 20, 40}};
+    spec.sims = 4;
+    spec.seed = 21;
+    rt::LocalExecutor local(4, sq, spec.grid, spec.options);
+    const auto r1 = rt::run_job(a, sq, spec, local);
+    rt::DeviceExecutor coll(0, 0, 1, rt::DeviceExecutor::nccl_unique_id());
+    const auto r2 = rt::run_job(a, sq, spec, coll);
+    EXPECT(r1.k_hat.values == r2.k_hat.values && r1.l_hat.values == r2.l_hat.values);
+    EXPECT(r1.upper_l->values == r2.upper_l->values && r1.lower_l->values == r2.lower_l->values);
+    EXPECT(r1.diff_upper->values == r2.diff_upper->values);
+    EXPECT(r1.telemetry.in_threshold_pairs == r2.telemetry.in_threshold_pairs);
+    EXPECT(throws([] { rt::DeviceExecutor bad(0, 0, 2); }).find("needs an NCCL unique id") !=
+           std::string::npos);
+    EXPECT(throws([] { rt::DeviceExecutor bad(0, 2, 2); }) == "rank must be < world");
+    EXPECT(rt::speedup_factor(10.0, 2.5) == 4.0);
+    EXPECT(throws([] { rt::speedup_factor(0.0, 1.0); }) == "times must be > 0");
+  }
   std::printf("selftest failures=%d\n", failures);
   return failures ? 1 : 0;
 }
