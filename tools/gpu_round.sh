@@ -3,7 +3,8 @@
 # the ncu launch list and full captures of the pair kernel.
 #   gpurun --timeout 2400 -- 'bash tools/gpu_round.sh [tag] [stages]'
 # stages: any of t (tests) s (smoke) b (bench default C4 + reference arm) c (other
-# configs) p (polygons) l (launch list) f (ncu full: C4 and C2)
+# configs) k (K1 on C5's observed pattern, permutation timing) p (polygons) l (launch
+# list) f (ncu full: C4 and C2)
 tag=${1:-r2}
 stages=${2:-tbclf}
 out=gpurun_out
@@ -21,13 +22,17 @@ fi
 if [[ $stages == *b* ]]; then
   timeout 900 python bench.py --steps 20 --warmup 5 > $out/bench_$tag.json 2> $out/bench_$tag.err
   echo "bench rc=$?" >> $out/bench_$tag.err
-  timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $out/bench_ref_$tag.json 2> $out/bench_ref_$tag.err
+  timeout 1200 python bench.py --impl reference --steps ${REF_STEPS:-3} --warmup ${REF_WARMUP:-1} > $out/bench_ref_$tag.json 2> $out/bench_ref_$tag.err
 fi
 if [[ $stages == *c* ]]; then
   for c in C1 C2 C3; do
     timeout 400 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > $out/bench_${c}_$tag.json 2> $out/bench_${c}_$tag.err
   done
   timeout 900 python bench.py --config C5 --steps 2 --warmup 3 --no-cpu-baseline > $out/bench_C5_$tag.json 2> $out/bench_C5_$tag.err
+fi
+if [[ $stages == *k* ]]; then  # K1 grid build on C5's clustered observed pattern alone
+  timeout 600 python bench.py --config C5 --sims 0 --steps 3 --warmup 2 --no-cpu-baseline > $out/bench_C5obs_$tag.json 2> $out/bench_C5obs_$tag.err
+  timeout 600 python tools/perm_time.py 1000000 10 > $out/perm_par_$tag.json 2>&1
 fi
 if [[ $stages == *p* ]]; then
   for v in 128 512 2048; do
