@@ -488,6 +488,7 @@ RegionView region_view(stk_ctx* c) {
   // on_segment tolerance (d - h > 4 box_m)
   r.sw_dmin = 1e-8 * S;
   r.sw_margin = 4.0 * r.box_m;
+  r.sw_q_min = r.sw_dmin * r.sw_dmin * (1.0 + 1e-12);
   r.slab_start = c->slab_ok ? c->d_slab_start.p : nullptr;
   r.slab_edge = c->slab_ok ? c->d_slab_edge.p : nullptr;
   r.nslab = c->nslab;

@@ -615,54 +615,81 @@ __device__ __forceinline__ double spatial_weight_buf(double cx, double cy, doubl
 }
 
 // spatial_isotropic_weight in closed form for the dominant rectangle case:
-// the center strictly inside, exactly one edge within reach d*(1+1e-6) and
-// that edge's quadratic accepted (the same expression as the reference, so
-// the accept / reject decision is identical).  The reference then finds two
-// crossings strictly inside the edge (the perpendicular edges are out of
-// reach, so the chord ends lie >= 1e-6 d inside the segment), two distinct
-// angles (separation 2*theta >= 4e-5), an outside arc of 2*theta whose
-// midpoint probe lies beyond the edge by ~(d - h) > 4 box_m (PIP false) and
-// an inside arc whose probe is >= 1e-6 d inside (PIP true):
+// the center strictly inside, exactly one side crossed, the other three out of
+// reach d*(1+1e-6), and that side's quadratic accepted.  The reference then
+// finds two crossings strictly inside the side (the perpendicular sides are
+// out of reach, so the chord ends lie >= 1e-6 d inside the segment), two
+// distinct angles, an outside arc of 2*theta whose midpoint probe lies beyond
+// the side by ~(d - h) > 4 box_m (PIP false) and an inside arc whose probe is
+// >= 1e-6 d inside (PIP true):
 //   omega_ref = (2*pi - 2*theta_ref) / (2*pi),  cos(theta) = h / d.
 // theta_ref carries the reference's own rounding (the quadratic's
 // cancellation: <= 2^-53 * scale / (len * sqrt(disc) * d) rad), which the
-// gate qa*disc*d^2 >= 1e-10*scale^2 bounds by ~1e-11; ours, from
-// atan2(sqrt((d-h)(d+h)), h), is within ~1e-11 too.
-// Returns -1 when the gate fails (the caller uses the general routine).
-__device__ __forceinline__ double rect_single_edge_weight(double cx, double cy, double d,
-                                                          const RegionView& R) {
-  if (d <= 0.0) return 1.0;
-  if (!(cx > R.xmin && cx < R.xmax && cy > R.ymin && cy < R.ymax) || d < R.sw_dmin) return -1.0;
-  const double reach = d * (1.0 + 1e-6);
-  // distances to the four side lines: with the center inside, cx - xmin is
-  // exactly the reference's fabs(A.x - cx) (RN is symmetric), etc.
+// gate qa*disc*d^2 >= 1e-10*scale^2 bounds by ~1e-11.
+// atan2(y, x) for y > 0, x > 0 finite (fast_atan2 without the sign cases).
+__device__ __forceinline__ double atan2_pos(double y, double x) {
+  constexpr double kTanPi8 = 0.41421356237309504880;
+  constexpr double kPi4 = 0.78539816339744830962;
+  constexpr double kPi2 = 1.57079632679489661923;
+  const bool steep = y > x;
+  const double mx = steep ? y : x, mn = steep ? x : y;
+  const bool small = mn <= kTanPi8 * mx;
+  const double t = (small ? mn : mn - mx) / (small ? mx : mn + mx);
+  const double s = t * t;
+  double r = -0.0192025292684122813793;
+  r = fma(r, s, 0.0392536963206185629612);
+  r = fma(r, s, -0.0508625488582314312944);
+  r = fma(r, s, 0.0585831181050115303872);
+  r = fma(r, s, -0.0666453136980500884962);
+  r = fma(r, s, 0.0769218469937177728423);
+  r = fma(r, s, -0.090909046476956795219);
+  r = fma(r, s, 0.111111110171003266375);
+  r = fma(r, s, -0.142857142846913806166);
+  r = fma(r, s, 0.199999999999956505772);
+  r = fma(r, s, -0.333333333333333302719);
+  const double a = (small ? 0.0 : kPi4) + fma(t * s, r, t);
+  return steep ? kPi2 - a : a;
+}
+
+// The single-edge closed form, evaluated on q = d^2 itself (the pair kernel's
+// arc drains), without forming d = RN(sqrt(q)): every gate
+// is a sufficient condition in q for the reference's own decision with d =
+// RN(sqrt(q)) (d^2 = q (1 +- 2.3e-16)), slack included for the roundings of
+// the reference's quadratic:
+//   other sides out of reach  h2 >= d (1 + 1e-6)        <=  h2^2 > q (1 + 2.1e-6)
+//   d >= sw_dmin                                         <=  q >= sw_q_min
+//   d - h > 4 box_m + 1e-12 d                            <=  q (1 - 2.5e-12) > (h + 4 box_m)^2
+//   disc > 1e-9 scale (accept), qa disc d^2 >= 1e-10 scale^2, with
+//   disc = 4 D^2 (d^2 - h^2) +- 3e-15 (fa^2 + d^2) 4 D^2 and
+//   scale = 4 D^2 (fa^2 + |h^2 + fa^2 - d^2|) (1 +- 1e-15):
+//     E > 1.00001e-9 S + 4e-15 (fa^2 + q),  (E - 4e-15 (fa^2 + q)) q >= 4.0001e-10 (S + 3e-16 q)^2
+//   with E = q - h^2 (one rounding) and S = fa^2 + |h^2 + fa^2 - q|.
+// Then omega = 1 - atan2(sqrt(E), h) / pi, within ~1e-13 of the d-based form
+// (theta moves by h * 2.3e-16 / (2 w) with w = sqrt(E) bounded below by the
+// gates).  Returns -1 when a gate fails (the caller defers to the exact path).
+__device__ __forceinline__ double rect_single_edge_omega_q(double cx, double cy, double q,
+                                                           const RegionView& R) {
   const double hl = cx - R.xmin, hr = R.xmax - cx, hb = cy - R.ymin, ht = R.ymax - cy;
-  const bool il = hl <= reach, ir = hr <= reach, ib = hb <= reach, it = ht <= reach;
-  const int m = (int)il + (int)ir + (int)ib + (int)it;
-  if (m == 0) return 1.0;  // the reference accepts no edge (reach argument)
-  if (m > 1) return -1.0;
-  // the one side's segment in the reference's frame: f = A - c splits into
-  // fp (across the side, = +-h) and fa (along it); B - A = (0, D) or (D, 0).
-  // The reference's qa = dx*dx + dy*dy = D*D, qb = 2(fx*dx + fy*dy) = 2(fa*D)
-  // (adding the exact zero product), qc = fx*fx + fy*fy - r^2 = h*h + fa*fa - r^2
-  // (addition commutes): bit-identical.
-  const double h = il ? hl : ir ? hr : ib ? hb : ht;
-  const int sd = il ? 0 : ir ? 1 : ib ? 2 : 3;
-  const double fa = R.sd_start[sd] - (sd < 2 ? cy : cx);
-  const double D = R.sd_len[sd];
-  const double r2 = d * d;
-  const double qa = D * D;
-  const double qb = 2.0 * (fa * D);
-  const double qc = h * h + fa * fa - r2;
-  const double disc = qb * qb - 4.0 * qa * qc;
-  const double scale = qb * qb + fabs(4.0 * qa * qc);
-  if (!(qa != 0.0 && disc > 1e-9 * scale)) return 1.0;  // no crossing: omega == 1
-  if (qa * disc * r2 < 1e-10 * scale * scale) return -1.0;
-  const double dm = d - h;
-  if (dm <= R.sw_margin + 1e-12 * d) return -1.0;
-  const double w = sqrt(dm * (d + h));
-  const double theta = fast_atan2(w, h);
-  return 1.0 - theta * 0.31830988618379067154;  // 1 - theta / pi
+  const bool xr = hr < hl, yt = ht < hb;
+  const double a = xr ? hr : hl, A = xr ? hl : hr;
+  const double b = yt ? ht : hb, Bm = yt ? hb : ht;
+  const bool hz = b < a;  // the nearest side is horizontal (y = ymin / ymax)
+  const double h = hz ? b : a;
+  const double h2 = fmin(hz ? a : b, fmin(A, Bm));
+  const int sd = hz ? (yt ? 3 : 2) : (xr ? 1 : 0);
+  const double fa = R.sd_start[sd] - (hz ? cx : cy);
+  const double E = fma(-h, h, q);
+  const double fa2 = fa * fa;
+  const double S = fa2 + fabs(fma(h, h, fa2) - q);
+  const double slack = 4e-15 * (fa2 + q);
+  const double Sx = fma(3e-16, q, S);
+  const double hm = h + R.sw_margin;
+  const bool ok = h > 0.0 && q >= R.sw_q_min && h2 * h2 > q * (1.0 + 2.1e-6) &&
+                  q * (1.0 - 2.5e-12) > hm * hm && E > fma(1.00001e-9, S, slack) &&
+                  (E - slack) * q >= 4.0001e-10 * (Sx * Sx);
+  if (!ok) return -1.0;
+  const double theta = atan2_pos(sqrt(E), h);
+  return fma(theta, -0.31830988618379067154, 1.0);  // 1 - theta / pi
 }
 
 // rect_probe_certified for the arc running counter-clockwise from crossing
@@ -692,7 +719,7 @@ __device__ __forceinline__ int rect_probe_chord(double cx, double cy, double d, 
 // (cos theta = h / d; phi = 0, pi/2, pi, 3pi/2 for the right, top, left, bottom
 // side), each of which lies on the segment iff the corner on its side of the
 // foot is outside the circle.  Gates (else -1, the general routine): the
-// single-side gates of rect_single_edge_weight for every accepted side, no side
+// single-side gates of rect_single_edge_omega_q for every accepted side, no side
 // rejected while its line is nearer than d (a tangency the reference drops),
 // and every corner between two sides within reach away from the circle by
 // |K - c|^2 - d^2 > 1e-5 d^2 — then crossings are 2.5e-6 d or more from the

@@ -959,17 +959,31 @@ __device__ __forceinline__ void drain_main(int count, int lane, const uint4* rin
   double ws = -1.0;
   if (valid) {
     e = ring[(head + lane) & (kArcRing - 1)];
-    if (reg.rect) {
+    if (RECT) {
       const double2 c = pxy[e.x];
-      const double d = sqrt(__hiloint2double((int)e.w, (int)e.z));
-      ws = rect_single_edge_weight(c.x, c.y, d, reg);
+      ws = rect_single_edge_omega_q(c.x, c.y, __hiloint2double((int)e.w, (int)e.z), reg);
     }
   }
   const bool defer = valid && ws < 0.0;
   const unsigned m = __ballot_sync(FULL_MASK, defer);
   if (defer) cring[(*ctail + __popc(m & lanemask_lt)) & (kCplxRing - 1)] = e;
   *ctail += __popc(m);
-  if (valid && !defer) add_arc_term(ws, e.y, sa_arc, sa_ch, n_arc);
+  if (valid && !defer) {
+    // omega in [1/2, 1): term 1/(omega v) in (1, 4], so (term - 1) 2^53 is a
+    // non-negative integer below 2^55; added to the bin's 128-bit sum with two
+    // native 32-bit shared atomics and their carries (a 64-bit shared atomic
+    // add is a compare-and-swap loop on sm_100)
+    ++*n_arc;
+    const double term = (1.0 / ws) * ((e.y >> 31) ? 2.0 : 1.0);
+    const uint64_t v = __double2ull_rn(term * 0x1p53) - (1ULL << kFixedFracBits);
+    const uint32_t a = sa_arc + (e.y & 0x7fffffffu) * (uint32_t)sizeof(ArcSum);
+    const uint32_t v0 = (uint32_t)v;
+    uint32_t v1 = (uint32_t)(v >> 32), o0, o1;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o0) : "r"(a), "r"(v0) : "memory");
+    v1 += (o0 + v0 < o0) ? 1u : 0u;  // v1 < 2^23: no overflow
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o1) : "r"(a + 4u), "r"(v1) : "memory");
+    if (o1 + v1 < o1) asm volatile("red.shared.add.u64 [%0], 1;" ::"r"(a + 8u) : "memory");
+  }
 }
 
 // Deferred ring: the reference's general spatial_isotropic_weight.
@@ -1085,7 +1099,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   // crossing scratch of the general weight (deferred drains only): global,
   // L1-resident, element k of lane l at [k * 32 + l]
   double* angs = A.angs_g + ((uint64_t)blockIdx.x * kPairWarps + w) * (slots * 32);
-  int overflow = 0;
+  int overflow = 0;       // general weights' crossing-buffer flag (address taken)
+  bool ring_ovf = false;  // arc ring overflow (a register: no local-memory traffic per drain)
   unsigned long long tot_in = 0, tot_cand = 0, tot_exact = 0, tot_arc = 0;
 
   for (;;) {
@@ -1235,7 +1250,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         }
         if (pending >= 32 || (done && pending > 0)) {
           // <= 31 + kArcChunk * 64 by construction; checked here, off the hot path
-          if (pending > (uint32_t)kArcRing) overflow |= 2;  // reported as an error
+          if (pending > (uint32_t)kArcRing) ring_ovf = true;  // reported as an error
           const int cnt_ = (int)min(pending, 32u);
           __syncwarp();
           uint4* const arcq = *reinterpret_cast<uint4* volatile*>(&s_ring[w]);
@@ -1476,6 +1491,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     atomicAdd(&B.stats[2], tot_exact);
     atomicAdd(&B.stats[4], tot_arc);
   }
+  if (ring_ovf) overflow |= 2;
   if (overflow) atomicOr(&B.stats[3], (unsigned long long)overflow);
 }
 
@@ -1671,7 +1687,7 @@ __global__ void weights_kernel(const double* cx, const double* cy, const double*
     return;
   }
   // the pair kernel's order: closed form (rectangles), then the general routines
-  double ws = reg.rect ? rect_single_edge_weight(cx[i], cy[i], d[i], reg) : -1.0;
+  double ws = reg.rect ? rect_single_edge_omega_q(cx[i], cy[i], d[i] * d[i], reg) : -1.0;
   if (ws < 0.0 && reg.rect) ws = rect_multi_edge_weight(cx[i], cy[i], d[i], reg);
   if (ws < 0.0)
     ws = reg.rect ? spatial_weight_buf<true>(cx[i], cy[i], d[i], reg, angs + threadIdx.x, 128,
@@ -1729,7 +1745,7 @@ __global__ void __launch_bounds__(128) task_kernel(TaskArgs T, RegionView reg,
         atomicMin(T.bad, (unsigned long long)c);
         continue;
       }
-      ws = reg.rect ? rect_single_edge_weight(cx, cy, d, reg) : -1.0;
+      ws = reg.rect ? rect_single_edge_omega_q(cx, cy, d * d, reg) : -1.0;
       if (ws < 0.0 && reg.rect) ws = rect_multi_edge_weight(cx, cy, d, reg);
       if (ws < 0.0)
         ws = reg.rect ? spatial_weight_buf<true>(cx, cy, d, reg, angs + threadIdx.x, 128,

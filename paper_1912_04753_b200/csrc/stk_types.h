@@ -64,6 +64,7 @@ struct RegionView {
   double sd_start[4], sd_len[4];
   double sw_dmin;       // rect single-edge closed form: smallest radius it accepts
   double sw_margin;     // ... and smallest d - h (outside midpoint clear of the boundary)
+  double sw_q_min;      // q-form of sw_dmin: q >= sw_q_min implies RN(sqrt(q)) >= sw_dmin
   // General polygons.  Horizontal slabs: slab s lists every
   // edge k (ring[k] -> ring[k+1]) whose y-range, widened by the on_segment
   // tolerance, meets the slab; point_in_polygon of a probe then visits only
