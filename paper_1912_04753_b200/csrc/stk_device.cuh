@@ -626,6 +626,18 @@ __device__ __forceinline__ double spatial_weight_buf(double cx, double cy, doubl
 // theta_ref carries the reference's own rounding (the quadratic's
 // cancellation: <= 2^-53 * scale / (len * sqrt(disc) * d) rad), which the
 // gate qa*disc*d^2 >= 1e-10*scale^2 bounds by ~1e-11.
+// 1/x for a normal positive x to ~1 ulp: the hardware approximation plus two
+// Newton steps, without the IEEE division's special-case path (the arc
+// drains' operands are bounded away from zero and infinity by their gates).
+__device__ __forceinline__ double rcp_pos(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
 // atan2(y, x) for y > 0, x > 0 finite (fast_atan2 without the sign cases).
 __device__ __forceinline__ double atan2_pos(double y, double x) {
   constexpr double kTanPi8 = 0.41421356237309504880;
@@ -634,7 +646,7 @@ __device__ __forceinline__ double atan2_pos(double y, double x) {
   const bool steep = y > x;
   const double mx = steep ? y : x, mn = steep ? x : y;
   const bool small = mn <= kTanPi8 * mx;
-  const double t = (small ? mn : mn - mx) / (small ? mx : mn + mx);
+  const double t = (small ? mn : mn - mx) * rcp_pos(small ? mx : mn + mx);
   const double s = t * t;
   double r = -0.0192025292684122813793;
   r = fma(r, s, 0.0392536963206185629612);

@@ -886,14 +886,46 @@ __device__ __forceinline__ PtMeta<TT> lds_meta(uint32_t a) {
     return PtMeta<TT>{(TT)t, (TT)vt, w.x, w.y};
   }
 }
+// One 16-byte load of a 32-bit-time record (the struct's own alignment is 4,
+// which would split it into four loads).
 template <typename TT>
-__device__ __forceinline__ TBucket<TT> lds_tbucket(uint32_t a) {
+__device__ __forceinline__ PtMeta<TT> ld_meta(const PtMeta<TT>* p) {
+  if constexpr (sizeof(TT) == 4) {
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    return PtMeta<TT>{(TT)v.x, (TT)v.y, v.z, v.w};
+  } else {
+    return *p;
+  }
+}
+// Bin-table entries as the pair kernel keeps them in shared memory.  With
+// SINGLE they hold addresses: the q entry the byte offsets of the bin row for
+// a value <= thr (lo) and above it (hi = lo + ct * 8), the t entry the
+// shared-space address of the (count, half) pair of its bin within the row
+// (count section + bin * 8; + 8 above thr), so a pair's counter address is
+// two selects and one three-operand add.  Otherwise lo is the bucket's lowest
+// bin (compare loop).  The t entry stays 8 bytes (int32 times): the random
+// table reads are a shared-memory-bandwidth cost of the candidate loop.
+struct QEntry {
+  double thr;
+  uint32_t lo, hi;
+};
+template <typename TT>
+struct TEntry {
+  TT thr;
+  uint32_t lo;
+};
+__device__ __forceinline__ QEntry lds_qentry(uint32_t a) {
+  const ulonglong2 v = lds_u64x2(a);
+  return QEntry{__longlong_as_double((long long)v.x), (uint32_t)v.y, (uint32_t)(v.y >> 32)};
+}
+template <typename TT>
+__device__ __forceinline__ TEntry<TT> lds_tentry(uint32_t a) {
   if constexpr (sizeof(TT) == 4) {
     const uint2 v = lds_u32x2(a);
-    return TBucket<TT>{(TT)v.x, v.y};
+    return TEntry<TT>{(TT)v.x, v.y};
   } else {
     const ulonglong2 v = lds_u64x2(a);
-    return TBucket<TT>{(TT)v.x, (uint32_t)v.y};
+    return TEntry<TT>{(TT)v.x, (uint32_t)v.y};
   }
 }
 
@@ -906,8 +938,8 @@ struct PairLayout {
   static constexpr size_t Q = al(cpos + sizeof(uint32_t) * kPairWarps * 32);
   static constexpr size_t T = al(Q + sizeof(double) * kMaxAxis);
   static constexpr size_t qtab = al(T + sizeof(TT) * kMaxAxis);
-  static constexpr size_t ttab = al(qtab + sizeof(QBucket) * kQBuckets);
-  static constexpr size_t ch = al(ttab + sizeof(TBucket<TT>) * kBucketTable);
+  static constexpr size_t ttab = al(qtab + sizeof(QEntry) * kQBuckets);
+  static constexpr size_t ch = al(ttab + sizeof(TEntry<TT>) * kBucketTable);
   static size_t __host__ __device__ lh(uint32_t bins) { return al(ch + sizeof(uint2) * bins); }
   static size_t __host__ __device__ total(uint32_t bins) { return al(lh(bins) + sizeof(ArcSum) * bins); }
 };
@@ -927,8 +959,8 @@ __device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, uint32_t sa
   const double term = 1.0 / w;                      // PairHistogram::add(.., 1.0 / w)
   const uint32_t bin = bw & 0x7fffffffu;
   if (w == 0.0) {  // omega == 0: the reference adds 1/0 = inf and its bin ends NaN
-    // bit 0 of the (always even) count: "infinite term"
-    asm volatile("red.shared.or.b32 [%0], 1;" ::"r"(sa_ch + bin * (uint32_t)sizeof(uint2)));
+    // bit 31 of the bin's pair count (< 2^31 per task): "infinite term"
+    asm volatile("red.shared.or.b32 [%0], 0x80000000;" ::"r"(sa_ch + bin * (uint32_t)sizeof(uint2)));
     return;
   }
   uint64_t lo, hi;
@@ -974,7 +1006,7 @@ __device__ __forceinline__ void drain_main(int count, int lane, const uint4* rin
     // native 32-bit shared atomics and their carries (a 64-bit shared atomic
     // add is a compare-and-swap loop on sm_100)
     ++*n_arc;
-    const double term = (1.0 / ws) * ((e.y >> 31) ? 2.0 : 1.0);
+    const double term = rcp_pos(ws) * ((e.y >> 31) ? 2.0 : 1.0);
     const uint64_t v = __double2ull_rn(term * 0x1p53) - (1ULL << kFixedFracBits);
     const uint32_t a = sa_arc + (e.y & 0x7fffffffu) * (uint32_t)sizeof(ArcSum);
     const uint32_t v0 = (uint32_t)v;
@@ -1047,8 +1079,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     uint32_t* cpos;
     double* Q;
     TT* T;
-    QBucket* qtab;
-    TBucket<TT>* ttab;
+    QEntry* qtab;
+    TEntry<TT>* ttab;
     uint2* ch;  // (count, half-count) per bin
     ArcSum* arc;
   } S;
@@ -1057,8 +1089,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   S.cpos = (uint32_t*)(smem_raw + Lay::cpos);
   S.Q = (double*)(smem_raw + Lay::Q);
   S.T = (TT*)(smem_raw + Lay::T);
-  S.qtab = (QBucket*)(smem_raw + Lay::qtab);
-  S.ttab = (TBucket<TT>*)(smem_raw + Lay::ttab);
+  S.qtab = (QEntry*)(smem_raw + Lay::qtab);
+  S.ttab = (TEntry<TT>*)(smem_raw + Lay::ttab);
   S.ch = (uint2*)(smem_raw + Lay::ch);
   S.arc = (ArcSum*)(smem_raw + Lay::lh(bins));
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -1071,9 +1103,19 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   // clamping larger thresholds to TT's range preserves every comparison
   const int64_t tclamp = sizeof(TT) == 4 ? 0x7fffffffLL : 0x7fffffffffffffffLL;
   for (uint32_t b = tid; b < ct; b += blockDim.x) S.T[b] = (TT)min(BV.T[b], tclamp);
-  for (uint32_t b = tid; b < kQBuckets; b += blockDim.x) S.qtab[b] = BV.q_tab[b];
-  for (uint32_t b = tid; b < kBucketTable; b += blockDim.x)
-    S.ttab[b] = TBucket<TT>{(TT)min(BV.t_tab[b].thr, tclamp), BV.t_tab[b].bin};
+  {  // bin tables (QEntry / TEntry above)
+    const uint32_t ch_base = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)Lay::ch;
+    for (uint32_t b = tid; b < kQBuckets; b += blockDim.x) {
+      const QBucket e = BV.q_tab[b];
+      const uint32_t lo = SINGLE ? e.bin * ct * (uint32_t)sizeof(uint2) : e.bin;
+      S.qtab[b] = QEntry{e.thr, lo, lo + ct * (uint32_t)sizeof(uint2)};
+    }
+    for (uint32_t b = tid; b < kBucketTable; b += blockDim.x) {
+      const TBucket<int64_t> e = BV.t_tab[b];
+      const uint32_t lo = SINGLE ? ch_base + e.bin * (uint32_t)sizeof(uint2) : e.bin;
+      S.ttab[b] = TEntry<TT>{(TT)min(e.thr, tclamp), lo};
+    }
+  }
   const double Qmax = BV.Qmax;
   const TT Tmax = (TT)min(BV.Tmax, tclamp);
   const int t_shift = BV.t_shift;
@@ -1167,7 +1209,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       bool cdeep = true;
       if (lane < (int)nc) {
         const uint32_t pos = sel_p ? B.center_pos[pb + start + lane] : start + lane;
-        const PtMeta<TT> m = pmeta_b[pb + pos];
+        const PtMeta<TT> m = ld_meta<TT>(pmeta_b + pb + pos);
         cxy_w[lane] = B.pxy[pb + pos];
         cm_w[lane] = m;
         cpos_w[lane] = pos;
@@ -1222,10 +1264,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       // part `part` of `np` walks virtual indices [V part / np, V (part + 1) / np)
       uint32_t v0 = (uint32_t)((uint64_t)V * part / np);
       const uint32_t v_hi = (uint32_t)((uint64_t)V * (part + 1) / np);
+      // candidates of this unit: every (center, neighbour) of its tiles
+      const unsigned long long n_cand = (unsigned long long)(v_hi - v0) * nc;
       uint32_t qh = 0, qt = 0;    // arc ring head / tail (monotone)
       uint32_t ch_ = 0, ct_ = 0;  // deferred ring head / tail
       uint32_t n_arc = 0;
-      unsigned long long n_cand = 0;
       // flat walk over (tile, center chunk); one inline copy of the drain
       int kc = 0;
       for (;;) {
@@ -1307,7 +1350,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         PtMeta<TT> nm{0, 0, 0u, 0u};
         if (has) {
           nxy = B.pxy[pb + jp];
-          nm = pmeta_b[pb + jp];
+          nm = ld_meta<TT>(pmeta_b + pb + jp);
         }
         if (kc == 0) {
           if (has && jp + 32 < (uint32_t)B.n) {  // the lane's likely next neighbour into L1
@@ -1324,7 +1367,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           const bool same_c = v0 + (uint32_t)lane < row0_end && jp < own_end;
           s_lim[tid] = make_uint2(same_c ? (sel_p ? 0u : jp - first_pos) : 0xffffffffu,
                                   (sel_p && same_c) ? nm.idx : 0u);
-          n_cand += (unsigned long long)min(32u, v_hi - v0) * nc;
           __syncwarp();
         }
         // some lane's neighbour lies in the item's own cell: the ordering rule applies
@@ -1384,21 +1426,21 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               // Tmax >> t_shift < kBucketTable): only q's lower clamp remains
               const uint32_t qh = (uint32_t)__double2hiint(q);
               const int bq = max((int)(qh >> q_shift) - q_base, 0);
-              const ulonglong2 qe2 = lds_u64x2(a_q + (uint32_t)bq * (uint32_t)sizeof(QBucket));
-              const QBucket qe{__longlong_as_double((long long)qe2.x), (uint32_t)qe2.y, 0u};
-              uint32_t sb = qe.bin;
+              const QEntry qe = lds_qentry(a_q + (uint32_t)bq * (uint32_t)sizeof(QEntry));
               const int bt = (int)(du >> t_shift);
-              const TBucket<TT> te = lds_tbucket<TT>(a_t + (uint32_t)bt * (uint32_t)sizeof(TBucket<TT>));
-              uint32_t tb = te.bin;
+              const TEntry<TT> te = lds_tentry<TT>(a_t + (uint32_t)bt * (uint32_t)sizeof(TEntry<TT>));
+              uint32_t a_bin;  // shared-space address of the bin's (count, half) pair
               if constexpr (SINGLE) {
-                sb += q > qe.thr ? 1u : 0u;
-                tb += du > te.thr ? 1u : 0u;
+                a_bin = (q > qe.thr ? qe.hi : qe.lo) + te.lo + (du > te.thr ? 8u : 0u);
+                bin = (a_bin - a_ch) >> 3;
               } else {
+                uint32_t sb = qe.lo, tb = te.lo;
                 while (q > S.Q[sb]) ++sb;
                 while (du > S.T[tb]) ++tb;
+                bin = sb * ct + tb;
+                a_bin = a_ch + bin * 8u;
               }
-              bin = sb * ct + tb;
-              reds_add_u32(a_ch + bin * 8u, 2u);
+              reds_add_u32(a_bin, 1u);  // one per unordered pair (x2 at the flush)
               if (DEEP) return;
               half_i = du > cmk.vt;
               half_j = du > nm.vt;
@@ -1408,7 +1450,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               arc_i = qh >= cmk.sqh;
               arc_j = qh >= nm.sqh;
               const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
-              if (h) reds_add_u32(a_ch + bin * 8u + 4u, h);
+              if (h) reds_add_u32(a_bin + 4u, h);
             }
             if (DEEP) return;
             if (__any_sync(FULL_MASK, arc_i || arc_j)) {  // one vote on the common path
@@ -1466,10 +1508,12 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     const uint64_t hb = (uint64_t)p * bins;
     for (uint32_t b = tid; b < bins; b += blockDim.x) {
       const uint2 chb = S.ch[b];
-      // counts are even (2 per unordered pair); bit 0 flags an infinite term
-      tot_in += chb.x & ~1u;  // in-threshold pairs (telemetry)
-      if (chb.x > 1u) atomicAdd(&B.h_cnt[hb + b], (unsigned long long)(chb.x & ~1u));
-      if (chb.x & 1u) atomicOr(&B.h_cnt[hb + b], 1ULL);
+      // one count per unordered pair (two ordered pairs); bit 31 flags an
+      // infinite term (the global count keeps the flag in its bit 0)
+      const unsigned long long c2 = 2ull * (chb.x & 0x7fffffffu);
+      tot_in += c2;  // in-threshold ordered pairs (telemetry)
+      if (c2) atomicAdd(&B.h_cnt[hb + b], c2);
+      if (chb.x >> 31) atomicOr(&B.h_cnt[hb + b], 1ULL);
       if (chb.y) atomicAdd(&B.h_half[hb + b], (unsigned long long)chb.y);
       const unsigned long long lo = S.arc[b].lo;
       unsigned long long hi = S.arc[b].hi;

@@ -108,16 +108,22 @@ def subset_parity(name, workers):
     out = dict(s=s, tv=tv, seed=cfg.seed, sims=m, realisations=np.array(rs),
                **fingerprint(x, y, t))
     path = os.path.join(OUT, f"{name.lower()}_parity.npz")
+    if os.path.exists(path):  # resume: keep the patterns a previous run finished
+        old = np.load(path)
+        if all(np.array_equal(old[k], np.asarray(v)) for k, v in out.items()):
+            out.update({k: old[k] for k in old.files})
     for which in [-1] + rs:
+        key = "obs" if which < 0 else f"r{which}"
+        if f"{key}_k" in out:
+            log(f"{name} {key}: already in {os.path.basename(path)}")
+            continue
         t0 = time.time()
         res = job.pattern(which)
         dt = time.time() - t0
         if which < 0:
             px, py, pt = x, y, t
-            key = "obs"
         else:
             px, py, pt = ref.generate_cstr(len(x), ring, 0, cfg.period_s, cfg.seed + which)
-            key = f"r{which}"
         t1 = time.time()
         counts = ref.pair_counts_indexed(px, py, pt, s, tv, threads=workers)
         log(f"{name} {key}: job {dt:.0f}s counts {time.time() - t1:.0f}s "
