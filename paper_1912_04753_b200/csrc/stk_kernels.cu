@@ -960,7 +960,7 @@ __device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, uint32_t sa
   const uint32_t bin = bw & 0x7fffffffu;
   if (w == 0.0) {  // omega == 0: the reference adds 1/0 = inf and its bin ends NaN
     // bit 31 of the bin's pair count (< 2^31 per task): "infinite term"
-    asm volatile("red.shared.or.b32 [%0], 0x80000000;" ::"r"(sa_ch + bin * (uint32_t)sizeof(uint2)));
+    asm volatile("red.shared.or.b32 [%0], 0x80000000;" ::"r"(sa_ch + bin * 4u));
     return;
   }
   uint64_t lo, hi;
@@ -1081,7 +1081,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     TT* T;
     QEntry* qtab;
     TEntry<TT>* ttab;
-    uint2* ch;  // (count, half-count) per bin
+    uint32_t* ch;  // count[bins] (unordered pairs), then half[bins] (v = 1/2 ordered pairs):
+                   // separate arrays so random bins spread over all 32 banks
     ArcSum* arc;
   } S;
   S.cxy = (double2*)(smem_raw + Lay::cxy);
@@ -1091,7 +1092,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   S.T = (TT*)(smem_raw + Lay::T);
   S.qtab = (QEntry*)(smem_raw + Lay::qtab);
   S.ttab = (TEntry<TT>*)(smem_raw + Lay::ttab);
-  S.ch = (uint2*)(smem_raw + Lay::ch);
+  S.ch = (uint32_t*)(smem_raw + Lay::ch);
   S.arc = (ArcSum*)(smem_raw + Lay::lh(bins));
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   // an input point failed region.contains (validate_kernel ran on this stream
@@ -1107,12 +1108,12 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     const uint32_t ch_base = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)Lay::ch;
     for (uint32_t b = tid; b < kQBuckets; b += blockDim.x) {
       const QBucket e = BV.q_tab[b];
-      const uint32_t lo = SINGLE ? e.bin * ct * (uint32_t)sizeof(uint2) : e.bin;
-      S.qtab[b] = QEntry{e.thr, lo, lo + ct * (uint32_t)sizeof(uint2)};
+      const uint32_t lo = SINGLE ? e.bin * ct * 4u : e.bin;
+      S.qtab[b] = QEntry{e.thr, lo, lo + ct * 4u};
     }
     for (uint32_t b = tid; b < kBucketTable; b += blockDim.x) {
       const TBucket<int64_t> e = BV.t_tab[b];
-      const uint32_t lo = SINGLE ? ch_base + e.bin * (uint32_t)sizeof(uint2) : e.bin;
+      const uint32_t lo = SINGLE ? ch_base + e.bin * 4u : e.bin;
       S.ttab[b] = TEntry<TT>{(TT)min(e.thr, tclamp), lo};
     }
   }
@@ -1152,7 +1153,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       s_next = 0;
     }
     for (uint32_t b = tid; b < bins; b += blockDim.x) {
-      S.ch[b] = make_uint2(0u, 0u);
+      S.ch[b] = 0u;
+      S.ch[bins + b] = 0u;
       S.arc[b].lo = 0ULL;
       S.arc[b].hi = 0ULL;
     }
@@ -1402,6 +1404,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           const uint32_t a_q = sbase + (uint32_t)Lay::qtab;
           const uint32_t a_t = sbase + (uint32_t)Lay::ttab;
           const uint32_t a_ch = sbase + (uint32_t)Lay::ch;
+          const uint32_t bins4 = bins * 4u;
           auto pair_step = [&](int k) {
             const double2 c = lds_f64x2(a_cxy + k * (uint32_t)sizeof(double2));  // center k
             const PtMeta<TT> cmk = lds_meta<TT>(a_cm + k * (uint32_t)sizeof(PtMeta<TT>));
@@ -1429,16 +1432,16 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               const QEntry qe = lds_qentry(a_q + (uint32_t)bq * (uint32_t)sizeof(QEntry));
               const int bt = (int)(du >> t_shift);
               const TEntry<TT> te = lds_tentry<TT>(a_t + (uint32_t)bt * (uint32_t)sizeof(TEntry<TT>));
-              uint32_t a_bin;  // shared-space address of the bin's (count, half) pair
+              uint32_t a_bin;  // shared-space address of the bin's count (its half count: + bins4)
               if constexpr (SINGLE) {
-                a_bin = (q > qe.thr ? qe.hi : qe.lo) + te.lo + (du > te.thr ? 8u : 0u);
-                bin = (a_bin - a_ch) >> 3;
+                a_bin = (q > qe.thr ? qe.hi : qe.lo) + te.lo + (du > te.thr ? 4u : 0u);
+                bin = (a_bin - a_ch) >> 2;
               } else {
                 uint32_t sb = qe.lo, tb = te.lo;
                 while (q > S.Q[sb]) ++sb;
                 while (du > S.T[tb]) ++tb;
                 bin = sb * ct + tb;
-                a_bin = a_ch + bin * 8u;
+                a_bin = a_ch + bin * 4u;
               }
               reds_add_u32(a_bin, 1u);  // one per unordered pair (x2 at the flush)
               if (DEEP) return;
@@ -1450,7 +1453,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               arc_i = qh >= cmk.sqh;
               arc_j = qh >= nm.sqh;
               const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
-              if (h) reds_add_u32(a_bin + 4u, h);
+              if (h) reds_add_u32(a_bin + bins4, h);
             }
             if (DEEP) return;
             if (__any_sync(FULL_MASK, arc_i || arc_j)) {  // one vote on the common path
@@ -1507,7 +1510,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     // flush the CTA histogram of pattern p (exact integer adds)
     const uint64_t hb = (uint64_t)p * bins;
     for (uint32_t b = tid; b < bins; b += blockDim.x) {
-      const uint2 chb = S.ch[b];
+      const uint2 chb = make_uint2(S.ch[b], S.ch[bins + b]);
       // one count per unordered pair (two ordered pairs); bit 31 flags an
       // infinite term (the global count keeps the flag in its bit 0)
       const unsigned long long c2 = 2ull * (chb.x & 0x7fffffffu);
