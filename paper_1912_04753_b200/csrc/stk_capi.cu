@@ -200,6 +200,11 @@ struct stk_ctx {
   int q_shift = 0, q_base = 0;
   int t_shift = 0;
   bool single_step = false;
+  bool q_single = false;  // the q table alone is single-step
+  int t_uni = 0;          // BinView::t_uni and its constants
+  int32_t t_add = 0, t_lo = 0;
+  uint32_t t_magic = 0;
+  int t_sh = 0;
   DevBuf<double> d_Q, d_s;
   DevBuf<int64_t> d_T;
   DevBuf<QBucket> d_qtab;
@@ -528,6 +533,11 @@ BinView bin_view(stk_ctx* c) {
   b.q_base = c->q_base;
   b.t_shift = c->t_shift;
   b.single_step = c->single_step ? 1 : 0;
+  b.t_uni = c->t_uni;
+  b.t_add = c->t_add;
+  b.t_lo = c->t_lo;
+  b.t_magic = c->t_magic;
+  b.t_sh = c->t_sh;
   return b;
 }
 
@@ -895,7 +905,9 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   CK(cudaGetLastError());
   ++c->launches;
   const size_t smem = pair_kernel_smem(P.bins, B.wide);
-  const int mode = (c->fast_rect ? 1 : 0) | (c->single_step ? 2 : 0);
+  // bit 2: q table single-step and evenly spaced time thresholds (32-bit lags)
+  const bool tuni = c->t_uni && !B.wide && c->q_single;
+  const int mode = (c->fast_rect ? 1 : 0) | ((c->single_step || tuni) ? 2 : 0) | (tuni ? 4 : 0);
   const int per_sm = pair_occupancy(c, B.wide, mode, smem);
   tasks_kernel<<<1, 1, 0, c->stream>>>(B, G, (uint32_t)(c->num_sms * per_sm));
   CK(cudaGetLastError());
@@ -1638,6 +1650,36 @@ int stk_set_grid(stk_ctx* c, const double* s_values, uint32_t cs, const int64_t*
       if (lo <= tmax && k + 1 < (int)ct && t_values[k + 1] < std::min(last, tmax)) t_single = false;
     }
     c->single_step = q_single && t_single;
+    c->q_single = q_single;
+    // evenly spaced time thresholds: exact multiply-high division (BinView::t_uni)
+    c->t_uni = 0;
+    if (ct >= 2 && t_values[0] >= 0) {
+      const int64_t D = t_values[1] - t_values[0], T0 = t_values[0];
+      bool even = D >= 2 && (int64_t)ct * D < (1ll << 31) && T0 < (1ll << 31);
+      for (uint32_t k = 0; even && k < ct; ++k) even = t_values[k] == T0 + (int64_t)k * D;
+      if (even) {
+        int N = 0, l = 0;
+        while ((1ll << N) < (int64_t)ct * D) ++N;
+        while ((1ll << l) < D) ++l;
+        const int E = N + l;  // m = ceil(2^E / D) < 2^(N+1) <= 2^32
+        const unsigned __int128 pw = (unsigned __int128)1 << E;
+        const uint64_t m = (uint64_t)((pw + (unsigned __int128)(D - 1)) / (unsigned __int128)D);
+        const uint64_t magic = E >= 32 ? m : m << (32 - E);
+        const int sh = E >= 32 ? E - 32 : 0;
+        bool exact = magic < (1ull << 32);
+        auto div = [&](uint64_t x) { return ((x * magic) >> 32) >> sh; };
+        for (int64_t j = 0; exact && j <= (int64_t)ct; ++j)
+          for (int64_t x : {j * D - 1, j * D})
+            if (x >= D - 1 && x <= (int64_t)ct * D - 1) exact = div((uint64_t)x) == (uint64_t)(x / D);
+        if (exact) {
+          c->t_uni = 1;
+          c->t_add = (int32_t)(D - 1 - T0);
+          c->t_lo = (int32_t)(D - 1);
+          c->t_magic = (uint32_t)magic;
+          c->t_sh = sh;
+        }
+      }
+    }
     c->d_Q.ensure(cs);
     c->d_s.ensure(cs);
     c->d_T.ensure(ct);

@@ -1054,7 +1054,9 @@ constexpr int kDeepUnroll = STK_DEEP_UNROLL;
 // SINGLE: every bin-table bucket straddles at most one threshold (the host's
 // BinView::single_step), so one compare per axis finds the bin — a template
 // flag rather than a runtime test inside the candidate loops.
-template <typename TT, bool RECT, bool SINGLE>
+// TUNI (with SINGLE, 32-bit times): evenly spaced time thresholds, the t bin
+// by one multiply-high instead of a table read (BinView::t_uni).
+template <typename TT, bool RECT, bool SINGLE, bool TUNI>
 __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(PairArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_task, s_next;
@@ -1108,7 +1110,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
     const uint32_t ch_base = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)Lay::ch;
     for (uint32_t b = tid; b < kQBuckets; b += blockDim.x) {
       const QBucket e = BV.q_tab[b];
-      const uint32_t lo = SINGLE ? e.bin * ct * 4u : e.bin;
+      // TUNI: the q entry holds absolute addresses (the t bin adds 4 tb)
+      const uint32_t lo = SINGLE ? (TUNI ? ch_base : 0u) + e.bin * ct * 4u : e.bin;
       S.qtab[b] = QEntry{e.thr, lo, lo + ct * 4u};
     }
     for (uint32_t b = tid; b < kBucketTable; b += blockDim.x) {
@@ -1121,6 +1124,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   const TT Tmax = (TT)min(BV.Tmax, tclamp);
   const int t_shift = BV.t_shift;
   const int q_shift = BV.q_shift, q_base = BV.q_base;
+  const int32_t t_add = BV.t_add, t_lo = BV.t_lo;
+  const uint32_t t_magic = BV.t_magic;
+  const int t_sh = BV.t_sh;
   // deep: hi32(q) < sqh for every in-threshold q (q <= Qmax)
   const uint32_t Qmax_hi = (uint32_t)__double2hiint(BV.Qmax);
   const uint32_t total_tasks = B.task_start[B.R];
@@ -1402,7 +1408,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           const uint32_t a_cxy = sbase + (uint32_t)Lay::cxy + wo * (uint32_t)sizeof(double2);
           const uint32_t a_cm = sbase + (uint32_t)Lay::cmeta + wo * (uint32_t)sizeof(PtMeta<TT>);
           const uint32_t a_q = sbase + (uint32_t)Lay::qtab;
-          const uint32_t a_t = sbase + (uint32_t)Lay::ttab;
+          [[maybe_unused]] const uint32_t a_t = sbase + (uint32_t)Lay::ttab;  // table t bins
           const uint32_t a_ch = sbase + (uint32_t)Lay::ch;
           const uint32_t bins4 = bins * 4u;
           auto pair_step = [&](int k) {
@@ -1430,13 +1436,20 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               const uint32_t qh = (uint32_t)__double2hiint(q);
               const int bq = max((int)(qh >> q_shift) - q_base, 0);
               const QEntry qe = lds_qentry(a_q + (uint32_t)bq * (uint32_t)sizeof(QEntry));
-              const int bt = (int)(du >> t_shift);
-              const TEntry<TT> te = lds_tentry<TT>(a_t + (uint32_t)bt * (uint32_t)sizeof(TEntry<TT>));
               uint32_t a_bin;  // shared-space address of the bin's count (its half count: + bins4)
-              if constexpr (SINGLE) {
+              if constexpr (TUNI) {
+                const int32_t x = max((int32_t)du + t_add, t_lo);
+                const uint32_t tb = __umulhi((uint32_t)x, t_magic) >> t_sh;
+                a_bin = (q > qe.thr ? qe.hi : qe.lo) + tb * 4u;
+                bin = (a_bin - a_ch) >> 2;
+              } else if constexpr (SINGLE) {
+                const int bt = (int)(du >> t_shift);
+                const TEntry<TT> te = lds_tentry<TT>(a_t + (uint32_t)bt * (uint32_t)sizeof(TEntry<TT>));
                 a_bin = (q > qe.thr ? qe.hi : qe.lo) + te.lo + (du > te.thr ? 4u : 0u);
                 bin = (a_bin - a_ch) >> 2;
               } else {
+                const int bt = (int)(du >> t_shift);
+                const TEntry<TT> te = lds_tentry<TT>(a_t + (uint32_t)bt * (uint32_t)sizeof(TEntry<TT>));
                 uint32_t sb = qe.lo, tb = te.lo;
                 while (q > S.Q[sb]) ++sb;
                 while (du > S.T[tb]) ++tb;
@@ -1543,14 +1556,18 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
 }
 
 // Host-side launch helpers (keep the kernel templates in this translation unit).
-// mode = rect | single_step << 1.
+// mode = rect | single_step << 1 | evenly spaced times << 2 (32-bit times).
 template <typename TT>
 static const void* pair_fn2(int mode) {
+  if constexpr (sizeof(TT) == 4) {
+    if (mode == 6) return (const void*)pair_kernel<TT, false, true, true>;
+    if (mode == 7) return (const void*)pair_kernel<TT, true, true, true>;
+  }
   switch (mode & 3) {
-    case 0: return (const void*)pair_kernel<TT, false, false>;
-    case 1: return (const void*)pair_kernel<TT, true, false>;
-    case 2: return (const void*)pair_kernel<TT, false, true>;
-    default: return (const void*)pair_kernel<TT, true, true>;
+    case 0: return (const void*)pair_kernel<TT, false, false, false>;
+    case 1: return (const void*)pair_kernel<TT, true, false, false>;
+    case 2: return (const void*)pair_kernel<TT, false, true, false>;
+    default: return (const void*)pair_kernel<TT, true, true, false>;
   }
 }
 static const void* pair_fn(int wide, int mode) {

@@ -112,6 +112,14 @@ struct BinView {
   int q_shift, q_base;     // bucket = clamp((hi32(q) >> q_shift) - q_base): log-spaced
   int t_shift;             // time bucket = min(u >> t_shift, kBucketTable - 1)
   int single_step;         // every bucket straddles <= 1 threshold: one compare finds the bin
+  // Evenly spaced time thresholds T_k = T_0 + k D (32-bit lags): the t bin is
+  // ceil(max(u - T_0, 0) / D) = floor(x / D), x = max(u + t_add, t_lo) with
+  // t_add = D - 1 - T_0, t_lo = D - 1, by one multiply-high: (x * t_magic) >> 32
+  // >> t_sh (host-verified exact at every bin boundary of the lag range).
+  int t_uni;
+  int32_t t_add, t_lo;
+  uint32_t t_magic;
+  int t_sh;
 };
 
 // Uniform space-time cell grid (replaces the STR R-tree, st_index.cpp:54-130).

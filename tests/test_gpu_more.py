@@ -344,6 +344,34 @@ def test_bin_tables_close_thresholds_and_wide_range(api, port):
     _compare(api, port, x, y, t, ring, p0, p1, wide, [1, 2, 3, 20, 40, 9000])
 
 
+def test_evenly_spaced_time_bins(api, port):
+    """Evenly spaced time thresholds T_k = T_0 + k D take the multiply-high t
+    bin (BinView::t_uni): offsets T_0 below, at and above D, D = 2, large D,
+    and lags exactly on, one below and one above every threshold."""
+    ring, p0, p1 = square(1000.0, 0, 200_000)
+    rng = np.random.default_rng(91)
+    n = 2500
+    x = rng.uniform(0, 1000, n)
+    y = rng.uniform(0, 1000, n)
+    t = rng.integers(0, 200_001, n)
+    s = [10.0, 20.0, 40.0, 80.0]
+    for t0, d, ct in [(7, 13, 9), (13, 13, 6), (40, 13, 5), (0, 2, 40), (1, 2, 33),
+                      (5000, 9999, 12)]:
+        tv = [t0 + k * d for k in range(ct)]
+        # lags on, just below and just above each threshold from a few anchors
+        xx, yy, tt = x.copy(), y.copy(), t.copy()
+        m = 0
+        for k, T in enumerate(tv):
+            for du in (T - 1, T, T + 1):
+                if du < 0 or m + 2 > n:
+                    continue
+                xx[m:m + 2] = [300.0 + k, 300.0 + k + 1.0]
+                yy[m:m + 2] = [600.0 + m, 600.0 + m]
+                tt[m:m + 2] = [50_000, 50_000 + du]
+                m += 2
+        _compare(api, port, xx, yy, tt, ring, p0, p1, s, tv)
+
+
 def test_dense_cell_item_parts(api, port):
     """A cluster of 5,000 points inside one grid cell (> kPartCells): items
     are walked as several parts by different warps; sums must not change."""
