@@ -638,37 +638,43 @@ __device__ __forceinline__ double rcp_pos(double x) {
   return fma(y, e, y);
 }
 
+// Constants of the arc drains' closed form in the constant bank: FP64
+// instructions take a constant-bank operand directly, whereas a literal
+// double costs two uniform moves per use.
+// [0, 11): the atan polynomial of fast_atan2 (highest degree first)
+// [11, 19): tan(pi/8), pi/4, pi/2, -1/pi, 1 + 2.1e-6, 1 - 2.5e-12, 1.00001e-9,
+//           4.0001e-10;  [19, 21): 4e-15, 3e-16
+static __constant__ double kArcC[21] = {
+    -0.0192025292684122813793, 0.0392536963206185629612, -0.0508625488582314312944,
+    0.0585831181050115303872,  -0.0666453136980500884962, 0.0769218469937177728423,
+    -0.090909046476956795219,  0.111111110171003266375,   -0.142857142846913806166,
+    0.199999999999956505772,   -0.333333333333333302719,
+    0.41421356237309504880,    0.78539816339744830962,    1.57079632679489661923,
+    -0.31830988618379067154,   1.0 + 2.1e-6,              1.0 - 2.5e-12,
+    1.00001e-9,                4.0001e-10,                4e-15,
+    3e-16};
+
 // atan2(y, x) for y > 0, x > 0 finite (fast_atan2 without the sign cases).
 __device__ __forceinline__ double atan2_pos(double y, double x) {
-  constexpr double kTanPi8 = 0.41421356237309504880;
-  constexpr double kPi4 = 0.78539816339744830962;
-  constexpr double kPi2 = 1.57079632679489661923;
   const bool steep = y > x;
   const double mx = steep ? y : x, mn = steep ? x : y;
-  const bool small = mn <= kTanPi8 * mx;
+  const bool small = mn <= kArcC[11] * mx;
   const double t = (small ? mn : mn - mx) * rcp_pos(small ? mx : mn + mx);
   const double s = t * t;
-  double r = -0.0192025292684122813793;
-  r = fma(r, s, 0.0392536963206185629612);
-  r = fma(r, s, -0.0508625488582314312944);
-  r = fma(r, s, 0.0585831181050115303872);
-  r = fma(r, s, -0.0666453136980500884962);
-  r = fma(r, s, 0.0769218469937177728423);
-  r = fma(r, s, -0.090909046476956795219);
-  r = fma(r, s, 0.111111110171003266375);
-  r = fma(r, s, -0.142857142846913806166);
-  r = fma(r, s, 0.199999999999956505772);
-  r = fma(r, s, -0.333333333333333302719);
-  const double a = (small ? 0.0 : kPi4) + fma(t * s, r, t);
-  return steep ? kPi2 - a : a;
+  double r = kArcC[0];
+#pragma unroll
+  for (int i = 1; i < 11; ++i) r = fma(r, s, kArcC[i]);
+  const double a = (small ? 0.0 : kArcC[12]) + fma(t * s, r, t);
+  return steep ? kArcC[13] - a : a;
 }
 
 // The single-edge closed form, evaluated on q = d^2 itself (the pair kernel's
-// arc drains), without forming d = RN(sqrt(q)): every gate
-// is a sufficient condition in q for the reference's own decision with d =
-// RN(sqrt(q)) (d^2 = q (1 +- 2.3e-16)), slack included for the roundings of
-// the reference's quadratic:
-//   other sides out of reach  h2 >= d (1 + 1e-6)        <=  h2^2 > q (1 + 2.1e-6)
+// arc drains), without forming d = RN(sqrt(q)): every gate is a sufficient
+// condition in q for the reference's own decision with d = RN(sqrt(q))
+// (d^2 = q (1 +- 2.3e-16)), slack included for the roundings of the
+// reference's quadratic:
+//   exactly one side in reach, the other three out of reach h >= d (1 + 1e-6)
+//                                                       <=  h^2 > q (1 + 2.1e-6)
 //   d >= sw_dmin                                         <=  q >= sw_q_min
 //   d - h > 4 box_m + 1e-12 d                            <=  q (1 - 2.5e-12) > (h + 4 box_m)^2
 //   disc > 1e-9 scale (accept), qa disc d^2 >= 1e-10 scale^2, with
@@ -682,26 +688,24 @@ __device__ __forceinline__ double atan2_pos(double y, double x) {
 __device__ __forceinline__ double rect_single_edge_omega_q(double cx, double cy, double q,
                                                            const RegionView& R) {
   const double hl = cx - R.xmin, hr = R.xmax - cx, hb = cy - R.ymin, ht = R.ymax - cy;
-  const bool xr = hr < hl, yt = ht < hb;
-  const double a = xr ? hr : hl, A = xr ? hl : hr;
-  const double b = yt ? ht : hb, Bm = yt ? hb : ht;
-  const bool hz = b < a;  // the nearest side is horizontal (y = ymin / ymax)
-  const double h = hz ? b : a;
-  const double h2 = fmin(hz ? a : b, fmin(A, Bm));
-  const int sd = hz ? (yt ? 3 : 2) : (xr ? 1 : 0);
-  const double fa = R.sd_start[sd] - (hz ? cx : cy);
+  const double reach2 = q * kArcC[15];
+  const bool il = hl * hl <= reach2, ir = hr * hr <= reach2;
+  const bool ib = hb * hb <= reach2, it = ht * ht <= reach2;
+  if ((int)il + (int)ir + (int)ib + (int)it != 1) return -1.0;
+  const double h = il ? hl : ir ? hr : ib ? hb : ht;
+  const int sd = il ? 0 : ir ? 1 : ib ? 2 : 3;
+  const double fa = R.sd_start[sd] - (sd < 2 ? cy : cx);
   const double E = fma(-h, h, q);
   const double fa2 = fa * fa;
   const double S = fa2 + fabs(fma(h, h, fa2) - q);
-  const double slack = 4e-15 * (fa2 + q);
-  const double Sx = fma(3e-16, q, S);
+  const double slack = kArcC[19] * (fa2 + q);
+  const double Sx = fma(kArcC[20], q, S);
   const double hm = h + R.sw_margin;
-  const bool ok = h > 0.0 && q >= R.sw_q_min && h2 * h2 > q * (1.0 + 2.1e-6) &&
-                  q * (1.0 - 2.5e-12) > hm * hm && E > fma(1.00001e-9, S, slack) &&
-                  (E - slack) * q >= 4.0001e-10 * (Sx * Sx);
+  const bool ok = h > 0.0 && q >= R.sw_q_min && q * kArcC[16] > hm * hm &&
+                  E > fma(kArcC[17], S, slack) && (E - slack) * q >= kArcC[18] * (Sx * Sx);
   if (!ok) return -1.0;
   const double theta = atan2_pos(sqrt(E), h);
-  return fma(theta, -0.31830988618379067154, 1.0);  // 1 - theta / pi
+  return fma(theta, kArcC[14], 1.0);  // 1 - theta / pi
 }
 
 // rect_probe_certified for the arc running counter-clockwise from crossing

@@ -346,7 +346,7 @@ def test_bin_tables_close_thresholds_and_wide_range(api, port):
 
 def test_evenly_spaced_time_bins(api, port):
     """Evenly spaced time thresholds T_k = T_0 + k D take the multiply-high t
-    bin (BinView::t_uni): offsets T_0 below, at and above D, D = 2, large D,
+    bin (BinView::t_uni): offsets T_0 below, at and above D (t = 0 is not a valid threshold), D = 2, large D,
     and lags exactly on, one below and one above every threshold."""
     ring, p0, p1 = square(1000.0, 0, 200_000)
     rng = np.random.default_rng(91)
@@ -355,7 +355,7 @@ def test_evenly_spaced_time_bins(api, port):
     y = rng.uniform(0, 1000, n)
     t = rng.integers(0, 200_001, n)
     s = [10.0, 20.0, 40.0, 80.0]
-    for t0, d, ct in [(7, 13, 9), (13, 13, 6), (40, 13, 5), (0, 2, 40), (1, 2, 33),
+    for t0, d, ct in [(7, 13, 9), (13, 13, 6), (40, 13, 5), (2, 2, 40), (1, 2, 33),
                       (5000, 9999, 12)]:
         tv = [t0 + k * d for k in range(ct)]
         # lags on, just below and just above each threshold from a few anchors
