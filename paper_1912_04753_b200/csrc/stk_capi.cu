@@ -214,6 +214,7 @@ struct stk_ctx {
   DevBuf<double> x, y;
   DevBuf<int64_t> t;
   DevBuf<double2> pxy;
+  DevBuf<double2> parc;  // rectangles: per sorted point arc record (Batch::parc)
   DevBuf<unsigned char> pmeta;
   DevBuf<uint32_t> key, rank, cell_count, cell_start, item_start, task_start, task_counter;
   DevBuf<uint2> items;
@@ -607,7 +608,7 @@ Plan make_plan(stk_ctx* c, uint64_t n, uint64_t patterns) {
   P.G = make_grid_geom(c, n);
   P.bins = (uint32_t)(c->s_values.size() * c->t_values.size());
   P.max_items = (uint32_t)((n + kItemCenters - 1) / kItemCenters + P.G.cells);
-  const uint64_t per = n * (8 * 3 + 16 + 24 + 4 * 4) + (uint64_t)(P.G.cells + 1) * 4 * 3 +
+  const uint64_t per = n * (8 * 3 + 16 + 16 + 24 + 4 * 4) + (uint64_t)(P.G.cells + 1) * 4 * 3 +
                        (uint64_t)P.max_items * 8 + (uint64_t)P.bins * 8 * 6 + 64;
   uint64_t R = std::max<uint64_t>(1, c->mem_budget / per);
   R = std::min<uint64_t>(R, std::max<uint64_t>(patterns, 1));
@@ -626,6 +627,7 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   c->t.ensure(R * n);
   const int wide = (c->p1 - c->p0) >= 0x7fffffffLL ? 1 : 0;
   c->pxy.ensure(R * n);
+  if (c->fast_rect) c->parc.ensure(R * n);
   c->pmeta.ensure(R * n * (wide ? sizeof(PtMeta<int64_t>) : sizeof(PtMeta<int32_t>)));
   c->key.ensure(R * n);
   c->rank.ensure(R * n);
@@ -647,6 +649,7 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   B.y = c->y.p;
   B.t = c->t.p;
   B.pxy = c->pxy.p;
+  B.parc = c->fast_rect ? c->parc.p : nullptr;
   B.pmeta = c->pmeta.p;
   B.wide = wide;
   B.key = c->key.p;
@@ -1406,7 +1409,7 @@ void stk_destroy(stk_ctx* c) {
   c->d_ring.release(); c->d_Q.release(); c->d_s.release(); c->d_T.release();
   c->d_qtab.release(); c->d_ttab.release();
   c->x.release(); c->y.release(); c->t.release();
-  c->pxy.release(); c->pmeta.release(); c->key.release(); c->rank.release();
+  c->pxy.release(); c->parc.release(); c->pmeta.release(); c->key.release(); c->rank.release();
   c->cell_count.release(); c->cell_start.release(); c->item_start.release();
   c->task_start.release(); c->task_counter.release(); c->items.release();
   c->hist.release(); c->stats.release(); c->bad.release(); c->K.release(); c->L.release();

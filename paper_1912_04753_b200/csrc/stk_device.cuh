@@ -638,21 +638,70 @@ __device__ __forceinline__ double rcp_pos(double x) {
   return fma(y, e, y);
 }
 
+// The single-edge closed form, per center and q = d^2 (the pair kernel's arc
+// drains), without forming d = RN(sqrt(q)).  Sufficient conditions in q for the
+// reference's own decisions with d = RN(sqrt(q)) (d^2 = q (1 +- 2.3e-16)),
+// slack included for the roundings of the reference's quadratic (DESIGN.md
+// §4.4), with h the nearest side's distance, h2 the second nearest and fa the
+// along-side offset of the reference's segment start (fa^2 >= h2^2 > q):
+//   the other three sides out of reach h_s >= d (1 + 1e-6) <=  q < h2^2 / (1 + 2.1e-6)
+//   d >= sw_dmin                                          <=  q >= sw_q_min
+//   d - h > 4 box_m + 1e-12 d                             <=  q (1 - 2.5e-12) > (h + 4 box_m)^2
+//   disc > 1e-9 scale (accept) and qa disc d^2 >= 1e-10 scale^2, with
+//   disc = 4 D^2 (d^2 - h^2) +- 3e-15 (fa^2 + d^2) 4 D^2 and
+//   scale = 4 D^2 (fa^2 + |h^2 + fa^2 - d^2|) (1 +- 1e-15) = 4 D^2 (K - d^2), K = 2 fa^2 + h^2:
+//     E > 1.00001e-9 S + 4e-15 (fa^2 + q)  and
+//     (E - 4e-15 (fa^2 + q)) q >= 4.0001e-10 (S + 3e-16 q)^2,  E = q - h^2, S = K - q.
+// All are intervals in q: the last is q >= the larger root of a quadratic.  So
+// each center carries {h, [q_lo, q_hi)} (rect_arc_record, computed once per
+// point in the grid build, bounds widened by 1e-12 relative against their own
+// rounding), stored as the high words of q_lo rounded up and of q_hi rounded
+// down: hi32(q) in [lo, hi) implies q in [q_lo, q_hi).  Then
+// omega = 1 - atan2(sqrt(E), h) / pi, within ~1e-13 of the d-based form (theta
+// moves by h * 2.3e-16 / (2 w), w = sqrt(E) bounded below by the interval).
+// An empty interval (lo = ~0) sends every arc pair of the center to the exact
+// path.
+__device__ __forceinline__ double2 rect_arc_record(double cx, double cy, const RegionView& R) {
+  const double hl = cx - R.xmin, hr = R.xmax - cx, hb = cy - R.ymin, ht = R.ymax - cy;
+  const bool xr = hr < hl, yt = ht < hb;
+  const double a = xr ? hr : hl, A = xr ? hl : hr;
+  const double b = yt ? ht : hb, Bm = yt ? hb : ht;
+  const bool hz = b < a;  // the nearest side is horizontal (y = ymin / ymax)
+  const double h = hz ? b : a;
+  const double h2 = fmin(hz ? a : b, fmin(A, Bm));
+  const int sd = hz ? (yt ? 3 : 2) : (xr ? 1 : 0);
+  const double fa = R.sd_start[sd] - (hz ? cx : cy);
+  const double h_2 = h * h, fa2 = fa * fa, K = 2.0 * fa2 + h_2;
+  const double c1 = 1.00001e-9, c2 = 4e-15, c4 = 4.0001e-10, k = 1.0 - 3e-16;
+  const double hm = h + R.sw_margin;
+  double lo = fmax(R.sw_q_min, hm * hm / (1.0 - 2.5e-12));
+  lo = fmax(lo, (h_2 * (1.0 + c1) + fa2 * (2.0 * c1 + c2)) / (1.0 + c1 - c2));
+  const double qa = (1.0 - c2) - c4 * k * k, qb = h_2 + c2 * fa2 - 2.0 * c4 * K * k,
+               qc = c4 * K * K;
+  lo = fmax(lo, (qb + sqrt(qb * qb + 4.0 * qa * qc)) / (2.0 * qa));
+  lo *= 1.0 + 1e-12;
+  const double hi = h2 * h2 / (1.0 + 2.1e-6) * (1.0 - 1e-12);
+  uint32_t lo_h = ~0u, hi_h = 0u;
+  if (h > 0.0 && lo < hi && lo < 1e300) {
+    const uint64_t lb = (uint64_t)__double_as_longlong(lo);
+    lo_h = (uint32_t)(lb >> 32) + ((uint32_t)lb != 0u ? 1u : 0u);
+    hi_h = (uint32_t)__double2hiint(hi);
+  }
+  return make_double2(h, __longlong_as_double((long long)(((uint64_t)hi_h << 32) | lo_h)));
+}
+
 // Constants of the arc drains' closed form in the constant bank: FP64
 // instructions take a constant-bank operand directly, whereas a literal
 // double costs two uniform moves per use.
-// [0, 11): the atan polynomial of fast_atan2 (highest degree first)
-// [11, 19): tan(pi/8), pi/4, pi/2, -1/pi, 1 + 2.1e-6, 1 - 2.5e-12, 1.00001e-9,
-//           4.0001e-10;  [19, 21): 4e-15, 3e-16
-static __constant__ double kArcC[21] = {
+// [0, 11): the atan polynomial of fast_atan2 (highest degree first);
+// [11, 15): tan(pi/8), pi/4, pi/2, -1/pi
+static __constant__ double kArcC[15] = {
     -0.0192025292684122813793, 0.0392536963206185629612, -0.0508625488582314312944,
     0.0585831181050115303872,  -0.0666453136980500884962, 0.0769218469937177728423,
     -0.090909046476956795219,  0.111111110171003266375,   -0.142857142846913806166,
     0.199999999999956505772,   -0.333333333333333302719,
     0.41421356237309504880,    0.78539816339744830962,    1.57079632679489661923,
-    -0.31830988618379067154,   1.0 + 2.1e-6,              1.0 - 2.5e-12,
-    1.00001e-9,                4.0001e-10,                4e-15,
-    3e-16};
+    -0.31830988618379067154};
 
 // atan2(y, x) for y > 0, x > 0 finite (fast_atan2 without the sign cases).
 __device__ __forceinline__ double atan2_pos(double y, double x) {
@@ -668,43 +717,13 @@ __device__ __forceinline__ double atan2_pos(double y, double x) {
   return steep ? kArcC[13] - a : a;
 }
 
-// The single-edge closed form, evaluated on q = d^2 itself (the pair kernel's
-// arc drains), without forming d = RN(sqrt(q)): every gate is a sufficient
-// condition in q for the reference's own decision with d = RN(sqrt(q))
-// (d^2 = q (1 +- 2.3e-16)), slack included for the roundings of the
-// reference's quadratic:
-//   exactly one side in reach, the other three out of reach h >= d (1 + 1e-6)
-//                                                       <=  h^2 > q (1 + 2.1e-6)
-//   d >= sw_dmin                                         <=  q >= sw_q_min
-//   d - h > 4 box_m + 1e-12 d                            <=  q (1 - 2.5e-12) > (h + 4 box_m)^2
-//   disc > 1e-9 scale (accept), qa disc d^2 >= 1e-10 scale^2, with
-//   disc = 4 D^2 (d^2 - h^2) +- 3e-15 (fa^2 + d^2) 4 D^2 and
-//   scale = 4 D^2 (fa^2 + |h^2 + fa^2 - d^2|) (1 +- 1e-15):
-//     E > 1.00001e-9 S + 4e-15 (fa^2 + q),  (E - 4e-15 (fa^2 + q)) q >= 4.0001e-10 (S + 3e-16 q)^2
-//   with E = q - h^2 (one rounding) and S = fa^2 + |h^2 + fa^2 - q|.
-// Then omega = 1 - atan2(sqrt(E), h) / pi, within ~1e-13 of the d-based form
-// (theta moves by h * 2.3e-16 / (2 w) with w = sqrt(E) bounded below by the
-// gates).  Returns -1 when a gate fails (the caller defers to the exact path).
-__device__ __forceinline__ double rect_single_edge_omega_q(double cx, double cy, double q,
-                                                           const RegionView& R) {
-  const double hl = cx - R.xmin, hr = R.xmax - cx, hb = cy - R.ymin, ht = R.ymax - cy;
-  const double reach2 = q * kArcC[15];
-  const bool il = hl * hl <= reach2, ir = hr * hr <= reach2;
-  const bool ib = hb * hb <= reach2, it = ht * ht <= reach2;
-  if ((int)il + (int)ir + (int)ib + (int)it != 1) return -1.0;
-  const double h = il ? hl : ir ? hr : ib ? hb : ht;
-  const int sd = il ? 0 : ir ? 1 : ib ? 2 : 3;
-  const double fa = R.sd_start[sd] - (sd < 2 ? cy : cx);
-  const double E = fma(-h, h, q);
-  const double fa2 = fa * fa;
-  const double S = fa2 + fabs(fma(h, h, fa2) - q);
-  const double slack = kArcC[19] * (fa2 + q);
-  const double Sx = fma(kArcC[20], q, S);
-  const double hm = h + R.sw_margin;
-  const bool ok = h > 0.0 && q >= R.sw_q_min && q * kArcC[16] > hm * hm &&
-                  E > fma(kArcC[17], S, slack) && (E - slack) * q >= kArcC[18] * (Sx * Sx);
-  if (!ok) return -1.0;
-  const double theta = atan2_pos(sqrt(E), h);
+// omega of a pair at q from its center's rect_arc_record, or -1 (exact path).
+__device__ __forceinline__ double rect_single_edge_omega(double q, double2 rec) {
+  const uint64_t iv = (uint64_t)__double_as_longlong(rec.y);
+  const uint32_t qh = (uint32_t)__double2hiint(q);
+  if (!(qh >= (uint32_t)iv && qh < (uint32_t)(iv >> 32))) return -1.0;
+  const double h = rec.x;
+  const double theta = atan2_pos(sqrt(fma(-h, h, q)), h);
   return fma(theta, kArcC[14], 1.0);  // 1 - theta / pi
 }
 
@@ -735,7 +754,7 @@ __device__ __forceinline__ int rect_probe_chord(double cx, double cy, double d, 
 // (cos theta = h / d; phi = 0, pi/2, pi, 3pi/2 for the right, top, left, bottom
 // side), each of which lies on the segment iff the corner on its side of the
 // foot is outside the circle.  Gates (else -1, the general routine): the
-// single-side gates of rect_single_edge_omega_q for every accepted side, no side
+// single-side gates of rect_single_edge_omega for every accepted side, no side
 // rejected while its line is nearer than d (a tangency the reference drops),
 // and every corner between two sides within reach away from the circle by
 // |K - c|^2 - d^2 > 1e-5 d^2 — then crossings are 2.5e-6 d or more from the

@@ -726,6 +726,7 @@ __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first) {
   const double x = B.x[o], y = B.y[o];
   const int64_t t = B.t[o];
   B.pxy[d] = make_double2(x, y);  // the input index travels in the meta record
+  if (B.parc) B.parc[d] = rect_arc_record(x, y, R);
   const uint32_t sq = R.no_safe ? 0u : safe_hi(safe_q(x, y, R));
   const int64_t vt = min(t - R.p0, R.p1 - t);
   if (B.wide) {
@@ -984,17 +985,14 @@ __device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, uint32_t sa
 template <bool RECT>
 __device__ __forceinline__ void drain_main(int count, int lane, const uint4* ring, uint32_t head,
                                            uint4* cring, uint32_t* ctail, unsigned lanemask_lt,
-                                           const double2* pxy, uint32_t sa_arc, uint32_t sa_ch,
-                                           const RegionView& reg, uint32_t* n_arc) {
+                                           const double2* parc, uint32_t sa_arc, uint32_t sa_ch,
+                                           uint32_t* n_arc) {
   const bool valid = lane < count;
   uint4 e = make_uint4(0u, 0u, 0u, 0u);
   double ws = -1.0;
   if (valid) {
     e = ring[(head + lane) & (kArcRing - 1)];
-    if (RECT) {
-      const double2 c = pxy[e.x];
-      ws = rect_single_edge_omega_q(c.x, c.y, __hiloint2double((int)e.w, (int)e.z), reg);
-    }
+    if (RECT) ws = rect_single_edge_omega(__hiloint2double((int)e.w, (int)e.z), parc[e.x]);
   }
   const bool defer = valid && ws < 0.0;
   const unsigned m = __ballot_sync(FULL_MASK, defer);
@@ -1307,8 +1305,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           uint4* const arcq = *reinterpret_cast<uint4* volatile*>(&s_ring[w]);
           const uint32_t sb_ = *reinterpret_cast<volatile uint32_t*>(&s_base);
           const uint32_t sa_arc = sb_ + *reinterpret_cast<volatile uint32_t*>(&s_arc_off);
-          drain_main<RECT>(cnt_, lane, arcq, qh, arcq + kArcRing, &ct_, lanemask_lt, B.pxy + pb, sa_arc,
-                           sb_ + (uint32_t)Lay::ch, A.reg, &n_arc);
+          drain_main<RECT>(cnt_, lane, arcq, qh, arcq + kArcRing, &ct_, lanemask_lt, B.parc + pb, sa_arc,
+                           sb_ + (uint32_t)Lay::ch, &n_arc);
           qh += (uint32_t)cnt_;
           continue;
         }
@@ -1751,7 +1749,7 @@ __global__ void weights_kernel(const double* cx, const double* cy, const double*
     return;
   }
   // the pair kernel's order: closed form (rectangles), then the general routines
-  double ws = reg.rect ? rect_single_edge_omega_q(cx[i], cy[i], d[i] * d[i], reg) : -1.0;
+  double ws = reg.rect ? rect_single_edge_omega(d[i] * d[i], rect_arc_record(cx[i], cy[i], reg)) : -1.0;
   if (ws < 0.0 && reg.rect) ws = rect_multi_edge_weight(cx[i], cy[i], d[i], reg);
   if (ws < 0.0)
     ws = reg.rect ? spatial_weight_buf<true>(cx[i], cy[i], d[i], reg, angs + threadIdx.x, 128,
@@ -1809,7 +1807,7 @@ __global__ void __launch_bounds__(128) task_kernel(TaskArgs T, RegionView reg,
         atomicMin(T.bad, (unsigned long long)c);
         continue;
       }
-      ws = reg.rect ? rect_single_edge_omega_q(cx, cy, d * d, reg) : -1.0;
+      ws = reg.rect ? rect_single_edge_omega(d * d, rect_arc_record(cx, cy, reg)) : -1.0;
       if (ws < 0.0 && reg.rect) ws = rect_multi_edge_weight(cx, cy, d, reg);
       if (ws < 0.0)
         ws = reg.rect ? spatial_weight_buf<true>(cx, cy, d, reg, angs + threadIdx.x, 128,

@@ -162,6 +162,7 @@ struct Batch {
   int64_t* t;
   // grid-sorted layout: interleaved coordinates + one meta record per point
   double2* pxy;   // (x, y)
+  double2* parc;  // rectangles: per sorted point rect_arc_record (h, q interval), else null
   void* pmeta;    // PtMeta<int32_t> (16 B) or PtMeta<int64_t> (24 B) when `wide`
   int wide;       // study period >= 2^31 time units: 64-bit relative times
   uint32_t* key;  // cell key per unsorted point
