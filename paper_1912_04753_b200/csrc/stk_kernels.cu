@@ -949,23 +949,30 @@ size_t pair_kernel_smem(uint32_t bins, int wide) {
   return wide ? PairLayout<int64_t>::total(bins) : PairLayout<int32_t>::total(bins);
 }
 
-// Adds one arc-path ordered pair to the CTA histogram: (1/(omega*v) - 1) as a
-// signed 128-bit fixed-point integer (53 fractional bits, two's complement,
-// carry detected on the low word); bw = bin | (v == 1/2) << 31.
+// Adds one arc-path ordered pair to the CTA histogram.  Its term in the
+// reference is 1/(omega v) (PairHistogram::add(.., 1.0 / w), w = omega v,
+// edge::pair_weight, edge_correction.cpp:88-103); the pair is already counted
+// once (count) and, with v = 1/2, once more (half count), so the arc sum takes
+// (1/omega - 1) / v as a signed 128-bit fixed-point integer (53 fractional
+// bits, two's complement, carry detected on the low word): 1/omega - 1 exactly
+// (fixed_term_minus_one), doubled by a shift for v = 1/2 (1/(omega/2) rounds to
+// exactly 2 RN(1/omega)).  bw = bin | (v == 1/2) << 31.
 // sa_arc / sa_ch: shared-space addresses of the arc-sum and count sections.
 __device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, uint32_t sa_arc,
                                              uint32_t sa_ch, uint32_t* n_arc) {
-  if (ws != 1.0) ++*n_arc;                           // omega != 1 (SURVEY's arc-pair definition)
-  const double w = ws * ((bw >> 31) ? 0.5 : 1.0);  // edge::pair_weight (edge_correction.cpp:88-103)
-  const double term = 1.0 / w;                      // PairHistogram::add(.., 1.0 / w)
+  if (ws != 1.0) ++*n_arc;  // omega != 1 (SURVEY's arc-pair definition)
   const uint32_t bin = bw & 0x7fffffffu;
-  if (w == 0.0) {  // omega == 0: the reference adds 1/0 = inf and its bin ends NaN
+  if (ws == 0.0) {  // omega == 0: the reference adds 1/0 = inf and its bin ends NaN
     // bit 31 of the bin's pair count (< 2^31 per task): "infinite term"
     asm volatile("red.shared.or.b32 [%0], 0x80000000;" ::"r"(sa_ch + bin * 4u));
     return;
   }
   uint64_t lo, hi;
-  fixed_term_minus_one(term, &lo, &hi);
+  fixed_term_minus_one(1.0 / ws, &lo, &hi);
+  if (bw >> 31) {  // x 2 (two's complement shift)
+    hi = (hi << 1) | (lo >> 63);
+    lo <<= 1;
+  }
   if (lo | hi) {
     const uint32_t a = sa_arc + bin * (uint32_t)sizeof(ArcSum);
     unsigned long long old;
@@ -999,18 +1006,18 @@ __device__ __forceinline__ void drain_main(int count, int lane, const uint4* rin
   if (defer) cring[(*ctail + __popc(m & lanemask_lt)) & (kCplxRing - 1)] = e;
   *ctail += __popc(m);
   if (valid && !defer) {
-    // omega in [1/2, 1): term 1/(omega v) in (1, 4], so (term - 1) 2^53 is a
-    // non-negative integer below 2^55; added to the bin's 128-bit sum with two
-    // native 32-bit shared atomics and their carries (a 64-bit shared atomic
-    // add is a compare-and-swap loop on sm_100)
+    // omega in [1/2, 1): the arc term (1/omega - 1) / v (add_arc_term) times
+    // 2^53 is a non-negative integer <= 2^54; added to the bin's 128-bit sum
+    // with two native 32-bit shared atomics and their carries (a 64-bit
+    // shared atomic add is a compare-and-swap loop on sm_100)
     ++*n_arc;
-    const double term = rcp_pos(ws) * ((e.y >> 31) ? 2.0 : 1.0);
-    const uint64_t v = __double2ull_rn(term * 0x1p53) - (1ULL << kFixedFracBits);
+    const uint64_t v = (__double2ull_rn(rcp_pos(ws) * 0x1p53) - (1ULL << kFixedFracBits))
+                       << (e.y >> 31);
     const uint32_t a = sa_arc + (e.y & 0x7fffffffu) * (uint32_t)sizeof(ArcSum);
     const uint32_t v0 = (uint32_t)v;
     uint32_t v1 = (uint32_t)(v >> 32), o0, o1;
     asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o0) : "r"(a), "r"(v0) : "memory");
-    v1 += (o0 + v0 < o0) ? 1u : 0u;  // v1 < 2^23: no overflow
+    v1 += (o0 + v0 < o0) ? 1u : 0u;  // v1 <= 2^22: no overflow
     asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o1) : "r"(a + 4u), "r"(v1) : "memory");
     if (o1 + v1 < o1) asm volatile("red.shared.add.u64 [%0], 1;" ::"r"(a + 8u) : "memory");
   }
@@ -1212,16 +1219,17 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       // stage the item's centers (<= 32) in shared memory: the inner loop
       // broadcasts one center to the 32 neighbour lanes
       __syncwarp();
-      bool cdeep = true;
+      bool c_sp = true, c_tm = true;  // no arc / no half weight possible for this center
       if (lane < (int)nc) {
         const uint32_t pos = sel_p ? B.center_pos[pb + start + lane] : start + lane;
         const PtMeta<TT> m = ld_meta<TT>(pmeta_b + pb + pos);
         cxy_w[lane] = B.pxy[pb + pos];
         cm_w[lane] = m;
         cpos_w[lane] = pos;
-        cdeep = m.sqh > Qmax_hi && m.vt >= Tmax;
+        c_sp = m.sqh > Qmax_hi;
+        c_tm = m.vt >= Tmax;
       }
-      const bool item_deep = __all_sync(FULL_MASK, cdeep);
+      const bool item_sp = __all_sync(FULL_MASK, c_sp), item_tm = __all_sync(FULL_MASK, c_tm);
       __syncwarp();
       const uint32_t first_pos = sel_p ? 0u : start;  // lowest center position (non-selected)
       const int kx = (int)(cell % (uint32_t)G.nx);
@@ -1378,15 +1386,20 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         // some lane's neighbour lies in the item's own cell: the ordering rule applies
         const bool tile_own =
             __any_sync(FULL_MASK, *reinterpret_cast<volatile uint32_t*>(&s_lim[tid].x) != 0xffffffffu);
-        const bool tile_deep =
-            __all_sync(FULL_MASK, !has || (nm.sqh > Qmax_hi && nm.vt >= Tmax));
+        // ARC: some pair of the (item, tile) block can have omega != 1 (a
+        // center or neighbour with safe radius < s_max); HALF: some can have
+        // v = 1/2 (temporal threshold < t_max)
+        const bool arc_any = !(item_sp && __all_sync(FULL_MASK, !has || nm.sqh > Qmax_hi));
+        const bool half_any = !(item_tm && __all_sync(FULL_MASK, !has || nm.vt >= Tmax));
         const int kend = min(kc + kArcChunk, (int)nc);
-        auto chunk = [&](auto own_tag, auto deep_tag) {
+        auto chunk = [&](auto own_tag, auto arc_tag, auto half_tag) {
           constexpr bool OWN = decltype(own_tag)::value;
-          // DEEP: every center of the item and every neighbour of the tile has
-          // safe radius >= s_max and temporal threshold >= t_max, so all their
-          // in-threshold pairs have omega == 1 and v == 1: count only
-          constexpr bool DEEP = decltype(deep_tag)::value;
+          // !ARC: every center of the item and every neighbour of the tile has
+          // safe radius >= s_max, so all their pairs have omega == 1; !HALF:
+          // every temporal threshold is >= t_max, so v == 1.  Neither: count only
+          constexpr bool ARC = decltype(arc_tag)::value;
+          constexpr bool HALF = decltype(half_tag)::value;
+          constexpr bool DEEP = !ARC && !HALF;
           // the warp's staged centers, addressed from a per-chunk read of the
           // thread index: a value the compiler cannot rematerialise inside
           // the loop (it otherwise rebuilds the address every iteration)
@@ -1422,7 +1435,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             const bool in = owner && q <= Qmax && du <= Tmax;
             bool arc_i = false, arc_j = false;
             uint32_t bin = 0;
-            bool half_i = false, half_j = false;
             if (in) {
               // bin_pair: first s_k >= d <=> first Q_k >= q; first t_l >= u.
               // q's bucket from the high word of its bits (log-spaced
@@ -1455,18 +1467,21 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
                 a_bin = a_ch + bin * 4u;
               }
               reds_add_u32(a_bin, 1u);  // one per unordered pair (x2 at the flush)
-              if (DEEP) return;
-              half_i = du > cmk.vt;
-              half_j = du > nm.vt;
-              // hi32(q) < sqh implies q below the safe radius^2 (omega == 1);
-              // the rest take the exact path (the few with q just under the
-              // safe radius get omega == 1 exactly there)
-              arc_i = qh >= cmk.sqh;
-              arc_j = qh >= nm.sqh;
-              const uint32_t h = (uint32_t)(!arc_i && half_i) + (uint32_t)(!arc_j && half_j);
-              if (h) reds_add_u32(a_bin + bins4, h);
+              if constexpr (HALF) {
+                // every ordered pair with v = 1/2 (arc pairs too: their arc
+                // term is (1/omega - 1) / v, so the sums split exactly)
+                const uint32_t h = (uint32_t)(du > cmk.vt) + (uint32_t)(du > nm.vt);
+                if (h) reds_add_u32(a_bin + bins4, h);
+              }
+              if constexpr (ARC) {
+                // hi32(q) < sqh implies q below the safe radius^2 (omega == 1);
+                // the rest take the exact path (the few with q just under the
+                // safe radius get omega == 1 exactly there)
+                arc_i = qh >= cmk.sqh;
+                arc_j = qh >= nm.sqh;
+              }
             }
-            if (DEEP) return;
+            if constexpr (!ARC) return;
             if (__any_sync(FULL_MASK, arc_i || arc_j)) {  // one vote on the common path
               const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
               const unsigned mj = __ballot_sync(FULL_MASK, arc_j);
@@ -1475,11 +1490,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
               if (arc_i)
                 ring_c[qt + __popc(mi & lt_c)] =
-                    make_uint4(cpos_c[k], bin | (half_i ? 0x80000000u : 0u), qlo, qhi);
+                    make_uint4(cpos_c[k], bin | (du > cmk.vt ? 0x80000000u : 0u), qlo, qhi);
               qt += __popc(mi);
               if (arc_j)
                 ring_c[qt + __popc(mj & lt_c)] =
-                    make_uint4(jpc, bin | (half_j ? 0x80000000u : 0u), qlo, qhi);
+                    make_uint4(jpc, bin | (du > nm.vt ? 0x80000000u : 0u), qlo, qhi);
               qt += __popc(mj);
             }
           };
@@ -1493,16 +1508,25 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             for (int k = kc; k < kend; ++k) pair_step(k);
           }
         };
-        // count-only loop when the item's centers and the tile's neighbours are
-        // all deep; else the weighted loop.  The own-cell ordering test only
-        // where some lane's neighbour shares the item's cell (tile_own).
-        const bool tile_deep_item = tile_deep && item_deep;
+        // count-only loop when no pair of the block can be weighted, else
+        // the loop with only the weight kinds that can occur (arcs near the
+        // region's boundary, v = 1/2 near the period's ends).  The own-cell
+        // ordering test only where some lane's neighbour shares the item's
+        // cell (tile_own).
+        using T_ = std::true_type;
+        using F_ = std::false_type;
         if (tile_own) {
-          if (tile_deep_item) chunk(std::true_type{}, std::true_type{});
-          else chunk(std::true_type{}, std::false_type{});
+          if (arc_any) {
+            if (half_any) chunk(T_{}, T_{}, T_{}); else chunk(T_{}, T_{}, F_{});
+          } else {
+            if (half_any) chunk(T_{}, F_{}, T_{}); else chunk(T_{}, F_{}, F_{});
+          }
         } else {
-          if (tile_deep_item) chunk(std::false_type{}, std::true_type{});
-          else chunk(std::false_type{}, std::false_type{});
+          if (arc_any) {
+            if (half_any) chunk(F_{}, T_{}, T_{}); else chunk(F_{}, T_{}, F_{});
+          } else {
+            if (half_any) chunk(F_{}, F_{}, T_{}); else chunk(F_{}, F_{}, F_{});
+          }
         }
         // advance: next chunk, next tile
         kc = kend;

@@ -185,8 +185,8 @@ struct Batch {
   uint32_t* task_counter;  // [0] dynamic task counter, [1] task_items, [2] parts per item
   // exact histograms [R][bins]
   unsigned long long* h_cnt;   // in-threshold pairs
-  unsigned long long* h_half;  // interior pairs with v = 1/2 (contribute 2)
-  unsigned long long* h_lo;    // arc-path sum of (1/w - 1), signed 128-bit fixed 53
+  unsigned long long* h_half;  // ordered pairs with v = 1/2 (each adds 1 more; arc terms are (1/omega - 1) / v)
+  unsigned long long* h_lo;    // arc-path sum of (1/omega - 1) / v, signed 128-bit fixed 53
   unsigned long long* h_hi;
   double* K;  // [R][bins]
   double* L;  // [R][bins]
