@@ -727,26 +727,6 @@ __device__ __forceinline__ double rect_single_edge_omega(double q, double2 rec) 
   return fma(theta, kArcC[14], 1.0);  // 1 - theta / pi
 }
 
-// rect_probe_certified for the arc running counter-clockwise from crossing
-// vector va to crossing vector vb (vectors from the center, length d): its
-// midpoint direction is the chord vb - va turned clockwise by 90 degrees, for
-// every arc length in (0, 2 pi).  The chord is formed in double (the crossing
-// vectors are accurate to ~1 ulp, and crossings are >= 2.5e-6 d apart) and
-// normalised in float: direction error ~2e-7 rad, well inside the 2e-6 d
-// certification margin.
-__device__ __forceinline__ int rect_probe_chord(double cx, double cy, double d, double vax,
-                                                double vay, double vbx, double vby,
-                                                const RegionView& R) {
-  const float mx = (float)(vby - vay), my = (float)(vax - vbx);
-  const float inv = rsqrtf(fmaf(mx, mx, my * my));
-  const double px = cx + d * (double)(mx * inv), py = cy + d * (double)(my * inv);
-  const double e = d * 2e-6 + 1e-12 * (R.maxabs + d + 1.0);
-  if (px >= R.xmin + e && px < R.xmax - e && py >= R.ymin + e && py < R.ymax - e) return 1;
-  const double o = e + R.box_m;
-  if (px < R.xmin - o || px > R.xmax + o || py < R.ymin - o || py > R.ymax + o) return 0;
-  return -1;
-}
-
 // spatial_isotropic_weight in closed form for a rectangle and a circle that
 // reaches several sides (corners; circles larger than the region).  For each
 // side within reach the reference's own quadratic decides accept / reject; an
@@ -757,9 +737,9 @@ __device__ __forceinline__ int rect_probe_chord(double cx, double cy, double d, 
 // single-side gates of rect_single_edge_omega for every accepted side, no side
 // rejected while its line is nearer than d (a tangency the reference drops),
 // and every corner between two sides within reach away from the circle by
-// |K - c|^2 - d^2 > 1e-5 d^2 — then crossings are 2.5e-6 d or more from the
-// segment ends and from each other, far above the reference's root error, and
-// its de-duplication keeps them all.  No crossing at all gives 1.0 (the
+// |g| = ||K - c|^2 - d^2| > 1e-4 d^2 — then crossings are 2.5e-5 d or more from
+// the segment ends and from each other, far above the reference's root error,
+// and its de-duplication keeps them all.  No crossing at all gives 1.0 (the
 // reference's rule when the circle contains the whole rectangle).
 //
 // The crossings come out in increasing angle without sorting: side s's
@@ -774,10 +754,26 @@ __device__ __forceinline__ int rect_probe_chord(double cx, double cy, double d, 
 // The theta sum is the argument of the product of (h_s + i w_s), w_s =
 // sqrt((d - h_s)(d + h_s)), one factor per end: one atan2 per pair instead of
 // one per side, with whole turns counted as the running product's imaginary
-// part turns non-negative again.  Each arc's midpoint
-// other than a side's own outside arc is classified by the certified probe
-// (rect_probe_chord) and must match the expected inside / outside pattern,
-// else -1.
+// part turns non-negative again.
+// The reference classifies each arc by a PIP probe at its midpoint, which its
+// crossing angles place within ~1e-11 d of the true midpoint; the corner gate
+// keeps every true midpoint farther than that (plus on_segment's 1e-12 scale)
+// from the boundary, so the probe returns the pattern above:
+//  * a side's own outside arc: beyond the side by d - h_s > 4 box_m (as in the
+//    single-side form);
+//  * an arc around a corner K inside the circle (its two ends dropped): outside,
+//    at least d - |K - c| > d (1 - sqrt(1 - 1e-4)) > 5e-5 d from the region;
+//  * an inside arc between sides s and s+1 around an outside corner: its ends
+//    P1, P2 lie g / (h + w) >= 5e-5 d from K along the sides, so its span is
+//    >= 7e-5 and its midpoint clears side s by 2 w_s sin(span / 4) >= 3.5e-8 d
+//    under the gate w >= 1e-3 d on every side with an end (likewise side
+//    s+1), and the two opposite sides by more than their distance h to the
+//    center (the midpoint lies in the quadrant between sides s and s+1).
+// With T = 1e-11 d + 4 box_m + 1e-12 (max|coord| + d + 1) the reference's
+// probe error plus every on_segment tolerance, the gates 3.5e-8 d > T and
+// min h > T leave each probe on the expected side.  (The round-1 form probed
+// every midpoint under a 1e-5 d^2 corner gate, where clearances fall to
+// ~1e-12 d.)
 // Results below 1e-3 go to the general routine (see the end).
 __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, double d,
                                                          const RegionView& R) {
@@ -815,6 +811,8 @@ __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, d
     acc |= 1u << s;
   }
   if (acc == 0) return 1.0;
+  const double T = 1e-11 * d + 4.0 * R.box_m + 1e-12 * (R.maxabs + d + 1.0);
+  if (!(3.5e-8 * d > T && fmin(fmin(h[0], h[1]), fmin(h[2], h[3])) > T)) return -1.0;
   // corner k sits between side k and side k+1 (counter-clockwise)
   unsigned cin = 0;
 #pragma unroll
@@ -822,7 +820,7 @@ __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, d
     const int k1 = (k + 1) & 3;
     if (!((inr >> k) & 1u) || !((inr >> k1) & 1u)) continue;  // beyond reach: outside
     const double g = h[k] * h[k] + h[k1] * h[k1] - r2;
-    if (fabs(g) <= 1e-5 * r2) return -1.0;
+    if (fabs(g) <= 1e-4 * r2) return -1.0;
     if (g < 0.0) cin |= 1u << k;
   }
   // crossing ends: slot 2s = side s's clockwise end (dropped when corner s-1
@@ -836,6 +834,9 @@ __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, d
   }
   if (E == 0) return 1.0;
   if (__popc(E) & 1) return -1.0;  // cannot happen (ends alternate); defensive
+#pragma unroll
+  for (int s = 0; s < 4; ++s)  // the inside-arc clearance gate (above)
+    if (((E >> (2 * s)) & 3u) && w[s] < 1e-3 * d) return -1.0;
   // theta sum = argument of prod_s (h_s + i w_s)^{c_s}, c_s = ends of side s;
   // each factor adds c_s * theta_s < pi, so whole turns show as the imaginary
   // part turning non-negative again
@@ -857,41 +858,7 @@ __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, d
     pr = nr;
     pim = ni;
   }
-  // probes, arc by arc in angular order (per-lane loop over the set slots):
-  // the arc from end i to the next end j is inside iff j is a clockwise end;
-  // a side's own outside arc (slots 2s -> 2s+1) needs no probe: its midpoint
-  // lies beyond side s by d - h_s > sw_margin, as in the single-side form
-  auto vec = [&](int k, double& vx, double& vy) {  // crossing vector of slot k
-    const int s = k >> 1;
-    const double hs = (s & 2) ? ((s & 1) ? h[3] : h[2]) : ((s & 1) ? h[1] : h[0]);
-    double ws = (s & 2) ? ((s & 1) ? w[3] : w[2]) : ((s & 1) ? w[1] : w[0]);
-    if (!(k & 1)) ws = -ws;  // (h, -w) clockwise, (h, w) counter-clockwise, turned by phi_s
-    const double x = (s & 1) ? -ws : hs, y = (s & 1) ? hs : ws;
-    vx = (s & 2) ? -x : x;
-    vy = (s & 2) ? -y : y;
-  };
-  const int i0 = __ffs(E) - 1;
-  const bool first_cw = !(i0 & 1);
-  double x0, y0;
-  vec(i0, x0, y0);
-  double xi = x0, yi = y0;
-  int i = i0;
-  unsigned rem = E & (E - 1);
-  int bad = 0;
-  for (;;) {
-    const bool last = rem == 0;
-    const int j = last ? i0 : __ffs(rem) - 1;
-    double xj = x0, yj = y0;
-    if (!last) vec(j, xj, yj);
-    if ((i & 1) || j != i + 1)
-      bad |= rect_probe_chord(cx, cy, d, xi, yi, xj, yj, R) != (int)!(j & 1);
-    if (last) break;
-    i = j;
-    xi = xj;
-    yi = yj;
-    rem &= rem - 1;
-  }
-  if (bad) return -1.0;
+  const bool first_cw = !((__ffs(E) - 1) & 1);  // the lowest end is a clockwise one
   const double kHalfPi = 1.57079632679489661923;
   double a = fast_atan2(pim, pr);
   if (a < 0.0) a += kTwoPi;

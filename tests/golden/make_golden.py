@@ -167,6 +167,50 @@ def rect_corner_stress():
     np.savez_compressed(os.path.join(OUT, "rect_corner.npz"), count=len(rects), **out)
 
 
+def rect_probe_free():
+    """Rectangle (center, d) cases at the boundaries of the multi-side closed
+    form's probe-free gates (stk_device.cuh rect_multi_edge_weight): corners at
+    |g| / d^2 around 1e-4 on both sides, crossing sides with w / d around 1e-3,
+    centers within 1e-9..1e-3 d of a side, thin rectangles, large offsets."""
+    rng = np.random.default_rng(23)
+    out = {}
+    rects = [(0.0, 0.0, 1000.0, 1000.0), (0.0, 0.0, 1000.0, 3.0),
+             (500000.0, 4000000.0, 501000.0, 4000700.0), (-50.0, -20.0, 50.0, 80.0)]
+    for k, (x0, y0, x1, y1) in enumerate(rects):
+        ring = np.array([[x0, y0], [x1, y0], [x1, y1], [x0, y1]], float)
+        W, H = x1 - x0, y1 - y0
+        corners = np.array([[x0, y0], [x1, y0], [x1, y1], [x0, y1]])
+        cx, cy, dd, ww = [], [], [], []
+        while len(cx) < 1200:
+            px = x0 + W * rng.uniform(0.0005, 0.9995)
+            py = y0 + H * rng.uniform(0.0005, 0.9995)
+            mode = rng.integers(4)
+            if mode == 0:    # |K - c|^2 - d^2 = +-eps d^2, eps around the 1e-4 gate
+                kd2 = np.sum((corners[rng.integers(4)] - [px, py]) ** 2)
+                eps = rng.choice([-1, 1]) * 10.0 ** rng.uniform(-5, -2)
+                d = np.sqrt(kd2 / (1.0 + eps))
+            elif mode == 1:  # a crossing side with w / d around 1e-3, plus larger circles
+                h = [px - x0, x1 - px, py - y0, y1 - py][rng.integers(4)]
+                wr = 10.0 ** rng.uniform(-4, -2)
+                d = h / np.sqrt(1.0 - wr * wr) * (rng.uniform(1.0, 3.0) if rng.random() < 0.2 else 1.0)
+            elif mode == 2:  # center within 1e-9..1e-3 d of a side, circle over corners
+                d = rng.uniform(0.3, 1.5) * np.hypot(W, H)
+                off = d * 10.0 ** rng.uniform(-9, -3)
+                side = rng.integers(4)
+                if side == 0: px = x0 + off
+                elif side == 1: px = x1 - off
+                elif side == 2: py = y0 + off
+                else: py = y1 - off
+            else:            # circles larger than the region
+                d = rng.uniform(0.5, 2.0) * np.hypot(W, H)
+            cx.append(px); cy.append(py); dd.append(d)
+            ww.append(ref.spatial_weight(px, py, d, ring))
+        out[f"{k}_ring"] = ring
+        out[f"{k}_cx"] = np.array(cx); out[f"{k}_cy"] = np.array(cy)
+        out[f"{k}_d"] = np.array(dd); out[f"{k}_w"] = np.array(ww)
+    np.savez_compressed(os.path.join(OUT, "rect_probe_free.npz"), count=len(rects), **out)
+
+
 def c1():
     """C1 (configs[0]) through the reference: K, per-bin counts, in_threshold."""
     cfg = configs.CONFIGS["C1"]
@@ -187,5 +231,10 @@ def mt():
 
 if __name__ == "__main__":
     oracle.build(with_ref=True)
-    sample(); polygons(); weights(); rect_stress(); rect_corner_stress(); c1(); mt()
+    only = sys.argv[1:]
+    jobs = dict(sample=sample, polygons=polygons, weights=weights, rect_stress=rect_stress,
+                rect_corner=rect_corner_stress, rect_probe_free=rect_probe_free, c1=c1, mt=mt)
+    for name, fn in jobs.items():
+        if not only or name in only:
+            fn()
     print("golden fixtures written to", OUT)
