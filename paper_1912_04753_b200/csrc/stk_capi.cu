@@ -877,7 +877,9 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
                                          B.stats + 5);
   CK(cudaGetLastError());
   ++c->launches;
-  scatter_kernel<<<gp, 256, 0, c->stream>>>(B, G, region_view(c), 0);
+  uint64_t qbits;
+  std::memcpy(&qbits, &c->Q.back(), 8);
+  scatter_kernel<<<gp, 256, 0, c->stream>>>(B, G, region_view(c), 0, (uint32_t)(qbits >> 32));
   CK(cudaGetLastError());
   ++c->launches;
   B.n_sel = std::min(n_sel, R);

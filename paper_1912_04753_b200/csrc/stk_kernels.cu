@@ -160,7 +160,11 @@ __global__ void csr_finish_kernel(Batch B, int p_first, RegionView reg, uint64_t
   uint64_t r = vt - q * ntl;
   if (r >= ntl) r -= ntl;
   B.t[o] = reg.p0 + (int64_t)r;
-  if (vt >= limit || !point_in_polygon(B.x[o], B.y[o], reg.ring, reg.nv)) B.flags[p] = 1;
+  // an axis-aligned rectangle contains its whole closed bounding box, and
+  // lo + RN((hi - lo) u) never leaves [lo, hi] (u < 1, RN monotone): only
+  // other rings need the reference's contains() check
+  if (vt >= limit || (!reg.rect && !point_in_polygon(B.x[o], B.y[o], reg.ring, reg.nv)))
+    B.flags[p] = 1;
 }
 
 // ---------------------------------------------------------- Philox (opt-in)
@@ -716,7 +720,9 @@ __device__ __forceinline__ uint32_t safe_hi(double v) {
   return v > 0.0 ? (uint32_t)__double2hiint(v) : 0u;
 }
 
-__global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first) {
+// qmax_hi: the high word of the largest in-threshold q; a point whose safe-q
+// word exceeds it is never an arc-pair center, so it gets no arc record.
+__global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first, uint32_t qmax_hi) {
   const int p = p_first + blockIdx.y;
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= B.n) return;
@@ -726,8 +732,8 @@ __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first) {
   const double x = B.x[o], y = B.y[o];
   const int64_t t = B.t[o];
   B.pxy[d] = make_double2(x, y);  // the input index travels in the meta record
-  if (B.parc) B.parc[d] = rect_arc_record(x, y, R);
   const uint32_t sq = R.no_safe ? 0u : safe_hi(safe_q(x, y, R));
+  if (B.parc && sq <= qmax_hi) B.parc[d] = rect_arc_record(x, y, R);
   const int64_t vt = min(t - R.p0, R.p1 - t);
   if (B.wide) {
     PtMeta<int64_t> m{t - R.p0, vt, sq, (uint32_t)i};
