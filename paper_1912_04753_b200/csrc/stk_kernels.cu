@@ -1281,6 +1281,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       }
       const uint32_t rowoff = my_rb - (incl - len);
       const uint32_t V = __shfl_sync(FULL_MASK, incl, 31);
+      // the own cell is the head of row 0: virtual indices [0, own_v) (the
+      // ordering rule applies there and nowhere else)
+      const uint32_t own_v = __shfl_sync(FULL_MASK, min(len, (uint32_t)max((int)own_end - (int)my_rb, 0)), 0);
       // part `part` of `np` walks virtual indices [V part / np, V (part + 1) / np)
       uint32_t v0 = (uint32_t)((uint64_t)V * part / np);
       const uint32_t v_hi = (uint32_t)((uint64_t)V * (part + 1) / np);
@@ -1345,17 +1348,14 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         if (kc == 0) {  // new tile: map the lanes to their rows (usually 1-2)
           const uint32_t v = v0 + (uint32_t)lane;
           unsigned m = __ballot_sync(FULL_MASK, len != 0 && incl > v0 && incl - len < v0 + 32u);
-          uint32_t off = 0, row0 = 0;
+          uint32_t off = 0;
           while (m) {
             const int rr = __ffs(m) - 1;
             m &= m - 1;
             const uint32_t e = __shfl_sync(FULL_MASK, incl, rr);
             const uint32_t st = e - __shfl_sync(FULL_MASK, len, rr);
             const uint32_t o = __shfl_sync(FULL_MASK, rowoff, rr);
-            if (v >= st && v < e) {
-              off = o;
-              row0 = rr == 0;
-            }
+            if (v >= st && v < e) off = o;
           }
           jp = v < v_hi ? v + off : 0xffffffffu;
           s_jp[tid] = jp;
@@ -1383,15 +1383,15 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           // owner <=> k < lim.x || center idx < lim.y.  Kept in shared memory
           // for the tile's chunks (with jp): the register allocator cannot
           // rebuild them inside the candidate loop
-          const uint32_t row0_end = __shfl_sync(FULL_MASK, incl, 0);  // row 0 = [0, len_0)
-          const bool same_c = v0 + (uint32_t)lane < row0_end && jp < own_end;
-          s_lim[tid] = make_uint2(same_c ? (sel_p ? 0u : jp - first_pos) : 0xffffffffu,
-                                  (sel_p && same_c) ? nm.idx : 0u);
-          __syncwarp();
+          if (v0 < own_v) {
+            const bool same_c = v0 + (uint32_t)lane < own_v && has;
+            s_lim[tid] = make_uint2(same_c ? (sel_p ? 0u : jp - first_pos) : 0xffffffffu,
+                                    (sel_p && same_c) ? nm.idx : 0u);
+            __syncwarp();
+          }
         }
         // some lane's neighbour lies in the item's own cell: the ordering rule applies
-        const bool tile_own =
-            __any_sync(FULL_MASK, *reinterpret_cast<volatile uint32_t*>(&s_lim[tid].x) != 0xffffffffu);
+        const bool tile_own = v0 < own_v;
         // ARC: some pair of the (item, tile) block can have omega != 1 (a
         // center or neighbour with safe radius < s_max); HALF: some can have
         // v = 1/2 (temporal threshold < t_max)
