@@ -1078,6 +1078,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   __shared__ uint4* s_ring[kPairWarps];
   __shared__ uint2 s_lim[kPairWarps * 32];  // per-tile owner limits (see below)
   __shared__ uint32_t s_jp[kPairWarps * 32];  // per-tile neighbour position of each lane
+  __shared__ uint2 s_cur[kPairWarps * 32];    // lane cursor: (virtual index, its row) of the next tile
   __shared__ uint32_t s_base;               // shared-space address of smem_raw
   __shared__ uint32_t s_arc_off;            // byte offset of the arc-sum section (runtime-sized)
   using Lay = PairLayout<TT>;
@@ -1289,6 +1290,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       const uint32_t v_hi = (uint32_t)((uint64_t)V * (part + 1) / np);
       // candidates of this unit: every (center, neighbour) of its tiles
       const unsigned long long n_cand = (unsigned long long)(v_hi - v0) * nc;
+      {  // lane cursor of the first tile: virtual index v0 + lane and its row
+         // (the number of rows ending at or before it; rows are in order)
+        const uint32_t v = v0 + (uint32_t)lane;
+        uint32_t row = 0;
+        for (int r = 0; r < nrows; ++r) row += __shfl_sync(FULL_MASK, incl, r) <= v ? 1u : 0u;
+        s_cur[tid] = make_uint2(v, row);
+      }
       uint32_t qh = 0, qt = 0;    // arc ring head / tail (monotone)
       uint32_t ch_ = 0, ct_ = 0;  // deferred ring head / tail
       uint32_t n_arc = 0;
@@ -1345,20 +1353,23 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           qt = pend;
         }
         uint32_t jp;
-        if (kc == 0) {  // new tile: map the lanes to their rows (usually 1-2)
-          const uint32_t v = v0 + (uint32_t)lane;
-          unsigned m = __ballot_sync(FULL_MASK, len != 0 && incl > v0 && incl - len < v0 + 32u);
-          uint32_t off = 0;
-          while (m) {
-            const int rr = __ffs(m) - 1;
-            m &= m - 1;
-            const uint32_t e = __shfl_sync(FULL_MASK, incl, rr);
-            const uint32_t st = e - __shfl_sync(FULL_MASK, len, rr);
-            const uint32_t o = __shfl_sync(FULL_MASK, rowoff, rr);
-            if (v >= st && v < e) off = o;
-          }
+        if (kc == 0) {  // new tile: the lane cursor's row gives the sorted position
+          const volatile uint32_t* cu = reinterpret_cast<volatile uint32_t*>(&s_cur[tid]);
+          const uint32_t v = cu[0];
+          uint32_t row = cu[1];
+          const uint32_t off = __shfl_sync(FULL_MASK, rowoff, row & 31u);  // every lane shuffles
           jp = v < v_hi ? v + off : 0xffffffffu;
           s_jp[tid] = jp;
+          // advance to the next tile: 32 virtual indices on, across row ends
+          // (rows of ~a few cells: usually one step for a few lanes)
+          const uint32_t nv = v + 32u;
+          for (;;) {
+            const uint32_t rend = __shfl_sync(FULL_MASK, incl, row & 31u);  // every lane shuffles
+            const bool adv = nv < v_hi && nv >= rend;
+            if (!__any_sync(FULL_MASK, adv)) break;
+            row += adv ? 1u : 0u;
+          }
+          s_cur[tid] = make_uint2(nv, row);
         } else {
           jp = *reinterpret_cast<volatile uint32_t*>(&s_jp[tid]);
         }
