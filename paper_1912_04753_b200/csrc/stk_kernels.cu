@@ -991,41 +991,55 @@ __device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, uint32_t sa
 // Ring entries: {center sorted position, bin | (v == 1/2) << 31, q = d^2 as
 // two words}, in the warp's rings (global, L1/L2-resident).
 //
-// Main ring, 32 entries at a time: rectangle entries that pass the closed
-// form's gate are weighted here; the rest (and every entry of a general
-// polygon) move to the warp's deferred ring, so the general routine runs on
-// full warps of entries that need it.
+// omega in [1/2, 1) from the closed form: the arc term (1/omega - 1) / v
+// (add_arc_term) times 2^53 is a non-negative integer <= 2^54, added to the
+// bin's 128-bit sum with two native 32-bit shared atomics and their carries (a
+// 64-bit shared atomic add is a compare-and-swap loop on sm_100).
+__device__ __forceinline__ void add_arc_term_closed(double ws, uint32_t bw, uint32_t sa_arc) {
+  const uint64_t v = (__double2ull_rn(rcp_pos(ws) * 0x1p53) - (1ULL << kFixedFracBits))
+                     << (bw >> 31);
+  const uint32_t a = sa_arc + (bw & 0x7fffffffu) * (uint32_t)sizeof(ArcSum);
+  const uint32_t v0 = (uint32_t)v;
+  uint32_t v1 = (uint32_t)(v >> 32), o0, o1;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o0) : "r"(a), "r"(v0) : "memory");
+  v1 += (o0 + v0 < o0) ? 1u : 0u;  // v1 <= 2^22: no overflow
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o1) : "r"(a + 4u), "r"(v1) : "memory");
+  if (o1 + v1 < o1) asm volatile("red.shared.add.u64 [%0], 1;" ::"r"(a + 8u) : "memory");
+}
+
+// Main ring, up to kMainDrain = 64 entries at a time, two per lane (their
+// closed forms interleave; the drain's fixed cost is paid once per 64):
+// rectangle entries that pass the closed form's gate are weighted here; the
+// rest (and every entry of a general polygon) move to the warp's deferred
+// ring, so the general routine runs on full warps of entries that need it.
+constexpr int kMainDrain = 64;
 template <bool RECT>
 __device__ __forceinline__ void drain_main(int count, int lane, const uint4* ring, uint32_t head,
                                            uint4* cring, uint32_t* ctail, unsigned lanemask_lt,
                                            const double2* parc, uint32_t sa_arc, uint32_t sa_ch,
                                            uint32_t* n_arc) {
-  const bool valid = lane < count;
-  uint4 e = make_uint4(0u, 0u, 0u, 0u);
-  double ws = -1.0;
-  if (valid) {
-    e = ring[(head + lane) & (kArcRing - 1)];
-    if (RECT) ws = rect_single_edge_omega(__hiloint2double((int)e.w, (int)e.z), parc[e.x]);
+  const bool valid0 = lane < count, valid1 = lane + 32 < count;
+  uint4 e0 = make_uint4(0u, 0u, 0u, 0u), e1 = e0;
+  double ws0 = -1.0, ws1 = -1.0;
+  if (valid0) e0 = ring[(head + lane) & (kArcRing - 1)];
+  if (valid1) e1 = ring[(head + 32 + lane) & (kArcRing - 1)];
+  if (RECT) {
+    if (valid0) ws0 = rect_single_edge_omega(__hiloint2double((int)e0.w, (int)e0.z), parc[e0.x]);
+    if (valid1) ws1 = rect_single_edge_omega(__hiloint2double((int)e1.w, (int)e1.z), parc[e1.x]);
   }
-  const bool defer = valid && ws < 0.0;
-  const unsigned m = __ballot_sync(FULL_MASK, defer);
-  if (defer) cring[(*ctail + __popc(m & lanemask_lt)) & (kCplxRing - 1)] = e;
-  *ctail += __popc(m);
-  if (valid && !defer) {
-    // omega in [1/2, 1): the arc term (1/omega - 1) / v (add_arc_term) times
-    // 2^53 is a non-negative integer <= 2^54; added to the bin's 128-bit sum
-    // with two native 32-bit shared atomics and their carries (a 64-bit
-    // shared atomic add is a compare-and-swap loop on sm_100)
+  const bool defer0 = valid0 && ws0 < 0.0, defer1 = valid1 && ws1 < 0.0;
+  const unsigned m0 = __ballot_sync(FULL_MASK, defer0), m1 = __ballot_sync(FULL_MASK, defer1);
+  if (defer0) cring[(*ctail + __popc(m0 & lanemask_lt)) & (kCplxRing - 1)] = e0;
+  *ctail += __popc(m0);
+  if (defer1) cring[(*ctail + __popc(m1 & lanemask_lt)) & (kCplxRing - 1)] = e1;
+  *ctail += __popc(m1);
+  if (valid0 && !defer0) {
     ++*n_arc;
-    const uint64_t v = (__double2ull_rn(rcp_pos(ws) * 0x1p53) - (1ULL << kFixedFracBits))
-                       << (e.y >> 31);
-    const uint32_t a = sa_arc + (e.y & 0x7fffffffu) * (uint32_t)sizeof(ArcSum);
-    const uint32_t v0 = (uint32_t)v;
-    uint32_t v1 = (uint32_t)(v >> 32), o0, o1;
-    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o0) : "r"(a), "r"(v0) : "memory");
-    v1 += (o0 + v0 < o0) ? 1u : 0u;  // v1 <= 2^22: no overflow
-    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o1) : "r"(a + 4u), "r"(v1) : "memory");
-    if (o1 + v1 < o1) asm volatile("red.shared.add.u64 [%0], 1;" ::"r"(a + 8u) : "memory");
+    add_arc_term_closed(ws0, e0.y, sa_arc);
+  }
+  if (valid1 && !defer1) {
+    ++*n_arc;
+    add_arc_term_closed(ws1, e1.y, sa_arc);
   }
 }
 
@@ -1305,10 +1319,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
       for (;;) {
         const bool done = v0 >= v_hi;
         // the single drain site, ahead of new candidates so the ring never
-        // holds more than 31 + kArcChunk * 64 entries: full batches while
+        // holds more than 63 + kArcChunk * 64 entries: full batches while
         // any are pending, and the remainder at the end
         const uint32_t pending = qt - qh, cpending = ct_ - ch_;
-        // deferred entries first (<= 31 + 32 pending), then the main ring
+        // deferred entries first (<= 31 + 64 pending), then the main ring
         if (cpending >= 32 || (done && pending == 0 && cpending > 0)) {
           const int cnt_ = (int)min(cpending, 32u);
           __syncwarp();
@@ -1322,10 +1336,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           ch_ += (uint32_t)cnt_;
           continue;
         }
-        if (pending >= 32 || (done && pending > 0)) {
-          // <= 31 + kArcChunk * 64 by construction; checked here, off the hot path
+        if (pending >= (uint32_t)kMainDrain || (done && pending > 0)) {
+          // <= 63 + kArcChunk * 64 by construction; checked here, off the hot path
           if (pending > (uint32_t)kArcRing) ring_ovf = true;  // reported as an error
-          const int cnt_ = (int)min(pending, 32u);
+          const int cnt_ = (int)min(pending, (uint32_t)kMainDrain);
           __syncwarp();
           uint4* const arcq = *reinterpret_cast<uint4* volatile*>(&s_ring[w]);
           const uint32_t sb_ = *reinterpret_cast<volatile uint32_t*>(&s_base);
@@ -1337,16 +1351,19 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         }
         if (done) break;
         if (qh != 0) {
-          // fewer than 32 entries pending: move them to the ring's front so
-          // the ring's working set stays its first ~2 KB (L1/L2-resident)
-          // instead of cycling all kArcRing entries through DRAM.  qh is a
-          // multiple of 32 > pending, so source and destination are disjoint
+          // fewer than kMainDrain entries pending: move them to the ring's
+          // front so the ring's working set stays its first few KB (L1/L2-
+          // resident) instead of cycling all kArcRing entries through DRAM.
+          // qh is a multiple of kMainDrain > pending, so source and
+          // destination are disjoint
           const uint32_t pend = qt - qh;
           uint4* const arcq = *reinterpret_cast<uint4* volatile*>(&s_ring[w]);
-          uint4 e = make_uint4(0, 0, 0, 0);
+          uint4 e = make_uint4(0, 0, 0, 0), f = e;
           if ((uint32_t)lane < pend) e = arcq[qh + lane];
+          if ((uint32_t)lane + 32u < pend) f = arcq[qh + 32 + lane];
           __syncwarp();
           if ((uint32_t)lane < pend) arcq[lane] = e;
+          if ((uint32_t)lane + 32u < pend) arcq[32 + lane] = f;
           __syncwarp();
           if (lane == 0) tot_exact += qh;
           qh = 0;
@@ -1502,8 +1519,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             if (__any_sync(FULL_MASK, arc_i || arc_j)) {  // one vote on the common path
               const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
               const unsigned mj = __ballot_sync(FULL_MASK, arc_j);
-              // no wrap: a chunk starts with < 32 entries (compaction) and adds
-              // <= kArcChunk * 64, below kArcRing (static_assert in stk_types.h)
+              // no wrap: a chunk starts with < kMainDrain entries (compaction) and
+              // adds <= kArcChunk * 64, below kArcRing (static_assert in stk_types.h)
               const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
               if (arc_i)
                 ring_c[qt + __popc(mi & lt_c)] =

@@ -44,9 +44,9 @@ constexpr int kFixedFracBits = 53;  // fixed-point weighted sums: value * 2^53 (
 #ifndef STK_ARC_RING
 #define STK_ARC_RING 4096
 #endif
-constexpr int kArcRing = STK_ARC_RING;  // per-warp arc ring entries (> 31 + kArcChunk * 64)
-static_assert(kArcRing > 31 + kArcChunk * 64, "the arc ring must hold a chunk's entries");
-constexpr int kCplxRing = 128;      // per-warp ring of entries deferred to the general weight (> 63)
+constexpr int kArcRing = STK_ARC_RING;  // per-warp arc ring entries (> 63 + kArcChunk * 64)
+static_assert(kArcRing > 63 + kArcChunk * 64, "the arc ring must hold a chunk's entries");
+constexpr int kCplxRing = 128;      // per-warp ring of entries deferred to the general weight (> 31 + 64)
 
 // Study region on the device (geom::StudyRegion, geometry.hpp:95-120).
 struct RegionView {
