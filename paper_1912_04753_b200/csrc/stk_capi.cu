@@ -2080,7 +2080,9 @@ int stk_spatial_weights(stk_ctx* c, const double* cx, const double* cy, const do
     CK(cudaStreamSynchronize(c->stream));
     b.release();
     if (bad != ~0ULL) throw InvalidArg("weight center outside study region");
-    if (ovf) throw Unsupported("more than 64 circle/boundary crossings in one edge weight");
+    // only spatial_weight_ring (rectangles, <= 8 crossings) can set it: a
+    // 64-entry buffer overflow there is an internal error, not a user input
+    if (ovf) throw CudaFail("internal error: crossing buffer overflow in the rectangle edge weight");
   });
 }
 
