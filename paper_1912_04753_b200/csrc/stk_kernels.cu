@@ -979,8 +979,20 @@ __device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, uint32_t sa
     hi = (hi << 1) | (lo >> 63);
     lo <<= 1;
   }
-  if (lo | hi) {
-    const uint32_t a = sa_arc + bin * (uint32_t)sizeof(ArcSum);
+  if ((lo | hi) == 0) return;  // omega == 1 exactly (entries at the safe radius)
+  const uint32_t a = sa_arc + bin * (uint32_t)sizeof(ArcSum);
+  if (hi == 0) {  // the usual term: below 2^64, non-negative — native 32-bit atomics
+    const uint32_t v0 = (uint32_t)lo;
+    uint32_t v1 = (uint32_t)(lo >> 32), o0, o1;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o0) : "r"(a), "r"(v0) : "memory");
+    const uint32_t c0 = (o0 + v0 < o0) ? 1u : 0u;
+    const uint32_t add1 = v1 + c0;  // wraps to 0 only for v1 = 2^32 - 1 with a carry
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o1) : "r"(a + 4u), "r"(add1) : "memory");
+    if (o1 + add1 < o1 || (add1 < c0))
+      asm volatile("red.shared.add.u64 [%0], 1;" ::"r"(a + 8u) : "memory");
+    return;
+  }
+  {
     unsigned long long old;
     asm volatile("atom.shared.add.u64 %0, [%1], %2;" : "=l"(old) : "r"(a), "l"(lo) : "memory");
     if (old + lo < old) ++hi;
