@@ -216,7 +216,7 @@ struct stk_ctx {
   DevBuf<double2> pxy;
   DevBuf<double2> parc;  // rectangles: per sorted point arc record (Batch::parc)
   DevBuf<unsigned char> pmeta;
-  DevBuf<uint32_t> key, rank, cell_count, cell_start, item_start, task_start, task_counter;
+  DevBuf<uint32_t> key, rank, sidx, cell_count, cell_start, item_start, task_start, task_counter;
   DevBuf<uint2> items;
   DevBuf<uint32_t> sel_start, center_pos;
   DevBuf<uint4> arcq;
@@ -608,7 +608,7 @@ Plan make_plan(stk_ctx* c, uint64_t n, uint64_t patterns) {
   P.G = make_grid_geom(c, n);
   P.bins = (uint32_t)(c->s_values.size() * c->t_values.size());
   P.max_items = (uint32_t)((n + kItemCenters - 1) / kItemCenters + P.G.cells);
-  const uint64_t per = n * (8 * 3 + 16 + 16 + 24 + 4 * 4) + (uint64_t)(P.G.cells + 1) * 4 * 3 +
+  const uint64_t per = n * (8 * 3 + 16 + 16 + 24 + 4 * 5) + (uint64_t)(P.G.cells + 1) * 4 * 3 +
                        (uint64_t)P.max_items * 8 + (uint64_t)P.bins * 8 * 6 + 64;
   uint64_t R = std::max<uint64_t>(1, c->mem_budget / per);
   R = std::min<uint64_t>(R, std::max<uint64_t>(patterns, 1));
@@ -631,6 +631,7 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   c->pmeta.ensure(R * n * (wide ? sizeof(PtMeta<int64_t>) : sizeof(PtMeta<int32_t>)));
   c->key.ensure(R * n);
   c->rank.ensure(R * n);
+  c->sidx.ensure(R * n);
   c->cell_count.ensure(R * P.G.cells);
   c->cell_start.ensure(R * (P.G.cells + 1));
   c->item_start.ensure(R * (P.G.cells + 1));
@@ -654,6 +655,7 @@ Batch alloc_batch(stk_ctx* c, const Plan& P) {
   B.wide = wide;
   B.key = c->key.p;
   B.rank = c->rank.p;
+  B.perm = c->sidx.p;
   B.cell_count = c->cell_count.p;
   B.cell_start = c->cell_start.p;
   B.item_start = c->item_start.p;
@@ -877,9 +879,12 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
                                          B.stats + 5);
   CK(cudaGetLastError());
   ++c->launches;
+  place_kernel<<<gp, 256, 0, c->stream>>>(B, G, 0);
+  CK(cudaGetLastError());
+  ++c->launches;
   uint64_t qbits;
   std::memcpy(&qbits, &c->Q.back(), 8);
-  scatter_kernel<<<gp, 256, 0, c->stream>>>(B, G, region_view(c), 0, (uint32_t)(qbits >> 32));
+  gather_kernel<<<gp, 256, 0, c->stream>>>(B, region_view(c), 0, (uint32_t)(qbits >> 32));
   CK(cudaGetLastError());
   ++c->launches;
   B.n_sel = std::min(n_sel, R);
@@ -1411,7 +1416,7 @@ void stk_destroy(stk_ctx* c) {
   c->d_ring.release(); c->d_Q.release(); c->d_s.release(); c->d_T.release();
   c->d_qtab.release(); c->d_ttab.release();
   c->x.release(); c->y.release(); c->t.release();
-  c->pxy.release(); c->parc.release(); c->pmeta.release(); c->key.release(); c->rank.release();
+  c->pxy.release(); c->parc.release(); c->pmeta.release(); c->key.release(); c->rank.release(); c->sidx.release();
   c->cell_count.release(); c->cell_start.release(); c->item_start.release();
   c->task_start.release(); c->task_counter.release(); c->items.release();
   c->hist.release(); c->stats.release(); c->bad.release(); c->K.release(); c->L.release();

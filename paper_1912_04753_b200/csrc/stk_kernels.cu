@@ -4,7 +4,7 @@
 //       device MT19937-64 point generators, bit-identical to
 //       sim::generate_cstr / generate_bootstrap / generate_permutation
 //       (proj/core/src/simulation.cpp:10-53, proj/core/include/stripley/rng.hpp:10-40)
-//   K1  key_kernel -> scan_kernel -> scatter_kernel -> items_kernel -> tasks_kernel
+//   K1  key_kernel -> scan_kernel -> place_kernel -> gather_kernel -> items_kernel -> tasks_kernel
 //       counting-sort uniform space-time grid (replaces STRTree::build/range_query,
 //       proj/core/src/st_index.cpp:54-130)
 //   K2  pair_kernel: all in-threshold ordered pairs, exact bins, edge weights,
@@ -720,15 +720,28 @@ __device__ __forceinline__ uint32_t safe_hi(double v) {
   return v > 0.0 ? (uint32_t)__double2hiint(v) : 0u;
 }
 
-// qmax_hi: the high word of the largest in-threshold q; a point whose safe-q
-// word exceeds it is never an arc-pair center, so it gets no arc record.
-__global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first, uint32_t qmax_hi) {
+// Counting sort, pass 2a: each point's sorted position (its cell's start plus
+// its rank) receives the point's input index (4-byte scattered writes).
+__global__ void place_kernel(Batch B, GridGeom G, int p_first) {
   const int p = p_first + blockIdx.y;
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= B.n) return;
   const uint64_t o = (uint64_t)p * B.n + i;
   const uint32_t pos = B.cell_start[(uint64_t)p * (G.cells + 1) + B.key[o]] + B.rank[o];
-  const uint64_t d = (uint64_t)p * B.n + pos;
+  B.perm[(uint64_t)p * B.n + pos] = (uint32_t)i;
+}
+
+// Pass 2b: the sorted records, written in sorted order (coalesced) from
+// gathered input points.  qmax_hi: the high word of the largest in-threshold q;
+// a point whose safe-q word exceeds it is never an arc-pair center, so it gets
+// no arc record.
+__global__ void gather_kernel(Batch B, RegionView R, int p_first, uint32_t qmax_hi) {
+  const int p = p_first + blockIdx.y;
+  const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (j >= B.n) return;
+  const uint64_t d = (uint64_t)p * B.n + j;
+  const uint32_t i = B.perm[d];
+  const uint64_t o = (uint64_t)p * B.n + i;
   const double x = B.x[o], y = B.y[o];
   const int64_t t = B.t[o];
   B.pxy[d] = make_double2(x, y);  // the input index travels in the meta record
@@ -736,11 +749,12 @@ __global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first, u
   if (B.parc && sq <= qmax_hi) B.parc[d] = rect_arc_record(x, y, R);
   const int64_t vt = min(t - R.p0, R.p1 - t);
   if (B.wide) {
-    PtMeta<int64_t> m{t - R.p0, vt, sq, (uint32_t)i};
+    PtMeta<int64_t> m{t - R.p0, vt, sq, i};
     reinterpret_cast<PtMeta<int64_t>*>(B.pmeta)[d] = m;
   } else {
-    PtMeta<int32_t> m{(int32_t)(t - R.p0), (int32_t)vt, sq, (uint32_t)i};
-    reinterpret_cast<PtMeta<int32_t>*>(B.pmeta)[d] = m;
+    const PtMeta<int32_t> m{(int32_t)(t - R.p0), (int32_t)vt, sq, i};
+    *reinterpret_cast<uint4*>(reinterpret_cast<PtMeta<int32_t>*>(B.pmeta) + d) =
+        make_uint4((uint32_t)m.t, (uint32_t)m.vt, m.sqh, m.idx);
   }
 }
 
@@ -751,7 +765,7 @@ __device__ __forceinline__ uint32_t sorted_input_index(const Batch& B, uint64_t 
 }
 
 // Center selection (patterns [0, n_sel)): count selected centers per cell.
-// Runs after scatter, so rank[] (per sorted position now) is free to reuse.
+// Runs after the gather, so rank[] (per sorted position now) is free to reuse.
 __device__ __forceinline__ bool selected(const Batch& B, uint32_t i) {
   return i >= B.c0 && i < B.c1 && (i % B.nshards) == B.shard;
 }

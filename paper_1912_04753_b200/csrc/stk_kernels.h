@@ -52,7 +52,8 @@ __global__ void scan_kernel(const uint32_t* counts, uint32_t* start, uint32_t* i
                             uint32_t cells, unsigned long long* max_cell);
 __global__ void select_count_kernel(Batch B, GridGeom G);
 __global__ void select_scatter_kernel(Batch B, GridGeom G);
-__global__ void scatter_kernel(Batch B, GridGeom G, RegionView R, int p_first, uint32_t qmax_hi);
+__global__ void place_kernel(Batch B, GridGeom G, int p_first);
+__global__ void gather_kernel(Batch B, RegionView R, int p_first, uint32_t qmax_hi);
 __global__ void items_kernel(Batch B, GridGeom G, int p_first);
 __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas);
 // mode = rect | single_step << 1 (kernel template flags)

@@ -167,6 +167,7 @@ struct Batch {
   int wide;       // study period >= 2^31 time units: 64-bit relative times
   uint32_t* key;  // cell key per unsorted point
   uint32_t* rank; // rank within the cell per unsorted point
+  uint32_t* perm; // input index per sorted position (counting sort pass 2)
   uint32_t* cell_count;  // [R][cells]
   uint32_t* cell_start;  // [R][cells+1]
   uint32_t* item_start;  // [R][cells+1] exclusive scan of ceil(count/32)
