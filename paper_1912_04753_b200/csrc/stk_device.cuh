@@ -881,6 +881,12 @@ __device__ __forceinline__ double rect_multi_edge_weight(double cx, double cy, d
 // nearest distance is >= min(listed nearest, ec_reach) and the radius below
 // stays a lower bound.
 __device__ __forceinline__ double safe_q(double cx, double cy, const RegionView& R) {
+  if (R.rect) {  // the nearest boundary point of a rectangle lies on a side's perpendicular
+    const double rs = fmin(fmin(cx - R.xmin, R.xmax - cx), fmin(cy - R.ymin, R.ymax - cy));
+    const double scale = fmax(R.maxabs, fmax(fabs(cx), fabs(cy)));
+    const double r_ok = rs - 1e-6 * (rs + scale);
+    return r_ok > 0.0 ? r_ok * r_ok * (1.0 - 1e-9) : -1.0;
+  }
   const double2* ring = R.ring;
   const uint32_t nv = R.nv;
   double r2 = 1.0e308;
