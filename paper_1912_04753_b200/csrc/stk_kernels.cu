@@ -1116,6 +1116,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   // allocator (it otherwise rebuilds them from special registers every
   // iteration)
   __shared__ uint4* s_ring[kPairWarps];
+  __shared__ const double2* s_nxy[kPairWarps];     // the unit's pattern: B.pxy + pb
+  __shared__ const PtMeta<TT>* s_nmeta[kPairWarps];  // ... and its meta records
   __shared__ uint2 s_lim[kPairWarps * 32];  // per-tile owner limits (see below)
   __shared__ uint32_t s_jp[kPairWarps * 32];  // per-tile neighbour position of each lane
   __shared__ uint2 s_cur[kPairWarps * 32];    // lane cursor: (virtual index, its row) of the next tile
@@ -1337,6 +1339,12 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         for (int r = 0; r < nrows; ++r) row += __shfl_sync(FULL_MASK, incl, r) <= v ? 1u : 0u;
         s_cur[tid] = make_uint2(v, row);
       }
+      if (lane == 0) {  // the pattern's sorted arrays, read back per tile (no 64-bit
+                        // base arithmetic, nothing held in registers across the loop)
+        s_nxy[w] = B.pxy + pb;
+        s_nmeta[w] = pmeta_b + pb;
+      }
+      __syncwarp();
       uint32_t qh = 0, qt = 0;    // arc ring head / tail (monotone)
       uint32_t ch_ = 0, ct_ = 0;  // deferred ring head / tail
       uint32_t n_arc = 0;
@@ -1422,15 +1430,16 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         const bool has = jp != 0xffffffffu;
         double2 nxy = make_double2(1e300, 1e300);  // no neighbour: q = inf > Qmax
         PtMeta<TT> nm{0, 0, 0u, 0u};
+        const double2* const nxy_p = *reinterpret_cast<const double2* const volatile*>(&s_nxy[w]);
+        const PtMeta<TT>* const nmeta_p =
+            *reinterpret_cast<const PtMeta<TT>* const volatile*>(&s_nmeta[w]);
         if (has) {
-          nxy = B.pxy[pb + jp];
-          nm = ld_meta<TT>(pmeta_b + pb + jp);
+          nxy = nxy_p[jp];
+          nm = ld_meta<TT>(nmeta_p + jp);
         }
         if (kc == 0) {
-          if (has && jp + 32 < (uint32_t)B.n) {  // the lane's likely next neighbour into L1
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(B.pxy + (pb + jp + 32)));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(pmeta_b + (pb + jp + 32)));
-          }
+          // (an L1 prefetch of the lane's next-tile neighbour cost 0.9%: the
+          // neighbour tiles stream from L2 fast enough, and the issue slots count)
           // own-cell rule: lower sorted position owns the pair — center k sits
           // at first_pos + k, so "jp > its position" is "k < jp - first_pos";
           // selected centers (shards) compare input indices instead:
@@ -1482,9 +1491,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           [[maybe_unused]] const uint32_t a_t = sbase + (uint32_t)Lay::ttab;  // table t bins
           const uint32_t a_ch = sbase + (uint32_t)Lay::ch;
           const uint32_t bins4 = bins * 4u;
-          auto pair_step = [&](int k) {
-            const double2 c = lds_f64x2(a_cxy + k * (uint32_t)sizeof(double2));  // center k
-            const PtMeta<TT> cmk = lds_meta<TT>(a_cm + k * (uint32_t)sizeof(PtMeta<TT>));
+          // center k at byte offset ka = 16 k of the coordinate section (the
+          // loop steps the offset: no index arithmetic per iteration)
+          auto pair_step = [&](uint32_t ka) {
+            const uint32_t k = ka >> 4;
+            const double2 c = lds_f64x2(a_cxy + ka);  // center k
+            const PtMeta<TT> cmk = lds_meta<TT>(
+                a_cm + (sizeof(PtMeta<TT>) == 16 ? ka : k * (uint32_t)sizeof(PtMeta<TT>)));
             const double dx = c.x - nxy.x, dy = c.y - nxy.y;
             const double q = dx * dx + dy * dy;  // spatial_distance^2, no FMA
             TT du = cmk.t - nm.t;
@@ -1562,10 +1575,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           // iterations per trip overlap their FP64 chains (experiment knob)
           if constexpr (DEEP) {
 #pragma unroll kDeepUnroll
-            for (int k = kc; k < kend; ++k) pair_step(k);
+            for (uint32_t ka = 16u * kc; ka < 16u * kend; ka += 16u) pair_step(ka);
           } else {
 #pragma unroll 1  // unrolling costs registers and I-cache (measured: 2x -> +25%)
-            for (int k = kc; k < kend; ++k) pair_step(k);
+            for (uint32_t ka = 16u * kc; ka < 16u * kend; ka += 16u) pair_step(ka);
           }
         };
         // count-only loop when no pair of the block can be weighted, else
