@@ -1460,6 +1460,75 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         // v = 1/2 (temporal threshold < t_max)
         const bool arc_any = !(item_sp && __all_sync(FULL_MASK, !has || nm.sqh > Qmax_hi));
         const bool half_any = !(item_tm && __all_sync(FULL_MASK, !has || nm.vt >= Tmax));
+        if constexpr (TUNI) {
+          // Two count-only tiles at once: when this tile and the next are both
+          // count-only and outside the own cell, each lane holds two
+          // neighbours and every center iteration tests both (the center loads,
+          // the loop control and the tile start are paid once per 64
+          // candidates)
+          if (kc == 0 && !tile_own && !arc_any && !half_any) {
+            const volatile uint32_t* cu = reinterpret_cast<volatile uint32_t*>(&s_cur[tid]);
+            const uint32_t v2 = cu[0];
+            uint32_t row2 = cu[1];
+            const uint32_t off2 = __shfl_sync(FULL_MASK, rowoff, row2 & 31u);
+            const uint32_t jp2 = v2 < v_hi ? v2 + off2 : 0xffffffffu;
+            const bool has2 = jp2 != 0xffffffffu;
+            double2 nxy2 = make_double2(1e300, 1e300);
+            PtMeta<TT> nm2{0, 0, 0u, 0u};
+            if (has2) {
+              nxy2 = nxy_p[jp2];
+              nm2 = ld_meta<TT>(nmeta_p + jp2);
+            }
+            const bool deep2 = __any_sync(FULL_MASK, has2) && v0 + 32u >= own_v &&
+                               __all_sync(FULL_MASK, !has2 || (nm2.sqh > Qmax_hi && nm2.vt >= Tmax));
+            if (deep2) {
+              uint32_t tidv;
+              asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tidv));
+              const uint32_t wo = (tidv >> 5) * 32;
+              const uint32_t sbase = *reinterpret_cast<volatile uint32_t*>(&s_base);
+              const uint32_t a_cxy = sbase + (uint32_t)Lay::cxy + wo * (uint32_t)sizeof(double2);
+              const uint32_t a_cm = sbase + (uint32_t)Lay::cmeta + wo * (uint32_t)sizeof(PtMeta<TT>);
+              const uint32_t a_q = sbase + (uint32_t)Lay::qtab;
+              auto count_pair = [&](double q, TT du) {
+                if (q <= Qmax && du <= Tmax) {
+                  const uint32_t qh = (uint32_t)__double2hiint(q);
+                  const int bq = max((int)(qh >> q_shift) - q_base, 0);
+                  const QEntry qe = lds_qentry(a_q + (uint32_t)bq * (uint32_t)sizeof(QEntry));
+                  const int32_t x = max((int32_t)du + t_add, t_lo);
+                  const uint32_t tb = __umulhi((uint32_t)x, t_magic) >> t_sh;
+                  reds_add_u32((q > qe.thr ? qe.hi : qe.lo) + tb * 4u, 1u);
+                }
+              };
+              for (uint32_t ka = 0; ka < 16u * nc; ka += 16u) {
+                const double2 c = lds_f64x2(a_cxy + ka);
+                TT tc;
+                if constexpr (sizeof(TT) == 4) {
+                  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tc) : "r"(a_cm + ka));
+                } else {
+                  tc = lds_meta<TT>(a_cm + (ka >> 4) * (uint32_t)sizeof(PtMeta<TT>)).t;
+                }
+                const double dx = c.x - nxy.x, dy = c.y - nxy.y;
+                const double dx2 = c.x - nxy2.x, dy2 = c.y - nxy2.y;
+                TT du = tc - nm.t, du2 = tc - nm2.t;
+                du = du < 0 ? -du : du;
+                du2 = du2 < 0 ? -du2 : du2;
+                count_pair(dx * dx + dy * dy, du);
+                count_pair(dx2 * dx2 + dy2 * dy2, du2);
+              }
+              // the cursor past the second tile
+              const uint32_t nv = v2 + 32u;
+              for (;;) {
+                const uint32_t rend = __shfl_sync(FULL_MASK, incl, row2 & 31u);
+                const bool adv = nv < v_hi && nv >= rend;
+                if (!__any_sync(FULL_MASK, adv)) break;
+                row2 += adv ? 1u : 0u;
+              }
+              s_cur[tid] = make_uint2(nv, row2);
+              v0 += 64;
+              continue;
+            }
+          }
+        }
         const int kend = min(kc + kArcChunk, (int)nc);
         auto chunk = [&](auto own_tag, auto arc_tag, auto half_tag) {
           constexpr bool OWN = decltype(own_tag)::value;
