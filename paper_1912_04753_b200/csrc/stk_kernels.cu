@@ -976,12 +976,13 @@ size_t pair_kernel_smem(uint32_t bins, int wide) {
 // (1/omega - 1) / v as a signed 128-bit fixed-point integer (53 fractional
 // bits, two's complement, carry detected on the low word): 1/omega - 1 exactly
 // (fixed_term_minus_one), doubled by a shift for v = 1/2 (1/(omega/2) rounds to
-// exactly 2 RN(1/omega)).  bw = bin | (v == 1/2) << 31.
-// sa_arc / sa_ch: shared-space addresses of the arc-sum and count sections.
+// exactly 2 RN(1/omega)).  bw = (shared-space address of the bin's count) |
+// (v == 1/2) << 31.  sa_arc / sa_ch: shared-space addresses of the arc-sum and
+// count sections.
 __device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, uint32_t sa_arc,
                                              uint32_t sa_ch, uint32_t* n_arc) {
   if (ws != 1.0) ++*n_arc;  // omega != 1 (SURVEY's arc-pair definition)
-  const uint32_t bin = bw & 0x7fffffffu;
+  const uint32_t bin = ((bw & 0x7fffffffu) - sa_ch) >> 2;
   if (ws == 0.0) {  // omega == 0: the reference adds 1/0 = inf and its bin ends NaN
     // bit 31 of the bin's pair count (< 2^31 per task): "infinite term"
     asm volatile("red.shared.or.b32 [%0], 0x80000000;" ::"r"(sa_ch + bin * 4u));
@@ -1014,17 +1015,20 @@ __device__ __forceinline__ void add_arc_term(double ws, uint32_t bw, uint32_t sa
   }
 }
 
-// Ring entries: {center sorted position, bin | (v == 1/2) << 31, q = d^2 as
-// two words}, in the warp's rings (global, L1/L2-resident).
+// Ring entries: {center sorted position, shared-space address of the bin's
+// count | (v == 1/2) << 31, q = d^2 as two words}, in the warp's rings (global,
+// L1/L2-resident).
 //
 // omega in [1/2, 1) from the closed form: the arc term (1/omega - 1) / v
 // (add_arc_term) times 2^53 is a non-negative integer <= 2^54, added to the
 // bin's 128-bit sum with two native 32-bit shared atomics and their carries (a
 // 64-bit shared atomic add is a compare-and-swap loop on sm_100).
-__device__ __forceinline__ void add_arc_term_closed(double ws, uint32_t bw, uint32_t sa_arc) {
+__device__ __forceinline__ void add_arc_term_closed(double ws, uint32_t bw, uint32_t sa_arc,
+                                                    uint32_t sa_ch) {
   const uint64_t v = (__double2ull_rn(rcp_pos(ws) * 0x1p53) - (1ULL << kFixedFracBits))
                      << (bw >> 31);
-  const uint32_t a = sa_arc + (bw & 0x7fffffffu) * (uint32_t)sizeof(ArcSum);
+  // the count address sa_ch + 4 bin -> the arc sum's sa_arc + 16 bin
+  const uint32_t a = sa_arc + ((bw & 0x7fffffffu) - sa_ch) * 4u;
   const uint32_t v0 = (uint32_t)v;
   uint32_t v1 = (uint32_t)(v >> 32), o0, o1;
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o0) : "r"(a), "r"(v0) : "memory");
@@ -1061,11 +1065,11 @@ __device__ __forceinline__ void drain_main(int count, int lane, const uint4* rin
   *ctail += __popc(m1);
   if (valid0 && !defer0) {
     ++*n_arc;
-    add_arc_term_closed(ws0, e0.y, sa_arc);
+    add_arc_term_closed(ws0, e0.y, sa_arc, sa_ch);
   }
   if (valid1 && !defer1) {
     ++*n_arc;
-    add_arc_term_closed(ws1, e1.y, sa_arc);
+    add_arc_term_closed(ws1, e1.y, sa_arc, sa_ch);
   }
 }
 
@@ -1558,7 +1562,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           const uint32_t a_cm = sbase + (uint32_t)Lay::cmeta + wo * (uint32_t)sizeof(PtMeta<TT>);
           const uint32_t a_q = sbase + (uint32_t)Lay::qtab;
           [[maybe_unused]] const uint32_t a_t = sbase + (uint32_t)Lay::ttab;  // table t bins
-          const uint32_t a_ch = sbase + (uint32_t)Lay::ch;
+          [[maybe_unused]] const uint32_t a_ch = sbase + (uint32_t)Lay::ch;
           const uint32_t bins4 = bins * 4u;
           // center k at byte offset ka = 16 k of the coordinate section (the
           // loop steps the offset: no index arithmetic per iteration)
@@ -1575,8 +1579,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             if (OWN) owner = (uint32_t)k < lim.x || cmk.idx < lim.y;
             // lanes without a neighbour hold coordinates 1e300: q = +inf fails
             const bool in = owner && q <= Qmax && du <= Tmax;
-            bool arc_i = false, arc_j = false;
-            uint32_t bin = 0;
+            uint32_t a_bin = 0;  // shared-space address of the bin's count (its half count: + bins4)
             if (in) {
               // bin_pair: first s_k >= d <=> first Q_k >= q; first t_l >= u.
               // q's bucket from the high word of its bits (log-spaced
@@ -1588,25 +1591,21 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               const uint32_t qh = (uint32_t)__double2hiint(q);
               const int bq = max((int)(qh >> q_shift) - q_base, 0);
               const QEntry qe = lds_qentry(a_q + (uint32_t)bq * (uint32_t)sizeof(QEntry));
-              uint32_t a_bin;  // shared-space address of the bin's count (its half count: + bins4)
               if constexpr (TUNI) {
                 const int32_t x = max((int32_t)du + t_add, t_lo);
                 const uint32_t tb = __umulhi((uint32_t)x, t_magic) >> t_sh;
                 a_bin = (q > qe.thr ? qe.hi : qe.lo) + tb * 4u;
-                bin = (a_bin - a_ch) >> 2;
               } else if constexpr (SINGLE) {
                 const int bt = (int)(du >> t_shift);
                 const TEntry<TT> te = lds_tentry<TT>(a_t + (uint32_t)bt * (uint32_t)sizeof(TEntry<TT>));
                 a_bin = (q > qe.thr ? qe.hi : qe.lo) + te.lo + (du > te.thr ? 4u : 0u);
-                bin = (a_bin - a_ch) >> 2;
               } else {
                 const int bt = (int)(du >> t_shift);
                 const TEntry<TT> te = lds_tentry<TT>(a_t + (uint32_t)bt * (uint32_t)sizeof(TEntry<TT>));
                 uint32_t sb = qe.lo, tb = te.lo;
                 while (q > S.Q[sb]) ++sb;
                 while (du > S.T[tb]) ++tb;
-                bin = sb * ct + tb;
-                a_bin = a_ch + bin * 4u;
+                a_bin = a_ch + (sb * ct + tb) * 4u;
               }
               reds_add_u32(a_bin, 1u);  // one per unordered pair (x2 at the flush)
               if constexpr (HALF) {
@@ -1615,15 +1614,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
                 const uint32_t h = (uint32_t)(du > cmk.vt) + (uint32_t)(du > nm.vt);
                 if (h) reds_add_u32(a_bin + bins4, h);
               }
-              if constexpr (ARC) {
-                // hi32(q) < sqh implies q below the safe radius^2 (omega == 1);
-                // the rest take the exact path (the few with q just under the
-                // safe radius get omega == 1 exactly there)
-                arc_i = qh >= cmk.sqh;
-                arc_j = qh >= nm.sqh;
-              }
             }
             if constexpr (!ARC) return;
+            // hi32(q) < sqh implies q below the safe radius^2 (omega == 1); the
+            // rest take the exact path (the few with q just under the safe
+            // radius get omega == 1 exactly there)
+            const uint32_t qh = (uint32_t)__double2hiint(q);
+            const bool arc_i = in && qh >= cmk.sqh, arc_j = in && qh >= nm.sqh;
             if (__any_sync(FULL_MASK, arc_i || arc_j)) {  // one vote on the common path
               const unsigned mi = __ballot_sync(FULL_MASK, arc_i);
               const unsigned mj = __ballot_sync(FULL_MASK, arc_j);
@@ -1632,11 +1629,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
               if (arc_i)
                 ring_c[qt + __popc(mi & lt_c)] =
-                    make_uint4(cpos_c[k], bin | (du > cmk.vt ? 0x80000000u : 0u), qlo, qhi);
+                    make_uint4(cpos_c[k], a_bin | (du > cmk.vt ? 0x80000000u : 0u), qlo, qhi);
               qt += __popc(mi);
               if (arc_j)
                 ring_c[qt + __popc(mj & lt_c)] =
-                    make_uint4(jpc, bin | (du > nm.vt ? 0x80000000u : 0u), qlo, qhi);
+                    make_uint4(jpc, a_bin | (du > nm.vt ? 0x80000000u : 0u), qlo, qhi);
               qt += __popc(mj);
             }
           };
