@@ -881,6 +881,11 @@ __device__ __forceinline__ uint4 lds_u32x4(uint32_t a) {
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
 }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ uint2 lds_u32x2(uint32_t a) {
   uint2 v;
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
@@ -1553,13 +1558,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
           const unsigned lt_c = (1u << lane_c) - 1u;
           // straight from the __shared__ array: the shared address space stays
           // visible (no generic-to-shared window arithmetic per load)
-          const uint32_t* cpos_c = reinterpret_cast<const uint32_t*>(smem_raw + Lay::cpos) + wo;
           const uint32_t jpc = *reinterpret_cast<volatile uint32_t*>(&s_jp[tidv]);  // == jp
           const volatile uint32_t* lim_v = reinterpret_cast<volatile uint32_t*>(&s_lim[tidv]);
           const uint2 lim = make_uint2(lim_v[0], lim_v[1]);
           const uint32_t sbase = *reinterpret_cast<volatile uint32_t*>(&s_base);
           const uint32_t a_cxy = sbase + (uint32_t)Lay::cxy + wo * (uint32_t)sizeof(double2);
           const uint32_t a_cm = sbase + (uint32_t)Lay::cmeta + wo * (uint32_t)sizeof(PtMeta<TT>);
+          const uint32_t a_cpos = sbase + (uint32_t)Lay::cpos + wo * 4u;  // centers' sorted positions
           const uint32_t a_q = sbase + (uint32_t)Lay::qtab;
           [[maybe_unused]] const uint32_t a_t = sbase + (uint32_t)Lay::ttab;  // table t bins
           [[maybe_unused]] const uint32_t a_ch = sbase + (uint32_t)Lay::ch;
@@ -1629,7 +1634,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
               const uint32_t qlo = (uint32_t)__double2loint(q), qhi = (uint32_t)__double2hiint(q);
               if (arc_i)
                 ring_c[qt + __popc(mi & lt_c)] =
-                    make_uint4(cpos_c[k], a_bin | (du > cmk.vt ? 0x80000000u : 0u), qlo, qhi);
+                    make_uint4(lds_u32(a_cpos + k * 4u), a_bin | (du > cmk.vt ? 0x80000000u : 0u), qlo, qhi);
               qt += __popc(mi);
               if (arc_j)
                 ring_c[qt + __popc(mj & lt_c)] =
