@@ -227,6 +227,7 @@ struct stk_ctx {
   DevBuf<double> scratch;
   DevBuf<uint32_t> perm;  // parallel permutation scratch (draws, lists, scans)
   DevBuf<unsigned long long> perm_mx;
+  DevBuf<uint2> scan_part;  // multi-CTA scan: chunk sums
   DevBuf<double> sx, sy;  // host-upload staging of the observed pattern
   DevBuf<int64_t> st;
 
@@ -749,14 +750,16 @@ enum class Source { Observed, Csr, Bootstrap, Permutation };
 // Fill patterns [p_first, p_first+count) of the batch.  Observed: copy from
 // device pointers (count must be 1).  Otherwise realisation seeds seed0 + j.
 void generate(stk_ctx* c, const Batch& B, Source src, int p_first, int count, uint64_t seed0,
-              const double* ox, const double* oy, const int64_t* ot) {
+              const double* ox, const double* oy, const int64_t* ot,
+              unsigned long long* validate_into = nullptr) {
   if (count <= 0) return;
   const uint64_t n = B.n;
-  if (src == Source::Observed) {  // one kernel for the three arrays (one graph node)
+  if (src == Source::Observed) {  // one kernel for the three arrays (one graph node),
+                                  // validating them on the way when asked
     const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)c->num_sms * 8);
     copy_points_kernel<<<std::max(blocks, 1u), 256, 0, c->stream>>>(
         B.x + (uint64_t)p_first * n, B.y + (uint64_t)p_first * n, B.t + (uint64_t)p_first * n,
-        ox, oy, ot, n);
+        ox, oy, ot, n, region_view(c), validate_into);
     CK(cudaGetLastError());
     ++c->launches;
     return;
@@ -831,7 +834,9 @@ void generate(stk_ctx* c, const Batch& B, Source src, int p_first, int count, ui
     CK(cudaMemsetAsync(cnt, 0, 4 * cn, c->stream));
     const dim3 g((unsigned)((n + 255) / 256), (unsigned)count);
     perm_count_kernel<<<g, 256, 0, c->stream>>>(n, J, cnt, rank);
-    scan_kernel<<<count, 1024, 0, c->stream>>>(cnt, start, istart, (uint32_t)n, c->perm_mx.p);
+    c->scan_part.ensure(scan_scratch((uint32_t)n, (unsigned)count));
+    c->launches += scan_launch(cnt, start, istart, (uint32_t)n, (unsigned)count, c->perm_mx.p,
+                               c->scan_part.p, c->stream) - 1;
     perm_scatter_kernel<<<g, 256, 0, c->stream>>>(n, J, start, rank, list);
     perm_sort_kernel<<<g, 256, 0, c->stream>>>(n, start, list);
     perm_final_kernel<<<g, 256, 0, c->stream>>>(B, p_first, ox, oy, ot, J, start, list);
@@ -871,14 +876,15 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
   CK(rec_event(e0, c->stream));
   CK(cudaMemsetAsync(B.cell_count, 0, sizeof(uint32_t) * (uint64_t)R * G.cells, c->stream));
   CK(cudaMemsetAsync(B.h_cnt, 0, sizeof(unsigned long long) * (uint64_t)R * P.bins * 4, c->stream));
-  dim3 gp((unsigned)((B.n + 255) / 256), (unsigned)R);
+  // K1 point kernels: 4 points per thread (kK1Per), 1,024 per CTA
+  dim3 gp((unsigned)((B.n + 1023) / 1024), (unsigned)R);
   key_kernel<<<gp, 256, 0, c->stream>>>(B, G, 0);
   CK(cudaGetLastError());
   ++c->launches;
-  scan_kernel<<<R, 1024, 0, c->stream>>>(B.cell_count, B.cell_start, B.item_start, G.cells,
-                                         B.stats + 5);
+  c->scan_part.ensure(scan_scratch(G.cells, (unsigned)R));
+  c->launches += scan_launch(B.cell_count, B.cell_start, B.item_start, G.cells, (unsigned)R,
+                             B.stats + 5, c->scan_part.p, c->stream);
   CK(cudaGetLastError());
-  ++c->launches;
   place_kernel<<<gp, 256, 0, c->stream>>>(B, G, 0);
   CK(cudaGetLastError());
   ++c->launches;
@@ -902,10 +908,9 @@ void run_batch(stk_ctx* c, const Plan& P, Batch& B, Timers& tm, int n_sel, uint3
     select_count_kernel<<<gs, 256, 0, c->stream>>>(B, G);
     CK(cudaGetLastError());
     ++c->launches;
-    scan_kernel<<<B.n_sel, 1024, 0, c->stream>>>(B.cell_count, B.sel_start, B.item_start, G.cells,
-                                                  B.stats + 5);
+    c->launches += scan_launch(B.cell_count, B.sel_start, B.item_start, G.cells,
+                               (unsigned)B.n_sel, B.stats + 5, c->scan_part.p, c->stream);
     CK(cudaGetLastError());
-    ++c->launches;
     select_scatter_kernel<<<gs, 256, 0, c->stream>>>(B, G);
     CK(cudaGetLastError());
     ++c->launches;
@@ -1134,7 +1139,15 @@ PipeInfo enqueue_pipeline(stk_ctx* c, const double* dx, const double* dy, const 
   const Source src = source_of(method);
   const uint32_t bins = P.bins;
   info.bins = bins;
-  if (out.validate) validate_points(c, dx, dy, dt, n);
+  // the observed pattern is validated by its copy-in kernel (no separate pass)
+  const bool fuse_validate = out.validate && with_observed;
+  if (fuse_validate) {
+    c->bad.ensure(1);
+    CK(cudaMemsetAsync(c->bad.p, 0xff, sizeof(unsigned long long), c->stream));
+    c->check_points = true;
+  } else if (out.validate) {
+    validate_points(c, dx, dy, dt, n);
+  }
   info.validated = c->check_points;
   CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * 8, c->stream));
   bool env_init = true;
@@ -1150,7 +1163,7 @@ PipeInfo enqueue_pipeline(stk_ctx* c, const double* dx, const double* dy, const 
     CK(rec_event(g0, c->stream));
     const bool obs_here = with_observed && done == 0;
     if (obs_here) {
-      generate(c, B, Source::Observed, 0, 1, 0, dx, dy, dt);
+      generate(c, B, Source::Observed, 0, 1, 0, dx, dy, dt, fuse_validate ? c->bad.p : nullptr);
       p = 1;
     }
     const int nsim = (int)(R - (obs_here ? 1 : 0));
@@ -1425,7 +1438,7 @@ void stk_destroy(stk_ctx* c) {
   c->scratch.release(); c->sx.release(); c->sy.release(); c->st.release();
   c->graph.reset();
   c->obsraw.release(); c->limbs.release(); c->d_rv.release();
-  c->perm.release(); c->perm_mx.release();
+  c->perm.release(); c->perm_mx.release(); c->scan_part.release();
   if (c->comm) nccl().comm_destroy(c->comm);
   if (c->hstage) cudaFreeHost(c->hstage);
   cudaStreamDestroy(c->stream);

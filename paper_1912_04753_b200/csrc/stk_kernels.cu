@@ -603,8 +603,8 @@ __global__ void resample_seq_kernel(Batch B, int p_first, int count, uint64_t se
 
 // ============================================================ K1 grid build
 __device__ __forceinline__ uint32_t cell_key(double x, double y, int64_t t, const GridGeom& G) {
-  int kx = (int)floor((x - G.x0) * G.inv_w);
-  int ky = (int)floor((y - G.y0) * G.inv_w);
+  int kx = __double2int_rd((x - G.x0) * G.inv_w);  // floor + convert: one F2I
+  int ky = __double2int_rd((y - G.y0) * G.inv_w);
   kx = min(max(kx, 0), G.nx - 1);
   ky = min(max(ky, 0), G.ny - 1);
   const int64_t dt = t - G.t0;
@@ -621,96 +621,216 @@ __device__ __forceinline__ uint32_t cell_key(double x, double y, int64_t t, cons
 // the leader adds the group size, each lane takes base + its position in the
 // group): clustered patterns put hundreds of a warp's points in few cells,
 // where per-point atomics on one counter serialise.  The order inside a cell
-// stays arbitrary, as before (results never depend on it).
-__global__ void key_kernel(Batch B, GridGeom G, int p_first) {
+// stays arbitrary, as before (results never depend on it).  kK1Per points per
+// thread (a CTA takes kK1Per * 256 consecutive points, coalesced per step):
+// their loads and returning atomics overlap (the kernel waited on one
+// load -> atomic chain per thread: long-scoreboard stalls 62%).
+constexpr int kK1Per = 4;
+__global__ void __launch_bounds__(256) key_kernel(Batch B, GridGeom G, int p_first) {
   const int p = p_first + blockIdx.y;
-  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const bool valid = i < B.n;
-  const uint64_t o = (uint64_t)p * B.n + i;
-  uint32_t k = 0xffffffffu;
-  if (valid) {
-    k = cell_key(B.x[o], B.y[o], B.t[o], G);
-    B.key[o] = k;
+  const uint64_t i0 = blockIdx.x * (uint64_t)(256 * kK1Per) + threadIdx.x;
+  const uint64_t pb = (uint64_t)p * B.n;
+  uint32_t k[kK1Per];
+#pragma unroll
+  for (int u = 0; u < kK1Per; ++u) {
+    const uint64_t i = i0 + u * 256;
+    k[u] = 0xffffffffu;
+    if (i < B.n) {
+      k[u] = cell_key(B.x[pb + i], B.y[pb + i], B.t[pb + i], G);
+      B.key[pb + i] = k[u];
+    }
   }
-  const unsigned peers = __match_any_sync(FULL_MASK, k);
   const int lane = threadIdx.x & 31;
-  const int leader = __ffs(peers) - 1;
-  uint32_t base = 0;
-  if (valid && lane == leader)
-    base = atomicAdd(&B.cell_count[(uint64_t)p * G.cells + k], (uint32_t)__popc(peers));
-  base = __shfl_sync(FULL_MASK, base, leader);
-  if (valid) B.rank[o] = base + (uint32_t)__popc(peers & ((1u << lane) - 1u));
+  uint32_t base[kK1Per], peers[kK1Per];
+#pragma unroll
+  for (int u = 0; u < kK1Per; ++u) {
+    peers[u] = __match_any_sync(FULL_MASK, k[u]);
+    const int leader = __ffs(peers[u]) - 1;
+    base[u] = 0;
+    if (k[u] != 0xffffffffu && lane == leader)
+      base[u] = atomicAdd(&B.cell_count[(uint64_t)p * G.cells + k[u]], (uint32_t)__popc(peers[u]));
+  }
+#pragma unroll
+  for (int u = 0; u < kK1Per; ++u) {
+    const uint32_t b = __shfl_sync(FULL_MASK, base[u], __ffs(peers[u]) - 1);
+    const uint64_t i = i0 + u * 256;
+    if (i < B.n) B.rank[pb + i] = b + (uint32_t)__popc(peers[u] & ((1u << lane) - 1u));
+  }
 }
 
-// Block-wide exclusive scan of two u32 streams (per-cell counts and their
-// 32-center chunk counts); one CTA of 1024 threads per pattern (blockIdx.x).
-__global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* counts, uint32_t* start_all,
-                                                     uint32_t* istart_all, uint32_t cells,
-                                                     unsigned long long* max_cell) {
+// Exclusive scan of two u32 streams per pattern (per-cell counts and their
+// 32-center item counts) over all SMs: chunks of kScanChunk cells, 8
+// consecutive cells per thread.  Pass 1 (scan_partial_kernel) sums each
+// chunk, pass 2 (scan_chunks_kernel, one CTA per pattern) scans the chunk
+// sums, pass 3 (scan_apply_kernel) scans each chunk from its offset.  A
+// pattern of one chunk takes pass 3 alone.  (One CTA per pattern walking all
+// cells serialised C5's 195k cells for 0.21 ms and a 1M-point permutation
+// for ~1 ms.)
+constexpr int kScanThreads = 512, kScanPer = 8, kScanChunk = kScanThreads * kScanPer;
+
+__device__ __forceinline__ void scan_load8(const uint32_t* cnt, uint32_t cells, uint32_t c0,
+                                           uint32_t (&a)[kScanPer]) {
+#pragma unroll
+  for (int j = 0; j < kScanPer; ++j) a[j] = c0 + j < cells ? cnt[c0 + j] : 0u;
+}
+
+// Block-wide exclusive scan of (va, vb) (kScanThreads threads); returns the
+// block totals through ta, tb.
+__device__ __forceinline__ void scan_block2(uint32_t& va, uint32_t& vb, uint32_t& ta,
+                                            uint32_t& tb) {
+  __shared__ uint32_t ws_a[kScanThreads / 32], ws_b[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t ia = va, ib = vb;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t xa = __shfl_up_sync(FULL_MASK, ia, o);
+    const uint32_t xb = __shfl_up_sync(FULL_MASK, ib, o);
+    if (lane >= o) {
+      ia += xa;
+      ib += xb;
+    }
+  }
+  if (lane == 31) {
+    ws_a[wid] = ia;
+    ws_b[wid] = ib;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    constexpr int nw = kScanThreads / 32;
+    uint32_t wa = lane < nw ? ws_a[lane] : 0u, wb = lane < nw ? ws_b[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < nw; o <<= 1) {
+      const uint32_t xa = __shfl_up_sync(FULL_MASK, wa, o);
+      const uint32_t xb = __shfl_up_sync(FULL_MASK, wb, o);
+      if (lane >= o) {
+        wa += xa;
+        wb += xb;
+      }
+    }
+    if (lane < nw) {
+      ws_a[lane] = wa;
+      ws_b[lane] = wb;
+    }
+  }
+  __syncthreads();
+  va = (wid ? ws_a[wid - 1] : 0u) + ia - va;
+  vb = (wid ? ws_b[wid - 1] : 0u) + ib - vb;
+  ta = ws_a[kScanThreads / 32 - 1];
+  tb = ws_b[kScanThreads / 32 - 1];
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_partial_kernel(const uint32_t* counts,
+                                                                     uint32_t cells,
+                                                                     uint2* partial,
+                                                                     unsigned long long* max_cell) {
+  const int p = blockIdx.y;
+  const uint32_t* cnt = counts + (uint64_t)p * cells;
+  uint32_t a[kScanPer];
+  scan_load8(cnt, cells, blockIdx.x * kScanChunk + threadIdx.x * kScanPer, a);
+  uint32_t sa = 0, sb = 0, amax = 0;
+#pragma unroll
+  for (int j = 0; j < kScanPer; ++j) {
+    sa += a[j];
+    sb += (a[j] + kItemCenters - 1) / kItemCenters;
+    amax = max(amax, a[j]);
+  }
+  uint32_t ta, tb;
+  scan_block2(sa, sb, ta, tb);
+  if (threadIdx.x == 0) partial[(uint64_t)p * gridDim.x + blockIdx.x] = make_uint2(ta, tb);
+  amax = __reduce_max_sync(FULL_MASK, amax);
+  if ((threadIdx.x & 31) == 0 && amax) atomicMax(max_cell, (unsigned long long)amax);
+}
+
+// Exclusive scan of a pattern's chunk sums (in place); the pattern totals go
+// to start[cells] / istart[cells].
+__global__ void __launch_bounds__(kScanThreads) scan_chunks_kernel(uint2* partial, uint32_t nchunks,
+                                                                    uint32_t* start_all,
+                                                                    uint32_t* istart_all,
+                                                                    uint32_t cells) {
   const int p = blockIdx.x;
+  uint2* pp = partial + (uint64_t)p * nchunks;
+  uint32_t carry_a = 0, carry_b = 0;
+  for (uint32_t base = 0; base < nchunks; base += kScanThreads) {
+    const uint32_t c = base + threadIdx.x;
+    const uint2 v = c < nchunks ? pp[c] : make_uint2(0u, 0u);
+    uint32_t va = v.x, vb = v.y, ta, tb;
+    scan_block2(va, vb, ta, tb);
+    if (c < nchunks) pp[c] = make_uint2(carry_a + va, carry_b + vb);
+    carry_a += ta;
+    carry_b += tb;
+    __syncthreads();  // ws_a/ws_b reuse
+  }
+  if (threadIdx.x == 0) {
+    start_all[(uint64_t)p * (cells + 1) + cells] = carry_a;
+    istart_all[(uint64_t)p * (cells + 1) + cells] = carry_b;
+  }
+}
+
+// partial == nullptr: the pattern is one chunk (offsets 0; writes the totals
+// and the largest count itself).
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* counts,
+                                                                   uint32_t cells,
+                                                                   const uint2* partial,
+                                                                   uint32_t* start_all,
+                                                                   uint32_t* istart_all,
+                                                                   unsigned long long* max_cell) {
+  const int p = blockIdx.y;
   const uint32_t* cnt = counts + (uint64_t)p * cells;
   uint32_t* start = start_all + (uint64_t)p * (cells + 1);
   uint32_t* istart = istart_all + (uint64_t)p * (cells + 1);
-  __shared__ uint32_t ws_a[32], ws_b[32];
-  __shared__ uint32_t carry_a, carry_b;
-  if (threadIdx.x == 0) carry_a = carry_b = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t amax = 0;
-  for (uint32_t base = 0; base < cells; base += 1024) {
-    const uint32_t c = base + threadIdx.x;
-    const uint32_t a = c < cells ? cnt[c] : 0u;
-    amax = max(amax, a);
-    const uint32_t b = (a + kItemCenters - 1) / kItemCenters;
-    uint32_t ia = a, ib = b;  // inclusive warp scan
+  const uint32_t c0 = blockIdx.x * kScanChunk + threadIdx.x * kScanPer;
+  uint32_t a[kScanPer];
+  scan_load8(cnt, cells, c0, a);
+  uint32_t sa = 0, sb = 0, amax = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t ta = __shfl_up_sync(FULL_MASK, ia, o);
-      const uint32_t tb = __shfl_up_sync(FULL_MASK, ib, o);
-      if (lane >= o) {
-        ia += ta;
-        ib += tb;
-      }
-    }
-    if (lane == 31) {
-      ws_a[wid] = ia;
-      ws_b[wid] = ib;
-    }
-    __syncthreads();
-    if (wid == 0) {
-      uint32_t va = ws_a[lane], vb = ws_b[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t ta = __shfl_up_sync(FULL_MASK, va, o);
-        const uint32_t tb = __shfl_up_sync(FULL_MASK, vb, o);
-        if (lane >= o) {
-          va += ta;
-          vb += tb;
-        }
-      }
-      ws_a[lane] = va;
-      ws_b[lane] = vb;
-    }
-    __syncthreads();
-    const uint32_t off_a = carry_a + (wid ? ws_a[wid - 1] : 0u);
-    const uint32_t off_b = carry_b + (wid ? ws_b[wid - 1] : 0u);
-    if (c < cells) {
-      start[c] = off_a + ia - a;
-      istart[c] = off_b + ib - b;
-    }
-    __syncthreads();
+  for (int j = 0; j < kScanPer; ++j) {
+    sa += a[j];
+    sb += (a[j] + kItemCenters - 1) / kItemCenters;
+    amax = max(amax, a[j]);
+  }
+  uint32_t ta, tb;
+  scan_block2(sa, sb, ta, tb);
+  if (partial) {
+    const uint2 off = partial[(uint64_t)p * gridDim.x + blockIdx.x];
+    sa += off.x;
+    sb += off.y;
+  } else {
     if (threadIdx.x == 0) {
-      carry_a += ws_a[31];
-      carry_b += ws_b[31];
+      start[cells] = ta;
+      istart[cells] = tb;
     }
-    __syncthreads();
+    amax = __reduce_max_sync(FULL_MASK, amax);
+    if ((threadIdx.x & 31) == 0 && amax) atomicMax(max_cell, (unsigned long long)amax);
   }
-  if (threadIdx.x == 0) {
-    start[cells] = carry_a;
-    istart[cells] = carry_b;
+#pragma unroll
+  for (int j = 0; j < kScanPer; ++j) {
+    if (c0 + j < cells) {
+      start[c0 + j] = sa;
+      istart[c0 + j] = sb;
+    }
+    sa += a[j];
+    sb += (a[j] + kItemCenters - 1) / kItemCenters;
   }
-  amax = __reduce_max_sync(FULL_MASK, amax);
-  if (lane == 0 && amax) atomicMax(max_cell, (unsigned long long)amax);
+}
+
+size_t scan_scratch(uint32_t cells, unsigned R) {
+  const size_t nch = (cells + kScanChunk - 1) / kScanChunk;
+  return nch > 1 ? nch * R : 0;
+}
+
+int scan_launch(const uint32_t* counts, uint32_t* start, uint32_t* istart, uint32_t cells,
+                unsigned R, unsigned long long* max_cell, uint2* partial, cudaStream_t s) {
+  const uint32_t nch = (cells + kScanChunk - 1) / kScanChunk;
+  if (nch <= 1) {
+    scan_apply_kernel<<<dim3(1, R), kScanThreads, 0, s>>>(counts, cells, nullptr, start, istart,
+                                                          max_cell);
+    return 1;
+  }
+  scan_partial_kernel<<<dim3(nch, R), kScanThreads, 0, s>>>(counts, cells, partial, max_cell);
+  scan_chunks_kernel<<<R, kScanThreads, 0, s>>>(partial, nch, start, istart, cells);
+  scan_apply_kernel<<<dim3(nch, R), kScanThreads, 0, s>>>(counts, cells, partial, start, istart,
+                                                          max_cell);
+  return 3;
 }
 
 // High word of a non-negative lower bound of v (the double with that high word
@@ -721,40 +841,78 @@ __device__ __forceinline__ uint32_t safe_hi(double v) {
 }
 
 // Counting sort, pass 2a: each point's sorted position (its cell's start plus
-// its rank) receives the point's input index (4-byte scattered writes).
-__global__ void place_kernel(Batch B, GridGeom G, int p_first) {
+// its rank) receives the point's input index (4-byte scattered writes);
+// kK1Per points per thread.
+__global__ void __launch_bounds__(256) place_kernel(Batch B, GridGeom G, int p_first) {
   const int p = p_first + blockIdx.y;
-  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (i >= B.n) return;
-  const uint64_t o = (uint64_t)p * B.n + i;
-  const uint32_t pos = B.cell_start[(uint64_t)p * (G.cells + 1) + B.key[o]] + B.rank[o];
-  B.perm[(uint64_t)p * B.n + pos] = (uint32_t)i;
+  const uint64_t i0 = blockIdx.x * (uint64_t)(256 * kK1Per) + threadIdx.x;
+  const uint64_t pb = (uint64_t)p * B.n;
+  const uint32_t* cst = B.cell_start + (uint64_t)p * (G.cells + 1);
+  uint32_t key[kK1Per], rk[kK1Per], pos[kK1Per];
+#pragma unroll
+  for (int u = 0; u < kK1Per; ++u) {
+    const uint64_t i = i0 + u * 256;
+    key[u] = 0;
+    rk[u] = 0;
+    if (i < B.n) {
+      key[u] = B.key[pb + i];
+      rk[u] = B.rank[pb + i];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kK1Per; ++u) pos[u] = cst[key[u]] + rk[u];
+#pragma unroll
+  for (int u = 0; u < kK1Per; ++u) {
+    const uint64_t i = i0 + u * 256;
+    if (i < B.n) B.perm[pb + pos[u]] = (uint32_t)i;
+  }
 }
 
 // Pass 2b: the sorted records, written in sorted order (coalesced) from
 // gathered input points.  qmax_hi: the high word of the largest in-threshold q;
 // a point whose safe-q word exceeds it is never an arc-pair center, so it gets
-// no arc record.
-__global__ void gather_kernel(Batch B, RegionView R, int p_first, uint32_t qmax_hi) {
+// no arc record.  kK1Per points per thread: the dependent perm -> x/y/t
+// loads of the four overlap.
+__global__ void __launch_bounds__(256) gather_kernel(Batch B, RegionView R, int p_first,
+                                                     uint32_t qmax_hi) {
   const int p = p_first + blockIdx.y;
-  const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (j >= B.n) return;
-  const uint64_t d = (uint64_t)p * B.n + j;
-  const uint32_t i = B.perm[d];
-  const uint64_t o = (uint64_t)p * B.n + i;
-  const double x = B.x[o], y = B.y[o];
-  const int64_t t = B.t[o];
-  B.pxy[d] = make_double2(x, y);  // the input index travels in the meta record
-  const uint32_t sq = R.no_safe ? 0u : safe_hi(safe_q(x, y, R));
-  if (B.parc && sq <= qmax_hi) B.parc[d] = rect_arc_record(x, y, R);
-  const int64_t vt = min(t - R.p0, R.p1 - t);
-  if (B.wide) {
-    PtMeta<int64_t> m{t - R.p0, vt, sq, i};
-    reinterpret_cast<PtMeta<int64_t>*>(B.pmeta)[d] = m;
-  } else {
-    const PtMeta<int32_t> m{(int32_t)(t - R.p0), (int32_t)vt, sq, i};
-    *reinterpret_cast<uint4*>(reinterpret_cast<PtMeta<int32_t>*>(B.pmeta) + d) =
-        make_uint4((uint32_t)m.t, (uint32_t)m.vt, m.sqh, m.idx);
+  const uint64_t j0 = blockIdx.x * (uint64_t)(256 * kK1Per) + threadIdx.x;
+  const uint64_t pb = (uint64_t)p * B.n;
+  uint32_t src[kK1Per];
+#pragma unroll
+  for (int u = 0; u < kK1Per; ++u) {
+    const uint64_t j = j0 + u * 256;
+    src[u] = j < B.n ? B.perm[pb + j] : 0u;
+  }
+  double x[kK1Per], y[kK1Per];
+  int64_t t[kK1Per];
+#pragma unroll
+  for (int u = 0; u < kK1Per; ++u) {
+    x[u] = y[u] = 0.0;
+    t[u] = R.p0;
+    if (j0 + u * 256 < B.n) {
+      x[u] = B.x[pb + src[u]];
+      y[u] = B.y[pb + src[u]];
+      t[u] = B.t[pb + src[u]];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kK1Per; ++u) {
+    const uint64_t j = j0 + u * 256;
+    if (j >= B.n) continue;
+    const uint64_t d = pb + j;
+    B.pxy[d] = make_double2(x[u], y[u]);  // the input index travels in the meta record
+    const uint32_t sq = R.no_safe ? 0u : safe_hi(safe_q(x[u], y[u], R));
+    if (B.parc && sq <= qmax_hi) B.parc[d] = rect_arc_record(x[u], y[u], R);
+    const int64_t vt = min(t[u] - R.p0, R.p1 - t[u]);
+    if (B.wide) {
+      PtMeta<int64_t> m{t[u] - R.p0, vt, sq, src[u]};
+      reinterpret_cast<PtMeta<int64_t>*>(B.pmeta)[d] = m;
+    } else {
+      const PtMeta<int32_t> m{(int32_t)(t[u] - R.p0), (int32_t)vt, sq, src[u]};
+      *reinterpret_cast<uint4*>(reinterpret_cast<PtMeta<int32_t>*>(B.pmeta) + d) =
+          make_uint4((uint32_t)m.t, (uint32_t)m.vt, m.sqh, m.idx);
+    }
   }
 }
 
@@ -1755,6 +1913,7 @@ void pair_kernel_launch(int wide, int mode, unsigned ctas, size_t smem, cudaStre
 }
 
 // ============================================================ K5 finalize
+constexpr int kFinSmemBins = 4096;  // bins staged in shared memory for the prefix
 // est::finalize_surface (estimator.cpp:94-114) + est::to_l (:51-57,71-82) per
 // pattern, in the reference's operation order.  One CTA per pattern: the exact
 // 128-bit sums are rounded once in parallel, the 2-D prefix runs as one
@@ -1788,7 +1947,31 @@ __global__ void __launch_bounds__(256) finalize_kernel(Batch B, uint32_t cs, uin
     K[b] = (cnt & 1ULL) ? __longlong_as_double(0x7ff8000000000000LL) : fixed128_to_double(hi, lo);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  // the 2-D prefix acc = h + up + left - diag, each bin with the reference's
+  // operation order; a bin needs only its final up / left / diag neighbours,
+  // so the anti-diagonals run in turn (cs + ct - 1 steps, one warp, shared
+  // memory) instead of one thread walking all bins
+  __shared__ double sK[kFinSmemBins];
+  if (bins <= (uint32_t)kFinSmemBins) {
+    for (uint32_t b = threadIdx.x; b < bins; b += blockDim.x) sK[b] = K[b];
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      for (uint32_t dg = 0; dg + 1 < cs + ct; ++dg) {
+        const uint32_t si_lo = dg >= ct ? dg - ct + 1 : 0u, si_hi = min(dg, cs - 1);
+        for (uint32_t si = si_lo + threadIdx.x; si <= si_hi; si += 32) {
+          const uint32_t ti = dg - si, b = si * ct + ti;
+          double acc = sK[b];
+          if (si > 0) acc += sK[b - ct];
+          if (ti > 0) acc += sK[b - 1];
+          if (si > 0 && ti > 0) acc -= sK[b - ct - 1];
+          sK[b] = acc;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < bins; b += blockDim.x) K[b] = sK[b];
+  } else if (threadIdx.x == 0) {
     for (uint32_t si = 0; si < cs; ++si) {
       double left = 0.0;
       for (uint32_t ti = 0; ti < ct; ++ti) {
@@ -1888,13 +2071,21 @@ __global__ void unpack_exact_kernel(const unsigned long long* limbs, uint32_t bi
 }
 
 // The observed pattern into its batch slot (x, y, t in one pass).
+// Copy-in of the observed pattern; with bad != nullptr it also runs
+// validate_kernel's region.contains check on the points it copies (one pass,
+// one graph node).
 __global__ void copy_points_kernel(double* x, double* y, int64_t* t, const double* ox,
-                                   const double* oy, const int64_t* ot, uint64_t n) {
+                                   const double* oy, const int64_t* ot, uint64_t n,
+                                   RegionView reg, unsigned long long* bad) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    x[i] = ox[i];
-    y[i] = oy[i];
-    t[i] = ot[i];
+    const double xi = ox[i], yi = oy[i];
+    const int64_t ti = ot[i];
+    x[i] = xi;
+    y[i] = yi;
+    t[i] = ti;
+    if (bad && !(point_in_region(xi, yi, reg) && ti >= reg.p0 && ti <= reg.p1))
+      atomicMin(bad, (unsigned long long)i);
   }
 }
 

@@ -48,8 +48,12 @@ __global__ void resample_seq_kernel(Batch B, int p_first, int count, uint64_t se
                                     const double* ox, const double* oy, const int64_t* ot,
                                     int mode);
 __global__ void key_kernel(Batch B, GridGeom G, int p_first);
-__global__ void scan_kernel(const uint32_t* counts, uint32_t* start, uint32_t* istart,
-                            uint32_t cells, unsigned long long* max_cell);
+// Exclusive scans of per-cell counts and item counts for R patterns of `cells`
+// cells (multi-CTA; `partial` holds scan_scratch(cells, R) entries); returns
+// the number of kernels launched.
+size_t scan_scratch(uint32_t cells, unsigned R);
+int scan_launch(const uint32_t* counts, uint32_t* start, uint32_t* istart, uint32_t cells,
+                unsigned R, unsigned long long* max_cell, uint2* partial, cudaStream_t s);
 __global__ void select_count_kernel(Batch B, GridGeom G);
 __global__ void select_scatter_kernel(Batch B, GridGeom G);
 __global__ void place_kernel(Batch B, GridGeom G, int p_first);
@@ -75,7 +79,8 @@ __global__ void unpack_exact_kernel(const unsigned long long* limbs, uint32_t bi
                                     unsigned long long* lo, unsigned long long* hi);
 __global__ void fill_kernel(double* p, uint32_t n, double v);
 __global__ void copy_points_kernel(double* x, double* y, int64_t* t, const double* ox,
-                                   const double* oy, const int64_t* ot, uint64_t n);
+                                   const double* oy, const int64_t* ot, uint64_t n,
+                                   RegionView reg, unsigned long long* bad);
 __global__ void weights_kernel(const double* cx, const double* cy, const double* d,
                                uint64_t count, RegionView reg, const RegionView* reg_g, double* w, int* overflow,
                                unsigned long long* bad);
