@@ -76,7 +76,8 @@ const char* stk_last_error(const stk_ctx* ctx);
 const char* stk_version(void);
 /* cudaStream_t the context launches on (for event timing by callers). */
 void* stk_stream(stk_ctx* ctx);
-/* Upper bound of device bytes for per-batch pattern buffers (default 16 GiB). */
+/* Upper bound of device bytes for per-batch pattern buffers (default: 40% of the device
+ * memory free at stk_create, clamped to [4 GiB, 64 GiB]). */
 int stk_set_memory_budget(stk_ctx* ctx, uint64_t bytes);
 
 /* ---- configuration ---------------------------------------------------- */

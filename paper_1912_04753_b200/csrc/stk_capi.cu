@@ -617,6 +617,10 @@ Plan make_plan(stk_ctx* c, uint64_t n, uint64_t patterns) {
   // the pair kernel indexes a batch with 32-bit offsets (pattern * n + j etc.)
   const uint64_t widest = std::max<uint64_t>({n, (uint64_t)P.G.cells + 1, P.max_items});
   R = std::max<uint64_t>(1, std::min<uint64_t>(R, 0xffffffffull / widest));
+  if (patterns > R) {  // equal batches: ceil(patterns / number of batches)
+    const uint64_t nb = (patterns + R - 1) / R;
+    R = (patterns + nb - 1) / nb;
+  }
   P.R = (int)R;
   return P;
 }
@@ -1412,6 +1416,15 @@ int stk_create(stk_ctx** out, int device) {
     if (const char* r = std::getenv("STK_STENCIL_RADIUS")) c->stencil_radius = std::max(1, std::min(4, std::atoi(r)));
     if (const char* r = std::getenv("STK_MIN_CELL_POP")) c->min_cell_pop = std::atof(r);
     if (const char* r = std::getenv("STK_TIME_RADIUS")) c->time_radius = std::max(0, std::min(8, std::atoi(r)));
+    {  // batch budget: 40% of the free device memory, between 4 and 64 GiB (a B200's
+       // 180 GB gives 64 GiB: C5 runs 3 batches of 67 patterns instead of 12 of 17, so
+       // the one-CTA-per-realisation generators and the pair kernel's tail see 4x the work)
+      size_t fr = 0, tot = 0;
+      if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+        c->mem_budget = std::min<uint64_t>(64ull << 30, std::max<uint64_t>(4ull << 30, fr / 5 * 2));
+      else
+        (void)cudaGetLastError();
+    }
     c->stats.ensure(8);
   } catch (const std::exception& e) {
     delete c;

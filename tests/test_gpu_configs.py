@@ -146,5 +146,5 @@ def test_c4_parity(api):
 
 def test_c5_parity(api):
     """configs[4]: 10M-point POI pattern + realisations {0, 1, 99, 198} of 199
-    (the job runs in several batches of the default 16 GiB budget)."""
+    (1 GB of device buffers per pattern)."""
     _subset_parity(api, "C5")
