@@ -1128,8 +1128,16 @@ struct PairLayout {
   static size_t __host__ __device__ total(uint32_t bins) { return al(lh(bins) + sizeof(ArcSum) * bins); }
 };
 
+// STK_NB_STAGE (experiment, 32-bit times): the next neighbour tile is staged in
+// shared memory by cp.async one tile ahead (north_star's staging, A/B against
+// the register-held tile): two 1 KB slots per warp after the arc sums.
+#ifdef STK_NB_STAGE
+constexpr size_t kStageBytes = (size_t)kPairWarps * 2 * 1024;
+#else
+constexpr size_t kStageBytes = 0;
+#endif
 size_t pair_kernel_smem(uint32_t bins, int wide) {
-  return wide ? PairLayout<int64_t>::total(bins) : PairLayout<int32_t>::total(bins);
+  return wide ? PairLayout<int64_t>::total(bins) : PairLayout<int32_t>::total(bins) + kStageBytes;
 }
 
 // Adds one arc-path ordered pair to the CTA histogram.  Its term in the
@@ -1289,6 +1297,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   __shared__ uint32_t s_jp[kPairWarps * 32];  // per-tile neighbour position of each lane
   __shared__ uint2 s_cur[kPairWarps * 32];    // lane cursor: (virtual index, its row) of the next tile
   __shared__ uint32_t s_base;               // shared-space address of smem_raw
+#ifdef STK_NB_STAGE
+  __shared__ uint32_t s_stag[kPairWarps];   // virtual index (lane 0) of the warp's staged tile
+  __shared__ uint32_t s_stage_off;          // byte offset of the staging slots
+#endif
   __shared__ uint32_t s_arc_off;            // byte offset of the arc-sum section (runtime-sized)
   using Lay = PairLayout<TT>;
   const Batch& B = A.B;
@@ -1364,6 +1376,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
   if (tid == 0) {
     s_base = (uint32_t)__cvta_generic_to_shared(smem_raw);
     s_arc_off = (uint32_t)Lay::lh(bins);
+#ifdef STK_NB_STAGE
+    s_stage_off = (uint32_t)Lay::total(bins);
+#endif
   }
   if (lane == 0) s_ring[w] = arcq0;
   // crossing scratch of the general weight (deferred drains only): global,
@@ -1510,7 +1525,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
                         // base arithmetic, nothing held in registers across the loop)
         s_nxy[w] = B.pxy + pb;
         s_nmeta[w] = pmeta_b + pb;
+#ifdef STK_NB_STAGE
+        s_stag[w] = 0xffffffffu;
+#endif
       }
+#ifdef STK_NB_STAGE
+      asm volatile("cp.async.wait_all;" ::: "memory");
+#endif
       __syncwarp();
       uint32_t qh = 0, qt = 0;    // arc ring head / tail (monotone)
       uint32_t ch_ = 0, ct_ = 0;  // deferred ring head / tail
@@ -1591,6 +1612,39 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         } else {
           jp = *reinterpret_cast<volatile uint32_t*>(&s_jp[tid]);
         }
+#ifdef STK_NB_STAGE
+        // slot of the tile at virtual index v: (v / 32) & 1 of the warp's two
+        auto stage_addr = [&](uint32_t v) {
+          return *reinterpret_cast<volatile uint32_t*>(&s_base) +
+                 *reinterpret_cast<volatile uint32_t*>(&s_stage_off) +
+                 ((uint32_t)threadIdx.x >> 5) * 2048u + ((v >> 5) & 1u) * 1024u +
+                 ((uint32_t)threadIdx.x & 31u) * 16u;
+        };
+        // requests the tile at the lane cursor (the one after the tiles taken so far)
+        auto stage_next = [&](uint32_t vt) {
+          if constexpr (sizeof(TT) == 4) {
+            // (votes: a branch on a value read back from shared memory is divergent to the
+            // compiler, which then gives up the uniform loop control of the whole walk)
+            if (__all_sync(FULL_MASK, vt < v_hi && *reinterpret_cast<volatile uint32_t*>(&s_stag[threadIdx.x >> 5]) != vt)) {
+              const volatile uint32_t* cu = reinterpret_cast<volatile uint32_t*>(&s_cur[tid]);
+              const uint32_t vn = cu[0], rown = cu[1];
+              const uint32_t offn = __shfl_sync(FULL_MASK, rowoff, rown & 31u);
+              if (vn < v_hi) {
+                const double2* const gx = *reinterpret_cast<const double2* const volatile*>(&s_nxy[w]) + (vn + offn);
+                const PtMeta<TT>* const gm =
+                    *reinterpret_cast<const PtMeta<TT>* const volatile*>(&s_nmeta[w]) + (vn + offn);
+                const uint32_t a = stage_addr(vt);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(a), "l"(gx) : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(a + 512u), "l"(gm) : "memory");
+              }
+              asm volatile("cp.async.commit_group;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) s_stag[w] = vt;
+              __syncwarp();
+            }
+          }
+        };
+#endif
         // this lane's neighbour, (re)loaded for every chunk (an L1 hit after the
         // first): nothing of the tile stays live across the drain site above,
         // whose register peak would otherwise push it to local memory
@@ -1600,10 +1654,27 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
         const double2* const nxy_p = *reinterpret_cast<const double2* const volatile*>(&s_nxy[w]);
         const PtMeta<TT>* const nmeta_p =
             *reinterpret_cast<const PtMeta<TT>* const volatile*>(&s_nmeta[w]);
+#ifdef STK_NB_STAGE
+        bool staged = false;
+        if constexpr (sizeof(TT) == 4)
+          staged = __all_sync(FULL_MASK, kc == 0 && *reinterpret_cast<volatile uint32_t*>(&s_stag[threadIdx.x >> 5]) == v0);
+        if (staged) {
+          asm volatile("cp.async.wait_all;" ::: "memory");
+          if (has) {
+            const uint32_t a = stage_addr(v0);
+            nxy = lds_f64x2(a);
+            const uint4 mv = lds_u32x4(a + 512u);
+            nm = PtMeta<TT>{(TT)mv.x, (TT)mv.y, mv.z, mv.w};
+          }
+        } else
+#endif
         if (has) {
           nxy = nxy_p[jp];
           nm = ld_meta<TT>(nmeta_p + jp);
         }
+#ifdef STK_NB_STAGE
+        if (kc == 0) stage_next(v0 + 32u);  // in flight while this tile's centers are walked
+#endif
         if (kc == 0) {
           // (an L1 prefetch of the lane's next-tile neighbour cost 0.9%: the
           // neighbour tiles stream from L2 fast enough, and the issue slots count)
@@ -1642,6 +1713,17 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             const bool has2 = jp2 != 0xffffffffu;
             double2 nxy2 = make_double2(1e300, 1e300);
             PtMeta<TT> nm2{0, 0, 0u, 0u};
+#ifdef STK_NB_STAGE
+            if (__all_sync(FULL_MASK, *reinterpret_cast<volatile uint32_t*>(&s_stag[threadIdx.x >> 5]) == v0 + 32u)) {
+              asm volatile("cp.async.wait_all;" ::: "memory");
+              if (has2) {
+                const uint32_t a = stage_addr(v0 + 32u);
+                nxy2 = lds_f64x2(a);
+                const uint4 mv = lds_u32x4(a + 512u);
+                nm2 = PtMeta<TT>{(TT)mv.x, (TT)mv.y, mv.z, mv.w};
+              }
+            } else
+#endif
             if (has2) {
               nxy2 = nxy_p[jp2];
               nm2 = ld_meta<TT>(nmeta_p + jp2);
@@ -1649,6 +1731,21 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
             const bool deep2 = __any_sync(FULL_MASK, has2) && v0 + 32u >= own_v &&
                                __all_sync(FULL_MASK, !has2 || (nm2.sqh > Qmax_hi && nm2.vt >= Tmax));
             if (deep2) {
+#ifdef STK_NB_STAGE
+              {  // the cursor past the second tile now: the tile after it is requested
+                 // before the centers are walked
+                const uint32_t nv = v2 + 32u;
+                for (;;) {
+                  const uint32_t rend = __shfl_sync(FULL_MASK, incl, row2 & 31u);
+                  const bool adv = nv < v_hi && nv >= rend;
+                  if (!__any_sync(FULL_MASK, adv)) break;
+                  row2 += adv ? 1u : 0u;
+                }
+                s_cur[tid] = make_uint2(nv, row2);
+                __syncwarp();
+                stage_next(v0 + 64u);
+              }
+#endif
               uint32_t tidv;
               asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tidv));
               const uint32_t wo = (tidv >> 5) * 32;
@@ -1682,6 +1779,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
                 count_pair(dx * dx + dy * dy, du);
                 count_pair(dx2 * dx2 + dy2 * dy2, du2);
               }
+#ifndef STK_NB_STAGE
               // the cursor past the second tile
               const uint32_t nv = v2 + 32u;
               for (;;) {
@@ -1691,6 +1789,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, STK_PAIR_MINB) pair_kernel(Pa
                 row2 += adv ? 1u : 0u;
               }
               s_cur[tid] = make_uint2(nv, row2);
+#endif
               v0 += 64;
               continue;
             }
