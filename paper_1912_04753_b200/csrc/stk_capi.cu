@@ -165,6 +165,7 @@ struct stk_ctx {
   uint64_t mem_budget = 16ull << 30;
   int time_radius = 0;     // time layers of the stencil, 0 = the spatial radius (STK_TIME_RADIUS env)
   double min_cell_pop = 8.0;  // finer cells only when this populous (STK_MIN_CELL_POP env)
+  double min_cell_pop_t = 12.5;  // ... and finer time layers only from here (STK_MIN_CELL_POP_T)
   int stencil_radius = 2;  // preferred cell refinement (STK_STENCIL_RADIUS env overrides)
   int rng = STK_RNG_MT19937_64;  // realisation generator (stk_set_rng)
 
@@ -565,19 +566,30 @@ GridGeom make_grid_geom(stk_ctx* c, uint64_t n) {
     // time cells may be finer or coarser than space cells (RT layers; the
     // half-stencil's (R + 1) + RT (2R + 1) rows must fit a warp); the density
     // test below uses the population of cells with R time layers
-    const int RT = std::max(1, std::min(c->time_radius > 0 ? c->time_radius : R,
-                                        (32 - (R + 1)) / (2 * R + 1)));
-    int64_t tw = std::max<int64_t>((tmax + RT - 1) / RT, 1);
-    int64_t nx, ny, nt;
-    for (;;) {
-      nx = ncell(ex, w);
-      ny = ncell(ey, w);
-      nt = (c->p1 - c->p0) / tw + 1;
-      if ((double)nx * (double)ny * (double)nt <= (double)cap) break;
-      if (nx * ny >= nt) w *= 1.5; else tw = tw + tw / 2 + 1;
-    }
+    int RT = std::max(1, std::min(c->time_radius > 0 ? c->time_radius : R,
+                                  (32 - (R + 1)) / (2 * R + 1)));
+    int64_t tw, nx, ny, nt;
+    auto size_cells = [&]() {
+      tw = std::max<int64_t>((tmax + RT - 1) / RT, 1);
+      for (;;) {
+        nx = ncell(ex, w);
+        ny = ncell(ey, w);
+        nt = (c->p1 - c->p0) / tw + 1;
+        if ((double)nx * (double)ny * (double)nt <= (double)cap) break;
+        if (nx * ny >= nt) w *= 1.5; else tw = tw + tw / 2 + 1;
+      }
+    };
+    size_cells();
     const double per_cell = (double)n / ((double)nx * ny * nt) * (double)RT / R;
     if (R > 1 && per_cell < c->min_cell_pop) continue;  // too sparse for finer cells
+    // Finer space cells but too few points per cell for R time layers as well:
+    // one time layer per t_max (twice the centers per item for 1.23x the
+    // candidates).  Measured crossover on B200 at ~12.5 points per cell
+    // (C2, 10 per cell: -5%; C4 at 800k points, 12.8: equal; C4, 16: +3.7%).
+    if (R > 1 && c->time_radius <= 0 && RT > 1 && per_cell < c->min_cell_pop_t) {
+      RT = 1;
+      size_cells();
+    }
     g.x0 = c->xmin;
     g.y0 = c->ymin;
     g.inv_w = 1.0 / w;
@@ -1415,6 +1427,7 @@ int stk_create(stk_ctx** out, int device) {
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* r = std::getenv("STK_STENCIL_RADIUS")) c->stencil_radius = std::max(1, std::min(4, std::atoi(r)));
     if (const char* r = std::getenv("STK_MIN_CELL_POP")) c->min_cell_pop = std::atof(r);
+    if (const char* r = std::getenv("STK_MIN_CELL_POP_T")) c->min_cell_pop_t = std::atof(r);
     if (const char* r = std::getenv("STK_TIME_RADIUS")) c->time_radius = std::max(0, std::min(8, std::atoi(r)));
     {  // batch budget: 40% of the free device memory, between 4 and 64 GiB (a B200's
        // 180 GB gives 64 GiB: C5 runs 3 batches of 67 patterns instead of 12 of 17, so

@@ -13,7 +13,7 @@ constexpr int kItemCenters = 32;    // centers per warp work item (one per lane)
 constexpr int kPartCells = STK_PART_CELLS;    // a cell this populous splits items into parts (>= 2)
 constexpr int kMaxParts = 32;       // ... up to this many parts per item
 #ifndef STK_TAIL_PARTS
-#define STK_TAIL_PARTS 4
+#define STK_TAIL_PARTS 3
 #endif
 constexpr int kTailParts = STK_TAIL_PARTS;  // slices of each of a task's last kTailItems items
 #ifndef STK_TAIL_ITEMS
