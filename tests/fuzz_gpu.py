@@ -1,7 +1,7 @@
 """Randomised differential test: the CUDA path against the oracle's C restatement on
 small random jobs (regions, periods, grids, patterns).  Counts must be bit-exact,
 weighted histograms and K within 1e-9 relative.
-    python tools/fuzz_gpu.py [cases] [first_seed]
+    python tests/fuzz_gpu.py [cases] [first_seed]
 Prints one line per failure and a summary; exit code 1 on any failure."""
 import os
 import sys
@@ -11,7 +11,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tests"))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 
 def random_case(seed):

@@ -1,7 +1,7 @@
 """Randomised differential test on the GPU: random regions (rectangles with offsets and
 extreme aspect ratios, convex polygons), periods (incl. wider than 32 bits), regular and
 irregular grids, CSR and clustered patterns, run_job with realisations — the CUDA path vs the
-oracle's C restatement (tools/fuzz_gpu.py; 3,000 further cases were run by hand).
+oracle's C restatement (tests/fuzz_gpu.py; 3,000 further cases were run by hand).
 Counts bit-exact, K and envelopes within 1e-9."""
 import os
 import sys
@@ -10,7 +10,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_random_jobs_match_oracle():
