@@ -76,7 +76,7 @@ def points(case, port):
 def run(cases, first, verbose=True):
     from conftest import rel_err, surfaces_close
     from oracle import port
-    from paper_1912_04753_b200.stripley import est, geom, rt
+    from paper_1912_04753_b200.stripley import est, geom, rt, sim
 
     bad = 0
     done = 0
@@ -114,6 +114,28 @@ def run(cases, first, verbose=True):
             ok_job = (res.telemetry.in_threshold_pairs == total and
                       np.all(np.abs(np.where(fl, res.upper_l.values - up, 0.0)) <= tol) and
                       np.all(np.abs(np.where(fl, res.lower_l.values - lo, 0.0)) <= tol))
+        rng = np.random.default_rng(seed)
+        if rng.random() < 0.25:  # shards of the pattern's pair work sum exactly to the whole
+            ns = int(rng.choice([2, 3, 5]))
+            parts = [est.pair_histogram((x, y, t), region, grid, shard=k_, nshards=ns)
+                     for k_ in range(ns)]
+            tot_c = sum(p_["counts"].astype(object) for p_ in parts)
+            tot_s = sum((p_["sum_hi"].astype(object) << 64) + p_["sum_lo"].astype(object)
+                        for p_ in parts) % (1 << 128)
+            whole = (h["sum_hi"].astype(object) << 64) + h["sum_lo"].astype(object)
+            ok_job = ok_job and bool(np.all(tot_c == h["counts"].astype(object))) and \
+                bool(np.all(tot_s == whole))
+        if rng.random() < 0.25 and c["n"] <= 4000:  # bootstrap / permutation null models
+            method = sim.Method.Bootstrap if rng.random() < 0.5 else sim.Method.Permutation
+            gen = port.generate_bootstrap if method == sim.Method.Bootstrap else \
+                port.generate_permutation
+            l_all, _, _ = sim.simulate((x, y, t), region, grid, method, 0, 2, c["jseed"])
+            for r in range(2):
+                bx, by, bt = gen(x, y, t, (c["jseed"] + r) % (2 ** 64))
+                e = port.estimate(bx, by, bt, c["ring"], c["p0"], c["p1"], c["s"], c["tv"])
+                fl = np.isfinite(e["l"])
+                tol = 1e-9 * max(1.0, float(np.max(np.abs(e["l"][fl])))) if fl.any() else 0.0
+                ok_job = ok_job and bool(np.all(np.abs(np.where(fl, l_all[r] - e["l"], 0.0)) <= tol))
         ok_counts = np.array_equal(h["counts"], o["counts"])
         fin = np.isfinite(o["k"])
         ok_k = surfaces_close(np.where(fin, k.values, 0.0), np.where(fin, o["k"], 0.0), 1e-9) and \

