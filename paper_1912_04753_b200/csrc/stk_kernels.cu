@@ -975,6 +975,20 @@ __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas) {
   // disjoint slices of its neighbour tiles taken by different warps.
   const uint64_t maxc = B.stats[5];
   uint64_t np = (maxc + kPartCells - 1) / kPartCells;
+  // Long items are cut as well, so that the warps of a task finish together: from
+  // the estimated warp-instructions per item (tiles x (tile start + 27 per
+  // center)), one part per ~12,000.  Each unit costs a few hundred instructions
+  // of set-up, which pays from ~100 tiles per item (measured on B200: C5's CSR
+  // realisations, 104 tiles of 32 centers: -3.4% at 8 parts; C4, 32 tiles of 15
+  // centers: +2.3% per extra part, and stays at whole items).
+  {
+    const double cells_st = (double)((G.rs + 1) + G.rt * (2 * G.rs + 1)) * (double)(2 * G.rs + 1);
+    const double ppc = (double)B.n / (double)G.cells;
+    const double work = cells_st * ppc / 32.0 * (95.0 + 27.0 * fmin(32.0, fmax(ppc, 1.0)));
+    uint64_t pw = (uint64_t)(work / 12000.0 + 0.5);
+    pw = pw > 10 ? 10 : pw;
+    np = np < pw ? pw : np;
+  }
   np = np < 1 ? 1 : (np > (uint64_t)kMaxParts ? (uint64_t)kMaxParts : np);
   const uint32_t parts = (uint32_t)np;
   uint64_t ti = total / ((uint64_t)STK_TASKS_PER_CTA * resident_ctas);
