@@ -974,7 +974,10 @@ __global__ void tasks_kernel(Batch B, GridGeom G, uint32_t resident_ctas) {
   // whole pattern in the extreme): each item is then walked as P parts,
   // disjoint slices of its neighbour tiles taken by different warps.
   const uint64_t maxc = B.stats[5];
-  uint64_t np = (maxc + kPartCells - 1) / kPartCells;
+  // (the parts are one value per call: a lone pattern cannot make other patterns'
+  // short items pay for its dense cells, so its threshold is half — C3 -3%)
+  const uint64_t part_cells = B.R == 1 ? (uint64_t)kPartCells / 2 : (uint64_t)kPartCells;
+  uint64_t np = (maxc + part_cells - 1) / part_cells;
   // Long items are cut as well, so that the warps of a task finish together: from
   // the estimated warp-instructions per item (tiles x (tile start + 27 per
   // center)), one part per ~12,000.  Each unit costs a few hundred instructions
