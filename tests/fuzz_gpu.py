@@ -14,6 +14,9 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 
+BIG = os.environ.get("FUZZ_BIG") == "1"  # larger patterns, polygons of up to 200 vertices
+
+
 def random_case(seed):
     rng = np.random.default_rng(seed)
     kind = rng.choice(["rect", "rect", "rect", "poly"])
@@ -24,7 +27,7 @@ def random_case(seed):
         ring = np.array([[off, off * 0.5], [off + w, off * 0.5], [off + w, off * 0.5 + h],
                          [off, off * 0.5 + h]])
     else:
-        nv = int(rng.integers(3, 41))
+        nv = int(rng.integers(3, 201 if BIG else 41))
         ang = np.sort(rng.uniform(0.0, 2.0 * np.pi, nv))
         while np.min(np.diff(np.concatenate([ang, [ang[0] + 2 * np.pi]]))) < 1e-3:
             ang = np.sort(rng.uniform(0.0, 2.0 * np.pi, nv))
@@ -33,7 +36,7 @@ def random_case(seed):
     p0 = int(rng.choice([0, 0, -86400 * 1000, 1_600_000_000]))
     dur = int(rng.choice([59, 10_000, 31_536_000, 31_536_000, 2 ** 33 + 12345]))
     p1 = p0 + dur
-    n = int(rng.choice([2, 3, 17, 200, 1000, 2500, 4000, 12000]))
+    n = int(rng.choice([6000, 12000, 20000, 30000] if BIG else [2, 3, 17, 200, 1000, 2500, 4000, 12000]))
     extent = max(w, h)
     s_max = float(min(w, h) * 10.0 ** rng.uniform(-2.0, 0.3))
     cs = int(rng.integers(1, 26))
